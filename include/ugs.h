@@ -1,0 +1,167 @@
+/*
+ * ugs.h -- C ABI of the B200-native (sm_100a) UltraGauss probe-plane
+ * rasterizer and training step ("libugs.so").
+ *
+ * Drop-in boundary for the reference's native path (echosplat,
+ * pkg/src/echosplat/):
+ *   ugs_bin            replaces _prepare (rasterizer.py:109-137) -- build_L,
+ *                      invert_lower_triangular, chi^2 boxes, cull, compact,
+ *                      clamped windows -- plus the tile binning / radix sort
+ *                      that the GPU forward needs (no counterpart in the ref)
+ *   ugs_forward        replaces forward_kernel (_kernels.py:19-47) and the
+ *                      background blend of rasterize (rasterizer.py:175-177)
+ *   ugs_backward       replaces backward_kernel (_kernels.py:50-101) and the
+ *                      raw-parameter chain + background grads of backward
+ *                      (gradients.py:84-113)
+ *   ugs_grad_stats     replaces the densify statistics (trainer.py:399-401)
+ *   ugs_adam_step      replaces adam_step (trainer.py:170-200)
+ *   ugs_densify_apply  replaces the row surgery of densify_prune_resample
+ *                      (trainer.py:208-279; selection/RNG stay on the host)
+ *
+ * Conventions (the reference kernels: caller owns and zeroes the outputs,
+ * no error path; here every entry point returns 0 on success or a negative
+ * ugs_status and ugs_last_error() describes the failure):
+ *   - every pointer marked (dev) is CUDA device memory, (host) host memory;
+ *   - work is enqueued on the given cudaStream_t (passed as void*), nothing
+ *     synchronizes except ugs_bin (one device->host read of the per-slice
+ *     counts, needed to size the tile lists);
+ *   - a ugs_plan owns the binning buffers of one batch; distinct plans may
+ *     be used concurrently from different threads/streams;
+ *   - no torch types: plain pointers and sizes, so ctypes / cffi / JNI /
+ *     cgo bindings are mechanical.
+ */
+#ifndef UGS_H
+#define UGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define UGS_API __attribute__((visibility("default")))
+#else
+#define UGS_API
+#endif
+
+#define UGS_ABI_VERSION 1
+#define UGS_TILE 16 /* pixels per tile side */
+
+typedef enum ugs_status {
+    UGS_OK = 0,
+    UGS_ERR_INVALID = -1, /* bad argument (InvalidParameterError in the ref) */
+    UGS_ERR_CUDA = -2,    /* CUDA runtime / launch failure */
+    UGS_ERR_OOM = -3,     /* device allocation failed */
+    UGS_ERR_RANGE = -4    /* sizes beyond the 32-bit index budget */
+} ugs_status;
+
+/* Per-slice constants, formed on the host exactly as the reference forms
+ * them (geometry.py:61-64 inverse, :107-120 plane_axes, rasterizer.py:115-135
+ * casts): everything float32. */
+typedef struct ugs_slice {
+    float rw[9];      /* f32(R^T), row-major: world -> probe rotation */
+    float tw[3];      /* f32(-R^T t) */
+    float origin[3];  /* f32(t - cx*du - cy*dv): world position of pixel (0,0) */
+    float du[3];      /* f32(R[:,0]*spacing) */
+    float dv[3];      /* f32(R[:,1]*spacing) */
+    float sqrt_cut;   /* sqrtf(f32(chi2.ppf(p, 3))) */
+    float s;          /* f32(spacing) */
+    float cx, cy;     /* f32((W-1)/2), f32((H-1)/2) */
+    float x1h, x2h;   /* f32((W-1)/2*spacing), f32((H-1)/2*spacing) */
+    int32_t width, height;
+    int32_t tiles_x, tiles_y; /* ceil(W/16), ceil(H/16): filled by ugs_bin */
+    int32_t tile_base;        /* first bin id of this slice: filled by ugs_bin */
+    int32_t reserved;
+    int64_t pix_base;         /* offset of this slice in the (S,H,W) outputs */
+} ugs_slice;
+
+/* The Gaussian cloud (GaussianCloud, model.py:31-89), structure of arrays. */
+typedef struct ugs_cloud {
+    const float *means;         /* (dev) (n,3) mm, world frame */
+    const float *l_raw;         /* (dev) (n,6): L11,L22,L33,L21,L31,L32 raw */
+    const float *intensity_raw; /* (dev) (n,) */
+    const float *opacity_raw;   /* (dev) (n,) */
+    const double *bg_raw;       /* (dev) [2]: bg_intensity_raw, bg_opacity_raw */
+    int64_t n;
+    double beta;                /* L_jj = l_jj^2 + beta, beta > 0 (f32(beta)
+                                   on the float32 render path, as the ref) */
+} ugs_cloud;
+
+typedef struct ugs_plan ugs_plan;
+
+UGS_API const char *ugs_last_error(void);
+UGS_API int ugs_abi_version(void);
+
+UGS_API int ugs_plan_create(ugs_plan **out);
+UGS_API int ugs_plan_destroy(ugs_plan *plan);
+
+/* Phase 1 + binning for a batch of S slices (host array `slices`; the
+ * library fills tiles_x/tiles_y/tile_base and keeps a device copy).
+ * Writes per-slice accepted counts m_out[S] and tile-instance counts
+ * k_out[S] (host).  Synchronizes `stream` once. */
+UGS_API int ugs_bin(ugs_plan *plan, const ugs_cloud *cloud, ugs_slice *slices, int S,
+            void *stream, int64_t *m_out, int64_t *k_out);
+
+/* Accepted Gaussian indices (ascending per slice, slices concatenated) and
+ * their inclusive pixel windows (iu0,iu1,iv0,iv1) -- the reference's
+ * RenderBuffers.accepted and _prepare windows.  Either pointer may be NULL. */
+UGS_API int ugs_export_accepted(const ugs_plan *plan, int32_t *accepted /* (dev) M */,
+                        int32_t *windows /* (dev) M x 4 */, void *stream);
+
+/* Sorted tile lists: bin_range (dev, n_bins x 2 = [start,end)) and, per
+ * sorted entry, the Gaussian index it refers to (dev, K).  n_bins_out and
+ * k_total_out (host) may be queried with NULL device pointers. */
+UGS_API int ugs_export_bins(const ugs_plan *plan, int32_t *bin_range,
+                    int32_t *sorted_gauss, int32_t *n_bins_out,
+                    int64_t *k_total_out, void *stream);
+
+/* Forward accumulation + background for every slice of the last ugs_bin:
+ * num/den (dev) float32, slice s at slices[s].pix_base, row-major H x W.
+ * Fully overwrites the covered pixels (no caller zeroing needed). */
+UGS_API int ugs_forward(ugs_plan *plan, const ugs_cloud *cloud, float *num, float *den,
+                void *stream);
+
+/* Backward for every slice of the last ugs_bin.  d_pixels (dev, same layout
+ * as num).  Accumulates `scale` x (raw-parameter gradients) into grad (dev,
+ * float32, 11n+2: [means 3n | l_raw 6n | intensity n | opacity n | bg 2])
+ * and sets touched[g] = 1 for every accepted Gaussian (touched may be NULL).
+ * Slices are reduced in order, without atomics: deterministic. */
+UGS_API int ugs_backward(ugs_plan *plan, const ugs_cloud *cloud, const float *num,
+                 const float *den, const float *d_pixels, float *grad,
+                 uint8_t *touched, float scale, void *stream);
+
+/* grad_sum[g] += ||d_means[g]||, grad_cnt[g] += 1 for touched Gaussians,
+ * then clears touched (trainer.py:399-401). */
+UGS_API int ugs_grad_stats(const float *grad, int64_t n, uint8_t *touched,
+                   float *grad_sum, int32_t *grad_cnt, void *stream);
+
+/* One Adam step over all groups, bit-compatible with trainer.py:170-200.
+ * lr[0] means, lr[1] l_raw, lr[2] intensity, lr[3] opacity, lr[4] bg.
+ * m, v (dev) flat like grad.  t is the step count after increment.
+ * If zero_grad != 0 the gradient buffer is cleared after use. */
+UGS_API int ugs_adam_step(float *means, float *l_raw, float *intensity_raw,
+                  float *opacity_raw, double *bg_raw, float *grad, float *m,
+                  float *v, int64_t n, int64_t t, const double *lr,
+                  double beta1, double beta2, double eps, int zero_grad,
+                  void *stream);
+
+/* Densify/prune row surgery (trainer.py:208-279, model.py:147-152):
+ * dst row j < n_keep copies src row keep[j]; then for each of the n_new
+ * candidates c (cand = index into the KEPT rows): split[c] != 0 ->
+ * parent row cand[c] gets child mean mu + Linv^T z[c][0:3] and the shrunk
+ * l_raw, and new row n_keep+c gets mu + Linv^T z[c][3:6] with the same
+ * l_raw; split[c] == 0 -> new row is a copy.  New rows' Adam moments are
+ * zero.  src/dst param and moment buffers must not alias. */
+UGS_API int ugs_densify_apply(const ugs_cloud *src, const float *m_src,
+                      const float *v_src, const int32_t *keep, int64_t n_keep,
+                      const int32_t *cand, const uint8_t *split,
+                      const double *z, int64_t n_new, double split_factor,
+                      float *means, float *l_raw, float *intensity_raw,
+                      float *opacity_raw, float *m_dst, float *v_dst,
+                      void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UGS_H */

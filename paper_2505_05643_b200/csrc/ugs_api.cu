@@ -1,0 +1,324 @@
+// C ABI entry points (include/ugs.h): plan lifetime, batch binning, forward,
+// backward, exports.  Error reporting: negative ugs_status + thread-local
+// message (ugs_last_error), the reference raises InvalidParameterError at
+// its API layer for the same conditions (gradients.py:43-52).
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ugs_internal.cuh"
+
+namespace ugs {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? UGS_ERR_OOM : UGS_ERR_CUDA;
+}
+
+namespace {
+
+template <typename T>
+int ensure(T **ptr, size_t *cap, size_t need, const char *what) {
+    if (need <= *cap && *ptr) return UGS_OK;
+    if (*ptr) {
+        cudaError_t e = cudaFree(*ptr);
+        *ptr = nullptr;
+        *cap = 0;
+        if (e != cudaSuccess) return cuda_fail(e, what);
+    }
+    size_t alloc = need + need / 4 + 64;   // headroom: counts drift per step
+    cudaError_t e = cudaMalloc((void **)ptr, alloc * sizeof(T));
+    if (e != cudaSuccess) {
+        *ptr = nullptr;
+        return cuda_fail(e, what);
+    }
+    *cap = alloc;
+    return UGS_OK;
+}
+
+int ensure_host(ugs_plan *p, int S) {
+    if (S <= p->h_cap) return UGS_OK;
+    delete[] p->h_slice_base;
+    delete[] p->h_m;
+    delete[] p->h_tile_base;
+    delete[] p->h_ntile;
+    p->h_slice_base = new int64_t[2 * S];
+    p->h_m = new int64_t[S];
+    p->h_tile_base = new int32_t[S];
+    p->h_ntile = new int32_t[S];
+    p->h_cap = S;
+    return UGS_OK;
+}
+
+int check_cloud(const ugs_cloud *c) {
+    if (!c) { set_error("cloud is NULL"); return UGS_ERR_INVALID; }
+    if (!(c->beta > 0)) { set_error("beta must be > 0"); return UGS_ERR_INVALID; }
+    if (c->n < 0 || c->n > 0x7fffffffLL) {
+        set_error("cloud size out of range (0 <= n < 2^31)");
+        return UGS_ERR_RANGE;
+    }
+    if (c->n > 0 && (!c->means || !c->l_raw || !c->intensity_raw || !c->opacity_raw)) {
+        set_error("cloud has NULL parameter arrays");
+        return UGS_ERR_INVALID;
+    }
+    if (!c->bg_raw) { set_error("cloud bg_raw is NULL"); return UGS_ERR_INVALID; }
+    return UGS_OK;
+}
+
+int bits_for(int64_t n) {
+    int b = 0;
+    while (((int64_t)1 << b) < n) ++b;
+    return b;
+}
+
+}  // namespace
+}  // namespace ugs
+
+using namespace ugs;
+
+extern "C" const char *ugs_last_error(void) { return g_err.c_str(); }
+
+extern "C" int ugs_abi_version(void) { return UGS_ABI_VERSION; }
+
+extern "C" int ugs_plan_create(ugs_plan **out) {
+    if (!out) { set_error("ugs_plan_create: out is NULL"); return UGS_ERR_INVALID; }
+    *out = new ugs_plan();
+    return UGS_OK;
+}
+
+extern "C" int ugs_plan_destroy(ugs_plan *p) {
+    if (!p) return UGS_OK;
+    PlanBuffers &b = p->b;
+    void *bufs[] = {b.blk_cnt, b.slice_tot, b.slice_base, b.slices, b.rec,
+                    b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
+                    b.vals2, b.partial, b.hist, b.scan_tmp, b.bin_range,
+                    b.bin_bg};
+    for (void *q : bufs)
+        if (q) cudaFree(q);
+    delete[] p->h_slice_base;
+    delete[] p->h_m;
+    delete[] p->h_tile_base;
+    delete[] p->h_ntile;
+    delete p;
+    return UGS_OK;
+}
+
+extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
+                       int S, void *stream, int64_t *m_out, int64_t *k_out) {
+    if (!p || !slices || S < 1 || S > 64) {
+        set_error("ugs_bin: need a plan and 1 <= S <= 64 slices");
+        return UGS_ERR_INVALID;
+    }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    PlanBuffers &b = p->b;
+    // tiles and bin ids
+    int tile_base = 0, max_tiles = 0;
+    for (int s = 0; s < S; ++s) {
+        ugs_slice &sl = slices[s];
+        if (sl.width < 1 || sl.height < 1 || sl.width > 32767 || sl.height > 32767 ||
+            !(sl.s > 0)) {
+            set_error("ugs_bin: slice width/height must be in [1, 32767], spacing > 0");
+            return UGS_ERR_INVALID;
+        }
+        sl.tiles_x = (sl.width + kTile - 1) / kTile;
+        sl.tiles_y = (sl.height + kTile - 1) / kTile;
+        sl.tile_base = tile_base;
+        const int nt = sl.tiles_x * sl.tiles_y;
+        tile_base += nt;
+        if (nt > max_tiles) max_tiles = nt;
+    }
+    const int n_bins = tile_base;
+    if ((rc = ensure_host(p, S))) return rc;
+    p->S = S;
+    p->n_bins = n_bins;
+    p->max_tiles = max_tiles;
+    p->n = c->n;
+    for (int s = 0; s < S; ++s) {
+        p->h_tile_base[s] = slices[s].tile_base;
+        p->h_ntile[s] = slices[s].tiles_x * slices[s].tiles_y;
+    }
+    size_t cap_sl = (size_t)b.slices_cap;
+    if ((rc = ensure(&b.slices, &cap_sl, (size_t)S, "alloc slices"))) return rc;
+    b.slices_cap = (int)cap_sl;
+    UGS_CUDA(cudaMemcpyAsync(b.slices, slices, sizeof(ugs_slice) * S,
+                             cudaMemcpyHostToDevice, st));
+    const int nblk = (int)((c->n + kPrepThreads - 1) / kPrepThreads);
+    if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, (size_t)S * (nblk > 0 ? nblk : 1),
+                     "alloc blk_cnt")))
+        return rc;
+    {
+        static_assert(sizeof(unsigned long long) == 8, "");
+        size_t cap = b.slice_tot ? 128 : 0;
+        if ((rc = ensure(&b.slice_tot, &cap, (size_t)128, "alloc slice_tot"))) return rc;
+        size_t cap2 = b.slice_base ? 128 : 0;
+        if ((rc = ensure(&b.slice_base, &cap2, (size_t)128, "alloc slice_base"))) return rc;
+    }
+    std::vector<unsigned long long> tot(2 * S, 0ull);
+    if (c->n > 0) {
+        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, nblk, st))) return rc;
+        if ((rc = launch_prepare_scan(b.blk_cnt, S, nblk, b.slice_tot, st))) return rc;
+        UGS_CUDA(cudaMemcpyAsync(tot.data(), b.slice_tot, sizeof(unsigned long long) * 2 * S,
+                                 cudaMemcpyDeviceToHost, st));
+        UGS_CUDA(cudaStreamSynchronize(st));
+    }
+    int64_t m_total = 0, k_total = 0;
+    for (int s = 0; s < S; ++s) {
+        p->h_slice_base[2 * s] = m_total;
+        p->h_slice_base[2 * s + 1] = k_total;
+        p->h_m[s] = (int64_t)tot[2 * s];
+        if (m_out) m_out[s] = (int64_t)tot[2 * s];
+        if (k_out) k_out[s] = (int64_t)tot[2 * s + 1];
+        m_total += (int64_t)tot[2 * s];
+        k_total += (int64_t)tot[2 * s + 1];
+    }
+    if (k_total >= 0x7fffffffLL || m_total >= 0x7fffffffLL) {
+        set_error("ugs_bin: batch exceeds 2^31 tile instances; use fewer slices");
+        return UGS_ERR_RANGE;
+    }
+    p->m_total = m_total;
+    p->k_total = k_total;
+    UGS_CUDA(cudaMemcpyAsync(b.slice_base, p->h_slice_base, sizeof(int64_t) * 2 * S,
+                             cudaMemcpyHostToDevice, st));
+    if ((rc = ensure(&b.rec, &b.rec_cap, (size_t)m_total + 1, "alloc rec"))) return rc;
+    if ((rc = ensure(&b.rec_gid, &b.rec_gid_cap, (size_t)m_total + 2, "alloc rec_gid")))
+        return rc;
+    if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)m_total + 2, "alloc rec_inst")))
+        return rc;
+    const size_t kneed = (size_t)k_total + 1;
+    if (kneed > b.inst_cap || !b.owner) {
+        void *olds[] = {b.owner, b.keys, b.vals, b.keys2, b.vals2, b.partial};
+        for (void *q : olds)
+            if (q) cudaFree(q);
+        b.inst_cap = kneed + kneed / 4 + 64;
+        UGS_CUDA(cudaMalloc(&b.owner, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.keys, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.vals, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.keys2, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.vals2, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.partial, sizeof(float) * 8 * b.inst_cap));
+    }
+    const size_t hn = radix_hist_entries(k_total) + 1;
+    if ((rc = ensure(&b.hist, &b.hist_cap, hn, "alloc hist"))) return rc;
+    if ((rc = ensure(&b.scan_tmp, &b.scan_tmp_cap, scan_tmp_entries(hn) + 1,
+                     "alloc scan_tmp")))
+        return rc;
+    if (b.bin_cap < (size_t)n_bins || !b.bin_range) {
+        if (b.bin_range) cudaFree(b.bin_range);
+        if (b.bin_bg) cudaFree(b.bin_bg);
+        b.bin_cap = (size_t)n_bins + 64;
+        UGS_CUDA(cudaMalloc(&b.bin_range, sizeof(int2) * b.bin_cap));
+        UGS_CUDA(cudaMalloc(&b.bin_bg, sizeof(float2) * b.bin_cap));
+    }
+    if (c->n > 0 && m_total > 0) {
+        if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
+                                      b.rec, b.rec_gid, b.rec_inst, b.owner, b.keys,
+                                      m_total, k_total, st)))
+            return rc;
+    } else {
+        int32_t zero = 0;
+        UGS_CUDA(cudaMemcpyAsync(b.rec_inst, &zero, sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+    }
+    if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, k_total,
+                               bits_for(n_bins), b.hist, b.scan_tmp, st,
+                               &p->sorted_keys, &p->sorted_vals)))
+        return rc;
+    if ((rc = launch_bin_ranges(p->sorted_keys, k_total, b.bin_range, n_bins, st)))
+        return rc;
+    return UGS_OK;
+}
+
+extern "C" int ugs_forward(ugs_plan *p, const ugs_cloud *c, float *num,
+                           float *den, void *stream) {
+    if (!p || !num || !den) { set_error("ugs_forward: NULL argument"); return UGS_ERR_INVALID; }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (c->n != p->n) {
+        set_error("ugs_forward: cloud size differs from the binned cloud");
+        return UGS_ERR_INVALID;
+    }
+    return launch_forward(*p, *c, p->sorted_vals, num, den, (cudaStream_t)stream);
+}
+
+extern "C" int ugs_backward(ugs_plan *p, const ugs_cloud *c, const float *num,
+                            const float *den, const float *d_pixels, float *grad,
+                            uint8_t *touched, float scale, void *stream) {
+    if (!p || !num || !den || !d_pixels || !grad) {
+        set_error("ugs_backward: NULL argument");
+        return UGS_ERR_INVALID;
+    }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (c->n != p->n) {
+        set_error("ugs_backward: buffers do not match this cloud");
+        return UGS_ERR_INVALID;
+    }
+    return launch_backward(*p, *c, p->sorted_vals, num, den, d_pixels, grad, touched,
+                           scale, (cudaStream_t)stream);
+}
+
+namespace ugs {
+namespace {
+__global__ void export_accepted_kernel(const Rec *__restrict__ rec,
+                                       const int32_t *__restrict__ gid, int64_t m,
+                                       int32_t *__restrict__ acc,
+                                       int32_t *__restrict__ win) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    if (acc) acc[r] = gid[r];
+    if (win) {
+        const int wu = __float_as_int(rec[r].r2.y), wv = __float_as_int(rec[r].r2.z);
+        win[4 * r + 0] = wu & 0xffff;
+        win[4 * r + 1] = wu >> 16;
+        win[4 * r + 2] = wv & 0xffff;
+        win[4 * r + 3] = wv >> 16;
+    }
+}
+
+__global__ void export_sorted_kernel(const uint32_t *__restrict__ vals,
+                                     const uint32_t *__restrict__ owner,
+                                     const int32_t *__restrict__ gid, int64_t k,
+                                     int32_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    out[i] = gid[owner[vals[i]]];
+}
+}  // namespace
+}  // namespace ugs
+
+extern "C" int ugs_export_accepted(const ugs_plan *p, int32_t *accepted,
+                                   int32_t *windows, void *stream) {
+    if (!p) { set_error("ugs_export_accepted: NULL plan"); return UGS_ERR_INVALID; }
+    if (p->m_total == 0) return UGS_OK;
+    const int th = 256;
+    export_accepted_kernel<<<(unsigned)((p->m_total + th - 1) / th), th, 0,
+                             (cudaStream_t)stream>>>(p->b.rec, p->b.rec_gid,
+                                                     p->m_total, accepted, windows);
+    UGS_LAUNCH_CHECK("export_accepted_kernel");
+    return UGS_OK;
+}
+
+extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
+                               int32_t *sorted_gauss, int32_t *n_bins_out,
+                               int64_t *k_total_out, void *stream) {
+    if (!p) { set_error("ugs_export_bins: NULL plan"); return UGS_ERR_INVALID; }
+    if (n_bins_out) *n_bins_out = p->n_bins;
+    if (k_total_out) *k_total_out = p->k_total;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (bin_range && p->n_bins > 0)
+        UGS_CUDA(cudaMemcpyAsync(bin_range, p->b.bin_range, sizeof(int2) * p->n_bins,
+                                 cudaMemcpyDeviceToDevice, st));
+    if (sorted_gauss && p->k_total > 0) {
+        const int th = 256;
+        export_sorted_kernel<<<(unsigned)((p->k_total + th - 1) / th), th, 0, st>>>(
+            p->sorted_vals, p->b.owner, p->b.rec_gid, p->k_total, sorted_gauss);
+        UGS_LAUNCH_CHECK("export_sorted_kernel");
+    }
+    return UGS_OK;
+}

@@ -1,0 +1,166 @@
+// Per-Gaussian phase-1 geometry, bit-exact with the reference's float32
+// numpy sequence (ref pkg/src/echosplat/rasterizer.py:109-137; SURVEY
+// section 8 a4').  Every operation is an explicitly rounded intrinsic so nvcc
+// can never contract or reassociate it.
+#pragma once
+#include "ugs_internal.cuh"
+
+namespace ugs {
+
+struct Factor {
+    float L00, L10, L11, L20, L21, L22;   // build_L (model.py:101-118)
+    float LT[3][3];                       // (L^-1)^T (model.py:121-138)
+};
+
+__device__ __forceinline__ Factor make_factor(const float *__restrict__ l_raw,
+                                              int64_t g, float beta) {
+    Factor f;
+    const float *l = l_raw + 6 * g;
+    float l0 = __ldg(l + 0), l1 = __ldg(l + 1), l2 = __ldg(l + 2);
+    f.L10 = __ldg(l + 3);
+    f.L20 = __ldg(l + 4);
+    f.L21 = __ldg(l + 5);
+    f.L00 = __fadd_rn(__fmul_rn(l0, l0), beta);
+    f.L11 = __fadd_rn(__fmul_rn(l1, l1), beta);
+    f.L22 = __fadd_rn(__fmul_rn(l2, l2), beta);
+    float i00 = __fdiv_rn(1.0f, f.L00);
+    float i11 = __fdiv_rn(1.0f, f.L11);
+    float i22 = __fdiv_rn(1.0f, f.L22);
+    float i10 = __fmul_rn(__fmul_rn(-f.L10, i00), i11);
+    float i21 = __fmul_rn(__fmul_rn(-f.L21, i11), i22);
+    float i20 = __fmul_rn(-__fadd_rn(__fmul_rn(f.L20, i00), __fmul_rn(f.L21, i10)), i22);
+    f.LT[0][0] = i00; f.LT[0][1] = i10; f.LT[0][2] = i20;
+    f.LT[1][0] = 0.f; f.LT[1][1] = i11; f.LT[1][2] = i21;
+    f.LT[2][0] = 0.f; f.LT[2][1] = 0.f; f.LT[2][2] = i22;
+    return f;
+}
+
+struct Window {
+    int iu0, iu1, iv0, iv1;
+};
+
+// Returns true iff the Gaussian is accepted for this slice (straddles the
+// plane, footprint meets the image rectangle, non-empty clamped window).
+__device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
+                                            const ugs_slice &sl, Window &w) {
+    float bmin[3], bmax[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        float r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float a0 = __fmul_rn(sl.rw[3 * i + 0], f.LT[0][k]);
+            float a1 = __fmul_rn(sl.rw[3 * i + 1], f.LT[1][k]);
+            float a2 = __fmul_rn(sl.rw[3 * i + 2], f.LT[2][k]);
+            r[k] = __fadd_rn(__fadd_rn(a0, a1), a2);   // einsum order
+        }
+        float nrm = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(r[0], r[0]),
+                                                   __fmul_rn(r[1], r[1])),
+                                         __fmul_rn(r[2], r[2])));
+        float half = __fmul_rn(sl.sqrt_cut, nrm);
+        // OpenBLAS sgemm (N,3)@(3,3): FMA chain, then + tw
+        float mp = __fmaf_rn(mu[2], sl.rw[3 * i + 2],
+                             __fmaf_rn(mu[1], sl.rw[3 * i + 1],
+                                       __fmul_rn(mu[0], sl.rw[3 * i + 0])));
+        mp = __fadd_rn(mp, sl.tw[i]);
+        bmin[i] = __fsub_rn(mp, half);
+        bmax[i] = __fadd_rn(mp, half);
+    }
+    bool keep = (bmin[2] <= 0.0f) && (bmax[2] >= 0.0f) &&
+                (bmax[0] >= -sl.x1h) && (bmin[0] <= sl.x1h) &&
+                (bmax[1] >= -sl.x2h) && (bmin[1] <= sl.x2h);
+    if (!keep) return false;
+    float fu0 = ceilf(__fadd_rn(__fdiv_rn(bmin[0], sl.s), sl.cx));
+    float fu1 = floorf(__fadd_rn(__fdiv_rn(bmax[0], sl.s), sl.cx));
+    float fv0 = ceilf(__fadd_rn(__fdiv_rn(bmin[1], sl.s), sl.cy));
+    float fv1 = floorf(__fadd_rn(__fdiv_rn(bmax[1], sl.s), sl.cy));
+    fu0 = fmaxf(fu0, 0.0f);
+    fv0 = fmaxf(fv0, 0.0f);
+    fu1 = fminf(fu1, (float)(sl.width - 1));
+    fv1 = fminf(fv1, (float)(sl.height - 1));
+    // accepted boxes overlap the image, so the clamped values are in range
+    w.iu0 = (int)fu0;
+    w.iu1 = (int)fu1;
+    w.iv0 = (int)fv0;
+    w.iv1 = (int)fv1;
+    return (w.iu0 <= w.iu1) && (w.iv0 <= w.iv1);
+}
+
+__device__ __forceinline__ int window_tiles(const Window &w) {
+    return ((w.iu1 >> 4) - (w.iu0 >> 4) + 1) * ((w.iv1 >> 4) - (w.iv0 >> 4) + 1);
+}
+
+__device__ __forceinline__ float sigmoid_f32(float x) {
+    // numpy float32: 1.0 / (1.0 + exp(-x))   (model.py:27-28)
+    return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+}
+
+__device__ __forceinline__ double sigmoid_f64(double x) {
+    return 1.0 / (1.0 + exp(-x));
+}
+
+// Plane-conditioned form of one accepted Gaussian on one slice (float64).
+// With e(u,v) = origin + u du + v dv - mu and y = L^T e, the reference's
+// q = |y|^2 is a 2-D quadratic in the pixel coordinates:
+//   q = H00 du^2 + 2 H01 du dv + H11 dv^2 + qmin   (du = u - u*, dv = v - v*)
+// where (u*, v*) is the in-plane conditional mean and qmin the out-of-plane
+// falloff.  Also used by the backward finalize, which needs e* = e(u*, v*).
+struct PlaneForm {
+    double H00, H01, H11;
+    double cu, cv;         // centre actually used (integer + f32 fraction)
+    float cu_i, cv_i, cu_f, cv_f;
+    double qmin;           // q at (cu, cv)
+    double ystar[3];       // L^T e(cu, cv)
+    double a[3], b[3];     // L^T du, L^T dv
+};
+
+__device__ __forceinline__ void lt_mul(const Factor &f, const double x[3],
+                                       double y[3]) {
+    // y = L^T x, L lower-triangular
+    y[0] = (double)f.L00 * x[0] + (double)f.L10 * x[1] + (double)f.L20 * x[2];
+    y[1] = (double)f.L11 * x[1] + (double)f.L21 * x[2];
+    y[2] = (double)f.L22 * x[2];
+}
+
+__device__ __forceinline__ PlaneForm plane_form(const float mu[3],
+                                                const Factor &f,
+                                                const ugs_slice &sl) {
+    PlaneForm P;
+    double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
+    double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
+    double d[3] = {(double)sl.origin[0] - mu[0], (double)sl.origin[1] - mu[1],
+                   (double)sl.origin[2] - mu[2]};
+    double c[3];
+    lt_mul(f, du, P.a);
+    lt_mul(f, dv, P.b);
+    lt_mul(f, d, c);
+    P.H00 = P.a[0] * P.a[0] + P.a[1] * P.a[1] + P.a[2] * P.a[2];
+    P.H01 = P.a[0] * P.b[0] + P.a[1] * P.b[1] + P.a[2] * P.b[2];
+    P.H11 = P.b[0] * P.b[0] + P.b[1] * P.b[1] + P.b[2] * P.b[2];
+    double g0 = P.a[0] * c[0] + P.a[1] * c[1] + P.a[2] * c[2];
+    double g1 = P.b[0] * c[0] + P.b[1] * c[1] + P.b[2] * c[2];
+    double det = P.H00 * P.H11 - P.H01 * P.H01;
+    double us = 0.0, vs = 0.0;
+    if (det > 0.0) {
+        us = (P.H01 * g1 - P.H11 * g0) / det;
+        vs = (P.H01 * g0 - P.H00 * g1) / det;
+    }
+    const double lim = 4194304.0;   // keep integer parts exact in float32
+    us = fmin(fmax(us, -lim), lim);
+    vs = fmin(fmax(vs, -lim), lim);
+    double ui = floor(us), vi = floor(vs);
+    P.cu_i = (float)ui;
+    P.cv_i = (float)vi;
+    P.cu_f = (float)(us - ui);
+    P.cv_f = (float)(vs - vi);
+    if (P.cu_f >= 1.0f) P.cu_f = 0.99999994f;
+    if (P.cv_f >= 1.0f) P.cv_f = 0.99999994f;
+    P.cu = ui + (double)P.cu_f;
+    P.cv = vi + (double)P.cv_f;
+    for (int k = 0; k < 3; ++k) P.ystar[k] = c[k] + P.cu * P.a[k] + P.cv * P.b[k];
+    P.qmin = P.ystar[0] * P.ystar[0] + P.ystar[1] * P.ystar[1] +
+             P.ystar[2] * P.ystar[2];
+    return P;
+}
+
+}  // namespace ugs

@@ -1,0 +1,130 @@
+// Internal declarations shared by the libugs translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/ugs.h"
+
+namespace ugs {
+
+constexpr int kTile = UGS_TILE;        // 16x16 pixel tiles
+constexpr int kPrepThreads = 256;      // phase-1 block size (one Gaussian per thread)
+constexpr int kSortThreads = 256;      // radix sort block size
+constexpr int kSortItems = 16;         // keys per thread per sort block
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// Per accepted (slice, Gaussian) record: three float4 = 48 B.
+//   r0 = (cu_int, cv_int, cu_frac, cv_frac)   in-plane conditional centre in
+//        pixel units, split into an exact integer part and a [0,1) fraction
+//   r1 = (A, B2, C, E0): exponent (log2 domain) of the plane-conditioned
+//        Gaussian: log2(w) = A dx^2 + B2 dx dy + C dy^2 + E0, dx = u - cu
+//   r2 = (color, bits(iu0 | iu1 << 16), bits(iv0 | iv1 << 16), alpha)
+struct Rec {
+    float4 r0, r1, r2;
+};
+
+// Per-batch binning state (device pointers are owned by the plan).
+struct PlanBuffers {
+    // phase 1
+    uint2 *blk_cnt = nullptr;       // [S][nblk] (accepted, tiles) -> exclusive offsets
+    size_t blk_cnt_cap = 0;
+    unsigned long long *slice_tot = nullptr; // [S][2] totals (accepted, tiles)
+    int64_t *slice_base = nullptr;  // [S][2] record base, instance base
+    ugs_slice *slices = nullptr;    // [S] device copy
+    int slices_cap = 0;
+    // records
+    Rec *rec = nullptr;             // [M]
+    int32_t *rec_gid = nullptr;     // [M]
+    int32_t *rec_inst = nullptr;    // [M+1] first instance of each record
+    size_t rec_cap = 0, rec_gid_cap = 0, rec_inst_cap = 0;
+    // instances
+    uint32_t *owner = nullptr;      // [K] record of each (unsorted) instance
+    uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)
+    uint32_t *keys2 = nullptr, *vals2 = nullptr;   // ping-pong
+    float *partial = nullptr;       // [K][8] backward per-instance partial sums
+    size_t inst_cap = 0;
+    // sort scratch
+    uint32_t *hist = nullptr;       // [kRadix][nblk_sort]
+    uint32_t *scan_tmp = nullptr;
+    size_t hist_cap = 0, scan_tmp_cap = 0;
+    // bins
+    int2 *bin_range = nullptr;      // [n_bins] [start, end) into sorted arrays
+    float2 *bin_bg = nullptr;       // [n_bins] per-tile (sum G, sum G*chat)
+    size_t bin_cap = 0;
+};
+
+}  // namespace ugs
+
+struct ugs_plan {
+    ugs::PlanBuffers b;
+    int S = 0;
+    int n_bins = 0;
+    int64_t m_total = 0;
+    int64_t k_total = 0;
+    int64_t n = 0;                 // cloud size the plan was binned for
+    int max_tiles = 0;
+    int64_t *h_slice_base = nullptr; // host copy [S][2]
+    int64_t *h_m = nullptr;          // host [S]
+    int32_t *h_tile_base = nullptr;  // host [S]
+    int32_t *h_ntile = nullptr;      // host [S]
+    int h_cap = 0;
+    uint32_t *sorted_keys = nullptr; // point into b.keys/b.keys2
+    uint32_t *sorted_vals = nullptr;
+    std::string err;
+};
+
+namespace ugs {
+
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define UGS_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, #call);  \
+    } while (0)
+
+#define UGS_LAUNCH_CHECK(what)                                      \
+    do {                                                            \
+        cudaError_t e_ = cudaGetLastError();                        \
+        if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, what);   \
+    } while (0)
+
+// phase 1 (ugs_prepare.cu)
+int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
+                         uint2 *blk_cnt, int nblk, cudaStream_t st);
+int launch_prepare_scan(uint2 *blk_cnt, int S, int nblk,
+                        unsigned long long *slice_tot, cudaStream_t st);
+int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
+                        const uint2 *blk_off, int nblk, const int64_t *slice_base,
+                        Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
+                        uint32_t *owner, uint32_t *keys, int64_t m_total,
+                        int64_t k_total, cudaStream_t st);
+
+// radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
+// bits, stable.  On return *keys_out/*vals_out point at the sorted arrays
+// (one of the two ping-pong buffers).
+int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
+                     uint32_t *vals2, int64_t n, int bits, uint32_t *hist,
+                     uint32_t *scan_tmp, cudaStream_t st, uint32_t **keys_out,
+                     uint32_t **vals_out);
+size_t radix_hist_entries(int64_t n);
+size_t scan_tmp_entries(size_t n);
+int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
+                      int n_bins, cudaStream_t st);
+
+// raster (ugs_raster.cu)
+int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
+                   float *num, float *den, cudaStream_t st);
+int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
+                    const float *num, const float *den, const float *dpix,
+                    float *grad, uint8_t *touched, float scale,
+                    cudaStream_t st);
+
+}  // namespace ugs

@@ -1,0 +1,231 @@
+// Phase 1 for a batch of slices: per-Gaussian factor + chi^2 box + cull +
+// compact + clamped windows (ref rasterizer.py:109-137), fused with the
+// per-(slice, Gaussian) record build and the tile-instance expansion.
+//
+// Three passes over the parameter SoA (44 B/Gaussian, L2-resident after the
+// first pass for N <= ~2M):
+//   count : one thread per Gaussian, loops over the S slices of the batch,
+//           block-reduces (accepted, tiles) per slice      -> blk_cnt[S][nblk]
+//   scan  : exclusive scan of blk_cnt along blocks, per slice (keeps ascending
+//           Gaussian order = the reference's compact() order)
+//   emit  : recompute, block-scan, write records + instances in order.
+#include "ugs_geometry.cuh"
+
+namespace ugs {
+
+namespace {
+
+constexpr int kMaxSlicesSmem = 64;
+
+__device__ __forceinline__ void load_slices_smem(ugs_slice *dst,
+                                                 const ugs_slice *src, int S) {
+    const int words = S * (int)(sizeof(ugs_slice) / 4);
+    const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
+    uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = s[i];
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+prepare_count_kernel(const float *__restrict__ means,
+                     const float *__restrict__ l_raw, int64_t n, float beta,
+                     const ugs_slice *__restrict__ slices, int S,
+                     uint2 *__restrict__ blk_cnt, int nblk) {
+    __shared__ ugs_slice sl[kMaxSlicesSmem];
+    __shared__ uint2 wsum[kMaxSlicesSmem][kPrepThreads / 32];
+    load_slices_smem(sl, slices, S);
+    __syncthreads();
+    const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
+    const bool valid = g < n;
+    Factor f;
+    float mu[3] = {0.f, 0.f, 0.f};
+    if (valid) {
+        f = make_factor(l_raw, g, beta);
+        mu[0] = __ldg(means + 3 * g);
+        mu[1] = __ldg(means + 3 * g + 1);
+        mu[2] = __ldg(means + 3 * g + 2);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = 0; s < S; ++s) {
+        unsigned acc = 0, tiles = 0;
+        Window w;
+        if (valid && cull_window(mu, f, sl[s], w)) {
+            acc = 1;
+            tiles = (unsigned)window_tiles(w);
+        }
+        acc = __reduce_add_sync(0xffffffffu, acc);
+        tiles = __reduce_add_sync(0xffffffffu, tiles);
+        if (lane == 0) wsum[s][warp] = make_uint2(acc, tiles);
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        uint2 t = make_uint2(0, 0);
+#pragma unroll
+        for (int w = 0; w < kPrepThreads / 32; ++w) {
+            t.x += wsum[s][w].x;
+            t.y += wsum[s][w].y;
+        }
+        blk_cnt[(size_t)s * nblk + blockIdx.x] = t;
+    }
+}
+
+// One block per slice: exclusive scan of blk_cnt[s][:] in place; totals in
+// 64-bit (the host rejects batches whose totals exceed the 31-bit budget).
+__global__ void __launch_bounds__(1024)
+prepare_scan_kernel(uint2 *__restrict__ blk_cnt, int nblk,
+                    unsigned long long *__restrict__ slice_tot) {
+    __shared__ unsigned long long wx[32], wy[32];
+    __shared__ unsigned long long carry_x, carry_y;
+    const int s = blockIdx.x;
+    uint2 *row = blk_cnt + (size_t)s * nblk;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { carry_x = 0; carry_y = 0; }
+    __syncthreads();
+    for (int base = 0; base < nblk; base += 1024) {
+        const int i = base + threadIdx.x;
+        uint2 v = i < nblk ? row[i] : make_uint2(0, 0);
+        unsigned long long x = v.x, y = v.y;
+        // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long tx = __shfl_up_sync(0xffffffffu, x, o);
+            unsigned long long ty = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += tx; y += ty; }
+        }
+        if (lane == 31) { wx[warp] = x; wy[warp] = y; }
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long a = wx[lane], b = wy[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long ta = __shfl_up_sync(0xffffffffu, a, o);
+                unsigned long long tb = __shfl_up_sync(0xffffffffu, b, o);
+                if (lane >= o) { a += ta; b += tb; }
+            }
+            wx[lane] = a;   // inclusive warp-sum prefix
+            wy[lane] = b;
+        }
+        __syncthreads();
+        unsigned long long px = (warp ? wx[warp - 1] : 0ull) + x - v.x + carry_x;
+        unsigned long long py = (warp ? wy[warp - 1] : 0ull) + y - v.y + carry_y;
+        if (i < nblk) row[i] = make_uint2((unsigned)px, (unsigned)py);
+        __syncthreads();
+        if (threadIdx.x == 0) { carry_x += wx[31]; carry_y += wy[31]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        slice_tot[2 * s] = carry_x;
+        slice_tot[2 * s + 1] = carry_y;
+    }
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+prepare_emit_kernel(const float *__restrict__ means,
+                    const float *__restrict__ l_raw,
+                    const float *__restrict__ intensity_raw,
+                    const float *__restrict__ opacity_raw, int64_t n,
+                    float beta, const ugs_slice *__restrict__ slices, int S,
+                    const uint2 *__restrict__ blk_off, int nblk,
+                    const int64_t *__restrict__ slice_base,
+                    Rec *__restrict__ rec, int32_t *__restrict__ rec_gid,
+                    int32_t *__restrict__ rec_inst, uint32_t *__restrict__ owner,
+                    uint32_t *__restrict__ keys, int64_t m_total,
+                    int64_t k_total) {
+    __shared__ ugs_slice sl[kMaxSlicesSmem];
+    __shared__ uint2 wpre[kPrepThreads / 32];
+    load_slices_smem(sl, slices, S);
+    __syncthreads();
+    const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
+    const bool valid = g < n;
+    Factor f;
+    float mu[3] = {0.f, 0.f, 0.f};
+    float color = 0.f, alpha = 0.f;
+    if (valid) {
+        f = make_factor(l_raw, g, beta);
+        mu[0] = __ldg(means + 3 * g);
+        mu[1] = __ldg(means + 3 * g + 1);
+        mu[2] = __ldg(means + 3 * g + 2);
+        color = sigmoid_f32(__ldg(intensity_raw + g));
+        alpha = sigmoid_f32(__ldg(opacity_raw + g));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
+    const double log2_alpha = log2((double)alpha);
+    const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
+    for (int s = 0; s < S; ++s) {
+        const ugs_slice &L = sl[s];
+        unsigned acc = 0, tiles = 0;
+        Window w;
+        if (valid && cull_window(mu, f, L, w)) {
+            acc = 1;
+            tiles = (unsigned)window_tiles(w);
+        }
+        // block exclusive scan of (acc, tiles)
+        unsigned xa = acc, xt = tiles;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned ta = __shfl_up_sync(0xffffffffu, xa, o);
+            unsigned tt = __shfl_up_sync(0xffffffffu, xt, o);
+            if (lane >= o) { xa += ta; xt += tt; }
+        }
+        __syncthreads();   // wpre reuse across slices
+        if (lane == 31) wpre[warp] = make_uint2(xa, xt);
+        __syncthreads();
+        unsigned oa = 0, ot = 0;
+        for (int k = 0; k < warp; ++k) { oa += wpre[k].x; ot += wpre[k].y; }
+        if (!acc) continue;
+        const uint2 bo = blk_off[(size_t)s * nblk + blockIdx.x];
+        const int64_t r = slice_base[2 * s] + bo.x + oa + xa - acc;
+        int64_t inst = slice_base[2 * s + 1] + bo.y + ot + xt - tiles;
+        PlaneForm P = plane_form(mu, f, L);
+        Rec R;
+        R.r0 = make_float4(P.cu_i, P.cv_i, P.cu_f, P.cv_f);
+        R.r1 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
+                           (float)(kq * P.H11),
+                           (float)(kq * P.qmin + log2_alpha));
+        R.r2 = make_float4(color, __int_as_float(w.iu0 | (w.iu1 << 16)),
+                           __int_as_float(w.iv0 | (w.iv1 << 16)), alpha);
+        rec[r] = R;
+        rec_gid[r] = (int32_t)g;
+        rec_inst[r] = (int32_t)inst;
+        const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
+        const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                owner[inst] = (uint32_t)r;
+                keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
+                ++inst;
+            }
+    }
+}
+
+}  // namespace
+
+int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
+                         uint2 *blk_cnt, int nblk, cudaStream_t st) {
+    prepare_count_kernel<<<nblk, kPrepThreads, 0, st>>>(
+        c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, nblk);
+    UGS_LAUNCH_CHECK("prepare_count_kernel");
+    return UGS_OK;
+}
+
+int launch_prepare_scan(uint2 *blk_cnt, int S, int nblk,
+                        unsigned long long *slice_tot, cudaStream_t st) {
+    prepare_scan_kernel<<<S, 1024, 0, st>>>(blk_cnt, nblk, slice_tot);
+    UGS_LAUNCH_CHECK("prepare_scan_kernel");
+    return UGS_OK;
+}
+
+int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
+                        const uint2 *blk_off, int nblk, const int64_t *slice_base,
+                        Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
+                        uint32_t *owner, uint32_t *keys, int64_t m_total,
+                        int64_t k_total, cudaStream_t st) {
+    prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
+        c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
+        S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, owner, keys,
+        m_total, k_total);
+    UGS_LAUNCH_CHECK("prepare_emit_kernel");
+    return UGS_OK;
+}
+
+}  // namespace ugs

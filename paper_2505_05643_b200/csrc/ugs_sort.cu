@@ -1,0 +1,272 @@
+// Hand-written stable LSD radix sort of (slice, tile) bin keys with the
+// original instance index as payload, plus the bin-range scan.
+//
+// The instance array is produced in ascending (slice, Gaussian, tile) order,
+// so a STABLE sort by bin key yields per-(slice, tile) lists in ascending
+// Gaussian index -- exactly the accumulation order of the reference's
+// sequential forward loop (ref _kernels.py:23) -- and the tile assignment is
+// bit-exact by construction.
+//
+// Per 8-bit digit pass: histogram (smem atomics, order-free) -> exclusive
+// scan of the digit-major [256][nblk] table -> scatter with a stable in-block
+// rank (warp match.any + per-warp running digit counters).
+#include "ugs_internal.cuh"
+
+namespace ugs {
+
+namespace {
+
+// ---------------------------------------------------------------- scan ----
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x,
+                                                         uint32_t *total) {
+    __shared__ uint32_t ws[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __syncthreads();
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t a = lane < nw ? ws[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, a, o);
+            if (lane >= o) a += t;
+        }
+        ws[lane] = a;
+    }
+    __syncthreads();
+    uint32_t pre = (warp ? ws[warp - 1] : 0u) + inc - x;
+    if (total) *total = ws[nw - 1];
+    return pre;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_reduce_kernel(const uint32_t *__restrict__ in, size_t n,
+                   uint32_t *__restrict__ sums) {
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        size_t i = base + (size_t)j * kScanThreads + threadIdx.x;
+        if (i < n) acc += in[i];
+    }
+    acc = __reduce_add_sync(0xffffffffu, acc);
+    __shared__ uint32_t ws[kScanThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+// single block, exclusive scan of up to 1024*8 entries in place
+__global__ void __launch_bounds__(1024)
+scan_sums_kernel(uint32_t *__restrict__ sums, int n) {
+    uint32_t v[8];
+    const int base = threadIdx.x * 8;
+    uint32_t local = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        v[j] = (base + j < n) ? sums[base + j] : 0u;
+        local += v[j];
+    }
+    uint32_t pre = block_exclusive_scan(local, nullptr);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (base + j < n) sums[base + j] = pre;
+        pre += v[j];
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_down_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
+                 size_t n, const uint32_t *__restrict__ sums) {
+    // each thread scans kScanItems consecutive entries (blocked layout)
+    __shared__ uint32_t tile[kScanTile];
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        size_t i = base + (size_t)j * kScanThreads + threadIdx.x;
+        tile[j * kScanThreads + threadIdx.x] = i < n ? in[i] : 0u;
+    }
+    __syncthreads();
+    uint32_t v[kScanItems], local = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        v[j] = tile[threadIdx.x * kScanItems + j];
+        local += v[j];
+    }
+    uint32_t pre = block_exclusive_scan(local, nullptr) + sums[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        tile[threadIdx.x * kScanItems + j] = pre;
+        pre += v[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        size_t i = base + (size_t)j * kScanThreads + threadIdx.x;
+        if (i < n) out[i] = tile[j * kScanThreads + threadIdx.x];
+    }
+}
+
+int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
+                   uint32_t *tmp, cudaStream_t st) {
+    if (n == 0) return UGS_OK;
+    const size_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb > 8192) {
+        set_error("exclusive_scan: input too large");
+        return UGS_ERR_RANGE;
+    }
+    scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, tmp);
+    scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
+    scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, tmp);
+    UGS_LAUNCH_CHECK("exclusive_scan");
+    return UGS_OK;
+}
+
+// ---------------------------------------------------------- radix sort ----
+__global__ void __launch_bounds__(kSortThreads)
+radix_hist_kernel(const uint32_t *__restrict__ keys, int64_t n, int shift,
+                  uint32_t *__restrict__ hist, int nblk) {
+    __shared__ uint32_t h[kRadix];
+    for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+    for (int j = 0; j < kSortItems; ++j) {
+        int64_t i = base + (int64_t)j * kSortThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[(__ldg(keys + i) >> shift) & (kRadix - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
+        hist[(size_t)d * nblk + blockIdx.x] = h[d];
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+radix_scatter_kernel(const uint32_t *__restrict__ keys_in,
+                     const uint32_t *__restrict__ vals_in,  // null: identity
+                     uint32_t *__restrict__ keys_out,
+                     uint32_t *__restrict__ vals_out, int64_t n, int shift,
+                     const uint32_t *__restrict__ offs, int nblk) {
+    constexpr int kWarps = kSortThreads / 32;
+    constexpr int kPerWarp = kSortItems * 32;
+    __shared__ uint32_t wcnt[kWarps][kRadix];
+    __shared__ uint32_t gofs[kRadix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads)
+        (&wcnt[0][0])[i] = 0;
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
+        gofs[d] = offs[(size_t)d * nblk + blockIdx.x];
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * kPerWarp;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t k[kSortItems], v[kSortItems], dr[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int64_t i = base + j * 32 + lane;
+        const bool ok = i < n;
+        k[j] = ok ? keys_in[i] : 0u;
+        v[j] = ok ? (vals_in ? vals_in[i] : (uint32_t)i) : 0u;
+        const uint32_t d = ok ? ((k[j] >> shift) & (kRadix - 1)) : (uint32_t)kRadix;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lt_mask);
+        uint32_t cnt_before = 0;
+        if (ok) cnt_before = wcnt[warp][d];
+        __syncwarp();
+        if (ok && rank == 0) wcnt[warp][d] = cnt_before + __popc(peers);
+        __syncwarp();
+        dr[j] = ok ? ((d << 16) | (cnt_before + rank)) : 0xffffffffu;
+    }
+    __syncthreads();
+    // exclusive prefix of the per-warp digit counts across warps
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            uint32_t t = wcnt[w][d];
+            wcnt[w][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        if (dr[j] == 0xffffffffu) continue;
+        const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
+        const uint32_t pos = gofs[d] + wcnt[warp][d] + r;
+        keys_out[pos] = k[j];
+        vals_out[pos] = v[j];
+    }
+}
+
+__global__ void bin_ranges_kernel(const uint32_t *__restrict__ keys, int64_t n,
+                                  int2 *__restrict__ range) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) range[k].x = (int)i;
+    if (i == n - 1 || keys[i + 1] != k) range[k].y = (int)(i + 1);
+}
+
+}  // namespace
+
+size_t radix_hist_entries(int64_t n) {
+    const size_t nblk = (size_t)((n + kSortTile - 1) / kSortTile);
+    return nblk * kRadix;
+}
+
+size_t scan_tmp_entries(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
+                     uint32_t *vals2, int64_t n, int bits, uint32_t *hist,
+                     uint32_t *scan_tmp, cudaStream_t st, uint32_t **keys_out,
+                     uint32_t **vals_out) {
+    *keys_out = keys;
+    *vals_out = vals;
+    if (n <= 0) return UGS_OK;
+    const int nblk = (int)((n + kSortTile - 1) / kSortTile);
+    const size_t hn = (size_t)nblk * kRadix;
+    uint32_t *kin = keys, *vin = nullptr, *kout = keys2, *vout = vals2;
+    const int passes = bits <= 0 ? 1 : (bits + kRadixBits - 1) / kRadixBits;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = p * kRadixBits;
+        radix_hist_kernel<<<nblk, kSortThreads, 0, st>>>(kin, n, shift, hist, nblk);
+        UGS_LAUNCH_CHECK("radix_hist_kernel");
+        int rc = exclusive_scan(hist, hist, hn, scan_tmp, st);
+        if (rc) return rc;
+        radix_scatter_kernel<<<nblk, kSortThreads, 0, st>>>(kin, vin, kout, vout,
+                                                            n, shift, hist, nblk);
+        UGS_LAUNCH_CHECK("radix_scatter_kernel");
+        // ping-pong: first pass reads identity values, writes vals2
+        uint32_t *tk = kin, *tv = vin;
+        kin = kout;
+        vin = vout;
+        kout = tk;
+        vout = (tv == nullptr) ? vals : tv;
+    }
+    *keys_out = kin;
+    *vals_out = vin;
+    return UGS_OK;
+}
+
+int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
+                      int n_bins, cudaStream_t st) {
+    UGS_CUDA(cudaMemsetAsync(bin_range, 0, sizeof(int2) * (size_t)n_bins, st));
+    if (n <= 0) return UGS_OK;
+    const int th = 256;
+    bin_ranges_kernel<<<(unsigned)((n + th - 1) / th), th, 0, st>>>(keys, n,
+                                                                    bin_range);
+    UGS_LAUNCH_CHECK("bin_ranges_kernel");
+    return UGS_OK;
+}
+
+}  // namespace ugs

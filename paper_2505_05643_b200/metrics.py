@@ -1,0 +1,162 @@
+"""SSIM / PSNR and the training loss on the device (ref metrics.py:17-105,
+trainer.py:130-151).
+
+Same formulation as the reference: 11x11 Gaussian window (sigma 1.5),
+C1 = 1e-4, C2 = 9e-4, valid windows only, float64 arithmetic; the analytic
+gradient of mean SSIM uses the adjoint (zero-padded full correlation) of the
+valid-window filter.  Batched over (B, H, W) with separable float64 conv2d.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from .geometry import InvalidParameterError
+
+WIN = 11
+PAD = WIN // 2
+SIGMA = 1.5
+C1 = 0.01 ** 2
+C2 = 0.03 ** 2
+
+_KCACHE: dict = {}
+
+
+def _kernels(device):
+    k = _KCACHE.get(device)
+    if k is None:
+        x = np.arange(WIN) - PAD
+        w = np.exp(-0.5 * (x / SIGMA) ** 2)
+        w = torch.tensor(w / w.sum(), dtype=torch.float64, device=device)
+        k = (w.view(1, 1, WIN, 1), w.view(1, 1, 1, WIN))
+        _KCACHE[device] = k
+    return k
+
+
+def _filt(x):
+    """Valid-window Gaussian mean of (B,1,H,W) -> (B,1,H-10,W-10)."""
+    kv, kh = _kernels(x.device)
+    return F.conv2d(F.conv2d(x, kv), kh)
+
+
+def _adj(f):
+    """Adjoint of _filt: (B,1,H-10,W-10) -> (B,1,H,W)."""
+    kv, kh = _kernels(f.device)
+    f = F.pad(f, (2 * PAD, 2 * PAD, 2 * PAD, 2 * PAD))
+    return F.conv2d(F.conv2d(f, kv), kh)
+
+
+def _as4d(a, device=None):
+    t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
+    if device is not None:
+        t = t.to(device)
+    t = t.to(torch.float64)
+    if t.dim() == 2:
+        t = t[None]
+    return t[:, None]
+
+
+def ssim_with_grad_batch(x, y):
+    """x, y (B,H,W) -> (mean SSIM per image (B,), d meanSSIM/dx (B,H,W))."""
+    x = _as4d(x)
+    y = _as4d(y, x.device)
+    if x.shape != y.shape:
+        raise InvalidParameterError("image dimensions differ")
+    if min(x.shape[-2:]) < WIN:
+        raise InvalidParameterError(f"images must be at least {WIN}x{WIN}")
+    mx, my = _filt(x), _filt(y)
+    sxx = _filt(x * x) - mx * mx
+    syy = _filt(y * y) - my * my
+    sxy = _filt(x * y) - mx * my
+    a1 = 2.0 * mx * my + C1
+    a2 = 2.0 * sxy + C2
+    b1 = mx * mx + my * my + C1
+    b2 = sxx + syy + C2
+    s = (a1 * a2) / (b1 * b2)
+    nv = s.shape[-1] * s.shape[-2]
+    d_mu = (2.0 * my * a2) / (b1 * b2) - (2.0 * mx * a1 * a2) / (b1 * b1 * b2)
+    d_sxx = -s / b2
+    d_sxy = 2.0 * a1 / (b1 * b2)
+    grad = (_adj(d_mu - 2.0 * mx * d_sxx - my * d_sxy) + 2.0 * x * _adj(d_sxx)
+            + y * _adj(d_sxy))
+    return s.mean(dim=(1, 2, 3)), (grad / nv)[:, 0]
+
+
+def ssim_batch(x, y):
+    x = _as4d(x)
+    y = _as4d(y, x.device)
+    if x.shape != y.shape:
+        raise InvalidParameterError("image dimensions differ")
+    if min(x.shape[-2:]) < WIN:
+        raise InvalidParameterError(f"images must be at least {WIN}x{WIN}")
+    mx, my = _filt(x), _filt(y)
+    sxx = _filt(x * x) - mx * mx
+    syy = _filt(y * y) - my * my
+    sxy = _filt(x * y) - mx * my
+    s = ((2.0 * mx * my + C1) * (2.0 * sxy + C2)) / \
+        ((mx * mx + my * my + C1) * (sxx + syy + C2))
+    return s.mean(dim=(1, 2, 3))
+
+
+def _dev_for(a, b):
+    for t in (a, b):
+        if isinstance(t, torch.Tensor) and t.is_cuda:
+            return t.device
+    return torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+
+
+def ssim(a, b) -> float:
+    """Mean SSIM of two [0,1] images (ref metrics.py:68-74)."""
+    dev = _dev_for(a, b)
+    return float(ssim_batch(_as4d(a, dev)[:, 0], _as4d(b, dev)[:, 0])[0])
+
+
+def ssim_with_grad(a, b):
+    dev = _dev_for(a, b)
+    s, g = ssim_with_grad_batch(_as4d(a, dev)[:, 0], _as4d(b, dev)[:, 0])
+    return float(s[0]), g[0]
+
+
+def psnr(a, b) -> float:
+    """PSNR in dB for range-1 images; inf when equal (ref metrics.py:101-107)."""
+    x = _as4d(a)
+    y = _as4d(b, x.device)
+    if x.shape != y.shape:
+        raise InvalidParameterError("image dimensions differ")
+    mse = float(torch.mean((x - y) ** 2))
+    return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+
+
+def loss_batch(pred, target, lam: float, l2: bool = False):
+    """Per-image training loss and its pixel gradient (ref trainer.py:130-151).
+
+    pred, target (B,H,W); returns (loss (B,) float64, d_pixels (B,H,W) float64).
+    """
+    x = pred.to(torch.float64)
+    y = target.to(device=x.device, dtype=torch.float64)
+    if x.shape != y.shape:
+        raise InvalidParameterError("prediction/target dimensions differ")
+    diff = x - y
+    npx = x.shape[-1] * x.shape[-2]
+    if l2:
+        return (diff * diff).mean(dim=(1, 2)), 2.0 * diff / npx
+    val = (1.0 - lam) * diff.abs().mean(dim=(1, 2))
+    d = (1.0 - lam) * torch.sign(diff) / npx
+    if lam > 0.0:
+        s, ds = ssim_with_grad_batch(x, y)
+        val = val + lam * (1.0 - s)
+        d = d - lam * ds
+    return val, d
+
+
+def loss(pred, target, lam: float, l2: bool = False):
+    """Reference signature: (float, (H,W) gradient)."""
+    dev = _dev_for(pred, target)
+    x = _as4d(pred, dev)[:, 0]
+    y = _as4d(target, dev)[:, 0]
+    v, d = loss_batch(x, y, lam, l2)
+    return float(v[0]), d[0]

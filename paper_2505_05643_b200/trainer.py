@@ -1,0 +1,492 @@
+"""Training on the B200 (ref pkg/src/echosplat/trainer.py).
+
+Same public surface as the reference -- TrainConfig, AdamState, init_cloud,
+loss, mean_lr, general_lr, adam_step, densify_prune_resample, train,
+save/load_checkpoint -- with the parameters, moments, gradients and
+densify statistics resident in HBM.  One training step is
+
+    ugs_bin -> ugs_forward -> loss (device, float64) -> ugs_backward
+      [-> NCCL all-reduce of the flat gradient when world_size > 1]
+      -> ugs_grad_stats -> ugs_adam_step
+
+over a batch of ``config.batch`` slices per GPU (the reference reads one
+slice per iteration and never uses ``batch``, trainer.py:60; batch=1 on one
+GPU reproduces its iteration exactly).  Densify/prune keeps its selection
+and RNG on the host with numpy (bit-compatible candidate order and draws)
+and applies the row surgery on the device (ugs_densify_apply).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+import struct
+import time
+from dataclasses import asdict, dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dataset import SliceDataset
+from .geometry import InvalidParameterError, fill_slice
+from .gradients import ParamGradients, grad_buffer
+from .metrics import loss_batch, ssim_batch
+from .metrics import loss as _loss
+from .model import GaussianCloud
+from .rasterizer import Renderer, _stream
+
+CHECKPOINT_MAGIC = b"UGSC"
+CHECKPOINT_VERSION = 1
+GROUPS = ("means", "l_raw", "intensity_raw", "opacity_raw")
+
+
+class TrainingDivergedError(RuntimeError):
+    def __init__(self, message, snapshot_path=None):
+        super().__init__(message)
+        self.snapshot_path = snapshot_path
+
+
+class CheckpointFormatError(ValueError):
+    pass
+
+
+@dataclass
+class TrainConfig:
+    """ref trainer.py:43-74 (same fields, defaults and validation)."""
+
+    n_gaussians: int = 20000
+    iterations: int = 3000
+    lr_general: float = 0.05
+    lr_general_final: float | None = None
+    lr_means_start: float = 0.00016
+    lr_means_final: float = 1.6e-6
+    ssim_loss_weight: float = 0.2
+    l2_loss: bool = False
+    heuristic_interval: int = 100
+    densify_grad_threshold: float | None = None
+    prune_alpha_threshold: float = 0.01
+    split_variance_factor: float = 1.6
+    split_scale_fraction: float = 0.01
+    p_mass: float = 0.95
+    seed: int = 0
+    batch: int = 1
+    workers: int = 1
+    eval_interval: int = 100
+    l_init_low: float = 4.0
+    l_init_high: float = 5.0
+    beta: float = 0.01
+
+    def __post_init__(self):
+        if self.n_gaussians < 1:
+            raise InvalidParameterError("n_gaussians must be >= 1")
+        if not 0.0 <= self.ssim_loss_weight <= 1.0:
+            raise InvalidParameterError("ssim_loss_weight must be in [0, 1]")
+        for name in ("lr_general", "lr_means_start", "lr_means_final"):
+            if not getattr(self, name) > 0:
+                raise InvalidParameterError(f"{name} must be > 0")
+        if self.batch < 1 or self.batch > 64:
+            raise InvalidParameterError("batch must be in [1, 64]")
+
+
+def _offsets(n):
+    return {"means": (0, 3 * n, (n, 3)), "l_raw": (3 * n, 9 * n, (n, 6)),
+            "intensity_raw": (9 * n, 10 * n, (n,)),
+            "opacity_raw": (10 * n, 11 * n, (n,)), "bg": (11 * n, 11 * n + 2, (2,))}
+
+
+class AdamState:
+    """First/second moments (ref trainer.py:77-107) as flat float32 device
+    buffers in the gradient layout; ``m``/``v`` give per-group views."""
+
+    def __init__(self, n, device, t=0, beta1=0.9, beta2=0.999, eps=1e-15,
+                 m_flat=None, v_flat=None):
+        self.n = n
+        self.m_flat = m_flat if m_flat is not None else torch.zeros(
+            11 * n + 2, dtype=torch.float32, device=device)
+        self.v_flat = v_flat if v_flat is not None else torch.zeros_like(self.m_flat)
+        self.t = t
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+
+    @staticmethod
+    def for_cloud(cloud: GaussianCloud) -> "AdamState":
+        return AdamState(cloud.n, cloud.device)
+
+    def _views(self, flat):
+        return {k: flat[a:b].view(shape) for k, (a, b, shape)
+                in _offsets(self.n).items()}
+
+    @property
+    def m(self):
+        return self._views(self.m_flat)
+
+    @property
+    def v(self):
+        return self._views(self.v_flat)
+
+
+def init_cloud(config: TrainConfig, bounds, device=None) -> GaussianCloud:
+    """Uniform means in `bounds`, default raws (ref trainer.py:110-127); the
+    same numpy stream as the reference, then uploaded."""
+    bounds = np.asarray(bounds, dtype=np.float64)
+    if bounds.shape != (2, 3) or np.any(bounds[1] <= bounds[0]):
+        raise InvalidParameterError("bounds must be a non-degenerate (2,3) box")
+    rng = np.random.default_rng(config.seed)
+    n = config.n_gaussians
+    means = rng.uniform(bounds[0], bounds[1], size=(n, 3))
+    l_raw = rng.uniform(config.l_init_low, config.l_init_high, size=(n, 6))
+    return GaussianCloud(means.astype(np.float32), l_raw.astype(np.float32),
+                         np.zeros(n, np.float32), np.full(n, 1.0, np.float32),
+                         0.0, -4.0, config.beta, device=device)
+
+
+def loss(pred, target, lam: float, l2: bool = False):
+    """(1-lam)*L1 + lam*(1-SSIM) or MSE, and the pixel gradient (ref :130-151)."""
+    return _loss(pred, target, lam, l2)
+
+
+def mean_lr(config: TrainConfig, t: int) -> float:
+    frac = min(t / max(config.iterations, 1), 1.0)
+    return config.lr_means_start * (config.lr_means_final / config.lr_means_start) ** frac
+
+
+def general_lr(config: TrainConfig, t: int) -> float:
+    if config.lr_general_final is None:
+        return config.lr_general
+    frac = min(t / max(config.iterations, 1), 1.0)
+    return config.lr_general * (config.lr_general_final / config.lr_general) ** frac
+
+
+def _adam_flat(state: AdamState, cloud: GaussianCloud, grad_flat: torch.Tensor,
+               lrs: dict, zero_grad: bool) -> None:
+    state.t += 1
+    lr = (ctypes.c_double * 5)(lrs["means"], lrs["l_raw"], lrs["intensity_raw"],
+                               lrs["opacity_raw"], lrs["bg"])
+    _lib.check(_lib.lib().ugs_adam_step(
+        cloud.means.data_ptr(), cloud.l_raw.data_ptr(),
+        cloud.intensity_raw.data_ptr(), cloud.opacity_raw.data_ptr(),
+        cloud.bg_raw.data_ptr(), grad_flat.data_ptr(), state.m_flat.data_ptr(),
+        state.v_flat.data_ptr(), cloud.n, state.t, lr, state.beta1, state.beta2,
+        state.eps, 1 if zero_grad else 0, _stream()), "ugs_adam_step")
+
+
+def adam_step(state: AdamState, cloud: GaussianCloud, grads: ParamGradients,
+              lrs: dict) -> GaussianCloud:
+    """One in-place Adam update (ref trainer.py:170-200), bit-compatible."""
+    n = cloud.n
+    if state.n != n:
+        raise InvalidParameterError("moment/gradient shape mismatch")
+    flat = grad_buffer(n, cloud.device)
+    o = _offsets(n)
+    for k in GROUPS:
+        a, b, shape = o[k]
+        g = getattr(grads, "d_" + k)
+        g = torch.as_tensor(g if isinstance(g, torch.Tensor) else np.asarray(g))
+        if tuple(g.shape) != shape:
+            raise InvalidParameterError(f"moment/gradient shape mismatch for {k}")
+        flat[a:b] = g.reshape(-1).to(device=cloud.device, dtype=torch.float32)
+    flat[11 * n] = float(np.float32(grads.d_bg_intensity_raw))
+    flat[11 * n + 1] = float(np.float32(grads.d_bg_opacity_raw))
+    _adam_flat(state, cloud, flat, lrs, zero_grad=False)
+    return cloud
+
+
+def _sigmoid32(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, np.float32)
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def densify_prune_resample(cloud: GaussianCloud, grad_norm_avg, state: AdamState,
+                           config: TrainConfig, rng: np.random.Generator,
+                           scene_extent: float, threshold: float, max_total: int):
+    """Prune transparent, split/clone high-gradient Gaussians (ref :203-279).
+
+    Selection and RNG draws on the host (numpy, the reference's exact order);
+    the row surgery, child means and shrunk factors on the device."""
+    avg = np.asarray(grad_norm_avg.cpu().numpy() if isinstance(
+        grad_norm_avg, torch.Tensor) else grad_norm_avg)
+    keep = _sigmoid32(cloud.opacity_raw.cpu().numpy()) >= config.prune_alpha_threshold
+    idx = np.nonzero(keep)[0]
+    avg = avg[idx]
+    n_keep = len(idx)
+    budget = max_total - n_keep
+    cand = np.nonzero(avg > threshold)[0]
+    if budget <= 0 or len(cand) == 0:
+        cand = cand[:0]
+    elif len(cand) > budget:
+        cand = cand[np.argsort(avg[cand])[::-1][:budget]]
+    split = np.zeros(len(cand), np.uint8)
+    z = np.zeros((len(cand), 6), np.float64)
+    if len(cand):
+        l_kept = cloud.l_raw[torch.as_tensor(idx[cand], device=cloud.device)].cpu().numpy()
+        l64 = l_kept.astype(np.float64)
+        beta = cloud.beta
+        L = np.zeros((len(cand), 3, 3))
+        for j in range(3):
+            L[:, j, j] = l64[:, j] ** 2 + beta
+        L[:, 1, 0], L[:, 2, 0], L[:, 2, 1] = l64[:, 3], l64[:, 4], l64[:, 5]
+        inv = np.zeros_like(L)
+        for j in range(3):
+            inv[:, j, j] = 1.0 / L[:, j, j]
+        inv[:, 1, 0] = -L[:, 1, 0] * inv[:, 0, 0] * inv[:, 1, 1]
+        inv[:, 2, 1] = -L[:, 2, 1] * inv[:, 1, 1] * inv[:, 2, 2]
+        inv[:, 2, 0] = -(L[:, 2, 0] * inv[:, 0, 0] + L[:, 2, 1] * inv[:, 1, 0]) * inv[:, 2, 2]
+        cov = np.swapaxes(inv, -1, -2) @ inv
+        max_var = np.max(np.diagonal(cov, axis1=-2, axis2=-1), axis=-1)
+        split = (np.sqrt(max_var) > config.split_scale_fraction * scene_extent).astype(np.uint8)
+        for j in range(len(cand)):
+            if split[j]:
+                z[j, :3] = rng.standard_normal(3)
+                z[j, 3:] = rng.standard_normal(3)
+    n_new = len(cand)
+    n_dst = n_keep + n_new
+    dev = cloud.device
+    out = GaussianCloud(torch.empty((n_dst, 3), device=dev), torch.empty((n_dst, 6), device=dev),
+                        torch.empty(n_dst, device=dev), torch.empty(n_dst, device=dev),
+                        beta=cloud.beta, bg_raw=cloud.bg_raw.clone())
+    st2 = AdamState(n_dst, dev, state.t, state.beta1, state.beta2, state.eps)
+    keep_t = torch.as_tensor(idx.astype(np.int32), device=dev)
+    cand_t = torch.as_tensor(cand.astype(np.int32), device=dev)
+    split_t = torch.as_tensor(split, device=dev)
+    z_t = torch.as_tensor(z, device=dev)
+    src = cloud.c_struct()
+    _lib.check(_lib.lib().ugs_densify_apply(
+        ctypes.byref(src), state.m_flat.data_ptr(), state.v_flat.data_ptr(),
+        keep_t.data_ptr() if n_keep else None, n_keep,
+        cand_t.data_ptr() if n_new else None, split_t.data_ptr() if n_new else None,
+        z_t.data_ptr() if n_new else None, n_new, float(config.split_variance_factor),
+        out.means.data_ptr(), out.l_raw.data_ptr(), out.intensity_raw.data_ptr(),
+        out.opacity_raw.data_ptr(), st2.m_flat.data_ptr(), st2.v_flat.data_ptr(),
+        _stream()), "ugs_densify_apply")
+    return out, st2
+
+
+def dataset_bounds(dataset: SliceDataset, margin: float = 0.0) -> np.ndarray:
+    """ref trainer.py:282-292."""
+    corners = []
+    for img in dataset.slices:
+        h, w = img.pixels.shape
+        x1 = (w - 1) / 2.0 * img.spacing
+        x2 = (h - 1) / 2.0 * img.spacing
+        local = np.array([[sx, sy, 0.0] for sx in (-x1, x1) for sy in (-x2, x2)])
+        corners.append(img.pose.apply(local))
+    pts = np.concatenate(corners)
+    return np.stack([pts.min(axis=0) - margin, pts.max(axis=0) + margin])
+
+
+def save_checkpoint(cloud: GaussianCloud, path, config: TrainConfig | None = None,
+                    iteration: int = 0) -> None:
+    """'UGSC' v1 little-endian checkpoint + JSON trailer, atomic (ref :295-313)."""
+    trailer = json.dumps({"config": asdict(config) if config else None,
+                          "iteration": iteration}).encode()
+    d = cloud.to_numpy()
+    parts = [CHECKPOINT_MAGIC, struct.pack("<II", CHECKPOINT_VERSION, cloud.n)]
+    for k in GROUPS:
+        parts.append(np.ascontiguousarray(d[k], "<f4").tobytes())
+    parts += [struct.pack("<fff", d["bg_intensity_raw"], d["bg_opacity_raw"], cloud.beta),
+              struct.pack("<I", len(trailer)), trailer]
+    tmp = str(path) + ".tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(b"".join(parts))
+    os.replace(tmp, path)
+
+
+def load_checkpoint(path, device=None):
+    """(cloud, meta) from a 'UGSC' file (ref trainer.py:316-348)."""
+    blob = open(path, "rb").read()
+    if blob[:4] != CHECKPOINT_MAGIC:
+        raise CheckpointFormatError(f"bad magic in {path}")
+    if len(blob) < 12:
+        raise CheckpointFormatError(f"truncated checkpoint {path}")
+    version, n = struct.unpack_from("<II", blob, 4)
+    if version != CHECKPOINT_VERSION:
+        raise CheckpointFormatError(f"unsupported checkpoint version {version}")
+    off = 12
+    need = off + 44 * n + 12 + 4
+    if len(blob) < need:
+        raise CheckpointFormatError(f"truncated checkpoint {path}")
+    arrs = {}
+    for k, cols in (("means", 3), ("l_raw", 6), ("intensity_raw", 1), ("opacity_raw", 1)):
+        a = np.frombuffer(blob, "<f4", count=n * cols, offset=off).copy()
+        arrs[k] = a.reshape(n, cols) if cols > 1 else a
+        off += 4 * n * cols
+    bg_c, bg_a, beta = struct.unpack_from("<fff", blob, off)
+    off += 12
+    (tlen,) = struct.unpack_from("<I", blob, off)
+    off += 4
+    if off + tlen != len(blob):
+        raise CheckpointFormatError(
+            f"trailer size mismatch in {path}: expected {off + tlen} bytes, "
+            f"file has {len(blob)}")
+    meta = json.loads(blob[off:off + tlen].decode())
+    cloud = GaussianCloud(arrs["means"], arrs["l_raw"], arrs["intensity_raw"],
+                          arrs["opacity_raw"], float(bg_c), float(bg_a), float(beta),
+                          device=device)
+    return cloud, meta
+
+
+# ---------------------------------------------------------------------------
+# the training step engine (shared by train() and bench.py)
+# ---------------------------------------------------------------------------
+
+class TrainEngine:
+    """Device-resident training state and the fused per-step pipeline."""
+
+    def __init__(self, cloud: GaussianCloud, config: TrainConfig, specs, targets,
+                 world_size: int = 1, rank: int = 0, process_group=None):
+        self.cloud = cloud
+        self.config = config
+        self.state = AdamState.for_cloud(cloud)
+        self.renderer = Renderer()
+        self.specs = list(specs)
+        self.targets = targets        # (n_slices, H, W) float32 on the device
+        h, w = self.targets.shape[-2:]
+        if any(s.height != h or s.width != w for s in self.specs):
+            raise InvalidParameterError("training slices must share width/height")
+        self.h, self.w = int(h), int(w)
+        self.world_size, self.rank, self.pg = world_size, rank, process_group
+        # per-slice constant structs, built once (host), copied per batch
+        self._consts = (_lib.Slice * len(self.specs))()
+        for i, s in enumerate(self.specs):
+            fill_slice(self._consts[i], s, config.p_mass, 0)
+        self._alloc_stats()
+        self.grad = grad_buffer(cloud.n, cloud.device)
+        self.last_loss = None
+        self.last_pred = None
+
+    def _alloc_stats(self):
+        n, dev = self.cloud.n, self.cloud.device
+        self.grad_sum = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.grad_cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.touched = torch.zeros(n, dtype=torch.uint8, device=dev)
+
+    def batch_structs(self, idx):
+        B = len(idx)
+        arr = (_lib.Slice * B)()
+        sz = ctypes.sizeof(_lib.Slice)
+        for j, i in enumerate(idx):
+            ctypes.memmove(ctypes.byref(arr, j * sz), ctypes.byref(self._consts, int(i) * sz), sz)
+            arr[j].pix_base = j * self.h * self.w
+        return arr
+
+    def forward_loss(self, idx):
+        """bin + forward + loss for the slices `idx` (this rank's batch)."""
+        cfg = self.config
+        B = len(idx)
+        structs = self.batch_structs(idx)
+        self.renderer.bin(self.cloud, [self.specs[i] for i in idx], cfg.p_mass, structs)
+        num = torch.empty((B, self.h, self.w), dtype=torch.float32, device=self.cloud.device)
+        den = torch.empty_like(num)
+        self.renderer.forward(self.cloud, num, den)
+        pred = num / den
+        tgt = self.targets[torch.as_tensor(np.asarray(idx), device=self.cloud.device)]
+        lv, dpix = loss_batch(pred, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
+        return num, den, pred, tgt, lv, dpix
+
+    def step(self, idx, it: int, check_finite: bool = True):
+        """One full training step; returns the mean loss (python float) when
+        check_finite, else the device tensor."""
+        cfg = self.config
+        num, den, pred, tgt, lv, dpix = self.forward_loss(idx)
+        loss_t = lv.mean()
+        if self.world_size > 1:
+            torch.distributed.all_reduce(loss_t, group=self.pg)
+            loss_t = loss_t / self.world_size
+        self.last_pred, self.last_tgt = pred, tgt
+        loss_val = None
+        if check_finite:
+            loss_val = float(loss_t.item())
+            if not math.isfinite(loss_val):
+                return loss_val
+        scale = 1.0 / (len(idx) * self.world_size)
+        self.renderer.backward(self.cloud, num, den, dpix.to(torch.float32).contiguous(),
+                               self.grad, self.touched, scale)
+        if self.world_size > 1:
+            torch.distributed.all_reduce(self.grad, group=self.pg)
+            torch.distributed.all_reduce(self.touched, op=torch.distributed.ReduceOp.MAX,
+                                         group=self.pg)
+        _lib.check(_lib.lib().ugs_grad_stats(
+            self.grad.data_ptr(), self.cloud.n, self.touched.data_ptr(),
+            self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
+            "ugs_grad_stats")
+        lr_g = general_lr(cfg, it)
+        lrs = {"means": mean_lr(cfg, it), "l_raw": lr_g, "intensity_raw": lr_g,
+               "opacity_raw": lr_g, "bg": lr_g}
+        _adam_flat(self.state, self.cloud, self.grad, lrs, zero_grad=True)
+        return loss_val if check_finite else loss_t
+
+    def densify(self, rng, scene_extent, threshold, max_total):
+        avg = (self.grad_sum.double() / torch.clamp(self.grad_cnt, min=1).double()).cpu().numpy()
+        if threshold is None:
+            threshold = float(np.quantile(avg, 0.9))
+        self.cloud, self.state = densify_prune_resample(
+            self.cloud, avg, self.state, self.config, rng, scene_extent, threshold,
+            max_total)
+        self._alloc_stats()
+        self.grad = grad_buffer(self.cloud.n, self.cloud.device)
+        return threshold
+
+
+def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
+          checkpoint_path=None, log_path=None, snapshot_path=None,
+          time_budget_s: float | None = None, device=None):
+    """Full optimisation run (ref trainer.py:351-434) -> (cloud, log).
+
+    Under torch.distributed (world_size > 1) every rank draws the same slice
+    order and takes its own `config.batch` slices of each global step."""
+    train_slices = dataset.subset("train")
+    if not train_slices:
+        raise InvalidParameterError("dataset has no training slices")
+    if bounds is None:
+        bounds = dataset_bounds(dataset)
+    bounds = np.asarray(bounds, np.float64)
+    world, rank, pg = 1, 0, None
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        world, rank = torch.distributed.get_world_size(), torch.distributed.get_rank()
+    rng = np.random.default_rng(config.seed)
+    cloud = init_cloud(config, bounds, device)
+    specs = [s.spec for s in train_slices]
+    targets = torch.as_tensor(np.stack([np.asarray(s.pixels, np.float32)
+                                        for s in train_slices]), device=cloud.device)
+    eng = TrainEngine(cloud, config, specs, targets, world, rank, pg)
+    scene_extent = float(np.linalg.norm(bounds[1] - bounds[0]))
+    max_total = 2 * config.n_gaussians
+    threshold = config.densify_grad_threshold
+    order = rng.permutation(len(train_slices))
+    cursor = 0
+    log = []
+    t0 = time.perf_counter()
+    B = config.batch
+    for it in range(1, config.iterations + 1):
+        picks = []
+        for _ in range(B * world):
+            if cursor >= len(order):
+                order = rng.permutation(len(train_slices))
+                cursor = 0
+            picks.append(int(order[cursor]))
+            cursor += 1
+        mine = picks[rank * B:(rank + 1) * B]
+        loss_val = eng.step(mine, it)
+        if not math.isfinite(loss_val):
+            snap = snapshot_path or (str(checkpoint_path or "echosplat") + ".diverged")
+            if rank == 0:
+                save_checkpoint(eng.cloud, snap, config, it)
+            raise TrainingDivergedError(
+                f"non-finite loss at iteration {it}; snapshot at {snap}", snap)
+        if config.heuristic_interval > 0 and it % config.heuristic_interval == 0:
+            threshold = eng.densify(rng, scene_extent, threshold, max_total)
+        if it % config.eval_interval == 0 or it == config.iterations:
+            s = ssim_batch(torch.clamp(eng.last_pred[:1], 0, 1), eng.last_tgt[:1])
+            entry = {"iter": it, "wall_ms": (time.perf_counter() - t0) * 1000.0,
+                     "loss": loss_val, "train_ssim": float(s[0])}
+            log.append(entry)
+            if log_path is not None and rank == 0:
+                with open(log_path, "a") as fh:
+                    fh.write(json.dumps(entry) + "\n")
+        if time_budget_s is not None and time.perf_counter() - t0 >= time_budget_s:
+            break
+    if checkpoint_path is not None and rank == 0:
+        save_checkpoint(eng.cloud, checkpoint_path, config, config.iterations)
+    return eng.cloud, log

@@ -1,0 +1,67 @@
+"""CPU-only checks of the boundary: libugs.so loads, exports exactly the
+entry points include/ugs.h declares, the ctypes structs match the C layout,
+and the host-side constants equal the oracle's (no GPU work here)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "ugs.h")).read()
+    return sorted(set(re.findall(r"UGS_API\s+[\w\s\*]*?\b(ugs_\w+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    names = header_functions()
+    assert "ugs_bin" in names and "ugs_forward" in names and "ugs_backward" in names
+    assert len(names) >= 12
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2505_05643_b200 import _lib
+    L = _lib.load()
+    for name in header_functions():
+        assert hasattr(L, name), name
+    assert set(header_functions()) == set(_lib.EXPORTS)
+    assert L.ugs_abi_version() == 1
+
+
+def test_struct_layout():
+    from paper_2505_05643_b200 import _lib
+    # ugs_slice: 27 floats + 6 int32 + pad + int64 = 144 bytes
+    assert ctypes.sizeof(_lib.Slice) == 144
+    assert _lib.Slice.pix_base.offset == 136
+    assert ctypes.sizeof(_lib.Cloud) == 56
+
+
+def test_error_path_without_gpu():
+    """Invalid arguments are rejected before any CUDA call."""
+    from paper_2505_05643_b200 import _lib
+    L = _lib.load()
+    assert L.ugs_bin(None, None, None, 0, None, None, None) == -1
+    assert b"S" in L.ugs_last_error() or b"plan" in L.ugs_last_error()
+
+
+def test_slice_constants_match_oracle():
+    from paper_2505_05643_b200 import _lib
+    from paper_2505_05643_b200.geometry import ProbePose, SliceSpec, fill_slice
+    from oracle import oracle as O
+    import cases
+    rng = np.random.default_rng(4)
+    for w, h, s, p in ((256, 256, 0.375, 0.95), (37, 53, 0.6, 0.9999), (512, 96, 0.1875, 0.95)):
+        R, t = cases.random_pose(rng, 12.0)
+        st = _lib.Slice()
+        fill_slice(st, SliceSpec(w, h, s, ProbePose(R, t)), p)
+        sc = O.slice_constants(R, t, w, h, s, p)
+        assert np.array_equal(np.array(st.rw, np.float32), sc["rw"])
+        assert np.array_equal(np.array(st.tw, np.float32), sc["tw"])
+        for k in ("origin", "du", "dv"):
+            assert np.array_equal(np.array(getattr(st, k), np.float32), sc[k])
+        for k in ("sqrt_cut", "s", "cx", "cy", "x1h", "x2h"):
+            assert np.float32(getattr(st, k)) == sc[k], k

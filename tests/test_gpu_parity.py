@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.  Bit-exact for the accepted set, windows and
+tile lists; rtol 1e-4 / atol 1e-5 for renders (north_star tolerance);
+per-group rtol 1e-4 / atol 1e-5 * max|group| for gradients."""
+
+import numpy as np
+import pytest
+
+import cases
+from conftest import load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2505_05643_b200 as ug  # noqa: E402
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+def spec_of(R, t, w, h, s):
+    return ug.SliceSpec(w, h, s, ug.ProbePose(R, t))
+
+
+def expected_tiles(win, acc, w, h):
+    """Per-16x16-tile ascending Gaussian lists from (oracle) windows."""
+    tx, ty = (w + 15) // 16, (h + 15) // 16
+    lists = [[] for _ in range(tx * ty)]
+    for (iu0, iu1, iv0, iv1), g in zip(win, acc):
+        for y in range(iv0 >> 4, (iv1 >> 4) + 1):
+            for x in range(iu0 >> 4, (iu1 >> 4) + 1):
+                lists[y * tx + x].append(int(g))
+    return lists
+
+
+def oracle_args(cloud, sc):
+    return (cloud["means"], cloud["l_raw"], cloud["intensity_raw"],
+            cloud["opacity_raw"], cloud["bg_intensity_raw"],
+            cloud["bg_opacity_raw"], cloud["beta"], sc)
+
+
+@pytest.fixture(scope="module")
+def prep():
+    return load_golden("prepare.npz")
+
+
+@pytest.fixture(scope="module")
+def rend():
+    return load_golden("render.npz")
+
+
+@pytest.mark.parametrize("case", cases.PREPARE_CASES, ids=lambda c: c[0])
+def test_prepare_and_tiles_bit_exact(case, prep):
+    cloud_np, R, t, w, h, s = cases.prepare_case(case)
+    name = case[0]
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    r = ug.Renderer()
+    r.bin(cloud, [spec_of(R, t, w, h, s)], 0.95)
+    accs, wins = r.accepted(cloud.device, windows=True)
+    acc = accs[0].cpu().numpy()
+    win = wins[0].cpu().numpy()
+    assert np.array_equal(acc, prep[f"{name}/accepted"])
+    assert np.array_equal(win, prep[f"{name}/windows"])
+    rng_, srt = r.bins(cloud.device)
+    rng_, srt = rng_.cpu().numpy(), srt.cpu().numpy()
+    lists = expected_tiles(win, acc, w, h)
+    assert len(rng_) == len(lists)
+    for b, lst in enumerate(lists):
+        got = srt[rng_[b, 0]:rng_[b, 1]].tolist() if rng_[b, 1] > rng_[b, 0] else []
+        assert got == lst, f"tile {b}"
+
+
+def test_batch_binning_matches_single(prep):
+    """S slices binned together == each slice binned alone (bit-exact)."""
+    cloud_np = cases.uniform_cloud(7, 30000, [[-40] * 3, [40] * 3], 0.5, 1.5)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    rng = np.random.default_rng(3)
+    specs = [spec_of(*cases.random_pose(rng, 10.0), 96, 96, 0.5) for _ in range(7)]
+    r = ug.Renderer()
+    r.bin(cloud, specs, 0.95)
+    accs, wins = r.accepted(cloud.device, windows=True)
+    num = torch.empty((7, 96, 96), device="cuda")
+    den = torch.empty_like(num)
+    r.forward(cloud, num, den)
+    for s, spec in enumerate(specs):
+        sc = O.slice_constants(spec.pose.rotation, spec.pose.translation, 96, 96, 0.5, 0.95)
+        a, wv, _ = O.prepare(cloud_np["means"], cloud_np["l_raw"], 0.01, sc)
+        assert np.array_equal(accs[s].cpu().numpy(), a)
+        assert np.array_equal(wins[s].cpu().numpy(), wv)
+        n1 = ug.rasterize(cloud, spec).intensity_num
+        assert torch.equal(n1, num[s])
+
+
+@pytest.mark.parametrize("case", cases.RENDER_CASES, ids=lambda c: c[0])
+def test_render_backward_vs_reference(case, rend):
+    cloud_np, R, t, w, h, s, p, dpix = cases.render_case(case)
+    name = case[0]
+    spec = spec_of(R, t, w, h, s)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    buf = ug.rasterize(cloud, spec, p=p)
+    assert np.array_equal(buf.accepted.cpu().numpy(), rend[f"{name}/accepted"])
+    np.testing.assert_allclose(buf.intensity_num.cpu().numpy(), rend[f"{name}/num"],
+                               rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(buf.opacity_sum.cpu().numpy(), rend[f"{name}/den"],
+                               rtol=RTOL, atol=ATOL)
+    g = ug.backward(cloud, spec, buf, dpix)
+    for k in ("d_means", "d_l_raw", "d_intensity_raw", "d_opacity_raw"):
+        ref = rend[f"{name}/{k}"]
+        np.testing.assert_allclose(getattr(g, k).cpu().numpy(), ref, rtol=RTOL,
+                                   atol=ATOL * np.abs(ref).max(), err_msg=k)
+    np.testing.assert_allclose([g.d_bg_intensity_raw, g.d_bg_opacity_raw],
+                               rend[f"{name}/d_bg"], rtol=1e-4)
+    if f"{name}/loss" in rend:
+        pred = buf.intensity_num / buf.opacity_sum
+        lv, lg = ug.loss(pred, rend[f"{name}/target"], 0.2)
+        assert lv == pytest.approx(float(rend[f"{name}/loss"]), rel=1e-4, abs=1e-6)
+        s_gpu = ug.ssim(torch.clamp(pred, 0, 1), rend[f"{name}/target"])
+        assert round(s_gpu, 4) == round(float(rend[f"{name}/ssim"]), 4)
+
+
+def test_kats(rend):
+    logit = lambda q: float(np.log(q / (1 - q)))
+    empty = ug.GaussianCloud(np.zeros((0, 3)), np.zeros((0, 6)), np.zeros(0),
+                             np.zeros(0), logit(0.37), -4.0)
+    img = ug.render_slice(empty, ug.SliceSpec(8, 8, 1.0))
+    assert np.allclose(img.pixels, 0.37, atol=1e-6)
+    ld = np.sqrt(1.0 / 2.0 - 0.01)
+    single = ug.GaussianCloud(np.zeros((1, 3)), np.array([[ld] * 3 + [0, 0, 0]]),
+                              np.array([logit(1 - 1e-7)]), np.array([logit(0.8)]),
+                              -30.0, -4.0)
+    img = ug.render_slice(single, ug.SliceSpec(17, 17, 1.0), p=0.9999)
+    assert img.pixels[8, 8] == pytest.approx(0.8 / 0.818, abs=1e-4)
+    np.testing.assert_allclose(img.pixels, rend["kat_single/pixels"], rtol=RTOL, atol=ATOL)
+
+
+def test_zero_upstream_and_culled(rng):
+    cloud_np = cases.random_cloud(rng, 100, extent=30.0)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    spec = ug.SliceSpec(12, 12, 1.0)
+    buf = ug.rasterize(cloud, spec)
+    g0 = ug.backward(cloud, spec, buf, np.zeros((12, 12), np.float32))
+    assert not g0.d_means.any() and not g0.d_l_raw.any()
+    assert g0.d_bg_intensity_raw == 0.0
+    g1 = ug.backward(cloud, spec, buf, np.ones((12, 12), np.float32))
+    rejected = np.setdiff1d(np.arange(cloud.n), buf.accepted.cpu().numpy())
+    assert len(rejected) > 0
+    assert not g1.d_means.cpu().numpy()[rejected].any()
+    assert not g1.d_opacity_raw.cpu().numpy()[rejected].any()
+    with pytest.raises(ug.InvalidParameterError):
+        ug.backward(cloud, spec, buf, np.zeros((4, 4), np.float32))
+
+
+def test_full_size_c3_parity():
+    """BASELINE config C3: 1M Gaussians, 256x256 @0.375 mm, random pose --
+    accepted set and windows bit-exact; render and gradients vs oracle."""
+    cloud_np = cases.uniform_cloud(0, 1_000_000, [[-48] * 3, [48] * 3], 0.85, 1.05)
+    rng = np.random.default_rng(5)
+    R, t = cases.random_pose(rng, 12.0)
+    spec = spec_of(R, t, 256, 256, 0.375)
+    sc = O.slice_constants(R, t, 256, 256, 0.375, 0.95)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    buf = ug.rasterize(cloud, spec)
+    num, den, acc, G = O.rasterize(*oracle_args(cloud_np, sc), workers=8)
+    assert np.array_equal(buf.accepted.cpu().numpy(), acc)
+    np.testing.assert_allclose(buf.intensity_num.cpu().numpy(), num, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(buf.opacity_sum.cpu().numpy(), den, rtol=RTOL, atol=ATOL)
+    dpix = np.random.default_rng(1).standard_normal((256, 256)).astype(np.float32)
+    g = ug.backward(cloud, spec, buf, dpix)
+    ref = O.backward(*oracle_args(cloud_np, sc), num, den, dpix, workers=8, gathered=G)
+    for k in ("d_means", "d_l_raw", "d_intensity_raw", "d_opacity_raw"):
+        np.testing.assert_allclose(getattr(g, k).cpu().numpy(), ref[k], rtol=RTOL,
+                                   atol=ATOL * np.abs(ref[k]).max(), err_msg=k)
+
+
+def test_forward_deterministic():
+    cloud_np = cases.uniform_cloud(1, 200_000, [[-48] * 3, [48] * 3], 0.85, 1.05)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    spec = spec_of(*cases.random_pose(np.random.default_rng(9), 12.0), 256, 256, 0.375)
+    b1 = ug.rasterize(cloud, spec)
+    n1 = b1.intensity_num.clone()
+    dp = np.random.default_rng(2).standard_normal((256, 256)).astype(np.float32)
+    g1 = ug.backward(cloud, spec, b1, dp)
+    b2 = ug.rasterize(cloud, spec)
+    g2 = ug.backward(cloud, spec, b2, dp)
+    assert torch.equal(n1, b2.intensity_num)
+    assert torch.equal(g1.d_means, g2.d_means) and torch.equal(g1.d_l_raw, g2.d_l_raw)
+
+
+def test_adam_bit_exact():
+    z = load_golden("adam_densify.npz")
+    cloud = ug.GaussianCloud(z["adam/init/means"], z["adam/init/l_raw"],
+                             z["adam/init/intensity_raw"], z["adam/init/opacity_raw"],
+                             float(z["adam/init/bg"][0]), float(z["adam/init/bg"][1]))
+    st = ug.AdamState.for_cloud(cloud)
+    lrs = {"means": 0.016, "l_raw": 0.05, "intensity_raw": 0.05,
+           "opacity_raw": 0.05, "bg": 0.05}
+    for step in range(5):
+        d = z[f"adam/step{step}/d_bg"]
+        g = ug.ParamGradients(*(torch.as_tensor(z[f"adam/step{step}/d_{k}"])
+                                for k in ("means", "l_raw", "intensity_raw", "opacity_raw")),
+                              float(d[0]), float(d[1]))
+        ug.adam_step(st, cloud, g, lrs)
+    for k in ("means", "l_raw", "intensity_raw", "opacity_raw"):
+        assert np.array_equal(getattr(cloud, k).cpu().numpy(), z[f"adam/final/{k}"]), k
+        assert np.array_equal(st.m[k].cpu().numpy(), z[f"adam/final/m_{k}"]), k
+        assert np.array_equal(st.v[k].cpu().numpy(), z[f"adam/final/v_{k}"]), k
+    assert [cloud.bg_intensity_raw, cloud.bg_opacity_raw] == list(z["adam/final/bg"])
+
+
+def test_densify_matches_reference():
+    z = load_golden("adam_densify.npz")
+    cloud = ug.GaussianCloud(z["densify/init/means"], z["densify/init/l_raw"],
+                             z["densify/init/intensity_raw"],
+                             z["densify/init/opacity_raw"], 0.0, -4.0)
+    st = ug.AdamState.for_cloud(cloud)
+    st.m_flat[:] = 0.5
+    st.v_flat[:] = 0.25
+    out, st2 = ug.densify_prune_resample(cloud, z["densify/avg"], st, ug.TrainConfig(),
+                                         np.random.default_rng(99), 60.0, 0.8, 48)
+    for k in ("l_raw", "intensity_raw", "opacity_raw"):
+        assert np.array_equal(getattr(out, k).cpu().numpy(), z[f"densify/final/{k}"]), k
+    np.testing.assert_allclose(out.means.cpu().numpy(), z["densify/final/means"],
+                               rtol=1e-6, atol=1e-6)
+    for k in ("means", "l_raw", "intensity_raw", "opacity_raw"):
+        assert np.array_equal(st2.m[k].cpu().numpy(), z[f"densify/final/m_{k}"]), k
+
+
+def _train_golden():
+    z = load_golden("train.npz")
+    slices = [ug.SliceImage(z["slices"][i], float(z["spacing"]),
+                            ug.ProbePose(z["rot"][i], z["trans"][i]))
+              for i in range(len(z["slices"]))]
+    return z, ug.SliceDataset(slices)
+
+
+def test_train_short_run_tracks_reference():
+    z, ds = _train_golden()
+    cfg = ug.TrainConfig(n_gaussians=300, iterations=40, seed=7, heuristic_interval=20,
+                         eval_interval=10, workers=1)
+    cloud, log = ug.train(ds, cfg)
+    assert [e["iter"] for e in log] == list(z["iters"])
+    np.testing.assert_allclose([e["loss"] for e in log], z["loss"], rtol=2e-3)
+    assert cloud.n == len(z["final/means"])
+    np.testing.assert_allclose(cloud.means.cpu().numpy(), z["final/means"], atol=2e-3)
+
+
+def test_train_bitwise_deterministic():
+    _, ds = _train_golden()
+    cfg = ug.TrainConfig(n_gaussians=300, iterations=60, seed=7, heuristic_interval=20)
+    a, _ = ug.train(ds, cfg)
+    b, _ = ug.train(ds, cfg)
+    assert torch.equal(a.means, b.means) and torch.equal(a.l_raw, b.l_raw)
+    assert a.bg_opacity_raw == b.bg_opacity_raw
+
+
+def test_autograd_matches_backward():
+    cloud_np, R, t, w, h, s, p, dpix = cases.render_case(cases.RENDER_CASES[3])
+    spec = spec_of(R, t, w, h, s)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    params = [x.clone().requires_grad_(True) for x in
+              (cloud.means, cloud.l_raw, cloud.intensity_raw, cloud.opacity_raw)]
+    bg = cloud.bg_raw.clone().requires_grad_(True)
+    pred = ug.rasterize_autograd(*params, bg, [spec], p=p)
+    (pred[0] * torch.as_tensor(dpix, device="cuda")).sum().backward()
+    g = ug.backward(cloud, spec, ug.rasterize(cloud, spec, p=p), dpix)
+    assert torch.allclose(params[0].grad, g.d_means)
+    assert torch.allclose(params[1].grad, g.d_l_raw)
