@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the UltraGauss training hot path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Metric: fwd+bwd slices/s at config C3 -- 1M Gaussians (fixed init cloud,
+init_cloud(seed=0, l_init U[0.85,1.05)) over the 160^3 shells phantom), 256x256
+slices @0.375 mm at random poses.  A step is one full training step over a
+batch of B slices per GPU: ugs_bin (phase 1 + tile sort) -> forward -> L1+SSIM
+loss -> backward -> [NCCL all-reduce] -> grad stats -> Adam.  `value` is the
+whole-job rate (B * N * K slices / max-over-ranks device time), inputs resident
+in HBM; `e2e` repeats it with every step's targets copied from pinned host
+memory and the loss read back.  `--impl reference` times the reference's CPU
+path (the oracle port of echosplat; the Python reference cannot travel to
+the GPU host) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "slices/sec fwd+bwd (1M Gaussians, 256x256)"
+UNIT = "slices/s"
+# algorithmic work per (Gaussian, pixel) pair: operator
+# counts of the reference kernels (_kernels.py:38-47 forward, :73-101 backward)
+FLOP_FWD_PER_PAIR = 28
+FLOP_BWD_PER_PAIR = 73
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=16, help="slices per GPU per step")
+    ap.add_argument("--n-gaussians", type=int, default=1_000_000)
+    ap.add_argument("--size", type=int, default=256)
+    ap.add_argument("--spacing", type=float, default=0.375)
+    ap.add_argument("--n-slices", type=int, default=256, help="dataset size")
+    ap.add_argument("--cpu-sample", type=int, default=12,
+                    help="slices in the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(a):
+    return (f"C3: {a.n_gaussians} Gaussians (init_cloud seed 0, l_init U[0.85,1.05), "
+            f"means U(+-48 mm)), {a.size}x{a.size} @{a.spacing} mm random-pose slices "
+            f"(uniform rotation, t~U(+-12 mm)^3) of the 160^3 @0.6 mm shells phantom")
+
+
+def make_phantom_and_specs(a):
+    from paper_2505_05643_b200.volume import make_phantom
+    from paper_2505_05643_b200.dataset import random_pose_specs
+    vol = make_phantom("shells", 160, 0.6, seed=1)
+    specs = random_pose_specs(a.n_slices, a.size, a.size, a.spacing, seed=0,
+                              translate=12.0)
+    return vol, specs
+
+
+def train_config(a):
+    from paper_2505_05643_b200.trainer import TrainConfig
+    # scene-scale hyper-parameters (ref tests/test_acceptance.py:40-46)
+    return TrainConfig(n_gaussians=a.n_gaussians, iterations=10000, seed=0,
+                       l_init_low=0.85, l_init_high=1.05, lr_means_start=0.016,
+                       lr_means_final=1.6e-4, lr_general_final=0.005,
+                       heuristic_interval=0, batch=a.batch)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        self.proc.wait()
+        self.tmp.seek(0)
+        rows = [r.split(",") for r in self.tmp.read().strip().splitlines() if r.strip()]
+        os.unlink(self.tmp.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for k, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU ---
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_reference_rate(a, vol, specs, n_slices, cfg, warmup=1):
+    """The reference's per-iteration path (oracle port, all host cores):
+    rasterize -> loss -> backward -> adam_step per slice.  Returns
+    (slices/s, seconds, cores)."""
+    from oracle import oracle as O
+    from paper_2505_05643_b200.volume import sample_slice
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import cases
+    cl = cases.uniform_cloud(cfg.seed, a.n_gaussians, vol.world_bounds(),
+                             cfg.l_init_low, cfg.l_init_high)
+    params = dict(cl)
+    m = {k: np.zeros_like(params[k]) for k in O.GROUPS}
+    v = {k: np.zeros_like(params[k]) for k in O.GROUPS}
+    m["bg"] = np.zeros(2, np.float32)
+    v["bg"] = np.zeros(2, np.float32)
+    cores = cpu_cores()
+    targets = [sample_slice(vol, specs[i]).pixels for i in range(n_slices + warmup)]
+    consts = [O.slice_constants(s.pose.rotation, s.pose.translation, s.width, s.height,
+                                s.spacing, cfg.p_mass) for s in specs[:n_slices + warmup]]
+    t = 0
+    t0 = None
+    for i in range(n_slices + warmup):
+        if i == warmup:
+            t0 = time.perf_counter()
+        t += 1
+        lr_g = O.general_lr(cfg.lr_general, cfg.lr_general_final, cfg.iterations, t)
+        lrs = {"means": O.mean_lr(cfg.lr_means_start, cfg.lr_means_final, cfg.iterations, t),
+               "l_raw": lr_g, "intensity_raw": lr_g, "opacity_raw": lr_g, "bg": lr_g}
+        O.train_iteration(params, m, v, t, consts[i], targets[i], cfg.ssim_loss_weight,
+                          lrs, cfg.p_mass, workers=cores)
+    dt = time.perf_counter() - t0
+    return n_slices / dt, dt, cores
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vol, specs = make_phantom_and_specs(a)
+    cfg = train_config(a)
+    rate, dt, cores = cpu_reference_rate(a, vol, specs, a.steps, cfg, warmup=a.warmup)
+    sample = (f"{a.steps} timed + {a.warmup} warm-up iterations, 1 slice each "
+              f"(rasterize->loss->backward->adam_step, workers={cores})")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1000.0 * dt / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 pair math / f32 accum",
+            "data": "synthetic", "config": {"workload": workload_desc(a),
+                                            "batch_per_step": 1,
+                                            "implementation": "oracle port of echosplat (C + numpy), host CPU"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU ---
+
+def fp32_peak_tflops(torch):
+    from paper_2505_05643_b200 import _lib
+    L = _lib.lib()
+    out = torch.zeros(1, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 8, 20000
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.ugs_fp32_peak_probe(out.data_ptr(), blocks, iters, st), "probe")
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = max(best, blocks * 256.0 * iters * 16 / (ms * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(a):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2505_05643_b200 as ug
+    from paper_2505_05643_b200 import _lib
+    from paper_2505_05643_b200.trainer import TrainEngine
+
+    vol, specs = make_phantom_and_specs(a)
+    targets = ug.sample_slices(vol, specs, device="cuda")
+    cfg = train_config(a)
+    cloud = ug.init_cloud(cfg, vol.world_bounds(), device="cuda")
+    eng = TrainEngine(cloud, cfg, specs, targets, world, rank, pg)
+    B = a.batch
+    order_rng = np.random.default_rng(1234)
+    order = order_rng.permutation(len(specs))
+    cursor = [0]
+
+    def next_batch():
+        picks = []
+        for _ in range(B * world):
+            if cursor[0] >= len(order):
+                cursor[0] = 0
+            picks.append(int(order[cursor[0]]))
+            cursor[0] += 1
+        return picks[rank * B:(rank + 1) * B]
+
+    it = [0]
+
+    def step(targets_batch=None, idx=None):
+        it[0] += 1
+        return eng.step(idx if idx is not None else next_batch(), it[0],
+                        targets_batch=targets_batch)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(a.warmup):
+        step()
+    # ---- timed region: device-resident inputs ----
+    eng.renderer.set_timing(True)
+    eng.renderer.timings(reset=True)
+    eng.profile = True
+    eng.event_times(reset=True)
+    eng.pairs_total = 0
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    l0 = _lib.lib().ugs_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    launches = _lib.lib().ugs_launch_count() - l0
+    clocks = sampler.stop()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    stage = eng.renderer.timings()
+    extra = eng.event_times()
+    pairs_per_step = eng.pairs_total / a.steps
+    eng.profile = False
+    eng.renderer.set_timing(False)
+    value = B * world * a.steps / (ms * 1e-3)
+
+    # ---- e2e: host-pinned targets copied every step, loss read back ----
+    e2e = None
+    if not a.no_e2e:
+        host_t = targets.cpu().pin_memory()
+        staging = torch.empty((B, a.size, a.size), dtype=torch.float32).pin_memory()
+        dev_t = torch.empty((B, a.size, a.size), dtype=torch.float32, device="cuda")
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        f0.record()
+        for _ in range(a.steps):
+            idx = next_batch()
+            torch.index_select(host_t, 0, torch.as_tensor(idx), out=staging)
+            dev_t.copy_(staging, non_blocking=True)
+            step(targets_batch=dev_t, idx=idx)     # loss .item() = the D2H read
+        f1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        ms_e2e = max_over_ranks(max(f0.elapsed_time(f1), wall * 1e3))
+        h2d = B * a.size * a.size * 4 + B * 144 + 16 * B
+        d2h = 8 + 24 * B
+        e2e = {"value": B * world * a.steps / (ms_e2e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- roofline (dominant kernel) ----
+    peak_fp32 = fp32_peak_tflops(torch)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    stage_ms = {k: v[0] / max(v[1], 1) for k, v in stage.items()}
+    stage_ms.update({k: v[0] / max(v[1], 1) for k, v in extra.items()})
+    dom = max(("forward", "backward"), key=lambda k: stage_ms.get(k, 0.0))
+    flop_pp = FLOP_BWD_PER_PAIR if dom == "backward" else FLOP_FWD_PER_PAIR
+    achieved = flop_pp * pairs_per_step / (stage_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(dom + "_kernel_dram_bytes")
+    except (OSError, ValueError):
+        pass
+    n = eng.cloud.n
+    adam_bytes = 32 * (11 * n + 2) + 4 * 2 * n + 3 * n   # p,g,m,v r/w + stats
+    roof_stages = {
+        "forward": {"flops": FLOP_FWD_PER_PAIR * pairs_per_step, "ms": stage_ms.get("forward"),
+                    "tflops": FLOP_FWD_PER_PAIR * pairs_per_step / (stage_ms.get("forward", 1e9) * 1e-3) / 1e12},
+        "backward": {"flops": FLOP_BWD_PER_PAIR * pairs_per_step, "ms": stage_ms.get("backward"),
+                     "tflops": FLOP_BWD_PER_PAIR * pairs_per_step / (stage_ms.get("backward", 1e9) * 1e-3) / 1e12},
+        "adam+stats": {"bytes": adam_bytes, "ms": stage_ms.get("adam"),
+                       "gbs": adam_bytes / (stage_ms.get("adam", 1e9) * 1e-3) / 1e9,
+                       "frac_of_hbm": adam_bytes / (stage_ms.get("adam", 1e9) * 1e-3) / 1e9 / hbm_peak},
+    }
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (160^3 shells phantom, random-pose GT slices, random-init cloud)",
+        "config": {"workload": workload_desc(a), "n_gaussians": a.n_gaussians,
+                   "slice": [a.size, a.size], "batch_per_gpu": B, "global_batch": B * world,
+                   "parallelism": f"dp{world}",
+                   "step": "ugs_bin+forward+loss(L1+0.2*SSIM, f64)+backward+"
+                           + ("allreduce+" if world > 1 else "") + "grad_stats+Adam",
+                   "l2": "inputs larger than L2: params+Adam moments+grads = "
+                         f"{(44 + 88 + 44) * n / 1e6:.0f} MB streamed per step",
+                   "pairs_per_slice": pairs_per_step / B},
+        "roofline": {"bound": "fp32", "kernel": dom + "_kernel", "achieved": achieved,
+                     "peak": peak_fp32, "unit": "TFLOP/s", "frac": achieved / peak_fp32,
+                     "traffic": traffic,
+                     "note": f"algorithmic {flop_pp} FLOP/pair (reference operator count, "
+                             "SURVEY 8d) x pairs per launch / CUDA-event launch time; peak = "
+                             "FP32 FFMA probe measured in this run (no tensor cores: not a "
+                             "dense contraction)"},
+        "roofline_stages": roof_stages,
+        "stage_ms_per_step": stage_ms,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            rate, dt, cores = cpu_reference_rate(a, vol, specs, a.cpu_sample, cfg, warmup=1)
+            line["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"{a.cpu_sample} slices of the same workload, one reference "
+                          f"iteration each (rasterize->loss->backward->adam_step), "
+                          f"{dt:.1f} s, workers={cores}"}
+        except Exception as exc:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_cores(),
+                                    "kind": "port", "sample": f"failed: {exc!r}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -98,10 +98,11 @@ UGS_API int ugs_plan_destroy(ugs_plan *plan);
 
 /* Phase 1 + binning for a batch of S slices (host array `slices`; the
  * library fills tiles_x/tiles_y/tile_base and keeps a device copy).
- * Writes per-slice accepted counts m_out[S] and tile-instance counts
- * k_out[S] (host).  Synchronizes `stream` once. */
+ * Writes per-slice accepted counts m_out[S], tile-instance counts k_out[S]
+ * and (Gaussian, pixel) pair counts p_out[S] (host; any may be NULL).
+ * Synchronizes `stream` once. */
 UGS_API int ugs_bin(ugs_plan *plan, const ugs_cloud *cloud, ugs_slice *slices, int S,
-            void *stream, int64_t *m_out, int64_t *k_out);
+            void *stream, int64_t *m_out, int64_t *k_out, int64_t *p_out);
 
 /* Accepted Gaussian indices (ascending per slice, slices concatenated) and
  * their inclusive pixel windows (iu0,iu1,iv0,iv1) -- the reference's
@@ -160,6 +161,28 @@ UGS_API int ugs_densify_apply(const ugs_cloud *src, const float *m_src,
                       float *means, float *l_raw, float *intensity_raw,
                       float *opacity_raw, float *m_dst, float *v_dst,
                       void *stream);
+
+/* ---- diagnostics (no counterpart in the reference, which has no tracing:
+ * SURVEY section 5) --------------------------------------------------- */
+
+/* Kernels launched by this library since it was loaded. */
+UGS_API long long ugs_launch_count(void);
+
+/* Enable CUDA-event timing of the plan's stages (phase-1 count, emit, sort,
+ * ranges, forward, backward, finalize).  Adds no synchronization of its own:
+ * finished events are harvested at the next ugs_bin (which synchronizes
+ * anyway) or by ugs_plan_timings. */
+UGS_API int ugs_plan_set_timing(ugs_plan *plan, int enabled);
+
+/* Accumulated milliseconds and call counts per stage (host arrays of n);
+ * returns the number of stages.  reset != 0 clears the accumulators. */
+/* FP32 FMA throughput probe: `blocks` x 256 threads each run `iters`
+ * iterations of 8 independent FMA chains; writes a checksum to out (dev).
+ * Flops = blocks*256*iters*16.  Used to measure the FP32 roofline peak. */
+UGS_API int ugs_fp32_peak_probe(float *out, int blocks, int iters, void *stream);
+
+UGS_API int ugs_plan_timings(ugs_plan *plan, double *ms_total, int64_t *calls,
+                             int n, int reset);
 
 #ifdef __cplusplus
 }

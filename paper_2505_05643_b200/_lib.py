@@ -51,7 +51,7 @@ EXPORTS = {
     "ugs_plan_destroy": (ctypes.c_int, [c_vp]),
     "ugs_bin": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), ctypes.POINTER(Slice),
                                ctypes.c_int, c_vp, ctypes.POINTER(c_i64),
-                               ctypes.POINTER(c_i64)]),
+                               ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "ugs_export_accepted": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "ugs_export_bins": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_i32),
                                        ctypes.POINTER(c_i64), c_vp]),
@@ -67,7 +67,16 @@ EXPORTS = {
                                          c_i64, c_vp, c_vp, c_vp, c_i64,
                                          ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
                                          c_vp, c_vp, c_vp]),
+    "ugs_launch_count": (ctypes.c_longlong, []),
+    "ugs_fp32_peak_probe": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
+    "ugs_plan_set_timing": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "ugs_plan_timings": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(c_i64), ctypes.c_int,
+                                        ctypes.c_int]),
 }
+
+STAGES = ("prepare_count", "prepare_emit", "sort", "bin_ranges", "forward",
+          "backward", "finalize")
 
 
 def load(path: str = LIB_PATH):

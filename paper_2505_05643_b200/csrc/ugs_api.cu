@@ -4,6 +4,7 @@
 // its API layer for the same conditions (gradients.py:43-52).
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <vector>
 
 #include "ugs_internal.cuh"
@@ -11,6 +12,37 @@
 namespace ugs {
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static void harvest(ugs_plan *p, int stage) {
+    if (!p->pending[stage]) return;
+    float ms = 0.f;
+    if (cudaEventSynchronize(p->ev[stage][1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, p->ev[stage][0], p->ev[stage][1]) == cudaSuccess) {
+        p->ms_total[stage] += ms;
+        p->calls[stage] += 1;
+    }
+    p->pending[stage] = false;
+}
+
+void stage_begin(ugs_plan *p, int stage, cudaStream_t st) {
+    if (!p->timing) return;
+    if (!p->ev_ready) {
+        for (int i = 0; i < kNumStages; ++i)
+            for (int j = 0; j < 2; ++j) cudaEventCreate(&p->ev[i][j]);
+        p->ev_ready = true;
+    }
+    harvest(p, stage);
+    cudaEventRecord(p->ev[stage][0], st);
+}
+
+void stage_end(ugs_plan *p, int stage, cudaStream_t st) {
+    if (!p->timing || !p->ev_ready) return;
+    cudaEventRecord(p->ev[stage][1], st);
+    p->pending[stage] = true;
+}
 
 void set_error(const std::string &msg) { g_err = msg; }
 
@@ -93,7 +125,7 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.slice_tot, b.slice_base, b.slices, b.rec,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.slice_tot, b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.hist, b.scan_tmp, b.bin_range,
                     b.bin_bg};
@@ -103,12 +135,16 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     delete[] p->h_m;
     delete[] p->h_tile_base;
     delete[] p->h_ntile;
+    if (p->ev_ready)
+        for (int i = 0; i < kNumStages; ++i)
+            for (int j = 0; j < 2; ++j) cudaEventDestroy(p->ev[i][j]);
     delete p;
     return UGS_OK;
 }
 
 extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
-                       int S, void *stream, int64_t *m_out, int64_t *k_out) {
+                       int S, void *stream, int64_t *m_out, int64_t *k_out,
+                       int64_t *p_out) {
     if (!p || !slices || S < 1 || S > 64) {
         set_error("ugs_bin: need a plan and 1 <= S <= 64 slices");
         return UGS_ERR_INVALID;
@@ -152,31 +188,41 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, (size_t)S * (nblk > 0 ? nblk : 1),
                      "alloc blk_cnt")))
         return rc;
+    if ((rc = ensure(&b.blk_pairs, &b.blk_pairs_cap, (size_t)S * (nblk > 0 ? nblk : 1),
+                     "alloc blk_pairs")))
+        return rc;
     {
         static_assert(sizeof(unsigned long long) == 8, "");
-        size_t cap = b.slice_tot ? 128 : 0;
-        if ((rc = ensure(&b.slice_tot, &cap, (size_t)128, "alloc slice_tot"))) return rc;
+        size_t cap = b.slice_tot ? 192 : 0;
+        if ((rc = ensure(&b.slice_tot, &cap, (size_t)192, "alloc slice_tot"))) return rc;
         size_t cap2 = b.slice_base ? 128 : 0;
         if ((rc = ensure(&b.slice_base, &cap2, (size_t)128, "alloc slice_base"))) return rc;
     }
-    std::vector<unsigned long long> tot(2 * S, 0ull);
+    std::vector<unsigned long long> tot(3 * S, 0ull);
+    stage_begin(p, kStageCount, st);
     if (c->n > 0) {
-        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, nblk, st))) return rc;
-        if ((rc = launch_prepare_scan(b.blk_cnt, S, nblk, b.slice_tot, st))) return rc;
-        UGS_CUDA(cudaMemcpyAsync(tot.data(), b.slice_tot, sizeof(unsigned long long) * 2 * S,
+        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk, st)))
+            return rc;
+        if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
+            return rc;
+        UGS_CUDA(cudaMemcpyAsync(tot.data(), b.slice_tot, sizeof(unsigned long long) * 3 * S,
                                  cudaMemcpyDeviceToHost, st));
-        UGS_CUDA(cudaStreamSynchronize(st));
     }
-    int64_t m_total = 0, k_total = 0;
+    stage_end(p, kStageCount, st);
+    UGS_CUDA(cudaStreamSynchronize(st));
+    int64_t m_total = 0, k_total = 0, p_total = 0;
     for (int s = 0; s < S; ++s) {
         p->h_slice_base[2 * s] = m_total;
         p->h_slice_base[2 * s + 1] = k_total;
-        p->h_m[s] = (int64_t)tot[2 * s];
-        if (m_out) m_out[s] = (int64_t)tot[2 * s];
-        if (k_out) k_out[s] = (int64_t)tot[2 * s + 1];
-        m_total += (int64_t)tot[2 * s];
-        k_total += (int64_t)tot[2 * s + 1];
+        p->h_m[s] = (int64_t)tot[3 * s];
+        if (m_out) m_out[s] = (int64_t)tot[3 * s];
+        if (k_out) k_out[s] = (int64_t)tot[3 * s + 1];
+        if (p_out) p_out[s] = (int64_t)tot[3 * s + 2];
+        m_total += (int64_t)tot[3 * s];
+        k_total += (int64_t)tot[3 * s + 1];
+        p_total += (int64_t)tot[3 * s + 2];
     }
+    p->p_total = p_total;
     if (k_total >= 0x7fffffffLL || m_total >= 0x7fffffffLL) {
         set_error("ugs_bin: batch exceeds 2^31 tile instances; use fewer slices");
         return UGS_ERR_RANGE;
@@ -215,6 +261,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         UGS_CUDA(cudaMalloc(&b.bin_range, sizeof(int2) * b.bin_cap));
         UGS_CUDA(cudaMalloc(&b.bin_bg, sizeof(float2) * b.bin_cap));
     }
+    stage_begin(p, kStageEmit, st);
     if (c->n > 0 && m_total > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.owner, b.keys,
@@ -225,12 +272,17 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         UGS_CUDA(cudaMemcpyAsync(b.rec_inst, &zero, sizeof(int32_t),
                                  cudaMemcpyHostToDevice, st));
     }
+    stage_end(p, kStageEmit, st);
+    stage_begin(p, kStageSort, st);
     if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, k_total,
                                bits_for(n_bins), b.hist, b.scan_tmp, st,
                                &p->sorted_keys, &p->sorted_vals)))
         return rc;
+    stage_end(p, kStageSort, st);
+    stage_begin(p, kStageRanges, st);
     if ((rc = launch_bin_ranges(p->sorted_keys, k_total, b.bin_range, n_bins, st)))
         return rc;
+    stage_end(p, kStageRanges, st);
     return UGS_OK;
 }
 
@@ -321,4 +373,25 @@ extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
         UGS_LAUNCH_CHECK("export_sorted_kernel");
     }
     return UGS_OK;
+}
+
+extern "C" long long ugs_launch_count(void) { return g_launches.load(); }
+
+extern "C" int ugs_plan_set_timing(ugs_plan *p, int enabled) {
+    if (!p) { set_error("ugs_plan_set_timing: NULL plan"); return UGS_ERR_INVALID; }
+    p->timing = enabled != 0;
+    return UGS_OK;
+}
+
+extern "C" int ugs_plan_timings(ugs_plan *p, double *ms_total, int64_t *calls,
+                                int n, int reset) {
+    if (!p) { set_error("ugs_plan_timings: NULL plan"); return UGS_ERR_INVALID; }
+    for (int s = 0; s < kNumStages; ++s) harvest(p, s);
+    for (int s = 0; s < n && s < kNumStages; ++s) {
+        if (ms_total) ms_total[s] = p->ms_total[s];
+        if (calls) calls[s] = p->calls[s];
+    }
+    if (reset)
+        for (int s = 0; s < kNumStages; ++s) { p->ms_total[s] = 0; p->calls[s] = 0; }
+    return kNumStages;
 }

@@ -34,6 +34,8 @@ struct PlanBuffers {
     // phase 1
     uint2 *blk_cnt = nullptr;       // [S][nblk] (accepted, tiles) -> exclusive offsets
     size_t blk_cnt_cap = 0;
+    unsigned *blk_pairs = nullptr;  // [S][nblk] (window pixel pairs)
+    size_t blk_pairs_cap = 0;
     unsigned long long *slice_tot = nullptr; // [S][2] totals (accepted, tiles)
     int64_t *slice_base = nullptr;  // [S][2] record base, instance base
     ugs_slice *slices = nullptr;    // [S] device copy
@@ -71,11 +73,19 @@ struct ugs_plan {
     int max_tiles = 0;
     int64_t *h_slice_base = nullptr; // host copy [S][2]
     int64_t *h_m = nullptr;          // host [S]
+    int64_t p_total = 0;             // (Gaussian, pixel) pairs of the batch
     int32_t *h_tile_base = nullptr;  // host [S]
     int32_t *h_ntile = nullptr;      // host [S]
     int h_cap = 0;
     uint32_t *sorted_keys = nullptr; // point into b.keys/b.keys2
     uint32_t *sorted_vals = nullptr;
+    // optional per-stage CUDA-event timing (ugs_plan_set_timing)
+    bool timing = false;
+    bool ev_ready = false;
+    cudaEvent_t ev[8][2];
+    bool pending[8] = {false, false, false, false, false, false, false, false};
+    double ms_total[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t calls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::string err;
 };
 
@@ -90,16 +100,35 @@ int cuda_fail(cudaError_t e, const char *what);
         if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, #call);  \
     } while (0)
 
+// every kernel launch is followed by exactly one UGS_LAUNCH_CHECK, which
+// also feeds the diagnostic launch counter (ugs_launch_count)
 #define UGS_LAUNCH_CHECK(what)                                      \
     do {                                                            \
+        ::ugs::note_launch();                                       \
         cudaError_t e_ = cudaGetLastError();                        \
         if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, what);   \
     } while (0)
 
+void note_launch();
+
+enum Stage {
+    kStageCount = 0,   // prepare_count + prepare_scan (+ the host read)
+    kStageEmit,        // prepare_emit: records + tile instances
+    kStageSort,        // radix sort
+    kStageRanges,      // bin ranges
+    kStageForward,     // forward_kernel
+    kStageBackward,    // backward_kernel
+    kStageFinalize,    // finalize + bg_finalize (all slices)
+    kNumStages
+};
+void stage_begin(ugs_plan *p, int stage, cudaStream_t st);
+void stage_end(ugs_plan *p, int stage, cudaStream_t st);
+
 // phase 1 (ugs_prepare.cu)
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
-                         uint2 *blk_cnt, int nblk, cudaStream_t st);
-int launch_prepare_scan(uint2 *blk_cnt, int S, int nblk,
+                         uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
+                         cudaStream_t st);
+int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st);
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,

@@ -29,9 +29,11 @@ __global__ void __launch_bounds__(kPrepThreads)
 prepare_count_kernel(const float *__restrict__ means,
                      const float *__restrict__ l_raw, int64_t n, float beta,
                      const ugs_slice *__restrict__ slices, int S,
-                     uint2 *__restrict__ blk_cnt, int nblk) {
+                     uint2 *__restrict__ blk_cnt, unsigned *__restrict__ blk_pairs,
+                     int nblk) {
     __shared__ ugs_slice sl[kMaxSlicesSmem];
     __shared__ uint2 wsum[kMaxSlicesSmem][kPrepThreads / 32];
+    __shared__ unsigned wpairs[kMaxSlicesSmem][kPrepThreads / 32];
     load_slices_smem(sl, slices, S);
     __syncthreads();
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
@@ -46,35 +48,58 @@ prepare_count_kernel(const float *__restrict__ means,
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int s = 0; s < S; ++s) {
-        unsigned acc = 0, tiles = 0;
+        unsigned acc = 0, tiles = 0, pairs = 0;
         Window w;
         if (valid && cull_window(mu, f, sl[s], w)) {
             acc = 1;
             tiles = (unsigned)window_tiles(w);
+            pairs = (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1));
         }
         acc = __reduce_add_sync(0xffffffffu, acc);
         tiles = __reduce_add_sync(0xffffffffu, tiles);
-        if (lane == 0) wsum[s][warp] = make_uint2(acc, tiles);
+        pairs = __reduce_add_sync(0xffffffffu, pairs);
+        if (lane == 0) {
+            wsum[s][warp] = make_uint2(acc, tiles);
+            wpairs[s][warp] = pairs;
+        }
     }
     __syncthreads();
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
         uint2 t = make_uint2(0, 0);
+        unsigned pr = 0;
 #pragma unroll
         for (int w = 0; w < kPrepThreads / 32; ++w) {
             t.x += wsum[s][w].x;
             t.y += wsum[s][w].y;
+            pr += wpairs[s][w];
         }
         blk_cnt[(size_t)s * nblk + blockIdx.x] = t;
+        blk_pairs[(size_t)s * nblk + blockIdx.x] = pr;
     }
 }
 
 // One block per slice: exclusive scan of blk_cnt[s][:] in place; totals in
 // 64-bit (the host rejects batches whose totals exceed the 31-bit budget).
 __global__ void __launch_bounds__(1024)
-prepare_scan_kernel(uint2 *__restrict__ blk_cnt, int nblk,
+prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
+                    const unsigned *__restrict__ blk_pairs, int nblk,
                     unsigned long long *__restrict__ slice_tot) {
-    __shared__ unsigned long long wx[32], wy[32];
+    __shared__ unsigned long long wx[32], wy[32], wp[32];
     __shared__ unsigned long long carry_x, carry_y;
+    {   // total (pairs) of this slice: plain reduction, fixed order
+        unsigned long long acc = 0;
+        for (int i = threadIdx.x; i < nblk; i += blockDim.x)
+            acc += blk_pairs[(size_t)blockIdx.x * nblk + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < 32; ++w) t += wp[w];
+            slice_tot[3 * blockIdx.x + 2] = t;
+        }
+    }
     const int s = blockIdx.x;
     uint2 *row = blk_cnt + (size_t)s * nblk;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,8 +138,8 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt, int nblk,
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        slice_tot[2 * s] = carry_x;
-        slice_tot[2 * s + 1] = carry_y;
+        slice_tot[3 * s] = carry_x;
+        slice_tot[3 * s + 1] = carry_y;
     }
 }
 
@@ -201,16 +226,17 @@ prepare_emit_kernel(const float *__restrict__ means,
 }  // namespace
 
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
-                         uint2 *blk_cnt, int nblk, cudaStream_t st) {
+                         uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
+                         cudaStream_t st) {
     prepare_count_kernel<<<nblk, kPrepThreads, 0, st>>>(
-        c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, nblk);
+        c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk);
     UGS_LAUNCH_CHECK("prepare_count_kernel");
     return UGS_OK;
 }
 
-int launch_prepare_scan(uint2 *blk_cnt, int S, int nblk,
+int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st) {
-    prepare_scan_kernel<<<S, 1024, 0, st>>>(blk_cnt, nblk, slice_tot);
+    prepare_scan_kernel<<<S, 1024, 0, st>>>(blk_cnt, blk_pairs, nblk, slice_tot);
     UGS_LAUNCH_CHECK("prepare_scan_kernel");
     return UGS_OK;
 }

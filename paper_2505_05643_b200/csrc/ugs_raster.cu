@@ -168,8 +168,8 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                 const int2 *__restrict__ bin_range,
                 const ugs_slice *__restrict__ slices,
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
-                const float *__restrict__ dpix, float *__restrict__ partial,
-                float2 *__restrict__ bin_bg) {
+                const float *__restrict__ dpix, const double *__restrict__ bg_raw,
+                float *__restrict__ partial, float2 *__restrict__ bin_bg) {
     constexpr int kWarps = kRasterThreads / 32;
     __shared__ float4 s0[kBwdBatch], s1[kBwdBatch], s2[kBwdBatch];
     __shared__ uint32_t s_inst[kBwdBatch];
@@ -184,16 +184,19 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
     // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
-    float G = 0.f, Gc = 0.f;
+    float G = 0.f, Gc = 0.f, Gb = 0.f;
     if (pc.u < sl.width && pc.v < sl.height) {
         const int64_t p = sl.pix_base + (int64_t)pc.v * sl.width + pc.u;
         const float ssum = den_in[p];
         const float chat = __fdiv_rn(num_in[p], ssum);
         G = __fdiv_rn(dpix[p], ssum);
         Gc = G * chat;
+        // background opacity term dpix*(c_bg - chat)/ssum, formed per pixel
+        // as the reference does (gradients.py:110) to avoid cancellation
+        Gb = G * ((float)sigmoid_f64(bg_raw[0]) - chat);
     }
-    {   // background partials of this tile (sum G, sum G*chat), fixed order
-        float a = G, c = Gc;
+    {   // background partials of this tile (sum G, sum G*(c_bg-chat)), fixed order
+        float a = G, c = Gb;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -367,9 +370,9 @@ __global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg, int tile_b
     }
     if (threadIdx.x == 0) {
         const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
-        const double sumG = sa[0], sumGc = sc_[0];
+        const double sumG = sa[0], sumGb = sc_[0];
         const double d_cbg = (double)(float)abg * sumG;   // sum dpix*f32(a_bg)/ssum
-        const double d_abg = (double)(float)cbg * sumG - sumGc;
+        const double d_abg = sumGb;                       // sum dpix*(c_bg-chat)/ssum
         grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
         grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
     }
@@ -381,9 +384,11 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
     dim3 grid(p.max_tiles, p.S);
+    stage_begin(const_cast<ugs_plan *>(&p), kStageForward, st);
     forward_kernel<<<grid, kRasterThreads, 0, st>>>(
         p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
     UGS_LAUNCH_CHECK("forward_kernel");
+    stage_end(const_cast<ugs_plan *>(&p), kStageForward, st);
     return UGS_OK;
 }
 
@@ -393,10 +398,14 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
     dim3 grid(p.max_tiles, p.S);
+    ugs_plan *pm = const_cast<ugs_plan *>(&p);
+    stage_begin(pm, kStageBackward, st);
     backward_kernel<<<grid, kRasterThreads, 0, st>>>(
         p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, num, den, dpix,
-        p.b.partial, p.b.bin_bg);
+        c.bg_raw, p.b.partial, p.b.bin_bg);
     UGS_LAUNCH_CHECK("backward_kernel");
+    stage_end(pm, kStageBackward, st);
+    stage_begin(pm, kStageFinalize, st);
     for (int s = 0; s < p.S; ++s) {
         const int64_t r0 = p.h_slice_base[2 * s];
         const int64_t m = p.h_m[s];
@@ -416,6 +425,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                                               grad + 11 * c.n, scale);
         UGS_LAUNCH_CHECK("bg_finalize_kernel");
     }
+    stage_end(pm, kStageFinalize, st);
     return UGS_OK;
 }
 

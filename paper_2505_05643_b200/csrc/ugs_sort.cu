@@ -127,9 +127,11 @@ int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
         return UGS_ERR_RANGE;
     }
     scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, tmp);
+    UGS_LAUNCH_CHECK("scan_reduce_kernel");
     scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
+    UGS_LAUNCH_CHECK("scan_sums_kernel");
     scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, tmp);
-    UGS_LAUNCH_CHECK("exclusive_scan");
+    UGS_LAUNCH_CHECK("scan_down_kernel");
     return UGS_OK;
 }
 

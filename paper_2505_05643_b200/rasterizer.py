@@ -77,9 +77,11 @@ class Renderer:
                 pix += spec.width * spec.height
         m = (ctypes.c_int64 * S)()
         k = (ctypes.c_int64 * S)()
+        pp = (ctypes.c_int64 * S)()
         cs = cloud.c_struct()
         _lib.check(_lib.lib().ugs_bin(self._plan, ctypes.byref(cs), slices, S,
-                                      _stream(), m, k), "ugs_bin")
+                                      _stream(), m, k, pp), "ugs_bin")
+        self.pairs = np.frombuffer(pp, np.int64).copy()
         self._slices = slices
         self.S = S
         self.m = np.frombuffer(m, np.int64).copy()
@@ -131,6 +133,20 @@ class Renderer:
         _lib.check(L.ugs_export_bins(self._plan, rng.data_ptr(), srt.data_ptr(),
                                      None, None, _stream()), "ugs_export_bins")
         return rng[:nb.value], srt[:kt.value]
+
+    def set_timing(self, enabled: bool = True):
+        _lib.check(_lib.lib().ugs_plan_set_timing(self._plan, int(enabled)),
+                   "ugs_plan_set_timing")
+
+    def timings(self, reset: bool = False) -> dict:
+        """{stage: (total ms, calls)} accumulated since the last reset."""
+        n = len(_lib.STAGES)
+        ms = (ctypes.c_double * n)()
+        calls = (ctypes.c_int64 * n)()
+        rc = _lib.lib().ugs_plan_timings(self._plan, ms, calls, n, int(reset))
+        if rc < 0:
+            _lib.check(rc, "ugs_plan_timings")
+        return {name: (ms[i], calls[i]) for i, name in enumerate(_lib.STAGES)}
 
     def slice_info(self):
         """Per slice: (tiles_x, tiles_y, tile_base) as filled by ugs_bin."""

@@ -371,25 +371,54 @@ class TrainEngine:
             arr[j].pix_base = j * self.h * self.w
         return arr
 
-    def forward_loss(self, idx):
+    # optional CUDA-event instrumentation of the non-library parts of a step
+    profile = False
+    pairs_total = 0
+
+    def _mark(self, name):
+        if self.profile:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._events.setdefault(name, []).append(ev)
+
+    def event_times(self, reset=True):
+        """{name: total ms} between paired '<name>0'/'<name>1' marks."""
+        torch.cuda.synchronize()
+        out = {}
+        ev = getattr(self, "_events", {})
+        for k in list(ev):
+            if k.endswith("0"):
+                a, b = ev[k], ev.get(k[:-1] + "1", [])
+                out[k[:-1]] = (sum(x.elapsed_time(y) for x, y in zip(a, b)), len(b))
+        if reset:
+            self._events = {}
+        return out
+
+    def forward_loss(self, idx, targets_batch=None):
         """bin + forward + loss for the slices `idx` (this rank's batch)."""
         cfg = self.config
         B = len(idx)
         structs = self.batch_structs(idx)
         self.renderer.bin(self.cloud, [self.specs[i] for i in idx], cfg.p_mass, structs)
+        self.pairs_total += int(self.renderer.pairs.sum())
         num = torch.empty((B, self.h, self.w), dtype=torch.float32, device=self.cloud.device)
         den = torch.empty_like(num)
         self.renderer.forward(self.cloud, num, den)
+        self._mark("loss0")
         pred = num / den
-        tgt = self.targets[torch.as_tensor(np.asarray(idx), device=self.cloud.device)]
+        if targets_batch is None:
+            tgt = self.targets[torch.as_tensor(np.asarray(idx), device=self.cloud.device)]
+        else:
+            tgt = targets_batch
         lv, dpix = loss_batch(pred, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
+        self._mark("loss1")
         return num, den, pred, tgt, lv, dpix
 
-    def step(self, idx, it: int, check_finite: bool = True):
+    def step(self, idx, it: int, check_finite: bool = True, targets_batch=None):
         """One full training step; returns the mean loss (python float) when
         check_finite, else the device tensor."""
         cfg = self.config
-        num, den, pred, tgt, lv, dpix = self.forward_loss(idx)
+        num, den, pred, tgt, lv, dpix = self.forward_loss(idx, targets_batch)
         loss_t = lv.mean()
         if self.world_size > 1:
             torch.distributed.all_reduce(loss_t, group=self.pg)
@@ -404,9 +433,12 @@ class TrainEngine:
         self.renderer.backward(self.cloud, num, den, dpix.to(torch.float32).contiguous(),
                                self.grad, self.touched, scale)
         if self.world_size > 1:
+            self._mark("allreduce0")
             torch.distributed.all_reduce(self.grad, group=self.pg)
             torch.distributed.all_reduce(self.touched, op=torch.distributed.ReduceOp.MAX,
                                          group=self.pg)
+            self._mark("allreduce1")
+        self._mark("adam0")
         _lib.check(_lib.lib().ugs_grad_stats(
             self.grad.data_ptr(), self.cloud.n, self.touched.data_ptr(),
             self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
@@ -415,6 +447,7 @@ class TrainEngine:
         lrs = {"means": mean_lr(cfg, it), "l_raw": lr_g, "intensity_raw": lr_g,
                "opacity_raw": lr_g, "bg": lr_g}
         _adam_flat(self.state, self.cloud, self.grad, lrs, zero_grad=True)
+        self._mark("adam1")
         return loss_val if check_finite else loss_t
 
     def densify(self, rng, scene_extent, threshold, max_total):

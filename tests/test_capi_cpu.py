@@ -44,7 +44,7 @@ def test_error_path_without_gpu():
     """Invalid arguments are rejected before any CUDA call."""
     from paper_2505_05643_b200 import _lib
     L = _lib.load()
-    assert L.ugs_bin(None, None, None, 0, None, None, None) == -1
+    assert L.ugs_bin(None, None, None, 0, None, None, None, None) == -1
     assert b"S" in L.ugs_last_error() or b"plan" in L.ugs_last_error()
 
 
