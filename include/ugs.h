@@ -162,6 +162,14 @@ UGS_API int ugs_densify_apply(const ugs_cloud *src, const float *m_src,
                       float *opacity_raw, float *m_dst, float *v_dst,
                       void *stream);
 
+/* Forward accumulation order.  0 (default): each of the 8 warps of a tile
+ * accumulates its share of the tile's records into a private buffer and the
+ * buffers are summed in fixed order -- the reference's multi-worker scheme
+ * (rasterizer.py:157-173).  1: every pixel adds its Gaussians strictly in
+ * ascending index, the reference's sequential workers=1 order
+ * (_kernels.py:23-47).  Both are deterministic. */
+UGS_API int ugs_plan_set_ordered(ugs_plan *plan, int ordered);
+
 /* ---- diagnostics (no counterpart in the reference, which has no tracing:
  * SURVEY section 5) --------------------------------------------------- */
 

@@ -127,7 +127,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     PlanBuffers &b = p->b;
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.slice_tot, b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.hist, b.scan_tmp, b.bin_range,
+                    b.vals2, b.partial, b.rgrad, b.hist, b.scan_tmp, b.bin_range,
                     b.bin_bg};
     for (void *q : bufs)
         if (q) cudaFree(q);
@@ -235,6 +235,8 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.rec_gid, &b.rec_gid_cap, (size_t)m_total + 2, "alloc rec_gid")))
         return rc;
     if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)m_total + 2, "alloc rec_inst")))
+        return rc;
+    if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
     const size_t kneed = (size_t)k_total + 1;
     if (kneed > b.inst_cap || !b.owner) {
@@ -376,6 +378,12 @@ extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
 }
 
 extern "C" long long ugs_launch_count(void) { return g_launches.load(); }
+
+extern "C" int ugs_plan_set_ordered(ugs_plan *p, int ordered) {
+    if (!p) { set_error("ugs_plan_set_ordered: NULL plan"); return UGS_ERR_INVALID; }
+    p->ordered = ordered != 0;
+    return UGS_OK;
+}
 
 extern "C" int ugs_plan_set_timing(ugs_plan *p, int enabled) {
     if (!p) { set_error("ugs_plan_set_timing: NULL plan"); return UGS_ERR_INVALID; }

@@ -45,6 +45,8 @@ struct PlanBuffers {
     int32_t *rec_gid = nullptr;     // [M]
     int32_t *rec_inst = nullptr;    // [M+1] first instance of each record
     size_t rec_cap = 0, rec_gid_cap = 0, rec_inst_cap = 0;
+    float *rgrad = nullptr;         // [M][12] per-record raw gradients (backward)
+    size_t rgrad_cap = 0;
     // instances
     uint32_t *owner = nullptr;      // [K] record of each (unsorted) instance
     uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)
@@ -79,6 +81,7 @@ struct ugs_plan {
     int h_cap = 0;
     uint32_t *sorted_keys = nullptr; // point into b.keys/b.keys2
     uint32_t *sorted_vals = nullptr;
+    bool ordered = false;            // strict per-pixel ascending-index forward
     // optional per-stage CUDA-event timing (ugs_plan_set_timing)
     bool timing = false;
     bool ev_ready = false;

@@ -1,27 +1,36 @@
 // Tile-resident forward accumulation and backward for a batch of slices.
 //
-// One CTA per (slice, 16x16 tile); 8 warps, each owning an 8x4 pixel block
-// so a Gaussian whose window misses the warp's block is skipped with a
-// warp-uniform branch.  Gaussian records of the tile's sorted list are staged
-// through shared memory in batches; every pixel then walks the list in
-// ascending Gaussian order (the reference's sequential order, ref
-// _kernels.py:23-47), so each f32 accumulator sees the same sequence of adds.
+// One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted Gaussian list
+// (ascending Gaussian index, from the stable radix sort) is staged through
+// shared memory in batches; while staging, one thread per record clips the
+// record's pixel window to the tile and precomputes everything a pixel needs
+// (rectangle, division magic, centre offsets).
 //
 // Per pair the reference evaluates w = alpha exp(-q/2), q = |L^T(p - mu)|^2
-// (28 flops, float64).  Here the preprocess has conditioned the Gaussian on
-// the slice plane (ugs_geometry.cuh, PlaneForm): log2 w is a 2-D quadratic
-// in the pixel offset from the in-plane centre, so a pair costs 4 FADD +
-// 5 FMA + one MUFU ex2, with the centre split into integer + fraction to
-// avoid cancellation.
+// (28 flops, float64).  Phase 1 has conditioned each Gaussian on the slice
+// plane (ugs_geometry.cuh, PlaneForm): log2 w is a 2-D quadratic in the pixel
+// offset from the in-plane centre, so a pair costs 4 FADD + 5 FMA + one MUFU
+// ex2, with the centre split into integer + fraction to avoid cancellation.
 //
-// Backward: each pixel computes t = dw*w and G*w (G = dpix/ssum); the
-// per-Gaussian gradient needs only 7 weighted moments over the window
-// (sum G w, sum t, sum t dx, sum t dy, sum t dx^2, sum t dx dy, sum t dy^2),
-// reduced per warp with a transpose-reduce (9 shuffles for 8 values), then
-// across warps in fixed order, and written per tile instance.  A finalize
-// pass per slice sums a record's instance partials in order and applies the
-// closed-form chain to d_mu, d_L and the raw parameters (float64) -- no
-// atomics anywhere, so gradients are bitwise reproducible.
+// Forward ("record per warp"): warp w takes records w, w+8, ... of each
+// staged batch and sweeps the record's window-clipped rectangle 32 pixels at
+// a time (lane-strided, ~93% lane utilisation at the C3 footprint), adding
+// into a PRIVATE per-warp (num, den) tile buffer in shared memory; the 8
+// buffers are summed in fixed warp order at the end -- the reference's own
+// multi-worker scheme (private accumulators summed, rasterizer.py:157-173),
+// deterministic.  `forward_ordered_kernel` keeps the strict sequential
+// ascending-index order per pixel (ref _kernels.py:23-47), selectable with
+// ugs_plan_set_ordered.
+//
+// Backward (record per warp): the per-Gaussian gradient needs only 7 weighted
+// moments of the window (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
+// sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
+// registers while the warp sweeps the rectangle, then one warp
+// transpose-reduce (9 shuffles for 8 values) per record and one 32-byte
+// store per tile instance.  A finalize pass sums a record's instance partials
+// in order and applies the closed-form chain to d_mu, d_L and the raw
+// parameters (float64); slices are accumulated into the gradient in slice
+// order -- no atomics anywhere, so gradients are bitwise reproducible.
 #include "ugs_geometry.cuh"
 
 namespace ugs {
@@ -29,8 +38,8 @@ namespace ugs {
 namespace {
 
 constexpr int kRasterThreads = 256;
-constexpr int kFwdBatch = 256;
-constexpr int kBwdBatch = 128;
+constexpr int kWarps = kRasterThreads / 32;
+constexpr int kBatch = 256;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -38,40 +47,65 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-struct PixelCoord {
-    int u, v;       // absolute pixel
-    int wu0, wv0;   // warp block origin (8 x 4)
+__device__ __forceinline__ float sigmoid_bg(const double *bg_raw, int i) {
+    return (float)sigmoid_f64(bg_raw[i]);
+}
+
+// exact float of a small non-negative int: 2^23 + x
+__device__ __forceinline__ float big_float(int x) {
+    return __int_as_float(0x4B000000 | x);
+}
+
+// Stage one record for the record-per-warp kernels.  Layout in smem:
+//   sA = (C1x, C1y, cu_frac, cv_frac)  with  dx = (big_float(x) - C1x) - cu_frac
+//   sB = (A, B2, C, E0)                 log2 w = A dx^2 + B2 dx dy + C dy^2 + E0
+//   sC = (color, rect, magic, area)     rect = x0 | y0<<4 | (w-1)<<8 | (h-1)<<12
+//                                        (tile-local), magic = ceil(65536/w)
+__device__ __forceinline__ void stage_record(const Rec &R, int tu0, int tv0,
+                                             float4 &a, float4 &b, float4 &c) {
+    const int wu = __float_as_int(R.r2.y), wv = __float_as_int(R.r2.z);
+    const int x0 = max((wu & 0xffff) - tu0, 0), x1 = min((wu >> 16) - tu0, kTile - 1);
+    const int y0 = max((wv & 0xffff) - tv0, 0), y1 = min((wv >> 16) - tv0, kTile - 1);
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    // integer offset of the rectangle origin from the integer centre (exact)
+    const float offx = (float)(tu0 + x0) - R.r0.x;
+    const float offy = (float)(tv0 + y0) - R.r0.y;
+    a = make_float4(8388608.0f - offx, 8388608.0f - offy, R.r0.z, R.r0.w);
+    b = R.r1;
+    c = make_float4(R.r2.x, __int_as_float(x0 | (y0 << 4) | ((w - 1) << 8) | ((h - 1) << 12)),
+                    __int_as_float((65536 + w - 1) / w), __int_as_float(w * h));
+}
+
+struct PairGeom {
+    float dx, dy;
+    int pix;    // tile-local pixel index (row-major 16 x 16)
 };
 
-__device__ __forceinline__ PixelCoord pixel_of_thread(int tx, int ty) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    PixelCoord p;
-    p.wu0 = tx * kTile + (warp & 1) * 8;
-    p.wv0 = ty * kTile + (warp >> 1) * 4;
-    p.u = p.wu0 + (lane & 7);
-    p.v = p.wv0 + (lane >> 3);
-    return p;
+__device__ __forceinline__ PairGeom pair_geom(int k, const float4 &a, int rect,
+                                              int magic) {
+    const int x0 = rect & 15, y0 = (rect >> 4) & 15, w = ((rect >> 8) & 15) + 1;
+    const int y = (k * magic) >> 16;
+    const int x = k - y * w;
+    PairGeom g;
+    g.dx = (big_float(x) - a.x) - a.z;
+    g.dy = (big_float(y) - a.y) - a.w;
+    g.pix = (y0 + y) * kTile + x0 + x;
+    return g;
 }
 
-__device__ __forceinline__ bool warp_misses(int wu, int wv, const PixelCoord &p) {
-    const int iu0 = wu & 0xffff, iu1 = wu >> 16;
-    const int iv0 = wv & 0xffff, iv1 = wv >> 16;
-    return iu0 > p.wu0 + 7 || iu1 < p.wu0 || iv0 > p.wv0 + 3 || iv1 < p.wv0;
+__device__ __forceinline__ float pair_weight(const PairGeom &g, const float4 &b) {
+    const float e = fmaf(fmaf(b.x, g.dx, b.y * g.dy), g.dx, fmaf(b.z * g.dy, g.dy, b.w));
+    return ex2_approx(e);
 }
 
-__device__ __forceinline__ bool in_window(int wu, int wv, int u, int v) {
-    const int iu0 = wu & 0xffff, iu1 = wu >> 16;
-    const int iv0 = wv & 0xffff, iv1 = wv >> 16;
-    return (unsigned)(u - iu0) <= (unsigned)(iu1 - iu0) &&
-           (unsigned)(v - iv0) <= (unsigned)(iv1 - iv0);
-}
-
-__device__ __forceinline__ void bg_values(const double *bg_raw, float *abg,
-                                          float *cbg) {
-    // rasterize: alpha_bg = f32(sigmoid64(bg_opacity_raw)); num += alpha_bg *
-    // f32(sigmoid64(bg_intensity_raw)); den += alpha_bg (rasterizer.py:175-177)
-    *cbg = (float)sigmoid_f64(bg_raw[0]);
-    *abg = (float)sigmoid_f64(bg_raw[1]);
+__device__ __forceinline__ void load_rec(const Rec *__restrict__ rec,
+                                         const uint32_t *__restrict__ owner,
+                                         uint32_t inst, Rec &R) {
+    const uint32_t r = __ldg(owner + inst);
+    const float4 *src = reinterpret_cast<const float4 *>(rec + r);
+    R.r0 = __ldg(src);
+    R.r1 = __ldg(src + 1);
+    R.r2 = __ldg(src + 2);
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
@@ -81,53 +115,109 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
                float *__restrict__ den_out) {
-    __shared__ float4 s0[kFwdBatch], s1[kFwdBatch], s2[kFwdBatch];
-    __shared__ float sh_bg[2];
+    __shared__ float4 sA[kBatch], sB[kBatch], sC[kBatch];
+    __shared__ float2 acc[kWarps][kTile * kTile];
     const ugs_slice &sl = slices[blockIdx.y];
-    const int ntile = sl.tiles_x * sl.tiles_y;
     const int t = blockIdx.x;
-    if (t >= ntile) return;
-    const int tx = t % sl.tiles_x, ty = t / sl.tiles_x;
-    const PixelCoord pc = pixel_of_thread(tx, ty);
+    if (t >= sl.tiles_x * sl.tiles_y) return;
+    const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
-    if (threadIdx.x == 0) {
-        float a, c;
-        bg_values(bg_raw, &a, &c);
-        sh_bg[0] = a;
-        sh_bg[1] = c;
-    }
-    const float fu = (float)pc.u, fv = (float)pc.v;
-    float num = 0.f, den = 0.f;
-    for (int b0 = rg.x; b0 < rg.y; b0 += kFwdBatch) {
-        const int nb = min(kFwdBatch, rg.y - b0);
+    for (int i = threadIdx.x; i < kWarps * kTile * kTile; i += kRasterThreads)
+        (&acc[0][0])[i] = make_float2(0.f, 0.f);
+    float2 *my = acc[warp];
+    for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
+        const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
         if (threadIdx.x < nb) {
-            const uint32_t r = __ldg(owner + __ldg(vals + b0 + threadIdx.x));
-            const float4 *src = reinterpret_cast<const float4 *>(rec + r);
-            s0[threadIdx.x] = __ldg(src);
-            s1[threadIdx.x] = __ldg(src + 1);
-            s2[threadIdx.x] = __ldg(src + 2);
+            Rec R;
+            load_rec(rec, owner, __ldg(vals + b0 + threadIdx.x), R);
+            stage_record(R, tu0, tv0, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x]);
+        }
+        __syncthreads();
+        for (int j = warp; j < nb; j += kWarps) {
+            const float4 a = sA[j], b = sB[j], c = sC[j];
+            const int rect = __float_as_int(c.y), magic = __float_as_int(c.z);
+            const int area = __float_as_int(c.w);
+            for (int k = lane; k < area; k += 32) {
+                const PairGeom g = pair_geom(k, a, rect, magic);
+                const float w = pair_weight(g, b);
+                float2 v = my[g.pix];
+                v.x = fmaf(w, c.x, v.x);
+                v.y += w;
+                my[g.pix] = v;
+            }
+        }
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int u = tu0 + lx, v = tv0 + ly;
+    if (u < sl.width && v < sl.height) {
+        float n = 0.f, d = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            n += acc[w][threadIdx.x].x;
+            d += acc[w][threadIdx.x].y;
+        }
+        const float abg = sigmoid_bg(bg_raw, 1), cbg = sigmoid_bg(bg_raw, 0);
+        const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;
+        num_out[p] = n + abg * cbg;
+        den_out[p] = d + abg;
+    }
+}
+
+// Strict-order variant: every pixel walks the tile's list in ascending
+// Gaussian order, one f32 add per pair (the reference's sequential loop).
+__global__ void __launch_bounds__(kRasterThreads)
+forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
+                       const uint32_t *__restrict__ vals,
+                       const int2 *__restrict__ bin_range,
+                       const ugs_slice *__restrict__ slices,
+                       const double *__restrict__ bg_raw, float *__restrict__ num_out,
+                       float *__restrict__ den_out) {
+    __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
+    const ugs_slice &sl = slices[blockIdx.y];
+    const int t = blockIdx.x;
+    if (t >= sl.tiles_x * sl.tiles_y) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp owns an 8 x 4 block so whole warps skip records that miss it
+    const int wu0 = (t % sl.tiles_x) * kTile + (warp & 1) * 8;
+    const int wv0 = (t / sl.tiles_x) * kTile + (warp >> 1) * 4;
+    const int u = wu0 + (lane & 7), v = wv0 + (lane >> 3);
+    const int2 rg = bin_range[sl.tile_base + t];
+    const float fu = (float)u, fv = (float)v;
+    float num = 0.f, den = 0.f;
+    for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
+        const int nb = min(kBatch, rg.y - b0);
+        __syncthreads();
+        if (threadIdx.x < nb) {
+            Rec R;
+            load_rec(rec, owner, __ldg(vals + b0 + threadIdx.x), R);
+            s0[threadIdx.x] = R.r0;
+            s1[threadIdx.x] = R.r1;
+            s2[threadIdx.x] = R.r2;
         }
         __syncthreads();
         for (int j = 0; j < nb; ++j) {
             const float4 r2 = s2[j];
             const int wu = __float_as_int(r2.y), wv = __float_as_int(r2.z);
-            if (warp_misses(wu, wv, pc)) continue;
+            const int iu0 = wu & 0xffff, iu1 = wu >> 16, iv0 = wv & 0xffff, iv1 = wv >> 16;
+            if (iu0 > wu0 + 7 || iu1 < wu0 || iv0 > wv0 + 3 || iv1 < wv0) continue;
             const float4 r0 = s0[j], r1 = s1[j];
             const float dx = (fu - r0.x) - r0.z;
             const float dy = (fv - r0.y) - r0.w;
-            const float e = fmaf(fmaf(r1.x, dx, r1.y * dy), dx,
-                                 fmaf(r1.z * dy, dy, r1.w));
+            const float e = fmaf(fmaf(r1.x, dx, r1.y * dy), dx, fmaf(r1.z * dy, dy, r1.w));
             float w = ex2_approx(e);
-            w = in_window(wu, wv, pc.u, pc.v) ? w : 0.f;
+            const bool in = (unsigned)(u - iu0) <= (unsigned)(iu1 - iu0) &&
+                            (unsigned)(v - iv0) <= (unsigned)(iv1 - iv0);
+            w = in ? w : 0.f;
             num = fmaf(w, r2.x, num);
             den += w;
         }
     }
-    __syncthreads();
-    if (pc.u < sl.width && pc.v < sl.height) {
-        const float abg = sh_bg[0], cbg = sh_bg[1];
-        const int64_t p = sl.pix_base + (int64_t)pc.v * sl.width + pc.u;
+    if (u < sl.width && v < sl.height) {
+        const float abg = sigmoid_bg(bg_raw, 1), cbg = sigmoid_bg(bg_raw, 0);
+        const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;
         num_out[p] = num + abg * cbg;
         den_out[p] = den + abg;
     }
@@ -170,33 +260,31 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg) {
-    constexpr int kWarps = kRasterThreads / 32;
-    __shared__ float4 s0[kBwdBatch], s1[kBwdBatch], s2[kBwdBatch];
-    __shared__ uint32_t s_inst[kBwdBatch];
-    __shared__ float part[kWarps][kBwdBatch][8];
+    __shared__ float4 sA[kBatch], sB[kBatch], sC[kBatch];
+    __shared__ uint32_t s_inst[kBatch];
+    __shared__ float2 pix[kTile * kTile];   // (G, G*chat) per tile pixel
     __shared__ float2 s_bg[kWarps];
     const ugs_slice &sl = slices[blockIdx.y];
-    const int ntile = sl.tiles_x * sl.tiles_y;
     const int t = blockIdx.x;
-    if (t >= ntile) return;
-    const int tx = t % sl.tiles_x, ty = t / sl.tiles_x;
-    const PixelCoord pc = pixel_of_thread(tx, ty);
+    if (t >= sl.tiles_x * sl.tiles_y) return;
+    const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
-    // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
-    float G = 0.f, Gc = 0.f, Gb = 0.f;
-    if (pc.u < sl.width && pc.v < sl.height) {
-        const int64_t p = sl.pix_base + (int64_t)pc.v * sl.width + pc.u;
-        const float ssum = den_in[p];
-        const float chat = __fdiv_rn(num_in[p], ssum);
-        G = __fdiv_rn(dpix[p], ssum);
-        Gc = G * chat;
-        // background opacity term dpix*(c_bg - chat)/ssum, formed per pixel
-        // as the reference does (gradients.py:110) to avoid cancellation
-        Gb = G * ((float)sigmoid_f64(bg_raw[0]) - chat);
-    }
-    {   // background partials of this tile (sum G, sum G*(c_bg-chat)), fixed order
-        float a = G, c = Gb;
+    {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
+        const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
+        float G = 0.f, Gc = 0.f, Gb = 0.f;
+        if (u < sl.width && v < sl.height) {
+            const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;
+            const float ssum = den_in[p];
+            const float chat = __fdiv_rn(num_in[p], ssum);
+            G = __fdiv_rn(dpix[p], ssum);
+            Gc = G * chat;
+            // background opacity term dpix*(c_bg - chat)/ssum, per pixel as the
+            // reference forms it (gradients.py:110), no cancellation
+            Gb = G * (sigmoid_bg(bg_raw, 0) - chat);
+        }
+        pix[threadIdx.x] = make_float2(G, Gc);
+        float a = G, c = Gb;   // background partials of this tile, fixed order
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -204,56 +292,38 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
         }
         if (lane == 0) s_bg[warp] = make_float2(a, c);
     }
-    const float fu = (float)pc.u, fv = (float)pc.v;
-    for (int b0 = rg.x; b0 < rg.y; b0 += kBwdBatch) {
-        const int nb = min(kBwdBatch, rg.y - b0);
+    for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
+        const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
         if (threadIdx.x < nb) {
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
-            const uint32_t r = __ldg(owner + inst);
-            const float4 *src = reinterpret_cast<const float4 *>(rec + r);
-            s0[threadIdx.x] = __ldg(src);
-            s1[threadIdx.x] = __ldg(src + 1);
-            s2[threadIdx.x] = __ldg(src + 2);
+            Rec R;
+            load_rec(rec, owner, inst, R);
+            stage_record(R, tu0, tv0, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x]);
             s_inst[threadIdx.x] = inst;
         }
         __syncthreads();
-        for (int j = 0; j < nb; ++j) {
-            const float4 r2 = s2[j];
-            const int wu = __float_as_int(r2.y), wv = __float_as_int(r2.z);
-            if (warp_misses(wu, wv, pc)) {
-                if (lane < 8) part[warp][j][lane] = 0.f;
-                continue;
+        for (int j = warp; j < nb; j += kWarps) {
+            const float4 a = sA[j], b = sB[j], c = sC[j];
+            const int rect = __float_as_int(c.y), magic = __float_as_int(c.z);
+            const int area = __float_as_int(c.w);
+            float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int k = lane; k < area; k += 32) {
+                const PairGeom g = pair_geom(k, a, rect, magic);
+                const float w = pair_weight(g, b);
+                const float2 gp = pix[g.pix];
+                const float tq = fmaf(gp.x, c.x, -gp.y) * w;   // dw * w
+                const float tx = tq * g.dx, ty = tq * g.dy;
+                m[0] = fmaf(gp.x, w, m[0]);
+                m[1] += tq;
+                m[2] += tx;
+                m[3] += ty;
+                m[4] = fmaf(tx, g.dx, m[4]);
+                m[5] = fmaf(tx, g.dy, m[5]);
+                m[6] = fmaf(ty, g.dy, m[6]);
             }
-            const float4 r0 = s0[j], r1 = s1[j];
-            const float dx = (fu - r0.x) - r0.z;
-            const float dy = (fv - r0.y) - r0.w;
-            const float e = fmaf(fmaf(r1.x, dx, r1.y * dy), dx,
-                                 fmaf(r1.z * dy, dy, r1.w));
-            float w = ex2_approx(e);
-            w = in_window(wu, wv, pc.u, pc.v) ? w : 0.f;
-            const float tq = fmaf(G, r2.x, -Gc) * w;   // dw * w
-            const float tx_ = tq * dx, ty_ = tq * dy;
-            float a[8];
-            a[0] = G * w;
-            a[1] = tq;
-            a[2] = tx_;
-            a[3] = ty_;
-            a[4] = tx_ * dx;
-            a[5] = tx_ * dy;
-            a[6] = ty_ * dy;
-            a[7] = 0.f;
-            const float red = warp_reduce8(a);
-            if ((lane & 3) == 0) part[warp][j][lane >> 2] = red;
-        }
-        __syncthreads();
-        // fixed-order cross-warp sum, one (record, moment) per thread
-        for (int idx = threadIdx.x; idx < nb * 8; idx += kRasterThreads) {
-            const int j = idx >> 3, k = idx & 7;
-            float sacc = 0.f;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) sacc += part[w][j][k];
-            partial[(size_t)s_inst[j] * 8 + k] = sacc;
+            const float red = warp_reduce8(m);
+            if ((lane & 3) == 0) partial[(size_t)s_inst[j] * 8 + (lane >> 2)] = red;
         }
     }
     __syncthreads();
@@ -268,29 +338,36 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     }
 }
 
-// Per slice (launched in slice order): sum a record's instance partials in
-// order and chain to the raw parameters (ref gradients.py:84-103, moments ->
-// d_mu = Lambda V, d_L = -M L; see the file comment).
-__global__ void finalize_kernel(const Rec *__restrict__ rec,
-                                const int32_t *__restrict__ rec_gid,
-                                const int32_t *__restrict__ rec_inst,
-                                const float *__restrict__ partial,
-                                int64_t r_begin, int64_t r_end,
-                                const ugs_slice *__restrict__ slice,
-                                const float *__restrict__ means,
-                                const float *__restrict__ l_raw, float beta,
-                                int64_t n, float *__restrict__ grad,
-                                uint8_t *__restrict__ touched, float scale) {
-    const int64_t r = r_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= r_end) return;
-    const ugs_slice &sl = *slice;
-    double S[7] = {0, 0, 0, 0, 0, 0, 0};
+// All records of the batch in one launch: sum a record's instance partials
+// in order and chain to raw-parameter gradients (ref gradients.py:84-103):
+// with e* = e(centre), V = S0 e* + Sx du + Sy dv and
+// M = S0 e*e*^T + e* w^T + w e*^T + Sxx du du^T + Sxy (du dv^T + dv du^T)
+//     + Syy dv dv^T  (w = Sx du + Sy dv, dq = -t/2):
+//   d_mu = Lambda V,  d_L = -(M L) lower,  d_c = Tc,  d_a = S0 / alpha.
+// Writes 12 floats per record: [d_mu 3 | d_l_raw 6 | d_c_raw | d_a_raw | -].
+__global__ void finalize_records_kernel(const Rec *__restrict__ rec,
+                                        const int32_t *__restrict__ rec_gid,
+                                        const int32_t *__restrict__ rec_inst,
+                                        const float *__restrict__ partial,
+                                        int64_t m_total,
+                                        const int64_t *__restrict__ slice_base, int S,
+                                        const ugs_slice *__restrict__ slices,
+                                        const float *__restrict__ means,
+                                        const float *__restrict__ l_raw, float beta,
+                                        float *__restrict__ rgrad,
+                                        uint8_t *__restrict__ touched) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m_total) return;
+    int s = 0;
+    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    const ugs_slice &sl = slices[s];
+    double Sm[7] = {0, 0, 0, 0, 0, 0, 0};
     const int i0 = rec_inst[r], i1 = rec_inst[r + 1];
     for (int i = i0; i < i1; ++i) {
         const float4 pa = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8);
         const float4 pb = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8 + 4);
-        S[0] += pa.x; S[1] += pa.y; S[2] += pa.z; S[3] += pa.w;
-        S[4] += pb.x; S[5] += pb.y; S[6] += pb.z;
+        Sm[0] += pa.x; Sm[1] += pa.y; Sm[2] += pa.z; Sm[3] += pa.w;
+        Sm[4] += pb.x; Sm[5] += pb.y; Sm[6] += pb.z;
     }
     const int64_t g = rec_gid[r];
     const Rec R = rec[r];
@@ -303,9 +380,8 @@ __global__ void finalize_kernel(const Rec *__restrict__ rec,
     double es[3];
     for (int k = 0; k < 3; ++k)
         es[k] = ((double)sl.origin[k] - mu[k]) + cu * du[k] + cv * dv[k];
-    const double Tc = S[0], S0 = S[1], Sx = S[2], Sy = S[3], Sxx = S[4],
-                 Sxy = S[5], Syy = S[6];
-    // V = sum t e ;  Mm = sum t e e^T     (dq = -t/2)
+    const double Tc = Sm[0], S0 = Sm[1], Sx = Sm[2], Sy = Sm[3], Sxx = Sm[4],
+                 Sxy = Sm[5], Syy = Sm[6];
     double V[3], wv[3];
     for (int k = 0; k < 3; ++k) {
         wv[k] = Sx * du[k] + Sy * dv[k];
@@ -318,34 +394,51 @@ __global__ void finalize_kernel(const Rec *__restrict__ rec,
                        Sxx * du[i] * du[j] + Sxy * (du[i] * dv[j] + dv[i] * du[j]) +
                        Syy * dv[i] * dv[j];
     const double L[3][3] = {{f.L00, 0.0, 0.0}, {f.L10, f.L11, 0.0}, {f.L20, f.L21, f.L22}};
-    // Lambda = L L^T ; d_mu = Lambda V
     double LtV[3];
     for (int k = 0; k < 3; ++k) LtV[k] = L[0][k] * V[0] + L[1][k] * V[1] + L[2][k] * V[2];
-    double dmu[3];
-    for (int i = 0; i < 3; ++i) dmu[i] = L[i][0] * LtV[0] + L[i][1] * LtV[1] + L[i][2] * LtV[2];
-    // d_L = -(Mm L), lower entries
+    float *o = rgrad + (size_t)r * 12;
+    for (int i = 0; i < 3; ++i)
+        o[i] = (float)(L[i][0] * LtV[0] + L[i][1] * LtV[1] + L[i][2] * LtV[2]);
     auto dL = [&](int i, int j) {
         return -(Mm[i][0] * L[0][j] + Mm[i][1] * L[1][j] + Mm[i][2] * L[2][j]);
     };
     const float *lr = l_raw + 6 * g;
+    o[3] = (float)(dL(0, 0) * 2.0 * (double)lr[0]);   // L_jj = l_jj^2 + beta
+    o[4] = (float)(dL(1, 1) * 2.0 * (double)lr[1]);
+    o[5] = (float)(dL(2, 2) * 2.0 * (double)lr[2]);
+    o[6] = (float)dL(1, 0);
+    o[7] = (float)dL(2, 0);
+    o[8] = (float)dL(2, 1);
     const double c = R.r2.x, a = R.r2.w;
-    double gl[6];
-    gl[0] = dL(0, 0) * 2.0 * (double)lr[0];
-    gl[1] = dL(1, 1) * 2.0 * (double)lr[1];
-    gl[2] = dL(2, 2) * 2.0 * (double)lr[2];
-    gl[3] = dL(1, 0);
-    gl[4] = dL(2, 0);
-    gl[5] = dL(2, 1);
-    const double gc = Tc * c * (1.0 - c);
-    const double ga = S0 * (1.0 - a);   // (S0 / a) * a (1 - a)
-    const double sc = (double)scale;
-    float *gm = grad + 3 * g;
-    for (int k = 0; k < 3; ++k) gm[k] += (float)(sc * dmu[k]);
-    float *gL = grad + 3 * n + 6 * g;
-    for (int k = 0; k < 6; ++k) gL[k] += (float)(sc * gl[k]);
-    grad[9 * n + g] += (float)(sc * gc);
-    grad[10 * n + g] += (float)(sc * ga);
+    o[9] = (float)(Tc * c * (1.0 - c));
+    o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
+    o[11] = 0.f;
     if (touched) touched[g] = 1;
+}
+
+// One slice (launched in slice order): grad[g] += scale * rgrad[r].
+__global__ void accumulate_slice_kernel(const float *__restrict__ rgrad,
+                                        const int32_t *__restrict__ rec_gid,
+                                        int64_t r_begin, int64_t r_end, int64_t n,
+                                        float *__restrict__ grad, float scale) {
+    const int64_t r = r_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= r_end) return;
+    const int64_t g = rec_gid[r];
+    const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * 12);
+    const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+    float *gm = grad + 3 * g;
+    gm[0] += scale * q0.x;
+    gm[1] += scale * q0.y;
+    gm[2] += scale * q0.z;
+    float *gl = grad + 3 * n + 6 * g;
+    gl[0] += scale * q0.w;
+    gl[1] += scale * q1.x;
+    gl[2] += scale * q1.y;
+    gl[3] += scale * q1.z;
+    gl[4] += scale * q1.w;
+    gl[5] += scale * q2.x;
+    grad[9 * n + g] += scale * q2.y;
+    grad[10 * n + g] += scale * q2.z;
 }
 
 // Background gradients of one slice: sum over its tiles in order.
@@ -370,9 +463,8 @@ __global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg, int tile_b
     }
     if (threadIdx.x == 0) {
         const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
-        const double sumG = sa[0], sumGb = sc_[0];
-        const double d_cbg = (double)(float)abg * sumG;   // sum dpix*f32(a_bg)/ssum
-        const double d_abg = sumGb;                       // sum dpix*(c_bg-chat)/ssum
+        const double d_cbg = (double)(float)abg * sa[0];   // sum dpix*f32(a_bg)/ssum
+        const double d_abg = sc_[0];                       // sum dpix*(c_bg-chat)/ssum
         grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
         grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
     }
@@ -384,11 +476,18 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
     dim3 grid(p.max_tiles, p.S);
-    stage_begin(const_cast<ugs_plan *>(&p), kStageForward, st);
-    forward_kernel<<<grid, kRasterThreads, 0, st>>>(
-        p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
-    UGS_LAUNCH_CHECK("forward_kernel");
-    stage_end(const_cast<ugs_plan *>(&p), kStageForward, st);
+    ugs_plan *pm = const_cast<ugs_plan *>(&p);
+    stage_begin(pm, kStageForward, st);
+    if (p.ordered) {
+        forward_ordered_kernel<<<grid, kRasterThreads, 0, st>>>(
+            p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+        UGS_LAUNCH_CHECK("forward_ordered_kernel");
+    } else {
+        forward_kernel<<<grid, kRasterThreads, 0, st>>>(
+            p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+        UGS_LAUNCH_CHECK("forward_kernel");
+    }
+    stage_end(pm, kStageForward, st);
     return UGS_OK;
 }
 
@@ -406,20 +505,22 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
     stage_begin(pm, kStageFinalize, st);
+    if (p.m_total > 0) {
+        const int th = 128;
+        finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
+            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base,
+            p.S, p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad, touched);
+        UGS_LAUNCH_CHECK("finalize_records_kernel");
+    }
     for (int s = 0; s < p.S; ++s) {
         const int64_t r0 = p.h_slice_base[2 * s];
         const int64_t m = p.h_m[s];
         if (m > 0) {
-            const int th = 128;
-            finalize_kernel<<<(unsigned)((m + th - 1) / th), th, 0, st>>>(
-                p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, r0, r0 + m,
-                p.b.slices + s, c.means, c.l_raw, (float)c.beta, c.n, grad, touched,
-                scale);
-            UGS_LAUNCH_CHECK("finalize_kernel");
+            const int th = 256;
+            accumulate_slice_kernel<<<(unsigned)((m + th - 1) / th), th, 0, st>>>(
+                p.b.rgrad, p.b.rec_gid, r0, r0 + m, c.n, grad, scale);
+            UGS_LAUNCH_CHECK("accumulate_slice_kernel");
         }
-    }
-    // background grads need the per-slice tile counts: read from the host copy
-    for (int s = 0; s < p.S; ++s) {
         bg_finalize_kernel<<<1, 256, 0, st>>>(p.b.bin_bg, p.h_tile_base[s],
                                               p.h_ntile[s], c.bg_raw,
                                               grad + 11 * c.n, scale);

@@ -134,6 +134,12 @@ class Renderer:
                                      None, None, _stream()), "ugs_export_bins")
         return rng[:nb.value], srt[:kt.value]
 
+    def set_ordered(self, ordered: bool = True):
+        """Strict per-pixel ascending-index accumulation (the reference's
+        workers=1 order) instead of per-warp private buffers."""
+        _lib.check(_lib.lib().ugs_plan_set_ordered(self._plan, int(ordered)),
+                   "ugs_plan_set_ordered")
+
     def set_timing(self, enabled: bool = True):
         _lib.check(_lib.lib().ugs_plan_set_timing(self._plan, int(enabled)),
                    "ugs_plan_set_timing")
