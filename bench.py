@@ -291,10 +291,12 @@ def run_ours(a):
     sampler.start()
     l0 = _lib.lib().ugs_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")      # ncu --nvtx-include "timed/"
     e0.record()
     for _ in range(a.steps):
         step()
     e1.record()
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     launches = _lib.lib().ugs_launch_count() - l0
     clocks = sampler.stop()

@@ -33,6 +33,7 @@
 #ifndef UGS_H
 #define UGS_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -161,6 +162,18 @@ UGS_API int ugs_densify_apply(const ugs_cloud *src, const float *m_src,
                       float *means, float *l_raw, float *intensity_raw,
                       float *opacity_raw, float *m_dst, float *v_dst,
                       void *stream);
+
+/* Training loss for S slices of H x W (ref trainer.py:130-151,
+ * metrics.py:23-98), float64 arithmetic: pred = f32(num/den);
+ * loss[s] = (1-lam)*mean|pred-target| + lam*(1 - SSIM)  (or mean squared
+ * error if l2 != 0) and d_pixels = d loss / d pred (float32, (S,H,W)).
+ * loss_out / ssim_out (dev, S doubles) may be NULL.  `workspace` (dev) must
+ * hold ugs_loss_workspace_bytes(S, H, W).  Deterministic. */
+UGS_API size_t ugs_loss_workspace_bytes(int S, int H, int W);
+UGS_API int ugs_loss(const float *num, const float *den, const float *target,
+                     int S, int H, int W, double lam, int l2, float *d_pixels,
+                     double *loss_out, double *ssim_out, void *workspace,
+                     void *stream);
 
 /* Forward accumulation order.  0 (default): each of the 8 warps of a tile
  * accumulates its share of the tile's records into a private buffer and the

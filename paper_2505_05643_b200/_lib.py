@@ -71,6 +71,11 @@ EXPORTS = {
     "ugs_fp32_peak_probe": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "ugs_plan_set_timing": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "ugs_plan_set_ordered": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "ugs_loss_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int]),
+    "ugs_loss": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int, ctypes.c_double, ctypes.c_int, c_vp,
+                                c_vp, c_vp, c_vp, c_vp]),
     "ugs_plan_timings": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(c_i64), ctypes.c_int,
                                         ctypes.c_int]),

@@ -1,0 +1,285 @@
+// Fused training loss: (1-lam)*L1 + lam*(1-SSIM) and its pixel gradient for
+// a batch of slices (ref trainer.py:130-151, metrics.py:23-98), float64 like
+// the reference, in two launches.
+//
+// SSIM: 11x11 Gaussian window (sigma 1.5), C1 = 1e-4, C2 = 9e-4, valid
+// windows only.  Its gradient is adj(A) + 2x adj(B) + y adj(C) with
+// A = dS/dmu - 2 mu_x dS/dsxx - mu_y dS/dsxy, B = dS/dsxx, C = dS/dsxy on the
+// valid grid and adj() the zero-padded full correlation (the adjoint of the
+// valid filter).  One CTA owns a 32x32 output tile: it loads the 52x52 input
+// neighbourhood, filters the five moments (x, y, x^2, y^2, xy) separably onto
+// the 42x42 valid points it needs, forms A, B, C there, applies the adjoint
+// separably back onto its 32x32 pixels and writes d_pixels (float32, what
+// the backward consumes -- gradients.py:62 casts the same way).  Per-tile
+// sums (sum|diff| over owned pixels, sum SSIM over owned valid points) are
+// reduced per slice in fixed order by a second tiny kernel: deterministic.
+#include "ugs_internal.cuh"
+
+namespace ugs {
+namespace {
+
+constexpr int kLT = 32;              // output tile
+constexpr int kPad = 5;              // window radius
+constexpr int kF = kLT + 2 * kPad;   // 42: valid points needed
+constexpr int kI = kF + 2 * kPad;    // 52: input points needed
+constexpr int kLossThreads = 512;
+
+__constant__ double c_win[11];
+
+struct LossSmem {
+    double X[kI][kI];                 // prediction (f64 of f32 num/den)
+    double Y[kI][kI];                 // target
+    union {
+        double h[5][kI][kF];          // horizontal moment pass
+        double ha[3][kF][kLT];        // horizontal adjoint pass
+    } u;
+    double F[3][kF][kF];              // A, B, C on the valid grid
+    double red[2][kLossThreads / 32];
+};
+
+__global__ void __launch_bounds__(kLossThreads)
+loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
+                 const float *__restrict__ target, int H, int W, double lam,
+                 int l2, float *__restrict__ dpix, double *__restrict__ tile_sums,
+                 int tiles_x, int tiles_per_slice) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LossSmem &sm = *reinterpret_cast<LossSmem *>(smem_raw);
+    const int s = blockIdx.y;
+    const int tile = blockIdx.x;
+    const int p0 = (tile / tiles_x) * kLT, q0 = (tile % tiles_x) * kLT;
+    const size_t base = (size_t)s * H * W;
+    const int tid = threadIdx.x;
+    const int HV = H - 2 * kPad, WV = W - 2 * kPad;   // valid grid
+    const double npx = (double)H * W, nv = (double)HV * WV;
+    // load the 52x52 neighbourhood (rows p0-10 .., cols q0-10 ..)
+    for (int i = tid; i < kI * kI; i += kLossThreads) {
+        const int r = i / kI, c = i % kI;
+        const int P = p0 - 2 * kPad + r, Q = q0 - 2 * kPad + c;
+        double x = 0.0, y = 0.0;
+        if (P >= 0 && P < H && Q >= 0 && Q < W) {
+            const size_t o = base + (size_t)P * W + Q;
+            x = (double)__fdiv_rn(num[o], den[o]);   // pred = num / den (float32)
+            y = (double)target[o];
+        }
+        sm.X[r][c] = x;
+        sm.Y[r][c] = y;
+    }
+    __syncthreads();
+    double ssim_sum = 0.0;
+    const bool ssim = !l2 && lam > 0.0;
+    if (ssim) {
+        // horizontal pass: h[f][r][c] = sum_b w[b] f(r, c+b), c in [0,42)
+        for (int i = tid; i < kI * kF; i += kLossThreads) {
+            const int r = i / kF, c = i % kF;
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+            for (int b = 0; b < 11; ++b) {
+                const double w = c_win[b], x = sm.X[r][c + b], y = sm.Y[r][c + b];
+                a0 += w * x;
+                a1 += w * y;
+                a2 += w * x * x;
+                a3 += w * y * y;
+                a4 += w * x * y;
+            }
+            sm.u.h[0][r][c] = a0;
+            sm.u.h[1][r][c] = a1;
+            sm.u.h[2][r][c] = a2;
+            sm.u.h[3][r][c] = a3;
+            sm.u.h[4][r][c] = a4;
+        }
+        __syncthreads();
+        // vertical pass -> moments at valid point (i, j) = (p0-10+r, q0-10+c)
+        for (int k = tid; k < kF * kF; k += kLossThreads) {
+            const int r = k / kF, c = k % kF;
+            const int i = p0 - 2 * kPad + r, j = q0 - 2 * kPad + c;
+            double A = 0, B = 0, C = 0;
+            if (i >= 0 && i < HV && j >= 0 && j < WV) {
+                double m[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+                for (int a = 0; a < 11; ++a) {
+                    const double w = c_win[a];
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) m[f] += w * sm.u.h[f][r + a][c];
+                }
+                const double mx = m[0], my = m[1];
+                const double sxx = m[2] - mx * mx, syy = m[3] - my * my;
+                const double sxy = m[4] - mx * my;
+                const double C1 = 1e-4, C2 = 9e-4;
+                const double a1 = 2.0 * mx * my + C1, a2 = 2.0 * sxy + C2;
+                const double b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
+                const double sv = (a1 * a2) / (b1 * b2);
+                const double d_mu = (2.0 * my * a2) / (b1 * b2) -
+                                    (2.0 * mx * a1 * a2) / (b1 * b1 * b2);
+                const double d_sxx = -sv / b2, d_sxy = 2.0 * a1 / (b1 * b2);
+                A = d_mu - 2.0 * mx * d_sxx - my * d_sxy;
+                B = d_sxx;
+                C = d_sxy;
+                if (r >= 2 * kPad && c >= 2 * kPad) ssim_sum += sv;   // owned point
+            }
+            sm.F[0][r][c] = A;
+            sm.F[1][r][c] = B;
+            sm.F[2][r][c] = C;
+        }
+        __syncthreads();
+        // adjoint horizontal: ha[f][r][q] = sum_b w[b] F[f][r][q+b], q in [0,32)
+        for (int i = tid; i < 3 * kF * kLT; i += kLossThreads) {
+            const int f = i / (kF * kLT), rem = i % (kF * kLT);
+            const int r = rem / kLT, q = rem % kLT;
+            double a = 0;
+#pragma unroll
+            for (int b = 0; b < 11; ++b) a += c_win[b] * sm.F[f][r][q + b];
+            sm.u.ha[f][r][q] = a;
+        }
+        __syncthreads();
+    }
+    // pixels of this tile: gradient and L1 term
+    double l1_sum = 0.0;
+    for (int k = tid; k < kLT * kLT; k += kLossThreads) {
+        const int p = k / kLT, q = k % kLT;
+        const int P = p0 + p, Q = q0 + q;
+        if (P >= H || Q >= W) continue;
+        const double x = sm.X[p + 2 * kPad][q + 2 * kPad];
+        const double y = sm.Y[p + 2 * kPad][q + 2 * kPad];
+        const double diff = x - y;
+        double g;
+        if (l2) {
+            l1_sum += diff * diff;
+            g = 2.0 * diff / npx;
+        } else {
+            l1_sum += fabs(diff);
+            const double sg = (diff > 0.0) ? 1.0 : ((diff < 0.0) ? -1.0 : 0.0);
+            g = (1.0 - lam) * sg / npx;
+            if (ssim) {
+                double aA = 0, aB = 0, aC = 0;
+#pragma unroll
+                for (int a = 0; a < 11; ++a) {
+                    const double w = c_win[a];
+                    aA += w * sm.u.ha[0][p + a][q];
+                    aB += w * sm.u.ha[1][p + a][q];
+                    aC += w * sm.u.ha[2][p + a][q];
+                }
+                g -= lam * (aA + 2.0 * x * aB + y * aC) / nv;
+            }
+        }
+        dpix[base + (size_t)P * W + Q] = (float)g;
+    }
+    // block sums in fixed order
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
+        ssim_sum += __shfl_xor_sync(0xffffffffu, ssim_sum, o);
+    }
+    if (lane == 0) {
+        sm.red[0][warp] = l1_sum;
+        sm.red[1][warp] = ssim_sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0, b = 0;
+        for (int w = 0; w < kLossThreads / 32; ++w) {
+            a += sm.red[0][w];
+            b += sm.red[1][w];
+        }
+        tile_sums[2 * ((size_t)s * tiles_per_slice + tile)] = a;
+        tile_sums[2 * ((size_t)s * tiles_per_slice + tile) + 1] = b;
+    }
+}
+
+__global__ void loss_reduce_kernel(const double *__restrict__ tile_sums,
+                                   int tiles_per_slice, int H, int W, double lam,
+                                   int l2, double *__restrict__ loss_out,
+                                   double *__restrict__ ssim_out) {
+    const int s = blockIdx.x;
+    __shared__ double ra[256], rb[256];
+    double a = 0, b = 0;
+    for (int t = threadIdx.x; t < tiles_per_slice; t += blockDim.x) {
+        a += tile_sums[2 * ((size_t)s * tiles_per_slice + t)];
+        b += tile_sums[2 * ((size_t)s * tiles_per_slice + t) + 1];
+    }
+    ra[threadIdx.x] = a;
+    rb[threadIdx.x] = b;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            ra[threadIdx.x] += ra[threadIdx.x + o];
+            rb[threadIdx.x] += rb[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double npx = (double)H * W;
+        const double nv = (double)(H - 2 * kPad) * (W - 2 * kPad);
+        double v;
+        const double mean_s = rb[0] / nv;
+        if (l2) {
+            v = ra[0] / npx;
+        } else {
+            v = (1.0 - lam) * (ra[0] / npx);
+            if (lam > 0.0) v += lam * (1.0 - mean_s);
+        }
+        if (loss_out) loss_out[s] = v;
+        if (ssim_out) ssim_out[s] = mean_s;
+    }
+}
+
+bool g_win_ready = false;
+
+int upload_window() {
+    if (g_win_ready) return UGS_OK;
+    double w[11], sum = 0.0;
+    for (int i = 0; i < 11; ++i) {
+        const double x = (double)(i - kPad) / 1.5;
+        w[i] = exp(-0.5 * x * x);
+        sum += w[i];
+    }
+    for (int i = 0; i < 11; ++i) w[i] /= sum;
+    UGS_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof(w)));
+    g_win_ready = true;
+    return UGS_OK;
+}
+
+}  // namespace
+}  // namespace ugs
+
+using namespace ugs;
+
+extern "C" size_t ugs_loss_workspace_bytes(int S, int H, int W) {
+    const int tx = (W + kLT - 1) / kLT, ty = (H + kLT - 1) / kLT;
+    return sizeof(double) * 2 * (size_t)S * tx * ty;
+}
+
+extern "C" int ugs_loss(const float *num, const float *den, const float *target,
+                        int S, int H, int W, double lam, int l2, float *d_pixels,
+                        double *loss_out, double *ssim_out, void *workspace,
+                        void *stream) {
+    if (!num || !den || !target || !d_pixels || !workspace || S < 1 || H < 1 || W < 1) {
+        set_error("ugs_loss: invalid arguments");
+        return UGS_ERR_INVALID;
+    }
+    if (!l2 && lam > 0.0 && (H < 11 || W < 11)) {
+        set_error("ugs_loss: images must be at least 11x11 for SSIM");
+        return UGS_ERR_INVALID;
+    }
+    int rc = upload_window();
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int tx = (W + kLT - 1) / kLT, ty = (H + kLT - 1) / kLT;
+    const size_t smem = sizeof(LossSmem);
+    static bool attr = false;
+    if (!attr) {
+        UGS_CUDA(cudaFuncSetAttribute(loss_tile_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+    }
+    dim3 grid(tx * ty, S);
+    double *sums = static_cast<double *>(workspace);
+    loss_tile_kernel<<<grid, kLossThreads, smem, st>>>(num, den, target, H, W, lam, l2,
+                                                       d_pixels, sums, tx, tx * ty);
+    UGS_LAUNCH_CHECK("loss_tile_kernel");
+    loss_reduce_kernel<<<S, 256, 0, st>>>(sums, tx * ty, H, W, lam, l2, loss_out,
+                                          ssim_out);
+    UGS_LAUNCH_CHECK("loss_reduce_kernel");
+    return UGS_OK;
+}

@@ -441,32 +441,39 @@ __global__ void accumulate_slice_kernel(const float *__restrict__ rgrad,
     grad[10 * n + g] += scale * q2.z;
 }
 
-// Background gradients of one slice: sum over its tiles in order.
-__global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg, int tile_base,
-                                   int ntile, const double *__restrict__ bg_raw,
+// Background gradients: one block walks the slices in order; per slice the
+// tile partials are tree-reduced in fixed order (gradients.py:106-112).
+__global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg,
+                                   const ugs_slice *__restrict__ slices, int S,
+                                   const double *__restrict__ bg_raw,
                                    float *__restrict__ grad_bg, float scale) {
     __shared__ double sa[256], sc_[256];
-    double a = 0.0, c = 0.0;
-    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
-        a += bin_bg[tile_base + i].x;
-        c += bin_bg[tile_base + i].y;
-    }
-    sa[threadIdx.x] = a;
-    sc_[threadIdx.x] = c;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            sa[threadIdx.x] += sa[threadIdx.x + o];
-            sc_[threadIdx.x] += sc_[threadIdx.x + o];
+    const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
+    for (int s = 0; s < S; ++s) {
+        const int tile_base = slices[s].tile_base;
+        const int ntile = slices[s].tiles_x * slices[s].tiles_y;
+        double a = 0.0, c = 0.0;
+        for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+            a += bin_bg[tile_base + i].x;
+            c += bin_bg[tile_base + i].y;
+        }
+        sa[threadIdx.x] = a;
+        sc_[threadIdx.x] = c;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+                sa[threadIdx.x] += sa[threadIdx.x + o];
+                sc_[threadIdx.x] += sc_[threadIdx.x + o];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const double d_cbg = (double)(float)abg * sa[0];   // sum dpix*f32(a_bg)/ssum
+            const double d_abg = sc_[0];                       // sum dpix*(c_bg-chat)/ssum
+            grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
+            grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
         }
         __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
-        const double d_cbg = (double)(float)abg * sa[0];   // sum dpix*f32(a_bg)/ssum
-        const double d_abg = sc_[0];                       // sum dpix*(c_bg-chat)/ssum
-        grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
-        grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
     }
 }
 
@@ -521,11 +528,10 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                 p.b.rgrad, p.b.rec_gid, r0, r0 + m, c.n, grad, scale);
             UGS_LAUNCH_CHECK("accumulate_slice_kernel");
         }
-        bg_finalize_kernel<<<1, 256, 0, st>>>(p.b.bin_bg, p.h_tile_base[s],
-                                              p.h_ntile[s], c.bg_raw,
-                                              grad + 11 * c.n, scale);
-        UGS_LAUNCH_CHECK("bg_finalize_kernel");
     }
+    bg_finalize_kernel<<<1, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.S, c.bg_raw,
+                                          grad + 11 * c.n, scale);
+    UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
 }

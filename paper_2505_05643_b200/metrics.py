@@ -131,6 +131,37 @@ def psnr(a, b) -> float:
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
+_WS: dict = {}
+
+
+def fused_loss(num: torch.Tensor, den: torch.Tensor, target: torch.Tensor,
+               lam: float, l2: bool = False):
+    """Training loss straight from the render accumulators, one fused CUDA
+    pass (ugs_loss): pred = num/den, (1-lam)*L1 + lam*(1-SSIM) per slice.
+
+    num, den, target: (S, H, W) float32 on the device.  Returns
+    (loss (S,) float64, d_pixels (S, H, W) float32, ssim (S,) float64)."""
+    import ctypes
+    from . import _lib
+    S, H, W = num.shape
+    L = _lib.lib()
+    nbytes = L.ugs_loss_workspace_bytes(S, H, W)
+    ws = _WS.get(num.device)
+    if ws is None or ws.numel() < nbytes:
+        ws = _WS[num.device] = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8,
+                                           device=num.device)
+    dpix = torch.empty((S, H, W), dtype=torch.float32, device=num.device)
+    lv = torch.empty(S, dtype=torch.float64, device=num.device)
+    sv = torch.empty(S, dtype=torch.float64, device=num.device)
+    tgt = target.to(dtype=torch.float32).contiguous()
+    _lib.check(L.ugs_loss(num.data_ptr(), den.data_ptr(), tgt.data_ptr(), S, H, W,
+                          float(lam), int(bool(l2)), dpix.data_ptr(), lv.data_ptr(),
+                          sv.data_ptr(), ws.data_ptr(),
+                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "ugs_loss")
+    return lv, dpix, sv
+
+
 def loss_batch(pred, target, lam: float, l2: bool = False):
     """Per-image training loss and its pixel gradient (ref trainer.py:130-151).
 

@@ -33,7 +33,7 @@ from . import _lib
 from .dataset import SliceDataset
 from .geometry import InvalidParameterError, fill_slice
 from .gradients import ParamGradients, grad_buffer
-from .metrics import loss_batch, ssim_batch
+from .metrics import fused_loss, ssim_batch
 from .metrics import loss as _loss
 from .model import GaussianCloud
 from .rasterizer import Renderer, _stream
@@ -405,14 +405,13 @@ class TrainEngine:
         den = torch.empty_like(num)
         self.renderer.forward(self.cloud, num, den)
         self._mark("loss0")
-        pred = num / den
         if targets_batch is None:
             tgt = self.targets[torch.as_tensor(np.asarray(idx), device=self.cloud.device)]
         else:
             tgt = targets_batch
-        lv, dpix = loss_batch(pred, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
+        lv, dpix, _ = fused_loss(num, den, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
         self._mark("loss1")
-        return num, den, pred, tgt, lv, dpix
+        return num, den, None, tgt, lv, dpix
 
     def step(self, idx, it: int, check_finite: bool = True, targets_batch=None):
         """One full training step; returns the mean loss (python float) when
@@ -423,7 +422,7 @@ class TrainEngine:
         if self.world_size > 1:
             torch.distributed.all_reduce(loss_t, group=self.pg)
             loss_t = loss_t / self.world_size
-        self.last_pred, self.last_tgt = pred, tgt
+        self.last_num, self.last_den, self.last_tgt = num, den, tgt
         loss_val = None
         if check_finite:
             loss_val = float(loss_t.item())
@@ -511,7 +510,8 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
         if config.heuristic_interval > 0 and it % config.heuristic_interval == 0:
             threshold = eng.densify(rng, scene_extent, threshold, max_total)
         if it % config.eval_interval == 0 or it == config.iterations:
-            s = ssim_batch(torch.clamp(eng.last_pred[:1], 0, 1), eng.last_tgt[:1])
+            pred = eng.last_num[:1] / eng.last_den[:1]
+            s = ssim_batch(torch.clamp(pred, 0, 1), eng.last_tgt[:1])
             entry = {"iter": it, "wall_ms": (time.perf_counter() - t0) * 1000.0,
                      "loss": loss_val, "train_ssim": float(s[0])}
             log.append(entry)
