@@ -127,7 +127,8 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     PlanBuffers &b = p->b;
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.slice_tot, b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.rgrad, b.hist, b.scan_tmp, b.bin_range,
+                    b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.hist,
+                    b.scan_tmp, b.bin_range,
                     b.bin_bg};
     for (void *q : bufs)
         if (q) cudaFree(q);
@@ -238,6 +239,15 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
+    if ((rc = ensure(&b.chunk_lo, &b.chunk_lo_cap, chunk_lo_entries(S, c->n) + 1,
+                     "alloc chunk_lo")))
+        return rc;
+    {
+        size_t cap = b.slice_m ? 64 : 0;
+        if ((rc = ensure(&b.slice_m, &cap, (size_t)64, "alloc slice_m"))) return rc;
+    }
+    UGS_CUDA(cudaMemcpyAsync(b.slice_m, p->h_m, sizeof(int64_t) * S,
+                             cudaMemcpyHostToDevice, st));
     const size_t kneed = (size_t)k_total + 1;
     if (kneed > b.inst_cap || !b.owner) {
         void *olds[] = {b.owner, b.keys, b.vals, b.keys2, b.vals2, b.partial};

@@ -47,6 +47,9 @@ struct PlanBuffers {
     size_t rec_cap = 0, rec_gid_cap = 0, rec_inst_cap = 0;
     float *rgrad = nullptr;         // [M][12] per-record raw gradients (backward)
     size_t rgrad_cap = 0;
+    int64_t *slice_m = nullptr;     // [S] accepted records per slice
+    int32_t *chunk_lo = nullptr;    // [S][nchunk+1] record bounds per Gaussian chunk
+    size_t chunk_lo_cap = 0;
     // instances
     uint32_t *owner = nullptr;      // [K] record of each (unsorted) instance
     uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)
@@ -152,6 +155,7 @@ int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 
 // raster (ugs_raster.cu)
+size_t chunk_lo_entries(int S, int64_t n);
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st);
 int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,

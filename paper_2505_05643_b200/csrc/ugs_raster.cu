@@ -2,9 +2,11 @@
 //
 // One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted Gaussian list
 // (ascending Gaussian index, from the stable radix sort) is staged through
-// shared memory in batches; while staging, one thread per record clips the
-// record's pixel window to the tile and precomputes everything a pixel needs
-// (rectangle, division magic, centre offsets).
+// shared memory in batches of 256 records.  While staging, one thread per
+// record clips the record's pixel window to the tile and precomputes what a
+// pixel needs (rectangle, centre offsets); the batch is then ordered by the
+// record's pixel count with a stable counting sort, so the records a warp
+// processes together need the same number of sweeps.
 //
 // Per pair the reference evaluates w = alpha exp(-q/2), q = |L^T(p - mu)|^2
 // (28 flops, float64).  Phase 1 has conditioned each Gaussian on the slice
@@ -12,25 +14,26 @@
 // offset from the in-plane centre, so a pair costs 4 FADD + 5 FMA + one MUFU
 // ex2, with the centre split into integer + fraction to avoid cancellation.
 //
-// Forward ("record per warp"): warp w takes records w, w+8, ... of each
-// staged batch and sweeps the record's window-clipped rectangle 32 pixels at
-// a time (lane-strided, ~93% lane utilisation at the C3 footprint), adding
-// into a PRIVATE per-warp (num, den) tile buffer in shared memory; the 8
-// buffers are summed in fixed warp order at the end -- the reference's own
-// multi-worker scheme (private accumulators summed, rasterizer.py:157-173),
-// deterministic.  `forward_ordered_kernel` keeps the strict sequential
-// ascending-index order per pixel (ref _kernels.py:23-47), selectable with
-// ugs_plan_set_ordered.
-//
-// Backward (record per warp): the per-Gaussian gradient needs only 7 weighted
-// moments of the window (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
-// sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
-// registers while the warp sweeps the rectangle, then one warp
-// transpose-reduce (9 shuffles for 8 values) per record and one 32-byte
-// store per tile instance.  A finalize pass sums a record's instance partials
-// in order and applies the closed-form chain to d_mu, d_L and the raw
-// parameters (float64); slices are accumulated into the gradient in slice
-// order -- no atomics anywhere, so gradients are bitwise reproducible.
+// Work split ("record per 8-lane group"): each warp holds 4 groups of 8 lanes;
+// a group sweeps one record's clipped rectangle 8 pixels at a time (k -> (x,y)
+// from a shared 16x256 lookup table).
+//   Forward: each group adds into its own PRIVATE (num, den) tile buffer in
+//   shared memory; the 32 buffers are summed in fixed order at the end -- the
+//   reference's multi-worker scheme (private accumulators summed,
+//   rasterizer.py:157-173), deterministic because the record -> group
+//   assignment is a stable sort.  `forward_ordered_kernel` keeps the strict
+//   sequential ascending-index order per pixel (ref _kernels.py:23-47),
+//   selectable with ugs_plan_set_ordered.
+//   Backward: the per-Gaussian gradient needs only 7 weighted moments of the
+//   window (sum G w, sum t, sum t dx, sum t dy, sum t dx^2, sum t dx dy,
+//   sum t dy^2; G = dpix/ssum, t = dw w), accumulated in registers; one
+//   3-level transpose-reduce inside the group (7 shuffles for 8 values, shared
+//   by the warp's 4 records) leaves lane j of the group with moment j, and the
+//   group writes one 32-byte partial per tile instance.
+// A finalize pass sums a record's instance partials in order and applies the
+// closed-form chain to d_mu, d_L and the raw parameters (float64); slices are
+// then accumulated into the gradient in slice order by Gaussian-range blocks
+// -- no atomics anywhere, so gradients are bitwise reproducible.
 #include "ugs_geometry.cuh"
 
 namespace ugs {
@@ -40,6 +43,10 @@ namespace {
 constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
+constexpr int kGL = 8;                       // lanes per record group
+constexpr int kGroups = kRasterThreads / kGL;  // 32 groups per CTA
+constexpr int kMaxTrips = (kTile * kTile + kGL - 1) / kGL;   // 32
+constexpr int kAccStride = kTile * kTile + 8;  // private buffer stride (bank skew)
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -56,48 +63,6 @@ __device__ __forceinline__ float big_float(int x) {
     return __int_as_float(0x4B000000 | x);
 }
 
-// Stage one record for the record-per-warp kernels.  Layout in smem:
-//   sA = (C1x, C1y, cu_frac, cv_frac)  with  dx = (big_float(x) - C1x) - cu_frac
-//   sB = (A, B2, C, E0)                 log2 w = A dx^2 + B2 dx dy + C dy^2 + E0
-//   sC = (color, rect, magic, area)     rect = x0 | y0<<4 | (w-1)<<8 | (h-1)<<12
-//                                        (tile-local), magic = ceil(65536/w)
-__device__ __forceinline__ void stage_record(const Rec &R, int tu0, int tv0,
-                                             float4 &a, float4 &b, float4 &c) {
-    const int wu = __float_as_int(R.r2.y), wv = __float_as_int(R.r2.z);
-    const int x0 = max((wu & 0xffff) - tu0, 0), x1 = min((wu >> 16) - tu0, kTile - 1);
-    const int y0 = max((wv & 0xffff) - tv0, 0), y1 = min((wv >> 16) - tv0, kTile - 1);
-    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
-    // integer offset of the rectangle origin from the integer centre (exact)
-    const float offx = (float)(tu0 + x0) - R.r0.x;
-    const float offy = (float)(tv0 + y0) - R.r0.y;
-    a = make_float4(8388608.0f - offx, 8388608.0f - offy, R.r0.z, R.r0.w);
-    b = R.r1;
-    c = make_float4(R.r2.x, __int_as_float(x0 | (y0 << 4) | ((w - 1) << 8) | ((h - 1) << 12)),
-                    __int_as_float((65536 + w - 1) / w), __int_as_float(w * h));
-}
-
-struct PairGeom {
-    float dx, dy;
-    int pix;    // tile-local pixel index (row-major 16 x 16)
-};
-
-__device__ __forceinline__ PairGeom pair_geom(int k, const float4 &a, int rect,
-                                              int magic) {
-    const int x0 = rect & 15, y0 = (rect >> 4) & 15, w = ((rect >> 8) & 15) + 1;
-    const int y = (k * magic) >> 16;
-    const int x = k - y * w;
-    PairGeom g;
-    g.dx = (big_float(x) - a.x) - a.z;
-    g.dy = (big_float(y) - a.y) - a.w;
-    g.pix = (y0 + y) * kTile + x0 + x;
-    return g;
-}
-
-__device__ __forceinline__ float pair_weight(const PairGeom &g, const float4 &b) {
-    const float e = fmaf(fmaf(b.x, g.dx, b.y * g.dy), g.dx, fmaf(b.z * g.dy, g.dy, b.w));
-    return ex2_approx(e);
-}
-
 __device__ __forceinline__ void load_rec(const Rec *__restrict__ rec,
                                          const uint32_t *__restrict__ owner,
                                          uint32_t inst, Rec &R) {
@@ -108,6 +73,107 @@ __device__ __forceinline__ void load_rec(const Rec *__restrict__ rec,
     R.r2 = __ldg(src + 2);
 }
 
+// Shared-memory state of one staged batch.
+//   sA = (C1x, C1y, cu_frac, cv_frac)  dx = (big_float(x) - C1x) - cu_frac
+//   sB = (A, B2, C, E0)                log2 w = A dx^2 + B2 dx dy + C dy^2 + E0
+//   sC = (color, base | (w-1) << 8, area, instance)   base = y0*16 + x0
+struct Batch {
+    float4 sA[kBatch], sB[kBatch], sC[kBatch];
+    uint16_t order[kBatch];            // staged slot of the j-th record by trips
+    uint32_t wcnt[kWarps][kMaxTrips + 2];
+    uint32_t base[kMaxTrips + 2];
+};
+
+__device__ __forceinline__ int stage_record(const Rec &R, int tu0, int tv0,
+                                            uint32_t inst, float4 &a, float4 &b,
+                                            float4 &c) {
+    const int wu = __float_as_int(R.r2.y), wv = __float_as_int(R.r2.z);
+    const int x0 = max((wu & 0xffff) - tu0, 0), x1 = min((wu >> 16) - tu0, kTile - 1);
+    const int y0 = max((wv & 0xffff) - tv0, 0), y1 = min((wv >> 16) - tv0, kTile - 1);
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    // integer offset of the rectangle origin from the integer centre (exact)
+    const float offx = (float)(tu0 + x0) - R.r0.x;
+    const float offy = (float)(tv0 + y0) - R.r0.y;
+    a = make_float4(8388608.0f - offx, 8388608.0f - offy, R.r0.z, R.r0.w);
+    b = R.r1;
+    c = make_float4(R.r2.x, __int_as_float((y0 * kTile + x0) | ((w - 1) << 8)),
+                    __int_as_float(w * h), __int_as_float((int)inst));
+    return (w * h + kGL - 1) / kGL;
+}
+
+// Stable counting sort of the staged slots by trip count (warp match-any
+// ranks + per-warp bucket counters): deterministic record -> group mapping.
+__device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t key = valid ? (uint32_t)trips : (uint32_t)(kMaxTrips + 1);
+    for (int i = threadIdx.x; i < kWarps * (kMaxTrips + 2); i += kRasterThreads)
+        (&B.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (rank == 0) B.wcnt[warp][key] = __popc(peers);
+    __syncthreads();
+    if (threadIdx.x < 32) {   // bucket bases (exclusive over keys), then per warp
+        uint32_t tot = 0;
+        for (int k = lane; k < kMaxTrips + 2; k += 32) {
+            uint32_t col = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) col += B.wcnt[w][k];
+            B.base[k] = col;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (int k = 0; k < kMaxTrips + 2; ++k) {
+                const uint32_t c = B.base[k];
+                B.base[k] = tot;
+                tot += c;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxTrips + 2) {
+        uint32_t run = B.base[threadIdx.x];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = B.wcnt[w][threadIdx.x];
+            B.wcnt[w][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    if (valid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
+    __syncthreads();
+}
+
+// Per-kernel constant: k -> tile-local (y*16 + x) offset for each width w.
+__device__ __forceinline__ void build_kxy(uint8_t *kxy) {
+    for (int i = threadIdx.x; i < kTile * kTile * kTile; i += kRasterThreads) {
+        const int w = (i >> 8) + 1, k = i & 255;
+        const int y = k / w, x = k - y * w;
+        kxy[i] = (uint8_t)(y < kTile ? y * kTile + x : 0);
+    }
+}
+
+struct Pix {
+    float dx, dy;
+    int p;   // tile-local pixel
+};
+
+__device__ __forceinline__ Pix pix_of(const uint8_t *kxy_w, int k, int base,
+                                      const float4 &a) {
+    const int v = kxy_w[k];
+    Pix q;
+    q.p = base + v;
+    q.dx = (big_float(v & 15) - a.x) - a.z;
+    q.dy = (big_float(v >> 4) - a.y) - a.w;
+    return q;
+}
+
+__device__ __forceinline__ float pair_weight(const Pix &q, const float4 &b) {
+    const float e = fmaf(fmaf(b.x, q.dx, b.y * q.dy), q.dx, fmaf(b.z * q.dy, q.dy, b.w));
+    return ex2_approx(e);
+}
+
 __global__ void __launch_bounds__(kRasterThreads)
 forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                const uint32_t *__restrict__ vals,
@@ -115,49 +181,59 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
                float *__restrict__ den_out) {
-    __shared__ float4 sA[kBatch], sB[kBatch], sC[kBatch];
-    __shared__ float2 acc[kWarps][kTile * kTile];
+    extern __shared__ __align__(16) unsigned char smem[];
+    Batch &B = *reinterpret_cast<Batch *>(smem);
+    uint8_t *kxy = smem + sizeof(Batch);
+    float *accn = reinterpret_cast<float *>(kxy + kTile * kTile * kTile);
+    float *accd = accn + kGroups * kAccStride;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = lane & (kGL - 1), grp = threadIdx.x / kGL;
     const int2 rg = bin_range[sl.tile_base + t];
-    for (int i = threadIdx.x; i < kWarps * kTile * kTile; i += kRasterThreads)
-        (&acc[0][0])[i] = make_float2(0.f, 0.f);
-    float2 *my = acc[warp];
+    build_kxy(kxy);
+    for (int i = threadIdx.x; i < 2 * kGroups * kAccStride; i += kRasterThreads)
+        accn[i] = 0.f;
+    float *my_n = accn + grp * kAccStride, *my_d = accd + grp * kAccStride;
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
+        int trips = 0;
         if (threadIdx.x < nb) {
             Rec R;
-            load_rec(rec, owner, __ldg(vals + b0 + threadIdx.x), R);
-            stage_record(R, tu0, tv0, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x]);
+            const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
+            load_rec(rec, owner, inst, R);
+            trips = stage_record(R, tu0, tv0, inst, B.sA[threadIdx.x],
+                                 B.sB[threadIdx.x], B.sC[threadIdx.x]);
         }
-        __syncthreads();
-        for (int j = warp; j < nb; j += kWarps) {
-            const float4 a = sA[j], b = sB[j], c = sC[j];
-            const int rect = __float_as_int(c.y), magic = __float_as_int(c.z);
-            const int area = __float_as_int(c.w);
-            for (int k = lane; k < area; k += 32) {
-                const PairGeom g = pair_geom(k, a, rect, magic);
-                const float w = pair_weight(g, b);
-                float2 v = my[g.pix];
-                v.x = fmaf(w, c.x, v.x);
-                v.y += w;
-                my[g.pix] = v;
+        sort_batch(B, trips, threadIdx.x < nb);
+        // warp w, group q handles sorted slots (w + 8 i) * 4 + q
+        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
+            const int slot = s0 + (lane >> 3);
+            if (slot >= nb) continue;
+            const int j = B.order[slot];
+            const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
+            const int bw = __float_as_int(c.y);
+            const int base = bw & 255;
+            const uint8_t *kxy_w = kxy + ((bw >> 8) << 8);
+            const int area = __float_as_int(c.z);
+            for (int k = gl; k < area; k += kGL) {
+                const Pix q = pix_of(kxy_w, k, base, a);
+                const float w = pair_weight(q, b);
+                my_n[q.p] = fmaf(w, c.x, my_n[q.p]);
+                my_d[q.p] += w;
             }
         }
     }
     __syncthreads();
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-    const int u = tu0 + lx, v = tv0 + ly;
+    const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
     if (u < sl.width && v < sl.height) {
         float n = 0.f, d = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            n += acc[w][threadIdx.x].x;
-            d += acc[w][threadIdx.x].y;
+        for (int g = 0; g < kGroups; ++g) {
+            n += accn[g * kAccStride + threadIdx.x];
+            d += accd[g * kAccStride + threadIdx.x];
         }
         const float abg = sigmoid_bg(bg_raw, 1), cbg = sigmoid_bg(bg_raw, 0);
         const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;
@@ -223,33 +299,27 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__
     }
 }
 
-// Transpose-reduce of 8 per-lane values across the warp.  On return lanes
-// with (lane & 3) == 0 hold the warp total of value (lane >> 2).
-__device__ __forceinline__ float warp_reduce8(float a[8]) {
-    const int lane = threadIdx.x & 31;
+// Transpose-reduce of 8 values across the 8 lanes of a group: on return
+// group lane j holds the group total of value j.
+__device__ __forceinline__ float group_reduce8(const float a[8]) {
+    const int gl = threadIdx.x & (kGL - 1);
+    const bool h4 = gl & 4, h2 = gl & 2, h1 = gl & 1;
     float b[4], c[2];
-    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float send = h16 ? a[k] : a[k + 4];
-        const float keep = h16 ? a[k + 4] : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        const float send = h4 ? a[k] : a[k + 4];
+        const float keep = h4 ? a[k + 4] : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float send = h8 ? b[k] : b[k + 2];
-        const float keep = h8 ? b[k + 2] : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        const float send = h2 ? b[k] : b[k + 2];
+        const float keep = h2 ? b[k + 2] : b[k];
+        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
-    float d;
-    {
-        const float send = h4 ? c[0] : c[1];
-        const float keep = h4 ? c[1] : c[0];
-        d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    d += __shfl_xor_sync(0xffffffffu, d, 2);
-    d += __shfl_xor_sync(0xffffffffu, d, 1);
-    return d;
+    const float send = h1 ? c[0] : c[1];
+    const float keep = h1 ? c[1] : c[0];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
@@ -260,16 +330,19 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg) {
-    __shared__ float4 sA[kBatch], sB[kBatch], sC[kBatch];
-    __shared__ uint32_t s_inst[kBatch];
-    __shared__ float2 pix[kTile * kTile];   // (G, G*chat) per tile pixel
-    __shared__ float2 s_bg[kWarps];
+    extern __shared__ __align__(16) unsigned char smem[];
+    Batch &B = *reinterpret_cast<Batch *>(smem);
+    uint8_t *kxy = smem + sizeof(Batch);
+    float2 *pix = reinterpret_cast<float2 *>(kxy + kTile * kTile * kTile);  // (G, G chat)
+    float2 *s_bg = pix + kTile * kTile;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = lane & (kGL - 1);
     const int2 rg = bin_range[sl.tile_base + t];
+    build_kxy(kxy);
     {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
         const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
         float G = 0.f, Gc = 0.f, Gb = 0.f;
@@ -295,35 +368,43 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
+        int trips = 0;
         if (threadIdx.x < nb) {
-            const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             Rec R;
+            const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_rec(rec, owner, inst, R);
-            stage_record(R, tu0, tv0, sA[threadIdx.x], sB[threadIdx.x], sC[threadIdx.x]);
-            s_inst[threadIdx.x] = inst;
+            trips = stage_record(R, tu0, tv0, inst, B.sA[threadIdx.x],
+                                 B.sB[threadIdx.x], B.sC[threadIdx.x]);
         }
-        __syncthreads();
-        for (int j = warp; j < nb; j += kWarps) {
-            const float4 a = sA[j], b = sB[j], c = sC[j];
-            const int rect = __float_as_int(c.y), magic = __float_as_int(c.z);
-            const int area = __float_as_int(c.w);
+        sort_batch(B, trips, threadIdx.x < nb);
+        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
+            // every lane takes part in the shuffles; empty groups carry zeros
+            const int slot = s0 + (lane >> 3);
+            const bool live = slot < nb;
+            const int j = live ? B.order[slot] : B.order[s0];
+            const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
+            const int bw = __float_as_int(c.y);
+            const int base = bw & 255;
+            const uint8_t *kxy_w = kxy + ((bw >> 8) << 8);
+            const int area = live ? __float_as_int(c.z) : 0;
             float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int k = lane; k < area; k += 32) {
-                const PairGeom g = pair_geom(k, a, rect, magic);
-                const float w = pair_weight(g, b);
-                const float2 gp = pix[g.pix];
+            for (int k = gl; k < area; k += kGL) {
+                const Pix q = pix_of(kxy_w, k, base, a);
+                const float w = pair_weight(q, b);
+                const float2 gp = pix[q.p];
                 const float tq = fmaf(gp.x, c.x, -gp.y) * w;   // dw * w
-                const float tx = tq * g.dx, ty = tq * g.dy;
+                const float tx = tq * q.dx, ty = tq * q.dy;
                 m[0] = fmaf(gp.x, w, m[0]);
                 m[1] += tq;
                 m[2] += tx;
                 m[3] += ty;
-                m[4] = fmaf(tx, g.dx, m[4]);
-                m[5] = fmaf(tx, g.dy, m[5]);
-                m[6] = fmaf(ty, g.dy, m[6]);
+                m[4] = fmaf(tx, q.dx, m[4]);
+                m[5] = fmaf(tx, q.dy, m[5]);
+                m[6] = fmaf(ty, q.dy, m[6]);
             }
-            const float red = warp_reduce8(m);
-            if ((lane & 3) == 0) partial[(size_t)s_inst[j] * 8 + (lane >> 2)] = red;
+            const float red = group_reduce8(m);
+            if (live)
+                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + gl] = red;
         }
     }
     __syncthreads();
@@ -416,29 +497,63 @@ __global__ void finalize_records_kernel(const Rec *__restrict__ rec,
     if (touched) touched[g] = 1;
 }
 
-// One slice (launched in slice order): grad[g] += scale * rgrad[r].
-__global__ void accumulate_slice_kernel(const float *__restrict__ rgrad,
-                                        const int32_t *__restrict__ rec_gid,
-                                        int64_t r_begin, int64_t r_end, int64_t n,
-                                        float *__restrict__ grad, float scale) {
-    const int64_t r = r_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= r_end) return;
-    const int64_t g = rec_gid[r];
-    const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * 12);
-    const float4 q0 = src[0], q1 = src[1], q2 = src[2];
-    float *gm = grad + 3 * g;
-    gm[0] += scale * q0.x;
-    gm[1] += scale * q0.y;
-    gm[2] += scale * q0.z;
-    float *gl = grad + 3 * n + 6 * g;
-    gl[0] += scale * q0.w;
-    gl[1] += scale * q1.x;
-    gl[2] += scale * q1.y;
-    gl[3] += scale * q1.z;
-    gl[4] += scale * q1.w;
-    gl[5] += scale * q2.x;
-    grad[9 * n + g] += scale * q2.y;
-    grad[10 * n + g] += scale * q2.z;
+constexpr int kChunk = 1024;   // Gaussians per accumulate block
+
+// chunk_lo[s][c] = first record of slice s whose Gaussian index >= c*kChunk
+// (records of a slice are sorted by Gaussian index).
+__global__ void chunk_bounds_kernel(const int32_t *__restrict__ rec_gid,
+                                    const int64_t *__restrict__ slice_base,
+                                    const int64_t *__restrict__ slice_m, int S,
+                                    int nchunk, int64_t m_total,
+                                    int32_t *__restrict__ chunk_lo) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m_total) return;
+    int s = 0;
+    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    const int64_t r0 = slice_base[2 * s], r1 = r0 + slice_m[s];
+    const int c = rec_gid[r] / kChunk;
+    const int cprev = (r == r0) ? -1 : rec_gid[r - 1] / kChunk;
+    int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
+    for (int k = cprev + 1; k <= c; ++k) lo[k] = (int32_t)r;
+    if (r == r1 - 1)
+        for (int k = c + 1; k <= nchunk; ++k) lo[k] = (int32_t)r1;
+}
+
+// Block c owns Gaussians [c*kChunk, (c+1)*kChunk): it adds every slice's
+// records of that range into grad, slice by slice (a barrier between
+// slices), so each gradient entry sums its slices in slice order.
+__global__ void accumulate_kernel(const float *__restrict__ rgrad,
+                                  const int32_t *__restrict__ rec_gid,
+                                  const int32_t *__restrict__ chunk_lo,
+                                  const int64_t *__restrict__ slice_base,
+                                  const int64_t *__restrict__ slice_m, int S,
+                                  int nchunk, int64_t n, float *__restrict__ grad,
+                                  float scale) {
+    const int c = blockIdx.x;
+    for (int s = 0; s < S; ++s) {
+        const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
+        int64_t a = lo[c], e = lo[c + 1];
+        if (slice_m[s] == 0) { a = 0; e = 0; }
+        for (int64_t r = a + threadIdx.x; r < e; r += blockDim.x) {
+            const int64_t g = rec_gid[r];
+            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * 12);
+            const float4 q0 = src[0], q1 = src[1], q2 = src[2];
+            float *gm = grad + 3 * g;
+            gm[0] += scale * q0.x;
+            gm[1] += scale * q0.y;
+            gm[2] += scale * q0.z;
+            float *gl = grad + 3 * n + 6 * g;
+            gl[0] += scale * q0.w;
+            gl[1] += scale * q1.x;
+            gl[2] += scale * q1.y;
+            gl[3] += scale * q1.z;
+            gl[4] += scale * q1.w;
+            gl[5] += scale * q2.x;
+            grad[9 * n + g] += scale * q2.y;
+            grad[10 * n + g] += scale * q2.z;
+        }
+        __syncthreads();
+    }
 }
 
 // Background gradients: one block walks the slices in order; per slice the
@@ -477,11 +592,31 @@ __global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg,
     }
 }
 
+constexpr size_t kFwdSmem = sizeof(Batch) + kTile * kTile * kTile +
+                            2 * sizeof(float) * kGroups * kAccStride;
+constexpr size_t kBwdSmem = sizeof(Batch) + kTile * kTile * kTile +
+                            sizeof(float2) * (kTile * kTile + kWarps);
+
+int set_smem_attrs() {
+    static bool done = false;
+    if (done) return UGS_OK;
+    UGS_CUDA(cudaFuncSetAttribute(forward_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kFwdSmem));
+    UGS_CUDA(cudaFuncSetAttribute(backward_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kBwdSmem));
+    done = true;
+    return UGS_OK;
+}
+
 }  // namespace
 
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
+    int rc = set_smem_attrs();
+    if (rc) return rc;
     dim3 grid(p.max_tiles, p.S);
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageForward, st);
@@ -490,7 +625,7 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
-        forward_kernel<<<grid, kRasterThreads, 0, st>>>(
+        forward_kernel<<<grid, kRasterThreads, kFwdSmem, st>>>(
             p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
         UGS_LAUNCH_CHECK("forward_kernel");
     }
@@ -503,10 +638,12 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     float *grad, uint8_t *touched, float scale,
                     cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
+    int rc = set_smem_attrs();
+    if (rc) return rc;
     dim3 grid(p.max_tiles, p.S);
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
-    backward_kernel<<<grid, kRasterThreads, 0, st>>>(
+    backward_kernel<<<grid, kRasterThreads, kBwdSmem, st>>>(
         p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, num, den, dpix,
         c.bg_raw, p.b.partial, p.b.bin_bg);
     UGS_LAUNCH_CHECK("backward_kernel");
@@ -518,22 +655,25 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base,
             p.S, p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad, touched);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
-    }
-    for (int s = 0; s < p.S; ++s) {
-        const int64_t r0 = p.h_slice_base[2 * s];
-        const int64_t m = p.h_m[s];
-        if (m > 0) {
-            const int th = 256;
-            accumulate_slice_kernel<<<(unsigned)((m + th - 1) / th), th, 0, st>>>(
-                p.b.rgrad, p.b.rec_gid, r0, r0 + m, c.n, grad, scale);
-            UGS_LAUNCH_CHECK("accumulate_slice_kernel");
-        }
+        const int nchunk = (int)((c.n + kChunk - 1) / kChunk);
+        chunk_bounds_kernel<<<(unsigned)((p.m_total + 255) / 256), 256, 0, st>>>(
+            p.b.rec_gid, p.b.slice_base, p.b.slice_m, p.S, nchunk, p.m_total,
+            p.b.chunk_lo);
+        UGS_LAUNCH_CHECK("chunk_bounds_kernel");
+        accumulate_kernel<<<nchunk, 256, 0, st>>>(p.b.rgrad, p.b.rec_gid, p.b.chunk_lo,
+                                                  p.b.slice_base, p.b.slice_m, p.S,
+                                                  nchunk, c.n, grad, scale);
+        UGS_LAUNCH_CHECK("accumulate_kernel");
     }
     bg_finalize_kernel<<<1, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.S, c.bg_raw,
                                           grad + 11 * c.n, scale);
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
+}
+
+size_t chunk_lo_entries(int S, int64_t n) {
+    return (size_t)S * ((n + kChunk - 1) / kChunk + 1);
 }
 
 }  // namespace ugs
