@@ -127,7 +127,8 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     PlanBuffers &b = p->b;
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.slice_tot, b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.hist,
+                    b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.bg_sums,
+                    b.hist,
                     b.scan_tmp, b.bin_range,
                     b.bin_bg};
     for (void *q : bufs)
@@ -245,6 +246,8 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     {
         size_t cap = b.slice_m ? 64 : 0;
         if ((rc = ensure(&b.slice_m, &cap, (size_t)64, "alloc slice_m"))) return rc;
+        size_t cap2 = b.bg_sums ? 64 : 0;
+        if ((rc = ensure(&b.bg_sums, &cap2, (size_t)64, "alloc bg_sums"))) return rc;
     }
     UGS_CUDA(cudaMemcpyAsync(b.slice_m, p->h_m, sizeof(int64_t) * S,
                              cudaMemcpyHostToDevice, st));

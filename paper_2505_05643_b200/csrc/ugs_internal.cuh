@@ -50,6 +50,7 @@ struct PlanBuffers {
     int64_t *slice_m = nullptr;     // [S] accepted records per slice
     int32_t *chunk_lo = nullptr;    // [S][nchunk+1] record bounds per Gaussian chunk
     size_t chunk_lo_cap = 0;
+    double2 *bg_sums = nullptr;     // [64] per-slice background gradient sums
     // instances
     uint32_t *owner = nullptr;      // [K] record of each (unsorted) instance
     uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)

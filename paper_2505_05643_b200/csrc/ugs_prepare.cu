@@ -174,8 +174,6 @@ prepare_emit_kernel(const float *__restrict__ means,
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
-    const double log2_alpha = log2((double)alpha);
-    const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
     for (int s = 0; s < S; ++s) {
         const ugs_slice &L = sl[s];
         unsigned acc = 0, tiles = 0;
@@ -201,26 +199,51 @@ prepare_emit_kernel(const float *__restrict__ means,
         const uint2 bo = blk_off[(size_t)s * nblk + blockIdx.x];
         const int64_t r = slice_base[2 * s] + bo.x + oa + xa - acc;
         int64_t inst = slice_base[2 * s + 1] + bo.y + ot + xt - tiles;
-        PlaneForm P = plane_form(mu, f, L);
-        Rec R;
-        R.r0 = make_float4(P.cu_i, P.cv_i, P.cu_f, P.cv_f);
-        R.r1 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
-                           (float)(kq * P.H11),
-                           (float)(kq * P.qmin + log2_alpha));
-        R.r2 = make_float4(color, __int_as_float(w.iu0 | (w.iu1 << 16)),
-                           __int_as_float(w.iv0 | (w.iv1 << 16)), alpha);
-        rec[r] = R;
+        // the float64 plane conditioning and the tile expansion run in
+        // build_records_kernel (one thread per record, full occupancy)
+        rec[r].r2 = make_float4(color, __int_as_float(w.iu0 | (w.iu1 << 16)),
+                                __int_as_float(w.iv0 | (w.iv1 << 16)), alpha);
         rec_gid[r] = (int32_t)g;
         rec_inst[r] = (int32_t)inst;
-        const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
-        const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) {
-                owner[inst] = (uint32_t)r;
-                keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
-                ++inst;
-            }
     }
+}
+
+// One thread per accepted (slice, Gaussian) record: plane-conditioned
+// exponent (float64, ugs_geometry.cuh PlaneForm) and the record's tile
+// instances in row-major tile order.
+__global__ void __launch_bounds__(128)
+build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
+                     float beta, const ugs_slice *__restrict__ slices, int S,
+                     const int64_t *__restrict__ slice_base, int64_t m_total,
+                     Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
+                     const int32_t *__restrict__ rec_inst, uint32_t *__restrict__ owner,
+                     uint32_t *__restrict__ keys) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m_total) return;
+    int s = 0;
+    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    const ugs_slice &L = slices[s];
+    const int64_t g = rec_gid[r];
+    const Factor f = make_factor(l_raw, g, beta);
+    const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
+                         __ldg(means + 3 * g + 2)};
+    const float4 r2 = rec[r].r2;
+    const PlaneForm P = plane_form(mu, f, L);
+    const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
+    rec[r].r0 = make_float4(P.cu_i, P.cv_i, P.cu_f, P.cv_f);
+    rec[r].r1 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
+                            (float)(kq * P.H11),
+                            (float)(kq * P.qmin + log2((double)r2.w)));
+    const int wu = __float_as_int(r2.y), wv = __float_as_int(r2.z);
+    const int tx0 = (wu & 0xffff) >> 4, tx1 = (wu >> 16) >> 4;
+    const int ty0 = (wv & 0xffff) >> 4, ty1 = (wv >> 16) >> 4;
+    int64_t inst = rec_inst[r];
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            owner[inst] = (uint32_t)r;
+            keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
+            ++inst;
+        }
 }
 
 }  // namespace
@@ -251,6 +274,10 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
         S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, owner, keys,
         m_total, k_total);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
+    build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
+        c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,
+        rec_inst, owner, keys);
+    UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;
 }
 

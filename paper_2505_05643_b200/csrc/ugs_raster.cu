@@ -43,10 +43,11 @@ namespace {
 constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
-constexpr int kGL = 8;                       // lanes per record group
-constexpr int kGroups = kRasterThreads / kGL;  // 32 groups per CTA
-constexpr int kMaxTrips = (kTile * kTile + kGL - 1) / kGL;   // 32
-constexpr int kAccStride = kTile * kTile + 8;  // private buffer stride (bank skew)
+constexpr int kGL = 8;                       // backward: lanes per record group
+constexpr int kMaxTrips = (kTile * kTile + kGL - 1) / kGL;   // 32 (sort buckets)
+constexpr int kFGL = 16;                     // forward: lanes per record group
+constexpr int kFGroups = kRasterThreads / kFGL;   // 16 private buffers per CTA
+constexpr int kAccStride = kTile * kTile + 16;    // buffer stride (16-bank skew)
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -85,8 +86,8 @@ struct Batch {
 };
 
 __device__ __forceinline__ int stage_record(const Rec &R, int tu0, int tv0,
-                                            uint32_t inst, float4 &a, float4 &b,
-                                            float4 &c) {
+                                            uint32_t inst, int glen, float4 &a,
+                                            float4 &b, float4 &c) {
     const int wu = __float_as_int(R.r2.y), wv = __float_as_int(R.r2.z);
     const int x0 = max((wu & 0xffff) - tu0, 0), x1 = min((wu >> 16) - tu0, kTile - 1);
     const int y0 = max((wv & 0xffff) - tv0, 0), y1 = min((wv >> 16) - tv0, kTile - 1);
@@ -98,7 +99,7 @@ __device__ __forceinline__ int stage_record(const Rec &R, int tu0, int tv0,
     b = R.r1;
     c = make_float4(R.r2.x, __int_as_float((y0 * kTile + x0) | ((w - 1) << 8)),
                     __int_as_float(w * h), __int_as_float((int)inst));
-    return (w * h + kGL - 1) / kGL;
+    return (w * h + glen - 1) / glen;
 }
 
 // Stable counting sort of the staged slots by trip count (warp match-any
@@ -185,16 +186,16 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     Batch &B = *reinterpret_cast<Batch *>(smem);
     uint8_t *kxy = smem + sizeof(Batch);
     float *accn = reinterpret_cast<float *>(kxy + kTile * kTile * kTile);
-    float *accd = accn + kGroups * kAccStride;
+    float *accd = accn + kFGroups * kAccStride;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gl = lane & (kGL - 1), grp = threadIdx.x / kGL;
+    const int gl = lane & (kFGL - 1), grp = threadIdx.x / kFGL;
     const int2 rg = bin_range[sl.tile_base + t];
     build_kxy(kxy);
-    for (int i = threadIdx.x; i < 2 * kGroups * kAccStride; i += kRasterThreads)
+    for (int i = threadIdx.x; i < 2 * kFGroups * kAccStride; i += kRasterThreads)
         accn[i] = 0.f;
     float *my_n = accn + grp * kAccStride, *my_d = accd + grp * kAccStride;
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
@@ -205,13 +206,13 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             Rec R;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_rec(rec, owner, inst, R);
-            trips = stage_record(R, tu0, tv0, inst, B.sA[threadIdx.x],
+            trips = stage_record(R, tu0, tv0, inst, kFGL, B.sA[threadIdx.x],
                                  B.sB[threadIdx.x], B.sC[threadIdx.x]);
         }
         sort_batch(B, trips, threadIdx.x < nb);
-        // warp w, group q handles sorted slots (w + 8 i) * 4 + q
-        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
-            const int slot = s0 + (lane >> 3);
+        // warp w, half h handles sorted slots (w + 8 i) * 2 + h
+        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
+            const int slot = s0 + (lane >> 4);
             if (slot >= nb) continue;
             const int j = B.order[slot];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
@@ -219,7 +220,7 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             const int base = bw & 255;
             const uint8_t *kxy_w = kxy + ((bw >> 8) << 8);
             const int area = __float_as_int(c.z);
-            for (int k = gl; k < area; k += kGL) {
+            for (int k = gl; k < area; k += kFGL) {
                 const Pix q = pix_of(kxy_w, k, base, a);
                 const float w = pair_weight(q, b);
                 my_n[q.p] = fmaf(w, c.x, my_n[q.p]);
@@ -231,7 +232,7 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
     if (u < sl.width && v < sl.height) {
         float n = 0.f, d = 0.f;
-        for (int g = 0; g < kGroups; ++g) {
+        for (int g = 0; g < kFGroups; ++g) {
             n += accn[g * kAccStride + threadIdx.x];
             d += accd[g * kAccStride + threadIdx.x];
         }
@@ -373,7 +374,7 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             Rec R;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_rec(rec, owner, inst, R);
-            trips = stage_record(R, tu0, tv0, inst, B.sA[threadIdx.x],
+            trips = stage_record(R, tu0, tv0, inst, kGL, B.sA[threadIdx.x],
                                  B.sB[threadIdx.x], B.sC[threadIdx.x]);
         }
         sort_batch(B, trips, threadIdx.x < nb);
@@ -556,44 +557,48 @@ __global__ void accumulate_kernel(const float *__restrict__ rgrad,
     }
 }
 
-// Background gradients: one block walks the slices in order; per slice the
-// tile partials are tree-reduced in fixed order (gradients.py:106-112).
-__global__ void bg_finalize_kernel(const float2 *__restrict__ bin_bg,
-                                   const ugs_slice *__restrict__ slices, int S,
+// Background gradients (gradients.py:106-112): block s tree-reduces slice
+// s's tile partials in fixed order; the last step adds the slices in order.
+__global__ void bg_slice_kernel(const float2 *__restrict__ bin_bg,
+                                const ugs_slice *__restrict__ slices,
+                                double2 *__restrict__ out) {
+    __shared__ double sa[256], sc_[256];
+    const int s = blockIdx.x;
+    const int tile_base = slices[s].tile_base;
+    const int ntile = slices[s].tiles_x * slices[s].tiles_y;
+    double a = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
+        a += bin_bg[tile_base + i].x;
+        c += bin_bg[tile_base + i].y;
+    }
+    sa[threadIdx.x] = a;
+    sc_[threadIdx.x] = c;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sa[threadIdx.x] += sa[threadIdx.x + o];
+            sc_[threadIdx.x] += sc_[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[s] = make_double2(sa[0], sc_[0]);
+}
+
+__global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
                                    const double *__restrict__ bg_raw,
                                    float *__restrict__ grad_bg, float scale) {
-    __shared__ double sa[256], sc_[256];
+    if (threadIdx.x != 0) return;
     const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
     for (int s = 0; s < S; ++s) {
-        const int tile_base = slices[s].tile_base;
-        const int ntile = slices[s].tiles_x * slices[s].tiles_y;
-        double a = 0.0, c = 0.0;
-        for (int i = threadIdx.x; i < ntile; i += blockDim.x) {
-            a += bin_bg[tile_base + i].x;
-            c += bin_bg[tile_base + i].y;
-        }
-        sa[threadIdx.x] = a;
-        sc_[threadIdx.x] = c;
-        __syncthreads();
-        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-            if (threadIdx.x < o) {
-                sa[threadIdx.x] += sa[threadIdx.x + o];
-                sc_[threadIdx.x] += sc_[threadIdx.x + o];
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            const double d_cbg = (double)(float)abg * sa[0];   // sum dpix*f32(a_bg)/ssum
-            const double d_abg = sc_[0];                       // sum dpix*(c_bg-chat)/ssum
-            grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
-            grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
-        }
-        __syncthreads();
+        const double d_cbg = (double)(float)abg * sums[s].x;   // sum dpix*f32(a_bg)/ssum
+        const double d_abg = sums[s].y;                        // sum dpix*(c_bg-chat)/ssum
+        grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
+        grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
     }
 }
 
 constexpr size_t kFwdSmem = sizeof(Batch) + kTile * kTile * kTile +
-                            2 * sizeof(float) * kGroups * kAccStride;
+                            2 * sizeof(float) * kFGroups * kAccStride;
 constexpr size_t kBwdSmem = sizeof(Batch) + kTile * kTile * kTile +
                             sizeof(float2) * (kTile * kTile + kWarps);
 
@@ -665,8 +670,10 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                                                   nchunk, c.n, grad, scale);
         UGS_LAUNCH_CHECK("accumulate_kernel");
     }
-    bg_finalize_kernel<<<1, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.S, c.bg_raw,
-                                          grad + 11 * c.n, scale);
+    bg_slice_kernel<<<p.S, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
+    UGS_LAUNCH_CHECK("bg_slice_kernel");
+    bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, c.bg_raw, grad + 11 * c.n,
+                                         scale);
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
