@@ -45,9 +45,14 @@ constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
 constexpr int kGL = 8;                       // backward: lanes per record group
 constexpr int kMaxTrips = (kTile * kTile + kGL - 1) / kGL;   // 32 (sort buckets)
-constexpr int kFGL = 16;                     // forward: lanes per record group
-constexpr int kFGroups = kRasterThreads / kFGL;   // 16 private buffers per CTA
-constexpr int kAccStride = kTile * kTile + 16;    // buffer stride (16-bank skew)
+constexpr int kFGL = 32;                     // forward: one record per warp
+constexpr int kFGroups = kRasterThreads / kFGL;   // 8 private buffers per CTA
+constexpr int kAccStride = kTile * kTile;
+
+// Private-buffer word of tile pixel p = 16*Y + X: X is XOR-ed with 8 on rows
+// with bit 1 of Y set, so the rows a warp sweeps (Y, Y+1 on opposite bank
+// halves; Y, Y+2 XOR-separated) rarely share a bank.
+__device__ __forceinline__ int acc_swizzle(int p) { return p ^ ((p >> 2) & 8); }
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -193,6 +198,7 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gl = lane & (kFGL - 1), grp = threadIdx.x / kFGL;
+    constexpr int kSlotsPerWarp = 32 / kFGL;
     const int2 rg = bin_range[sl.tile_base + t];
     build_kxy(kxy);
     for (int i = threadIdx.x; i < 2 * kFGroups * kAccStride; i += kRasterThreads)
@@ -206,13 +212,12 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             Rec R;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_rec(rec, owner, inst, R);
-            trips = stage_record(R, tu0, tv0, inst, kFGL, B.sA[threadIdx.x],
+            trips = stage_record(R, tu0, tv0, inst, 2 * kFGL, B.sA[threadIdx.x],
                                  B.sB[threadIdx.x], B.sC[threadIdx.x]);
         }
         sort_batch(B, trips, threadIdx.x < nb);
-        // warp w, half h handles sorted slots (w + 8 i) * 2 + h
-        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
-            const int slot = s0 + (lane >> 4);
+        for (int s0 = warp * kSlotsPerWarp; s0 < nb; s0 += kWarps * kSlotsPerWarp) {
+            const int slot = s0 + lane / kFGL;
             if (slot >= nb) continue;
             const int j = B.order[slot];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
@@ -220,11 +225,23 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             const int base = bw & 255;
             const uint8_t *kxy_w = kxy + ((bw >> 8) << 8);
             const int area = __float_as_int(c.z);
-            for (int k = gl; k < area; k += kFGL) {
-                const Pix q = pix_of(kxy_w, k, base, a);
-                const float w = pair_weight(q, b);
-                my_n[q.p] = fmaf(w, c.x, my_n[q.p]);
-                my_d[q.p] += w;
+            // two pixels per lane per sweep: both loads issue before either
+            // store (the two pixels are distinct), hiding the smem latency
+            for (int k = gl; k < area; k += 2 * kFGL) {
+                const bool two = k + kFGL < area;
+                const Pix q0 = pix_of(kxy_w, k, base, a);
+                const Pix q1 = pix_of(kxy_w, two ? k + kFGL : k, base, a);
+                const int p0 = acc_swizzle(q0.p), p1 = acc_swizzle(q1.p);
+                const float w0 = pair_weight(q0, b);
+                const float w1 = pair_weight(q1, b);
+                const float n0 = my_n[p0], d0 = my_d[p0];
+                const float n1 = my_n[p1], d1 = my_d[p1];
+                my_n[p0] = fmaf(w0, c.x, n0);
+                my_d[p0] = d0 + w0;
+                if (two) {
+                    my_n[p1] = fmaf(w1, c.x, n1);
+                    my_d[p1] = d1 + w1;
+                }
             }
         }
     }
@@ -232,9 +249,10 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
     if (u < sl.width && v < sl.height) {
         float n = 0.f, d = 0.f;
+        const int sp = acc_swizzle(threadIdx.x);
         for (int g = 0; g < kFGroups; ++g) {
-            n += accn[g * kAccStride + threadIdx.x];
-            d += accd[g * kAccStride + threadIdx.x];
+            n += accn[g * kAccStride + sp];
+            d += accd[g * kAccStride + sp];
         }
         const float abg = sigmoid_bg(bg_raw, 1), cbg = sigmoid_bg(bg_raw, 0);
         const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;

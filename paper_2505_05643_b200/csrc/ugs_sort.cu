@@ -179,7 +179,14 @@ radix_scatter_kernel(const uint32_t *__restrict__ keys_in,
         k[j] = ok ? keys_in[i] : 0u;
         v[j] = ok ? (vals_in ? vals_in[i] : (uint32_t)i) : 0u;
         const uint32_t d = ok ? ((k[j] >> shift) & (kRadix - 1)) : (uint32_t)kRadix;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        // lanes with the same digit: 9 ballots (8 digit bits + the invalid
+        // flag) -- constant cost, unlike match.any on many distinct values
+        unsigned peers = 0xffffffffu;
+#pragma unroll
+        for (int bit = 0; bit <= kRadixBits; ++bit) {
+            const unsigned bal = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+            peers &= ((d >> bit) & 1u) ? bal : ~bal;
+        }
         const uint32_t rank = __popc(peers & lt_mask);
         uint32_t cnt_before = 0;
         if (ok) cnt_before = wcnt[warp][d];
