@@ -43,8 +43,7 @@ namespace {
 constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
-constexpr int kGL = 8;                       // backward: lanes per record group
-constexpr int kMaxTrips = (kTile * kTile + kGL - 1) / kGL;   // 32 (sort buckets)
+constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
 constexpr int kAccStride = kTile * kTile;    // forward: one record per warp,
                                              // one private buffer per warp
 
@@ -153,34 +152,6 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
     __syncthreads();
 }
 
-// Per-kernel constant: k -> tile-local (y*16 + x) offset for each width w.
-__device__ __forceinline__ void build_kxy(uint8_t *kxy) {
-    for (int i = threadIdx.x; i < kTile * kTile * kTile; i += kRasterThreads) {
-        const int w = (i >> 8) + 1, k = i & 255;
-        const int y = k / w, x = k - y * w;
-        kxy[i] = (uint8_t)(y < kTile ? y * kTile + x : 0);
-    }
-}
-
-struct Pix {
-    float dx, dy;
-    int p;   // tile-local pixel
-};
-
-__device__ __forceinline__ Pix pix_of(const uint8_t *kxy_w, int k, int base,
-                                      const float4 &a) {
-    const int v = kxy_w[k];
-    Pix q;
-    q.p = base + v;
-    q.dx = (big_float(v & 15) - a.x) - a.z;
-    q.dy = (big_float(v >> 4) - a.y) - a.w;
-    return q;
-}
-
-__device__ __forceinline__ float pair_weight(const Pix &q, const float4 &b) {
-    const float e = fmaf(fmaf(b.x, q.dx, b.y * q.dy), q.dx, fmaf(b.z * q.dy, q.dy, b.w));
-    return ex2_approx(e);
-}
 
 __global__ void __launch_bounds__(kRasterThreads)
 forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
@@ -322,27 +293,29 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__
     }
 }
 
-// Transpose-reduce of 8 values across the 8 lanes of a group: on return
-// group lane j holds the group total of value j.
-__device__ __forceinline__ float group_reduce8(const float a[8]) {
-    const int gl = threadIdx.x & (kGL - 1);
-    const bool h4 = gl & 4, h2 = gl & 2, h1 = gl & 1;
+
+// Transpose-reduce of 8 values across a 16-lane half warp: on return lanes
+// with even group lane g hold the group total of value g >> 1.
+__device__ __forceinline__ float group_reduce16(const float a[8]) {
+    const int gl = threadIdx.x & 15;
+    const bool h8 = gl & 8, h4 = gl & 4, h2 = gl & 2;
     float b[4], c[2];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float send = h4 ? a[k] : a[k + 4];
-        const float keep = h4 ? a[k + 4] : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        const float send = h8 ? a[k] : a[k + 4];
+        const float keep = h8 ? a[k + 4] : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float send = h2 ? b[k] : b[k + 2];
-        const float keep = h2 ? b[k + 2] : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        const float send = h4 ? b[k] : b[k + 2];
+        const float keep = h4 ? b[k + 2] : b[k];
+        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
-    const float send = h1 ? c[0] : c[1];
-    const float keep = h1 ? c[1] : c[0];
-    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    const float send = h2 ? c[0] : c[1];
+    const float keep = h2 ? c[1] : c[0];
+    float d = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    return d + __shfl_xor_sync(0xffffffffu, d, 1);
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
@@ -355,17 +328,14 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg) {
     extern __shared__ __align__(16) unsigned char smem[];
     Batch &B = *reinterpret_cast<Batch *>(smem);
-    uint8_t *kxy = smem + sizeof(Batch);
-    float2 *pix = reinterpret_cast<float2 *>(kxy + kTile * kTile * kTile);  // (G, G chat)
+    float2 *pix = reinterpret_cast<float2 *>(smem + sizeof(Batch));  // (G, G chat)
     float2 *s_bg = pix + kTile * kTile;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gl = lane & (kGL - 1);
     const int2 rg = bin_range[sl.tile_base + t];
-    build_kxy(kxy);
     {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
         const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
         float G = 0.f, Gc = 0.f, Gb = 0.f;
@@ -396,38 +366,59 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             Rec R;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_rec(rec, owner, inst, R);
-            trips = stage_record(R, tu0, tv0, inst, kGL, B.sA[threadIdx.x],
-                                 B.sB[threadIdx.x], B.sC[threadIdx.x]);
+            float4 c;
+            stage_record(R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
+            // 16-lane group layout: cw = pow2 >= w columns x (16/cw) rows per sweep
+            const int bw = __float_as_int(c.y);
+            const int w = ((bw >> 8) & 15) + 1;
+            const int h = __float_as_int(c.z) / w;
+            const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
+            const int rows = 16 >> lcw;
+            trips = (h + rows - 1) / rows;
+            c.y = __int_as_float((bw & 255) | ((w - 1) << 8) | ((h - 1) << 12) | (lcw << 16));
+            B.sC[threadIdx.x] = c;
         }
         sort_batch(B, trips, threadIdx.x < nb);
-        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
-            // every lane takes part in the shuffles; empty groups carry zeros
-            const int slot = s0 + (lane >> 3);
+        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
+            // every lane takes part in the shuffles; empty lanes carry zeros
+            const int slot = s0 + (lane >> 4);
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
-            const int bw = __float_as_int(c.y);
-            const int base = bw & 255;
-            const uint8_t *kxy_w = kxy + ((bw >> 8) << 8);
-            const int area = live ? __float_as_int(c.z) : 0;
-            float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            for (int k = gl; k < area; k += kGL) {
-                const Pix q = pix_of(kxy_w, k, base, a);
-                const float w = pair_weight(q, b);
-                const float2 gp = pix[q.p];
-                const float tq = fmaf(gp.x, c.x, -gp.y) * w;   // dw * w
-                const float tx = tq * q.dx, ty = tq * q.dy;
-                m[0] = fmaf(gp.x, w, m[0]);
-                m[1] += tq;
-                m[2] += tx;
-                m[3] += ty;
-                m[4] = fmaf(tx, q.dx, m[4]);
-                m[5] = fmaf(tx, q.dy, m[5]);
-                m[6] = fmaf(ty, q.dy, m[6]);
+            const int pk = __float_as_int(c.y);
+            const int x0 = pk & 15, y0 = (pk >> 4) & 15;
+            const int w = ((pk >> 8) & 15) + 1, h = live ? ((pk >> 12) & 15) + 1 : 0;
+            const int lcw = (pk >> 16) & 7;
+            const int gl16 = lane & 15;
+            const int lx = gl16 & ((1 << lcw) - 1), ly = gl16 >> lcw;
+            const int rows = 16 >> lcw;
+            // per lane dx is fixed: log2 w = P + dy (Q + C dy); the x moments
+            // follow from the per-lane sums: sum t dx = dx S0, sum t dx^2 =
+            // dx^2 S0, sum t dx dy = dx Sy
+            const float dx = (big_float(lx) - a.x) - a.z;
+            const float P = fmaf(b.x * dx, dx, b.w), Q = b.y * dx;
+            float yo = big_float(ly) - a.y;
+            const float2 *gp = pix + (y0 + ly) * kTile + x0 + lx;
+            float m0 = 0.f, S0 = 0.f, Sy = 0.f, Syy = 0.f;
+            if (lx < w) {
+                for (int y = ly; y < h; y += rows) {
+                    const float dy = yo - a.w;
+                    const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
+                    const float2 g = *gp;
+                    const float tq = fmaf(g.x, c.x, -g.y) * wgt;   // dw * w
+                    m0 = fmaf(g.x, wgt, m0);
+                    S0 += tq;
+                    const float ty = tq * dy;
+                    Sy += ty;
+                    Syy = fmaf(ty, dy, Syy);
+                    yo += (float)rows;
+                    gp += rows * kTile;
+                }
             }
-            const float red = group_reduce8(m);
-            if (live)
-                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + gl] = red;
+            float m[8] = {m0, S0, dx * S0, Sy, dx * dx * S0, dx * Sy, Syy, 0.f};
+            const float red = group_reduce16(m);
+            if (live && (lane & 1) == 0)
+                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + (gl16 >> 1)] = red;
         }
     }
     __syncthreads();
@@ -620,8 +611,7 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
 }
 
 constexpr size_t kFwdSmem = sizeof(Batch) + sizeof(float2) * kWarps * kAccStride;
-constexpr size_t kBwdSmem = sizeof(Batch) + kTile * kTile * kTile +
-                            sizeof(float2) * (kTile * kTile + kWarps);
+constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(float2) * (kTile * kTile + kWarps);
 
 int set_smem_attrs() {
     static bool done = false;
