@@ -354,15 +354,26 @@ def run_ours(a):
     except (OSError, ValueError):
         pass
     n = eng.cloud.n
-    adam_bytes = 32 * (11 * n + 2) + 4 * 2 * n + 3 * n   # p,g,m,v r/w + stats
+    # parameter update: N=1 fuses accumulate + stats + Adam into the finalize
+    # stage (params 44 B + m, v 96 B read and written per Gaussian); N>1 runs
+    # a separate Adam over the dense AoS-12 gradient (+ gradient r/w 96 B)
+    upd_stage = "finalize" if world == 1 else "adam"
+    upd_bytes = (280 if world == 1 else 376) * n
+    upd_ms = stage_ms.get(upd_stage, float("nan"))
+
+    def tflops(fpp, k):
+        return fpp * pairs_per_step / (stage_ms.get(k, float("nan")) * 1e-3) / 1e12
+
     roof_stages = {
         "forward": {"flops": FLOP_FWD_PER_PAIR * pairs_per_step, "ms": stage_ms.get("forward"),
-                    "tflops": FLOP_FWD_PER_PAIR * pairs_per_step / (stage_ms.get("forward", 1e9) * 1e-3) / 1e12},
+                    "tflops": tflops(FLOP_FWD_PER_PAIR, "forward"),
+                    "frac": tflops(FLOP_FWD_PER_PAIR, "forward") / peak_fp32},
         "backward": {"flops": FLOP_BWD_PER_PAIR * pairs_per_step, "ms": stage_ms.get("backward"),
-                     "tflops": FLOP_BWD_PER_PAIR * pairs_per_step / (stage_ms.get("backward", 1e9) * 1e-3) / 1e12},
-        "adam+stats": {"bytes": adam_bytes, "ms": stage_ms.get("adam"),
-                       "gbs": adam_bytes / (stage_ms.get("adam", 1e9) * 1e-3) / 1e9,
-                       "frac_of_hbm": adam_bytes / (stage_ms.get("adam", 1e9) * 1e-3) / 1e9 / hbm_peak},
+                     "tflops": tflops(FLOP_BWD_PER_PAIR, "backward"),
+                     "frac": tflops(FLOP_BWD_PER_PAIR, "backward") / peak_fp32},
+        "update": {"stage": upd_stage, "bytes": upd_bytes, "ms": upd_ms,
+                   "gbs": upd_bytes / (upd_ms * 1e-3) / 1e9,
+                   "frac_of_hbm": upd_bytes / (upd_ms * 1e-3) / 1e9 / hbm_peak},
     }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

@@ -124,28 +124,47 @@ UGS_API int ugs_export_bins(const ugs_plan *plan, int32_t *bin_range,
 UGS_API int ugs_forward(ugs_plan *plan, const ugs_cloud *cloud, float *num, float *den,
                 void *stream);
 
+/* Gradient / Adam-moment layout ("AoS-12", float32, 12 n + 2 entries):
+ * Gaussian g owns [12 g, 12 g + 12) = [d_means 0..2 | d_l_raw 3..8 |
+ * d_intensity_raw 9 | d_opacity_raw 10 | pad 11]; [12 n, 12 n + 2) holds
+ * the background (intensity, opacity).  16-byte aligned. */
+
 /* Backward for every slice of the last ugs_bin.  d_pixels (dev, same layout
  * as num).  Accumulates `scale` x (raw-parameter gradients) into grad (dev,
- * float32, 11n+2: [means 3n | l_raw 6n | intensity n | opacity n | bg 2])
- * and sets touched[g] = 1 for every accepted Gaussian (touched may be NULL).
- * Slices are reduced in order, without atomics: deterministic. */
+ * AoS-12) and sets touched[g] = 1 for every accepted Gaussian (touched may
+ * be NULL).  Slices are reduced in order, without atomics: deterministic. */
 UGS_API int ugs_backward(ugs_plan *plan, const ugs_cloud *cloud, const float *num,
                  const float *den, const float *d_pixels, float *grad,
                  uint8_t *touched, float scale, void *stream);
 
+/* The single-GPU training step's backward half in one call: backward +
+ * ordered accumulation + densify statistics (grad_sum/grad_cnt, may be NULL)
+ * + Adam on every parameter (trainer.py:170-200, bit-compatible arithmetic),
+ * without materialising the dense gradient.  The cloud's parameter arrays
+ * and bg_raw are updated IN PLACE (the const in ugs_cloud notwithstanding).
+ * m, v: AoS-12 moments; t: step count after increment; lr as ugs_adam_step. */
+UGS_API int ugs_backward_adam(ugs_plan *plan, const ugs_cloud *cloud,
+                              const float *num, const float *den,
+                              const float *d_pixels, float scale, float *m,
+                              float *v, int64_t t, const double *lr,
+                              double beta1, double beta2, double eps,
+                              float *grad_sum, int32_t *grad_cnt, void *stream);
+
 /* grad_sum[g] += ||d_means[g]||, grad_cnt[g] += 1 for touched Gaussians,
- * then clears touched (trainer.py:399-401). */
+ * then clears touched (trainer.py:399-401).  grad: AoS-12. */
 UGS_API int ugs_grad_stats(const float *grad, int64_t n, uint8_t *touched,
                    float *grad_sum, int32_t *grad_cnt, void *stream);
 
 /* One Adam step over all groups, bit-compatible with trainer.py:170-200.
  * lr[0] means, lr[1] l_raw, lr[2] intensity, lr[3] opacity, lr[4] bg.
- * m, v (dev) flat like grad.  t is the step count after increment.
- * If zero_grad != 0 the gradient buffer is cleared after use. */
+ * grad, m, v (dev) AoS-12.  t is the step count after increment.  If
+ * zero_grad != 0 the gradient buffer is cleared after use.  touched /
+ * grad_sum / grad_cnt (all or none) fold in ugs_grad_stats. */
 UGS_API int ugs_adam_step(float *means, float *l_raw, float *intensity_raw,
                   float *opacity_raw, double *bg_raw, float *grad, float *m,
                   float *v, int64_t n, int64_t t, const double *lr,
                   double beta1, double beta2, double eps, int zero_grad,
+                  uint8_t *touched, float *grad_sum, int32_t *grad_cnt,
                   void *stream);
 
 /* Densify/prune row surgery (trainer.py:208-279, model.py:147-152):

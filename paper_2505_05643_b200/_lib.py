@@ -62,7 +62,13 @@ EXPORTS = {
     "ugs_adam_step": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                      c_i64, c_i64, ctypes.POINTER(ctypes.c_double),
                                      ctypes.c_double, ctypes.c_double,
-                                     ctypes.c_double, ctypes.c_int, c_vp]),
+                                     ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp,
+                                     c_vp]),
+    "ugs_backward_adam": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
+                                         c_f, c_vp, c_vp, c_i64,
+                                         ctypes.POINTER(ctypes.c_double),
+                                         ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, c_vp, c_vp, c_vp]),
     "ugs_densify_apply": (ctypes.c_int, [ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
                                          c_i64, c_vp, c_vp, c_vp, c_i64,
                                          ctypes.c_double, c_vp, c_vp, c_vp, c_vp,

@@ -45,9 +45,10 @@ class RasterizeSlices(torch.autograd.Function):
         grad = grad_buffer(n, num.device)
         r.backward(cloud, num, den, d_pred.to(torch.float32).contiguous(), grad,
                    None, 1.0)
-        return (grad[:3 * n].view(n, 3), grad[3 * n:9 * n].view(n, 6),
-                grad[9 * n:10 * n], grad[10 * n:11 * n],
-                grad[11 * n:11 * n + 2].double(), None, None, None, None)
+        rows = grad[:12 * n].view(n, 12)
+        return (rows[:, 0:3].contiguous(), rows[:, 3:9].contiguous(),
+                rows[:, 9].contiguous(), rows[:, 10].contiguous(),
+                grad[12 * n:12 * n + 2].double(), None, None, None, None)
 
 
 def rasterize_autograd(means, l_raw, intensity_raw, opacity_raw, bg_raw, specs,

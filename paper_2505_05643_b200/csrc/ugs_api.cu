@@ -7,6 +7,7 @@
 #include <atomic>
 #include <vector>
 
+#include "ugs_adam.cuh"
 #include "ugs_internal.cuh"
 
 namespace ugs {
@@ -327,7 +328,35 @@ extern "C" int ugs_backward(ugs_plan *p, const ugs_cloud *c, const float *num,
         return UGS_ERR_INVALID;
     }
     return launch_backward(*p, *c, p->sorted_vals, num, den, d_pixels, grad, touched,
-                           scale, (cudaStream_t)stream);
+                           scale, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int ugs_backward_adam(ugs_plan *p, const ugs_cloud *c, const float *num,
+                                 const float *den, const float *d_pixels, float scale,
+                                 float *m, float *v, int64_t t, const double *lr,
+                                 double beta1, double beta2, double eps,
+                                 float *grad_sum, int32_t *grad_cnt, void *stream) {
+    if (!p || !num || !den || !d_pixels || !m || !v || !lr || t < 1) {
+        set_error("ugs_backward_adam: invalid arguments");
+        return UGS_ERR_INVALID;
+    }
+    if ((grad_sum == nullptr) != (grad_cnt == nullptr)) {
+        set_error("ugs_backward_adam: grad_sum and grad_cnt go together");
+        return UGS_ERR_INVALID;
+    }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (c->n != p->n) {
+        set_error("ugs_backward_adam: buffers do not match this cloud");
+        return UGS_ERR_INVALID;
+    }
+    if ((((uintptr_t)m | (uintptr_t)v) & 15) != 0) {
+        set_error("ugs_backward_adam: m, v must be 16-byte aligned");
+        return UGS_ERR_INVALID;
+    }
+    AdamArgs a{m, v, make_adam_const(t, lr, beta1, beta2, eps), grad_sum, grad_cnt};
+    return launch_backward(*p, *c, p->sorted_vals, num, den, d_pixels, nullptr, nullptr,
+                           scale, &a, (cudaStream_t)stream);
 }
 
 namespace ugs {

@@ -159,9 +159,10 @@ int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
 size_t chunk_lo_entries(int S, int64_t n);
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st);
+struct AdamArgs;   // ugs_adam.cuh
 int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     const float *num, const float *den, const float *dpix,
-                    float *grad, uint8_t *touched, float scale,
+                    float *grad, uint8_t *touched, float scale, const AdamArgs *adam,
                     cudaStream_t st);
 
 }  // namespace ugs

@@ -34,6 +34,7 @@
 // closed-form chain to d_mu, d_L and the raw parameters (float64); slices are
 // then accumulated into the gradient in slice order by Gaussian-range blocks
 // -- no atomics anywhere, so gradients are bitwise reproducible.
+#include "ugs_adam.cuh"
 #include "ugs_geometry.cuh"
 
 namespace ugs {
@@ -449,8 +450,7 @@ __global__ void finalize_records_kernel(const Rec *__restrict__ rec,
                                         const ugs_slice *__restrict__ slices,
                                         const float *__restrict__ means,
                                         const float *__restrict__ l_raw, float beta,
-                                        float *__restrict__ rgrad,
-                                        uint8_t *__restrict__ touched) {
+                                        float *__restrict__ rgrad) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m_total) return;
     int s = 0;
@@ -508,10 +508,9 @@ __global__ void finalize_records_kernel(const Rec *__restrict__ rec,
     o[9] = (float)(Tc * c * (1.0 - c));
     o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
     o[11] = 0.f;
-    if (touched) touched[g] = 1;
 }
 
-constexpr int kChunk = 1024;   // Gaussians per accumulate block
+constexpr int kChunk = 512;   // Gaussians per accumulate block
 
 // chunk_lo[s][c] = first record of slice s whose Gaussian index >= c*kChunk
 // (records of a slice are sorted by Gaussian index).
@@ -533,40 +532,79 @@ __global__ void chunk_bounds_kernel(const int32_t *__restrict__ rec_gid,
         for (int k = c + 1; k <= nchunk; ++k) lo[k] = (int32_t)r1;
 }
 
+__device__ __forceinline__ float4 axpy4(float4 y, float s, float4 x) {
+    return make_float4(fmaf(s, x.x, y.x), fmaf(s, x.y, y.y), fmaf(s, x.z, y.z),
+                       fmaf(s, x.w, y.w));
+}
+
 // Block c owns Gaussians [c*kChunk, (c+1)*kChunk): it adds every slice's
-// records of that range into grad, slice by slice (a barrier between
-// slices), so each gradient entry sums its slices in slice order.
+// records of that range into the AoS-12 gradient, slice by slice (a barrier
+// between slices), so each entry sums its slices in slice order.
 __global__ void accumulate_kernel(const float *__restrict__ rgrad,
                                   const int32_t *__restrict__ rec_gid,
                                   const int32_t *__restrict__ chunk_lo,
-                                  const int64_t *__restrict__ slice_base,
                                   const int64_t *__restrict__ slice_m, int S,
-                                  int nchunk, int64_t n, float *__restrict__ grad,
-                                  float scale) {
+                                  int nchunk, float *__restrict__ grad, float scale,
+                                  uint8_t *__restrict__ touched) {
     const int c = blockIdx.x;
     for (int s = 0; s < S; ++s) {
         const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
-        int64_t a = lo[c], e = lo[c + 1];
-        if (slice_m[s] == 0) { a = 0; e = 0; }
+        const int64_t a = slice_m[s] ? lo[c] : 0, e = slice_m[s] ? lo[c + 1] : 0;
         for (int64_t r = a + threadIdx.x; r < e; r += blockDim.x) {
             const int64_t g = rec_gid[r];
-            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * 12);
-            const float4 q0 = src[0], q1 = src[1], q2 = src[2];
-            float *gm = grad + 3 * g;
-            gm[0] += scale * q0.x;
-            gm[1] += scale * q0.y;
-            gm[2] += scale * q0.z;
-            float *gl = grad + 3 * n + 6 * g;
-            gl[0] += scale * q0.w;
-            gl[1] += scale * q1.x;
-            gl[2] += scale * q1.y;
-            gl[3] += scale * q1.z;
-            gl[4] += scale * q1.w;
-            gl[5] += scale * q2.x;
-            grad[9 * n + g] += scale * q2.y;
-            grad[10 * n + g] += scale * q2.z;
+            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
+            float4 *dst = reinterpret_cast<float4 *>(grad + (size_t)g * kG);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) dst[q] = axpy4(dst[q], scale, src[q]);
+            if (touched) touched[g] = 1;
         }
         __syncthreads();
+    }
+}
+
+// Single-GPU step: the same ordered accumulation into a shared-memory chunk
+// of the gradient, then densify statistics and Adam for EVERY Gaussian of the
+// chunk (zero-gradient rows still move, trainer.py:182-199) -- the dense
+// gradient never touches HBM.
+__global__ void __launch_bounds__(256)
+accumulate_adam_kernel(const float *__restrict__ rgrad,
+                       const int32_t *__restrict__ rec_gid,
+                       const int32_t *__restrict__ chunk_lo,
+                       const int64_t *__restrict__ slice_m, int S, int nchunk,
+                       int64_t n, float scale, CloudMut p, float *__restrict__ m,
+                       float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
+                       int32_t *__restrict__ grad_cnt) {
+    __shared__ float4 acc[kChunk * 3];
+    __shared__ uint8_t hit[kChunk];
+    const int c = blockIdx.x;
+    const int64_t g0 = (int64_t)c * kChunk;
+    for (int i = threadIdx.x; i < kChunk * 3; i += blockDim.x)
+        acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) hit[i] = 0;
+    __syncthreads();
+    for (int s = 0; s < S; ++s) {
+        const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
+        const int64_t a = slice_m[s] ? lo[c] : 0, e = slice_m[s] ? lo[c + 1] : 0;
+        for (int64_t r = a + threadIdx.x; r < e; r += blockDim.x) {
+            const int gl = (int)(rec_gid[r] - g0);
+            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) acc[3 * gl + q] = axpy4(acc[3 * gl + q], scale, src[q]);
+            hit[gl] = 1;
+        }
+        __syncthreads();
+    }
+    for (int gl = threadIdx.x; gl < kChunk; gl += blockDim.x) {
+        const int64_t g = g0 + gl;
+        if (g >= n) break;
+        float gr[kG];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float4 t = acc[3 * gl + q];
+            gr[4 * q] = t.x; gr[4 * q + 1] = t.y; gr[4 * q + 2] = t.z; gr[4 * q + 3] = t.w;
+        }
+        adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit[gl] != 0, grad_sum,
+                      grad_cnt);
     }
 }
 
@@ -597,16 +635,27 @@ __global__ void bg_slice_kernel(const float2 *__restrict__ bin_bg,
     if (threadIdx.x == 0) out[s] = make_double2(sa[0], sc_[0]);
 }
 
+// Adds the background gradients into grad_bg, or (adam != 0) applies the
+// background Adam step with them.
 __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
-                                   const double *__restrict__ bg_raw,
-                                   float *__restrict__ grad_bg, float scale) {
+                                   double *__restrict__ bg_raw,
+                                   float *__restrict__ grad_bg, float scale, int adam,
+                                   float *__restrict__ m_bg, float *__restrict__ v_bg,
+                                   AdamConst k) {
     if (threadIdx.x != 0) return;
     const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
+    float g[2] = {adam ? 0.f : grad_bg[0], adam ? 0.f : grad_bg[1]};
     for (int s = 0; s < S; ++s) {
         const double d_cbg = (double)(float)abg * sums[s].x;   // sum dpix*f32(a_bg)/ssum
         const double d_abg = sums[s].y;                        // sum dpix*(c_bg-chat)/ssum
-        grad_bg[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
-        grad_bg[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
+        g[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
+        g[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
+    }
+    if (adam) {
+        adam_bg(bg_raw, g, m_bg, v_bg, k);
+    } else {
+        grad_bg[0] = g[0];
+        grad_bg[1] = g[1];
     }
 }
 
@@ -651,7 +700,7 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
 
 int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     const float *num, const float *den, const float *dpix,
-                    float *grad, uint8_t *touched, float scale,
+                    float *grad, uint8_t *touched, float scale, const AdamArgs *adam,
                     cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
     int rc = set_smem_attrs();
@@ -665,27 +714,48 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
     stage_begin(pm, kStageFinalize, st);
+    const int nchunk = (int)((c.n + kChunk - 1) / kChunk);
+    const CloudMut cm{const_cast<float *>(c.means), const_cast<float *>(c.l_raw),
+                      const_cast<float *>(c.intensity_raw),
+                      const_cast<float *>(c.opacity_raw)};
     if (p.m_total > 0) {
         const int th = 128;
         finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
             p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base,
-            p.S, p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad, touched);
+            p.S, p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
-        const int nchunk = (int)((c.n + kChunk - 1) / kChunk);
         chunk_bounds_kernel<<<(unsigned)((p.m_total + 255) / 256), 256, 0, st>>>(
             p.b.rec_gid, p.b.slice_base, p.b.slice_m, p.S, nchunk, p.m_total,
             p.b.chunk_lo);
         UGS_LAUNCH_CHECK("chunk_bounds_kernel");
-        accumulate_kernel<<<nchunk, 256, 0, st>>>(p.b.rgrad, p.b.rec_gid, p.b.chunk_lo,
-                                                  p.b.slice_base, p.b.slice_m, p.S,
-                                                  nchunk, c.n, grad, scale);
-        UGS_LAUNCH_CHECK("accumulate_kernel");
     }
     bg_slice_kernel<<<p.S, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
     UGS_LAUNCH_CHECK("bg_slice_kernel");
-    bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, c.bg_raw, grad + 11 * c.n,
-                                         scale);
-    UGS_LAUNCH_CHECK("bg_finalize_kernel");
+    if (adam) {
+        // every slice with m == 0 is skipped through slice_m, so the fused
+        // update also runs (for all rows) when nothing was accepted
+        if (p.m_total == 0)
+            UGS_CUDA(cudaMemsetAsync(p.b.slice_m, 0, sizeof(int64_t) * p.S, st));
+        accumulate_adam_kernel<<<nchunk, 256, 0, st>>>(
+            p.b.rgrad, p.b.rec_gid, p.b.chunk_lo, p.b.slice_m, p.S, nchunk, c.n, scale,
+            cm, adam->m, adam->v, adam->k, adam->grad_sum, adam->grad_cnt);
+        UGS_LAUNCH_CHECK("accumulate_adam_kernel");
+        bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+                                             nullptr, scale, 1, adam->m + kG * c.n,
+                                             adam->v + kG * c.n, adam->k);
+        UGS_LAUNCH_CHECK("bg_finalize_kernel");
+    } else {
+        if (p.m_total > 0) {
+            accumulate_kernel<<<nchunk, 256, 0, st>>>(p.b.rgrad, p.b.rec_gid, p.b.chunk_lo,
+                                                      p.b.slice_m, p.S, nchunk, grad,
+                                                      scale, touched);
+            UGS_LAUNCH_CHECK("accumulate_kernel");
+        }
+        bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+                                             grad + kG * c.n, scale, 0, nullptr, nullptr,
+                                             AdamConst{});
+        UGS_LAUNCH_CHECK("bg_finalize_kernel");
+    }
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
 }

@@ -32,17 +32,19 @@ class ParamGradients:
 
     @staticmethod
     def from_flat(flat: torch.Tensor, n: int, bg_as_float: bool = True):
-        bg = flat[11 * n:11 * n + 2]
-        bgv = bg.double().cpu().numpy() if bg_as_float else (bg[0], bg[1])
-        return ParamGradients(flat[:3 * n].view(n, 3),
-                              flat[3 * n:9 * n].view(n, 6),
-                              flat[9 * n:10 * n], flat[10 * n:11 * n],
-                              float(bgv[0]), float(bgv[1]))
+        """Views (made contiguous) of an AoS-12 gradient buffer."""
+        rows = flat[:12 * n].view(n, 12)
+        bg = flat[12 * n:12 * n + 2].double().cpu().numpy()
+        return ParamGradients(rows[:, 0:3].contiguous(), rows[:, 3:9].contiguous(),
+                              rows[:, 9].contiguous(), rows[:, 10].contiguous(),
+                              float(bg[0]), float(bg[1]))
 
 
 def grad_buffer(n: int, device) -> torch.Tensor:
-    """Flat float32 gradient layout [means 3n | l_raw 6n | c n | a n | bg 2]."""
-    return torch.zeros(11 * n + 2, dtype=torch.float32, device=device)
+    """AoS-12 float32 gradient (include/ugs.h): Gaussian g owns entries
+    [12g, 12g+12) = [d_means 3 | d_l_raw 6 | d_c | d_a | pad], background
+    entries at [12n, 12n+2)."""
+    return torch.zeros(12 * n + 2, dtype=torch.float32, device=device)
 
 
 def backward(cloud, spec: SliceSpec, buffers: RenderBuffers, d_pixels,

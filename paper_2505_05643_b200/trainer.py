@@ -91,21 +91,28 @@ class TrainConfig:
             raise InvalidParameterError("batch must be in [1, 64]")
 
 
-def _offsets(n):
-    return {"means": (0, 3 * n, (n, 3)), "l_raw": (3 * n, 9 * n, (n, 6)),
-            "intensity_raw": (9 * n, 10 * n, (n,)),
-            "opacity_raw": (10 * n, 11 * n, (n,)), "bg": (11 * n, 11 * n + 2, (2,))}
+# AoS-12 rows (include/ugs.h): column ranges of each group, plus background
+_COLS = {"means": (0, 3), "l_raw": (3, 9), "intensity_raw": (9, 10),
+         "opacity_raw": (10, 11)}
+
+
+def aos_views(flat: torch.Tensor, n: int) -> dict:
+    """Per-group (strided) views of an AoS-12 buffer of 12n+2 floats."""
+    rows = flat[:12 * n].view(n, 12)
+    out = {k: (rows[:, a:b] if b - a > 1 else rows[:, a]) for k, (a, b) in _COLS.items()}
+    out["bg"] = flat[12 * n:12 * n + 2]
+    return out
 
 
 class AdamState:
-    """First/second moments (ref trainer.py:77-107) as flat float32 device
-    buffers in the gradient layout; ``m``/``v`` give per-group views."""
+    """First/second moments (ref trainer.py:77-107) as float32 device buffers
+    in the AoS-12 gradient layout; ``m``/``v`` give per-group views."""
 
     def __init__(self, n, device, t=0, beta1=0.9, beta2=0.999, eps=1e-15,
                  m_flat=None, v_flat=None):
         self.n = n
         self.m_flat = m_flat if m_flat is not None else torch.zeros(
-            11 * n + 2, dtype=torch.float32, device=device)
+            12 * n + 2, dtype=torch.float32, device=device)
         self.v_flat = v_flat if v_flat is not None else torch.zeros_like(self.m_flat)
         self.t = t
         self.beta1, self.beta2, self.eps = beta1, beta2, eps
@@ -115,8 +122,7 @@ class AdamState:
         return AdamState(cloud.n, cloud.device)
 
     def _views(self, flat):
-        return {k: flat[a:b].view(shape) for k, (a, b, shape)
-                in _offsets(self.n).items()}
+        return aos_views(flat, self.n)
 
     @property
     def m(self):
@@ -159,17 +165,23 @@ def general_lr(config: TrainConfig, t: int) -> float:
     return config.lr_general * (config.lr_general_final / config.lr_general) ** frac
 
 
+def _lr_array(lrs: dict):
+    return (ctypes.c_double * 5)(lrs["means"], lrs["l_raw"], lrs["intensity_raw"],
+                                 lrs["opacity_raw"], lrs["bg"])
+
+
 def _adam_flat(state: AdamState, cloud: GaussianCloud, grad_flat: torch.Tensor,
-               lrs: dict, zero_grad: bool) -> None:
+               lrs: dict, zero_grad: bool, stats=None) -> None:
+    """ugs_adam_step on an AoS-12 gradient; stats = (touched, sum, cnt)."""
     state.t += 1
-    lr = (ctypes.c_double * 5)(lrs["means"], lrs["l_raw"], lrs["intensity_raw"],
-                               lrs["opacity_raw"], lrs["bg"])
+    touched, gsum, gcnt = stats if stats is not None else (None, None, None)
     _lib.check(_lib.lib().ugs_adam_step(
         cloud.means.data_ptr(), cloud.l_raw.data_ptr(),
         cloud.intensity_raw.data_ptr(), cloud.opacity_raw.data_ptr(),
         cloud.bg_raw.data_ptr(), grad_flat.data_ptr(), state.m_flat.data_ptr(),
-        state.v_flat.data_ptr(), cloud.n, state.t, lr, state.beta1, state.beta2,
-        state.eps, 1 if zero_grad else 0, _stream()), "ugs_adam_step")
+        state.v_flat.data_ptr(), cloud.n, state.t, _lr_array(lrs), state.beta1,
+        state.beta2, state.eps, 1 if zero_grad else 0, _lib.ptr(touched),
+        _lib.ptr(gsum), _lib.ptr(gcnt), _stream()), "ugs_adam_step")
 
 
 def adam_step(state: AdamState, cloud: GaussianCloud, grads: ParamGradients,
@@ -179,16 +191,17 @@ def adam_step(state: AdamState, cloud: GaussianCloud, grads: ParamGradients,
     if state.n != n:
         raise InvalidParameterError("moment/gradient shape mismatch")
     flat = grad_buffer(n, cloud.device)
-    o = _offsets(n)
+    views = aos_views(flat, n)
+    shapes = {"means": (n, 3), "l_raw": (n, 6), "intensity_raw": (n,),
+              "opacity_raw": (n,)}
     for k in GROUPS:
-        a, b, shape = o[k]
         g = getattr(grads, "d_" + k)
         g = torch.as_tensor(g if isinstance(g, torch.Tensor) else np.asarray(g))
-        if tuple(g.shape) != shape:
+        if tuple(g.shape) != shapes[k]:
             raise InvalidParameterError(f"moment/gradient shape mismatch for {k}")
-        flat[a:b] = g.reshape(-1).to(device=cloud.device, dtype=torch.float32)
-    flat[11 * n] = float(np.float32(grads.d_bg_intensity_raw))
-    flat[11 * n + 1] = float(np.float32(grads.d_bg_opacity_raw))
+        views[k].copy_(g.to(device=cloud.device, dtype=torch.float32))
+    flat[12 * n] = float(np.float32(grads.d_bg_intensity_raw))
+    flat[12 * n + 1] = float(np.float32(grads.d_bg_opacity_raw))
     _adam_flat(state, cloud, flat, lrs, zero_grad=False)
     return cloud
 
@@ -429,23 +442,34 @@ class TrainEngine:
             if not math.isfinite(loss_val):
                 return loss_val
         scale = 1.0 / (len(idx) * self.world_size)
-        self.renderer.backward(self.cloud, num, den, dpix.to(torch.float32).contiguous(),
-                               self.grad, self.touched, scale)
-        if self.world_size > 1:
-            self._mark("allreduce0")
-            torch.distributed.all_reduce(self.grad, group=self.pg)
-            torch.distributed.all_reduce(self.touched, op=torch.distributed.ReduceOp.MAX,
-                                         group=self.pg)
-            self._mark("allreduce1")
-        self._mark("adam0")
-        _lib.check(_lib.lib().ugs_grad_stats(
-            self.grad.data_ptr(), self.cloud.n, self.touched.data_ptr(),
-            self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
-            "ugs_grad_stats")
         lr_g = general_lr(cfg, it)
         lrs = {"means": mean_lr(cfg, it), "l_raw": lr_g, "intensity_raw": lr_g,
                "opacity_raw": lr_g, "bg": lr_g}
-        _adam_flat(self.state, self.cloud, self.grad, lrs, zero_grad=True)
+        dpix = dpix.to(torch.float32).contiguous()
+        if self.world_size == 1:
+            # single GPU: backward + ordered accumulation + stats + Adam in one
+            # call; the dense gradient is never materialised
+            self._mark("adam0")
+            st = self.state
+            st.t += 1
+            cs = self.cloud.c_struct()
+            _lib.check(_lib.lib().ugs_backward_adam(
+                self.renderer._plan, ctypes.byref(cs), num.data_ptr(), den.data_ptr(),
+                dpix.data_ptr(), float(scale), st.m_flat.data_ptr(),
+                st.v_flat.data_ptr(), st.t, _lr_array(lrs), st.beta1, st.beta2, st.eps,
+                self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
+                "ugs_backward_adam")
+            self._mark("adam1")
+            return loss_val if check_finite else loss_t
+        self.renderer.backward(self.cloud, num, den, dpix, self.grad, self.touched, scale)
+        self._mark("allreduce0")
+        torch.distributed.all_reduce(self.grad, group=self.pg)
+        torch.distributed.all_reduce(self.touched, op=torch.distributed.ReduceOp.MAX,
+                                     group=self.pg)
+        self._mark("allreduce1")
+        self._mark("adam0")
+        _adam_flat(self.state, self.cloud, self.grad, lrs, zero_grad=True,
+                   stats=(self.touched, self.grad_sum, self.grad_cnt))
         self._mark("adam1")
         return loss_val if check_finite else loss_t
 
