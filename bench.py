@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--size", type=int, default=256)
     ap.add_argument("--spacing", type=float, default=0.375)
     ap.add_argument("--n-slices", type=int, default=256, help="dataset size")
-    ap.add_argument("--cpu-sample", type=int, default=12,
+    ap.add_argument("--cpu-sample", type=int, default=48,
                     help="slices in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -36,6 +36,7 @@ from .gradients import ParamGradients, grad_buffer
 from .metrics import fused_loss, ssim_batch
 from .metrics import loss as _loss
 from .model import GaussianCloud
+from .parallel import SliceScheduler, allreduce_gradients, grad_scale
 from .rasterizer import Renderer, _stream
 
 CHECKPOINT_MAGIC = b"UGSC"
@@ -441,7 +442,7 @@ class TrainEngine:
             loss_val = float(loss_t.item())
             if not math.isfinite(loss_val):
                 return loss_val
-        scale = 1.0 / (len(idx) * self.world_size)
+        scale = grad_scale(len(idx), self.world_size)
         lr_g = general_lr(cfg, it)
         lrs = {"means": mean_lr(cfg, it), "l_raw": lr_g, "intensity_raw": lr_g,
                "opacity_raw": lr_g, "bg": lr_g}
@@ -463,9 +464,7 @@ class TrainEngine:
             return loss_val if check_finite else loss_t
         self.renderer.backward(self.cloud, num, den, dpix, self.grad, self.touched, scale)
         self._mark("allreduce0")
-        torch.distributed.all_reduce(self.grad, group=self.pg)
-        torch.distributed.all_reduce(self.touched, op=torch.distributed.ReduceOp.MAX,
-                                     group=self.pg)
+        allreduce_gradients(self.grad, self.touched, self.pg)
         self._mark("allreduce1")
         self._mark("adam0")
         _adam_flat(self.state, self.cloud, self.grad, lrs, zero_grad=True,
@@ -510,21 +509,11 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
     scene_extent = float(np.linalg.norm(bounds[1] - bounds[0]))
     max_total = 2 * config.n_gaussians
     threshold = config.densify_grad_threshold
-    order = rng.permutation(len(train_slices))
-    cursor = 0
+    sched = SliceScheduler(rng, len(train_slices), config.batch, world, rank)
     log = []
     t0 = time.perf_counter()
-    B = config.batch
     for it in range(1, config.iterations + 1):
-        picks = []
-        for _ in range(B * world):
-            if cursor >= len(order):
-                order = rng.permutation(len(train_slices))
-                cursor = 0
-            picks.append(int(order[cursor]))
-            cursor += 1
-        mine = picks[rank * B:(rank + 1) * B]
-        loss_val = eng.step(mine, it)
+        loss_val = eng.step(sched.next(), it)
         if not math.isfinite(loss_val):
             snap = snapshot_path or (str(checkpoint_path or "echosplat") + ".diverged")
             if rank == 0:
