@@ -434,28 +434,21 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
     }
 }
 
-// All records of the batch in one launch: sum a record's instance partials
-// in order and chain to raw-parameter gradients (ref gradients.py:84-103):
-// with e* = e(centre), V = S0 e* + Sx du + Sy dv and
+// Raw-parameter gradients of one record (ref gradients.py:84-103): sum its
+// instance partials in order, then with e* = e(centre),
+// V = S0 e* + Sx du + Sy dv and
 // M = S0 e*e*^T + e* w^T + w e*^T + Sxx du du^T + Sxy (du dv^T + dv du^T)
 //     + Syy dv dv^T  (w = Sx du + Sy dv, dq = -t/2):
 //   d_mu = Lambda V,  d_L = -(M L) lower,  d_c = Tc,  d_a = S0 / alpha.
-// Writes 12 floats per record: [d_mu 3 | d_l_raw 6 | d_c_raw | d_a_raw | -].
-__global__ void finalize_records_kernel(const Rec *__restrict__ rec,
-                                        const int32_t *__restrict__ rec_gid,
-                                        const int32_t *__restrict__ rec_inst,
-                                        const float *__restrict__ partial,
-                                        int64_t m_total,
-                                        const int64_t *__restrict__ slice_base, int S,
-                                        const ugs_slice *__restrict__ slices,
-                                        const float *__restrict__ means,
-                                        const float *__restrict__ l_raw, float beta,
-                                        float *__restrict__ rgrad) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m_total) return;
-    int s = 0;
-    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
-    const ugs_slice &sl = slices[s];
+// o = [d_mu 3 | d_l_raw 6 | d_c_raw | d_a_raw].
+__device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
+                                            const Rec *__restrict__ rec,
+                                            const int32_t *__restrict__ rec_gid,
+                                            const int32_t *__restrict__ rec_inst,
+                                            const float *__restrict__ partial,
+                                            const float *__restrict__ means,
+                                            const float *__restrict__ l_raw, float beta,
+                                            float o[11]) {
     double Sm[7] = {0, 0, 0, 0, 0, 0, 0};
     const int i0 = rec_inst[r], i1 = rec_inst[r + 1];
     for (int i = i0; i < i1; ++i) {
@@ -491,7 +484,6 @@ __global__ void finalize_records_kernel(const Rec *__restrict__ rec,
     const double L[3][3] = {{f.L00, 0.0, 0.0}, {f.L10, f.L11, 0.0}, {f.L20, f.L21, f.L22}};
     double LtV[3];
     for (int k = 0; k < 3; ++k) LtV[k] = L[0][k] * V[0] + L[1][k] * V[1] + L[2][k] * V[2];
-    float *o = rgrad + (size_t)r * 12;
     for (int i = 0; i < 3; ++i)
         o[i] = (float)(L[i][0] * LtV[0] + L[i][1] * LtV[1] + L[i][2] * LtV[2]);
     auto dL = [&](int i, int j) {
@@ -507,7 +499,6 @@ __global__ void finalize_records_kernel(const Rec *__restrict__ rec,
     const double c = R.r2.x, a = R.r2.w;
     o[9] = (float)(Tc * c * (1.0 - c));
     o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
-    o[11] = 0.f;
 }
 
 constexpr int kChunk = 512;   // Gaussians per accumulate block
@@ -532,79 +523,118 @@ __global__ void chunk_bounds_kernel(const int32_t *__restrict__ rec_gid,
         for (int k = c + 1; k <= nchunk; ++k) lo[k] = (int32_t)r1;
 }
 
-__device__ __forceinline__ float4 axpy4(float4 y, float s, float4 x) {
-    return make_float4(fmaf(s, x.x, y.x), fmaf(s, x.y, y.y), fmaf(s, x.z, y.z),
-                       fmaf(s, x.w, y.w));
-}
+constexpr int kStageCap = 1024;   // staged record gradients per pass
+constexpr int kGroupSlices = 16;  // slices per pass (slot-map rows)
+constexpr int kFinThreads = 256;
 
-// Block c owns Gaussians [c*kChunk, (c+1)*kChunk): it adds every slice's
-// records of that range into the AoS-12 gradient, slice by slice (a barrier
-// between slices), so each entry sums its slices in slice order.
-__global__ void accumulate_kernel(const float *__restrict__ rgrad,
-                                  const int32_t *__restrict__ rec_gid,
-                                  const int32_t *__restrict__ chunk_lo,
-                                  const int64_t *__restrict__ slice_m, int S,
-                                  int nchunk, float *__restrict__ grad, float scale,
-                                  uint8_t *__restrict__ touched) {
-    const int c = blockIdx.x;
-    for (int s = 0; s < S; ++s) {
-        const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
-        const int64_t a = slice_m[s] ? lo[c] : 0, e = slice_m[s] ? lo[c + 1] : 0;
-        for (int64_t r = a + threadIdx.x; r < e; r += blockDim.x) {
-            const int64_t g = rec_gid[r];
-            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
-            float4 *dst = reinterpret_cast<float4 *>(grad + (size_t)g * kG);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) dst[q] = axpy4(dst[q], scale, src[q]);
-            if (touched) touched[g] = 1;
-        }
-        __syncthreads();
-    }
-}
+struct FinSmem {
+    float stage[kStageCap][11];
+    int16_t slot[kGroupSlices][kChunk];
+    int32_t lo[kGroupSlices + 1];
+};
 
-// Single-GPU step: the same ordered accumulation into a shared-memory chunk
-// of the gradient, then densify statistics and Adam for EVERY Gaussian of the
-// chunk (zero-gradient rows still move, trainer.py:182-199) -- the dense
-// gradient never touches HBM.
-__global__ void __launch_bounds__(256)
-accumulate_adam_kernel(const float *__restrict__ rgrad,
-                       const int32_t *__restrict__ rec_gid,
+// Block c owns Gaussians [c*kChunk, (c+1)*kChunk).  In passes over groups of
+// slices whose records fit the staging area it
+//   A) computes every (slice, record) gradient of its range in parallel
+//      (record_grad, float64) into shared memory, noting each record's slot
+//      in a per-slice map, then
+//   B) lets the owner thread of each Gaussian add its slots in SLICE ORDER,
+// so every gradient sums its slices in a fixed order (deterministic, no
+// atomics).  Finally (adam != 0, single GPU) densify statistics and Adam run
+// for EVERY Gaussian of the range -- zero-gradient rows still move
+// (trainer.py:182-199) -- and the dense gradient never touches HBM; or
+// (adam == 0) the gradient rows are added into the dense AoS-12 buffer.
+__global__ void __launch_bounds__(kFinThreads)
+finalize_update_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
+                       const int32_t *__restrict__ rec_inst,
+                       const float *__restrict__ partial,
                        const int32_t *__restrict__ chunk_lo,
-                       const int64_t *__restrict__ slice_m, int S, int nchunk,
-                       int64_t n, float scale, CloudMut p, float *__restrict__ m,
+                       const int64_t *__restrict__ slice_m,
+                       const ugs_slice *__restrict__ slices, int S, int nchunk, int64_t n,
+                       const float *__restrict__ means, const float *__restrict__ l_raw,
+                       float beta, float scale, int adam, float *__restrict__ grad,
+                       uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
                        float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
                        int32_t *__restrict__ grad_cnt) {
-    __shared__ float4 acc[kChunk * 3];
-    __shared__ uint8_t hit[kChunk];
+    extern __shared__ __align__(16) unsigned char fsm[];
+    FinSmem &F = *reinterpret_cast<FinSmem *>(fsm);
+    constexpr int kOwn = kChunk / kFinThreads;   // Gaussians per thread
     const int c = blockIdx.x;
     const int64_t g0 = (int64_t)c * kChunk;
-    for (int i = threadIdx.x; i < kChunk * 3; i += blockDim.x)
-        acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) hit[i] = 0;
-    __syncthreads();
-    for (int s = 0; s < S; ++s) {
-        const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
-        const int64_t a = slice_m[s] ? lo[c] : 0, e = slice_m[s] ? lo[c + 1] : 0;
-        for (int64_t r = a + threadIdx.x; r < e; r += blockDim.x) {
-            const int gl = (int)(rec_gid[r] - g0);
-            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
+    float acc[kOwn][11];
+    bool hit[kOwn];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) acc[3 * gl + q] = axpy4(acc[3 * gl + q], scale, src[q]);
-            hit[gl] = 1;
+    for (int q = 0; q < kOwn; ++q) {
+        hit[q] = false;
+#pragma unroll
+        for (int j = 0; j < 11; ++j) acc[q][j] = 0.f;
+    }
+    int s0 = 0;
+    while (s0 < S) {
+        // next group of slices whose records of this range fit the stage
+        int s1 = s0, tot = 0;
+        while (s1 < S && s1 - s0 < kGroupSlices) {
+            const int32_t *lo = chunk_lo + (size_t)s1 * (nchunk + 1);
+            const int cnt = slice_m[s1] ? lo[c + 1] - lo[c] : 0;
+            if (s1 > s0 && tot + cnt > kStageCap) break;
+            tot += cnt;
+            ++s1;
+        }
+        __syncthreads();   // previous pass done with stage / slot
+        if (threadIdx.x <= s1 - s0) {
+            int pre = 0;
+            for (int s = s0; s < s0 + (int)threadIdx.x; ++s) {
+                const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
+                pre += slice_m[s] ? lo[c + 1] - lo[c] : 0;
+            }
+            F.lo[threadIdx.x] = pre;
+        }
+        for (int i = threadIdx.x; i < kGroupSlices * kChunk; i += kFinThreads)
+            (&F.slot[0][0])[i] = -1;
+        __syncthreads();
+        // A) all (slice, record) gradients of the pass, in parallel
+        for (int i = threadIdx.x; i < tot; i += kFinThreads) {
+            int sg = 0;
+            while (sg + 1 < s1 - s0 && F.lo[sg + 1] <= i) ++sg;
+            const int s = s0 + sg;
+            const int64_t r = chunk_lo[(size_t)s * (nchunk + 1) + c] + (i - F.lo[sg]);
+            float o[11];
+            record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw, beta, o);
+#pragma unroll
+            for (int j = 0; j < 11; ++j) F.stage[i][j] = o[j];
+            F.slot[sg][rec_gid[r] - g0] = (int16_t)i;
         }
         __syncthreads();
-    }
-    for (int gl = threadIdx.x; gl < kChunk; gl += blockDim.x) {
-        const int64_t g = g0 + gl;
-        if (g >= n) break;
-        float gr[kG];
+        // B) owner threads add their Gaussians' slots in slice order
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float4 t = acc[3 * gl + q];
-            gr[4 * q] = t.x; gr[4 * q + 1] = t.y; gr[4 * q + 2] = t.z; gr[4 * q + 3] = t.w;
+        for (int q = 0; q < kOwn; ++q) {
+            const int gl = threadIdx.x + q * kFinThreads;
+            for (int sg = 0; sg < s1 - s0; ++sg) {
+                const int sl = F.slot[sg][gl];
+                if (sl < 0) continue;
+                hit[q] = true;
+#pragma unroll
+                for (int j = 0; j < 11; ++j) acc[q][j] = fmaf(scale, F.stage[sl][j], acc[q][j]);
+            }
         }
-        adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit[gl] != 0, grad_sum,
-                      grad_cnt);
+        s0 = s1;
+    }
+#pragma unroll
+    for (int q = 0; q < kOwn; ++q) {
+        const int64_t g = g0 + threadIdx.x + q * kFinThreads;
+        if (g >= n) continue;
+        if (adam) {
+            float gr[kG];
+#pragma unroll
+            for (int j = 0; j < 11; ++j) gr[j] = acc[q][j];
+            gr[11] = 0.f;
+            adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit[q], grad_sum, grad_cnt);
+        } else if (hit[q]) {
+            float *row = grad + kG * g;
+#pragma unroll
+            for (int j = 0; j < 11; ++j) row[j] += acc[q][j];
+            if (touched) touched[g] = 1;
+        }
     }
 }
 
@@ -719,43 +749,43 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                       const_cast<float *>(c.intensity_raw),
                       const_cast<float *>(c.opacity_raw)};
     if (p.m_total > 0) {
-        const int th = 128;
-        finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
-            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base,
-            p.S, p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
-        UGS_LAUNCH_CHECK("finalize_records_kernel");
         chunk_bounds_kernel<<<(unsigned)((p.m_total + 255) / 256), 256, 0, st>>>(
             p.b.rec_gid, p.b.slice_base, p.b.slice_m, p.S, nchunk, p.m_total,
             p.b.chunk_lo);
         UGS_LAUNCH_CHECK("chunk_bounds_kernel");
+    } else {
+        // every slice is skipped through slice_m == 0; the fused update still
+        // runs for all rows
+        UGS_CUDA(cudaMemsetAsync(p.b.slice_m, 0, sizeof(int64_t) * p.S, st));
     }
     bg_slice_kernel<<<p.S, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
     UGS_LAUNCH_CHECK("bg_slice_kernel");
+    if (adam || p.m_total > 0) {
+        static bool attr = false;
+        if (!attr) {
+            UGS_CUDA(cudaFuncSetAttribute(finalize_update_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(FinSmem)));
+            attr = true;
+        }
+        finalize_update_kernel<<<nchunk, kFinThreads, sizeof(FinSmem), st>>>(
+            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.b.chunk_lo, p.b.slice_m,
+            p.b.slices, p.S, nchunk, c.n, c.means, c.l_raw, (float)c.beta, scale,
+            adam ? 1 : 0, grad, touched, cm, adam ? adam->m : nullptr,
+            adam ? adam->v : nullptr, adam ? adam->k : AdamConst{},
+            adam ? adam->grad_sum : nullptr, adam ? adam->grad_cnt : nullptr);
+        UGS_LAUNCH_CHECK("finalize_update_kernel");
+    }
     if (adam) {
-        // every slice with m == 0 is skipped through slice_m, so the fused
-        // update also runs (for all rows) when nothing was accepted
-        if (p.m_total == 0)
-            UGS_CUDA(cudaMemsetAsync(p.b.slice_m, 0, sizeof(int64_t) * p.S, st));
-        accumulate_adam_kernel<<<nchunk, 256, 0, st>>>(
-            p.b.rgrad, p.b.rec_gid, p.b.chunk_lo, p.b.slice_m, p.S, nchunk, c.n, scale,
-            cm, adam->m, adam->v, adam->k, adam->grad_sum, adam->grad_cnt);
-        UGS_LAUNCH_CHECK("accumulate_adam_kernel");
         bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                              nullptr, scale, 1, adam->m + kG * c.n,
                                              adam->v + kG * c.n, adam->k);
-        UGS_LAUNCH_CHECK("bg_finalize_kernel");
     } else {
-        if (p.m_total > 0) {
-            accumulate_kernel<<<nchunk, 256, 0, st>>>(p.b.rgrad, p.b.rec_gid, p.b.chunk_lo,
-                                                      p.b.slice_m, p.S, nchunk, grad,
-                                                      scale, touched);
-            UGS_LAUNCH_CHECK("accumulate_kernel");
-        }
         bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                              grad + kG * c.n, scale, 0, nullptr, nullptr,
                                              AdamConst{});
-        UGS_LAUNCH_CHECK("bg_finalize_kernel");
     }
+    UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
 }
