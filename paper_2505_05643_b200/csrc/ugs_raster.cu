@@ -523,6 +523,28 @@ __global__ void chunk_bounds_kernel(const int32_t *__restrict__ rec_gid,
         for (int k = c + 1; k <= nchunk; ++k) lo[k] = (int32_t)r1;
 }
 
+// One thread per record: its raw-parameter gradient (float64 chain) into
+// rgrad[r][0..10] (AoS-12 row), for the staged update below.
+__global__ void __launch_bounds__(128)
+finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
+                        const int32_t *__restrict__ rec_inst,
+                        const float *__restrict__ partial, int64_t m_total,
+                        const int64_t *__restrict__ slice_base, int S,
+                        const ugs_slice *__restrict__ slices,
+                        const float *__restrict__ means, const float *__restrict__ l_raw,
+                        float beta, float *__restrict__ rgrad) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m_total) return;
+    int s = 0;
+    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    float o[11];
+    record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw, beta, o);
+    float4 *dst = reinterpret_cast<float4 *>(rgrad + (size_t)r * kG);
+    dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    dst[2] = make_float4(o[8], o[9], o[10], 0.f);
+}
+
 constexpr int kStageCap = 1024;   // staged record gradients per pass
 constexpr int kGroupSlices = 16;  // slices per pass (slot-map rows)
 constexpr int kFinThreads = 256;
@@ -544,10 +566,11 @@ struct FinSmem {
 // for EVERY Gaussian of the range -- zero-gradient rows still move
 // (trainer.py:182-199) -- and the dense gradient never touches HBM; or
 // (adam == 0) the gradient rows are added into the dense AoS-12 buffer.
+template <bool kPre>
 __global__ void __launch_bounds__(kFinThreads)
 finalize_update_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                        const int32_t *__restrict__ rec_inst,
-                       const float *__restrict__ partial,
+                       const float *__restrict__ partial, const float *__restrict__ rgrad,
                        const int32_t *__restrict__ chunk_lo,
                        const int64_t *__restrict__ slice_m,
                        const ugs_slice *__restrict__ slices, int S, int nchunk, int64_t n,
@@ -598,8 +621,18 @@ finalize_update_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ 
             while (sg + 1 < s1 - s0 && F.lo[sg + 1] <= i) ++sg;
             const int s = s0 + sg;
             const int64_t r = chunk_lo[(size_t)s * (nchunk + 1) + c] + (i - F.lo[sg]);
-            float o[11];
-            record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw, beta, o);
+            float o[12];
+            if (kPre) {   // per-record gradients precomputed by finalize_records
+                const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float4 t = src[q];
+                    o[4 * q] = t.x; o[4 * q + 1] = t.y; o[4 * q + 2] = t.z; o[4 * q + 3] = t.w;
+                }
+            } else {
+                record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw,
+                            beta, o);
+            }
 #pragma unroll
             for (int j = 0; j < 11; ++j) F.stage[i][j] = o[j];
             F.slot[sg][rec_gid[r] - g0] = (int16_t)i;
@@ -763,13 +796,22 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     if (adam || p.m_total > 0) {
         static bool attr = false;
         if (!attr) {
-            UGS_CUDA(cudaFuncSetAttribute(finalize_update_kernel,
+            UGS_CUDA(cudaFuncSetAttribute(finalize_update_kernel<true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sizeof(FinSmem)));
             attr = true;
         }
-        finalize_update_kernel<<<nchunk, kFinThreads, sizeof(FinSmem), st>>>(
-            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.b.chunk_lo, p.b.slice_m,
+        if (p.m_total > 0) {
+            const int th = 128;
+            finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
+                p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total,
+                p.b.slice_base, p.S, p.b.slices, c.means, c.l_raw, (float)c.beta,
+                p.b.rgrad);
+            UGS_LAUNCH_CHECK("finalize_records_kernel");
+        }
+        finalize_update_kernel<true><<<nchunk, kFinThreads, sizeof(FinSmem), st>>>(
+            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.b.rgrad, p.b.chunk_lo,
+            p.b.slice_m,
             p.b.slices, p.S, nchunk, c.n, c.means, c.l_raw, (float)c.beta, scale,
             adam ? 1 : 0, grad, touched, cm, adam ? adam->m : nullptr,
             adam ? adam->v : nullptr, adam ? adam->k : AdamConst{},
