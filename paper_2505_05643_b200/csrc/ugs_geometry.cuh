@@ -41,33 +41,41 @@ struct Window {
 
 // Returns true iff the Gaussian is accepted for this slice (straddles the
 // plane, footprint meets the image rectangle, non-empty clamped window).
+// Probe-frame box along axis i: mean_probe_i -/+ sqrt(cut) * ||(Rw L^-T)_i||.
+__device__ __forceinline__ void box_axis(int i, const float mu[3], const Factor &f,
+                                         const ugs_slice &sl, float &bmin, float &bmax) {
+    float r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float a0 = __fmul_rn(sl.rw[3 * i + 0], f.LT[0][k]);
+        float a1 = __fmul_rn(sl.rw[3 * i + 1], f.LT[1][k]);
+        float a2 = __fmul_rn(sl.rw[3 * i + 2], f.LT[2][k]);
+        r[k] = __fadd_rn(__fadd_rn(a0, a1), a2);   // einsum order
+    }
+    float nrm = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(r[0], r[0]),
+                                               __fmul_rn(r[1], r[1])),
+                                     __fmul_rn(r[2], r[2])));
+    float half = __fmul_rn(sl.sqrt_cut, nrm);
+    // OpenBLAS sgemm (N,3)@(3,3): FMA chain, then + tw
+    float mp = __fmaf_rn(mu[2], sl.rw[3 * i + 2],
+                         __fmaf_rn(mu[1], sl.rw[3 * i + 1],
+                                   __fmul_rn(mu[0], sl.rw[3 * i + 0])));
+    mp = __fadd_rn(mp, sl.tw[i]);
+    bmin = __fsub_rn(mp, half);
+    bmax = __fadd_rn(mp, half);
+}
+
 __device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
                                             const ugs_slice &sl, Window &w) {
     float bmin[3], bmax[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        float r[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            float a0 = __fmul_rn(sl.rw[3 * i + 0], f.LT[0][k]);
-            float a1 = __fmul_rn(sl.rw[3 * i + 1], f.LT[1][k]);
-            float a2 = __fmul_rn(sl.rw[3 * i + 2], f.LT[2][k]);
-            r[k] = __fadd_rn(__fadd_rn(a0, a1), a2);   // einsum order
-        }
-        float nrm = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(r[0], r[0]),
-                                                   __fmul_rn(r[1], r[1])),
-                                         __fmul_rn(r[2], r[2])));
-        float half = __fmul_rn(sl.sqrt_cut, nrm);
-        // OpenBLAS sgemm (N,3)@(3,3): FMA chain, then + tw
-        float mp = __fmaf_rn(mu[2], sl.rw[3 * i + 2],
-                             __fmaf_rn(mu[1], sl.rw[3 * i + 1],
-                                       __fmul_rn(mu[0], sl.rw[3 * i + 0])));
-        mp = __fadd_rn(mp, sl.tw[i]);
-        bmin[i] = __fsub_rn(mp, half);
-        bmax[i] = __fadd_rn(mp, half);
-    }
-    bool keep = (bmin[2] <= 0.0f) && (bmax[2] >= 0.0f) &&
-                (bmax[0] >= -sl.x1h) && (bmin[0] <= sl.x1h) &&
+    // the plane-straddle test (axis z) rejects most Gaussians: evaluate it
+    // first; every axis is computed exactly as the reference does, so the
+    // early exit cannot change the (AND-ed) outcome
+    box_axis(2, mu, f, sl, bmin[2], bmax[2]);
+    if (!((bmin[2] <= 0.0f) && (bmax[2] >= 0.0f))) return false;
+    box_axis(0, mu, f, sl, bmin[0], bmax[0]);
+    box_axis(1, mu, f, sl, bmin[1], bmax[1]);
+    bool keep = (bmax[0] >= -sl.x1h) && (bmin[0] <= sl.x1h) &&
                 (bmax[1] >= -sl.x2h) && (bmin[1] <= sl.x2h);
     if (!keep) return false;
     float fu0 = ceilf(__fadd_rn(__fdiv_rn(bmin[0], sl.s), sl.cx));

@@ -22,7 +22,7 @@ constexpr int kLT = 32;              // output tile
 constexpr int kPad = 5;              // window radius
 constexpr int kF = kLT + 2 * kPad;   // 42: valid points needed
 constexpr int kI = kF + 2 * kPad;    // 52: input points needed
-constexpr int kLossThreads = 512;
+constexpr int kLossThreads = 1024;   // one 173 KB CTA per SM: all warps it can hold
 
 __constant__ double c_win[11];
 
