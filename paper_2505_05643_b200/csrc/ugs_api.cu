@@ -126,7 +126,8 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.slice_tot, b.slice_base, b.slices, b.rec,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.win_sparse, b.slice_tot,
+                    b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.bg_sums,
                     b.hist,
@@ -194,6 +195,14 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.blk_pairs, &b.blk_pairs_cap, (size_t)S * (nblk > 0 ? nblk : 1),
                      "alloc blk_pairs")))
         return rc;
+    // accept bits per (slice, warp) and the windows of accepted pairs,
+    // written by the count pass and read back by the emit pass
+    if ((rc = ensure(&b.amask, &b.amask_cap,
+                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc amask")))
+        return rc;
+    if ((rc = ensure(&b.win_sparse, &b.win_sparse_cap,
+                     (size_t)S * (c->n > 0 ? c->n : 1), "alloc win_sparse")))
+        return rc;
     {
         static_assert(sizeof(unsigned long long) == 8, "");
         size_t cap = b.slice_tot ? 192 : 0;
@@ -204,7 +213,8 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     std::vector<unsigned long long> tot(3 * S, 0ull);
     stage_begin(p, kStageCount, st);
     if (c->n > 0) {
-        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk, st)))
+        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
+                                       b.win_sparse, b.amask, st)))
             return rc;
         if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
             return rc;
@@ -281,7 +291,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if (c->n > 0 && m_total > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.owner, b.keys,
-                                      m_total, k_total, st)))
+                                      m_total, k_total, b.win_sparse, b.amask, st)))
             return rc;
     } else {
         int32_t zero = 0;

@@ -44,14 +44,17 @@ struct Window {
 // Probe-frame box along axis i: mean_probe_i -/+ sqrt(cut) * ||(Rw L^-T)_i||.
 __device__ __forceinline__ void box_axis(int i, const float mu[3], const Factor &f,
                                          const ugs_slice &sl, float &bmin, float &bmax) {
-    float r[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        float a0 = __fmul_rn(sl.rw[3 * i + 0], f.LT[0][k]);
-        float a1 = __fmul_rn(sl.rw[3 * i + 1], f.LT[1][k]);
-        float a2 = __fmul_rn(sl.rw[3 * i + 2], f.LT[2][k]);
-        r[k] = __fadd_rn(__fadd_rn(a0, a1), a2);   // einsum order
-    }
+    // einsum order (a0 + a1) + a2 with LT = (L^-1)^T upper-triangular: the
+    // terms with LT[j][k] == 0 are +-0 and adding +-0 leaves a sum unchanged
+    // up to the sign of zero, which the squares below discard -- so dropping
+    // them is bit-exact.
+    const float r[3] = {
+        __fmul_rn(sl.rw[3 * i + 0], f.LT[0][0]),
+        __fadd_rn(__fmul_rn(sl.rw[3 * i + 0], f.LT[0][1]),
+                  __fmul_rn(sl.rw[3 * i + 1], f.LT[1][1])),
+        __fadd_rn(__fadd_rn(__fmul_rn(sl.rw[3 * i + 0], f.LT[0][2]),
+                            __fmul_rn(sl.rw[3 * i + 1], f.LT[1][2])),
+                  __fmul_rn(sl.rw[3 * i + 2], f.LT[2][2]))};
     float nrm = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(r[0], r[0]),
                                                __fmul_rn(r[1], r[1])),
                                      __fmul_rn(r[2], r[2])));

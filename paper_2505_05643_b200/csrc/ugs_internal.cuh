@@ -36,6 +36,10 @@ struct PlanBuffers {
     size_t blk_cnt_cap = 0;
     unsigned *blk_pairs = nullptr;  // [S][nblk] (window pixel pairs)
     size_t blk_pairs_cap = 0;
+    uint32_t *amask = nullptr;      // [S][nblk*8] accept ballots of the count pass
+    size_t amask_cap = 0;
+    uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
+    size_t win_sparse_cap = 0;
     unsigned long long *slice_tot = nullptr; // [S][2] totals (accepted, tiles)
     int64_t *slice_base = nullptr;  // [S][2] record base, instance base
     ugs_slice *slices = nullptr;    // [S] device copy
@@ -134,14 +138,15 @@ void stage_end(ugs_plan *p, int stage, cudaStream_t st);
 // phase 1 (ugs_prepare.cu)
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
-                         cudaStream_t st);
+                         uint2 *win_sparse, uint32_t *amask, cudaStream_t st);
 int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st);
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         uint32_t *owner, uint32_t *keys, int64_t m_total,
-                        int64_t k_total, cudaStream_t st);
+                        int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
+                        cudaStream_t st);
 
 // radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
 // bits, stable.  On return *keys_out/*vals_out point at the sorted arrays

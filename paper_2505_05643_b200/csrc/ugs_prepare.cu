@@ -30,7 +30,8 @@ prepare_count_kernel(const float *__restrict__ means,
                      const float *__restrict__ l_raw, int64_t n, float beta,
                      const ugs_slice *__restrict__ slices, int S,
                      uint2 *__restrict__ blk_cnt, unsigned *__restrict__ blk_pairs,
-                     int nblk) {
+                     int nblk, uint2 *__restrict__ win_sparse,
+                     uint32_t *__restrict__ amask) {
     __shared__ ugs_slice sl[kMaxSlicesSmem];
     __shared__ uint2 wsum[kMaxSlicesSmem][kPrepThreads / 32];
     __shared__ unsigned wpairs[kMaxSlicesSmem][kPrepThreads / 32];
@@ -47,6 +48,8 @@ prepare_count_kernel(const float *__restrict__ means,
         mu[2] = __ldg(means + 3 * g + 2);
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
+    const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
     for (int s = 0; s < S; ++s) {
         unsigned acc = 0, tiles = 0, pairs = 0;
         Window w;
@@ -54,7 +57,12 @@ prepare_count_kernel(const float *__restrict__ means,
             acc = 1;
             tiles = (unsigned)window_tiles(w);
             pairs = (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1));
+            // the emit pass reads the window back instead of recomputing
+            win_sparse[(size_t)s * n + g] =
+                make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
         }
+        const unsigned bal = __ballot_sync(0xffffffffu, acc);
+        if (lane == 0) amask[(size_t)s * nwarp_all + gwarp] = bal;
         acc = __reduce_add_sync(0xffffffffu, acc);
         tiles = __reduce_add_sync(0xffffffffu, tiles);
         pairs = __reduce_add_sync(0xffffffffu, pairs);
@@ -154,32 +162,30 @@ prepare_emit_kernel(const float *__restrict__ means,
                     Rec *__restrict__ rec, int32_t *__restrict__ rec_gid,
                     int32_t *__restrict__ rec_inst, uint32_t *__restrict__ owner,
                     uint32_t *__restrict__ keys, int64_t m_total,
-                    int64_t k_total) {
-    __shared__ ugs_slice sl[kMaxSlicesSmem];
+                    int64_t k_total, const uint2 *__restrict__ win_sparse,
+                    const uint32_t *__restrict__ amask) {
     __shared__ uint2 wpre[kPrepThreads / 32];
-    load_slices_smem(sl, slices, S);
-    __syncthreads();
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
     const bool valid = g < n;
-    Factor f;
-    float mu[3] = {0.f, 0.f, 0.f};
     float color = 0.f, alpha = 0.f;
     if (valid) {
-        f = make_factor(l_raw, g, beta);
-        mu[0] = __ldg(means + 3 * g);
-        mu[1] = __ldg(means + 3 * g + 1);
-        mu[2] = __ldg(means + 3 * g + 2);
         color = sigmoid_f32(__ldg(intensity_raw + g));
         alpha = sigmoid_f32(__ldg(opacity_raw + g));
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
+    const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
     if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
     for (int s = 0; s < S; ++s) {
-        const ugs_slice &L = sl[s];
-        unsigned acc = 0, tiles = 0;
+        // the count pass left the accept bits and the windows of accepted
+        // (slice, Gaussian) pairs: no phase-1 recompute here
+        const unsigned acc = (__ldg(amask + (size_t)s * nwarp_all + gwarp) >> lane) & 1u;
+        unsigned tiles = 0;
         Window w;
-        if (valid && cull_window(mu, f, L, w)) {
-            acc = 1;
+        if (acc) {
+            const uint2 pw = __ldg(win_sparse + (size_t)s * n + g);
+            w.iu0 = pw.x & 0xffff; w.iu1 = pw.x >> 16;
+            w.iv0 = pw.y & 0xffff; w.iv1 = pw.y >> 16;
             tiles = (unsigned)window_tiles(w);
         }
         // block exclusive scan of (acc, tiles)
@@ -250,9 +256,10 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
 
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
-                         cudaStream_t st) {
+                         uint2 *win_sparse, uint32_t *amask, cudaStream_t st) {
     prepare_count_kernel<<<nblk, kPrepThreads, 0, st>>>(
-        c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk);
+        c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk,
+        win_sparse, amask);
     UGS_LAUNCH_CHECK("prepare_count_kernel");
     return UGS_OK;
 }
@@ -268,11 +275,12 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         uint32_t *owner, uint32_t *keys, int64_t m_total,
-                        int64_t k_total, cudaStream_t st) {
+                        int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
+                        cudaStream_t st) {
     prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
         S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, owner, keys,
-        m_total, k_total);
+        m_total, k_total, win_sparse, amask);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
         c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,
