@@ -128,7 +128,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     PlanBuffers &b = p->b;
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
-                    b.rec_gid, b.rec_inst, b.owner, b.keys, b.vals, b.keys2,
+                    b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.bg_sums,
                     b.hist,
                     b.scan_tmp, b.bin_range,
@@ -263,12 +263,12 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     UGS_CUDA(cudaMemcpyAsync(b.slice_m, p->h_m, sizeof(int64_t) * S,
                              cudaMemcpyHostToDevice, st));
     const size_t kneed = (size_t)k_total + 1;
-    if (kneed > b.inst_cap || !b.owner) {
-        void *olds[] = {b.owner, b.keys, b.vals, b.keys2, b.vals2, b.partial};
+    if (kneed > b.inst_cap || !b.idata) {
+        void *olds[] = {b.idata, b.keys, b.vals, b.keys2, b.vals2, b.partial};
         for (void *q : olds)
             if (q) cudaFree(q);
         b.inst_cap = kneed + kneed / 4 + 64;
-        UGS_CUDA(cudaMalloc(&b.owner, sizeof(uint32_t) * b.inst_cap));
+        UGS_CUDA(cudaMalloc(&b.idata, sizeof(Inst) * b.inst_cap));
         UGS_CUDA(cudaMalloc(&b.keys, sizeof(uint32_t) * b.inst_cap));
         UGS_CUDA(cudaMalloc(&b.vals, sizeof(uint32_t) * b.inst_cap));
         UGS_CUDA(cudaMalloc(&b.keys2, sizeof(uint32_t) * b.inst_cap));
@@ -290,7 +290,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     stage_begin(p, kStageEmit, st);
     if (c->n > 0 && m_total > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
-                                      b.rec, b.rec_gid, b.rec_inst, b.owner, b.keys,
+                                      b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
                                       m_total, k_total, b.win_sparse, b.amask, st)))
             return rc;
     } else {
@@ -379,7 +379,7 @@ __global__ void export_accepted_kernel(const Rec *__restrict__ rec,
     if (r >= m) return;
     if (acc) acc[r] = gid[r];
     if (win) {
-        const int wu = __float_as_int(rec[r].r2.y), wv = __float_as_int(rec[r].r2.z);
+        const int wu = __float_as_int(rec[r].r1.x), wv = __float_as_int(rec[r].r1.y);
         win[4 * r + 0] = wu & 0xffff;
         win[4 * r + 1] = wu >> 16;
         win[4 * r + 2] = wv & 0xffff;
@@ -388,12 +388,12 @@ __global__ void export_accepted_kernel(const Rec *__restrict__ rec,
 }
 
 __global__ void export_sorted_kernel(const uint32_t *__restrict__ vals,
-                                     const uint32_t *__restrict__ owner,
+                                     const Inst *__restrict__ idata,
                                      const int32_t *__restrict__ gid, int64_t k,
                                      int32_t *__restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
-    out[i] = gid[owner[vals[i]]];
+    out[i] = gid[__float_as_int(idata[vals[i]].w)];
 }
 }  // namespace
 }  // namespace ugs
@@ -423,7 +423,7 @@ extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
     if (sorted_gauss && p->k_total > 0) {
         const int th = 256;
         export_sorted_kernel<<<(unsigned)((p->k_total + th - 1) / th), th, 0, st>>>(
-            p->sorted_vals, p->b.owner, p->b.rec_gid, p->k_total, sorted_gauss);
+            p->sorted_vals, p->b.idata, p->b.rec_gid, p->k_total, sorted_gauss);
         UGS_LAUNCH_CHECK("export_sorted_kernel");
     }
     return UGS_OK;

@@ -111,18 +111,24 @@ __device__ __forceinline__ double sigmoid_f64(double x) {
 }
 
 // Plane-conditioned form of one accepted Gaussian on one slice (float64).
-// With e(u,v) = origin + u du + v dv - mu and y = L^T e, the reference's
-// q = |y|^2 is a 2-D quadratic in the pixel coordinates:
-//   q = H00 du^2 + 2 H01 du dv + H11 dv^2 + qmin   (du = u - u*, dv = v - v*)
-// where (u*, v*) is the in-plane conditional mean and qmin the out-of-plane
-// falloff.  Also used by the backward finalize, which needs e* = e(u*, v*).
+// With e(u,v) = origin + u du + v dv - mu and y = L^T e = c + u a + v b
+// (a = L^T du, b = L^T dv, c = L^T (origin - mu)), the reference's q = |y|^2
+// is a 2-D quadratic in the pixel coordinates.  Around any integer pixel
+// (pu, pv), with y_p = y(pu, pv) and exact integer offsets x = u - pu,
+// y = v - pv:
+//   q = H00 x^2 + 2 H01 x y + H11 y^2 + 2 (a.y_p) x + 2 (b.y_p) y + |y_p|^2.
+// plane_form computes H and the record's reference pixel (ui, vi): the
+// in-plane conditional mean rounded and clamped to the window (the window
+// centre when the in-plane precision is singular or ill-conditioned);
+// expansion() gives the linear/constant terms at a pixel.  Expanding each
+// tile instance around the point of its rectangle nearest (ui, vi) keeps the
+// float32 terms bounded by H times the tile size: no cancellation however
+// large or anisotropic the Gaussian (the reference evaluates every pair in
+// float64, _kernels.py:34-45).
 struct PlaneForm {
     double H00, H01, H11;
-    double cu, cv;         // centre actually used (integer + f32 fraction)
-    float cu_i, cv_i, cu_f, cv_f;
-    double qmin;           // q at (cu, cv)
-    double ystar[3];       // L^T e(cu, cv)
-    double a[3], b[3];     // L^T du, L^T dv
+    double a[3], b[3], c[3];
+    int ui, vi;            // reference pixel
 };
 
 __device__ __forceinline__ void lt_mul(const Factor &f, const double x[3],
@@ -135,43 +141,61 @@ __device__ __forceinline__ void lt_mul(const Factor &f, const double x[3],
 
 __device__ __forceinline__ PlaneForm plane_form(const float mu[3],
                                                 const Factor &f,
-                                                const ugs_slice &sl) {
+                                                const ugs_slice &sl,
+                                                const Window &w) {
     PlaneForm P;
     double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
     double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
     double d[3] = {(double)sl.origin[0] - mu[0], (double)sl.origin[1] - mu[1],
                    (double)sl.origin[2] - mu[2]};
-    double c[3];
     lt_mul(f, du, P.a);
     lt_mul(f, dv, P.b);
-    lt_mul(f, d, c);
+    lt_mul(f, d, P.c);
     P.H00 = P.a[0] * P.a[0] + P.a[1] * P.a[1] + P.a[2] * P.a[2];
     P.H01 = P.a[0] * P.b[0] + P.a[1] * P.b[1] + P.a[2] * P.b[2];
     P.H11 = P.b[0] * P.b[0] + P.b[1] * P.b[1] + P.b[2] * P.b[2];
-    double g0 = P.a[0] * c[0] + P.a[1] * c[1] + P.a[2] * c[2];
-    double g1 = P.b[0] * c[0] + P.b[1] * c[1] + P.b[2] * c[2];
-    double det = P.H00 * P.H11 - P.H01 * P.H01;
-    double us = 0.0, vs = 0.0;
-    if (det > 0.0) {
-        us = (P.H01 * g1 - P.H11 * g0) / det;
-        vs = (P.H01 * g0 - P.H00 * g1) / det;
+    const double h0 = P.a[0] * P.c[0] + P.a[1] * P.c[1] + P.a[2] * P.c[2];
+    const double h1 = P.b[0] * P.c[0] + P.b[1] * P.c[1] + P.b[2] * P.c[2];
+    const double det = P.H00 * P.H11 - P.H01 * P.H01;
+    double us = 0.5 * (double)(w.iu0 + w.iu1), vs = 0.5 * (double)(w.iv0 + w.iv1);
+    if (det > 1e-12 * P.H00 * P.H11) {
+        const double u1 = (P.H01 * h1 - P.H11 * h0) / det;
+        const double v1 = (P.H01 * h0 - P.H00 * h1) / det;
+        if (isfinite(u1) && isfinite(v1)) { us = u1; vs = v1; }
     }
-    const double lim = 4194304.0;   // keep integer parts exact in float32
-    us = fmin(fmax(us, -lim), lim);
-    vs = fmin(fmax(vs, -lim), lim);
-    double ui = floor(us), vi = floor(vs);
-    P.cu_i = (float)ui;
-    P.cv_i = (float)vi;
-    P.cu_f = (float)(us - ui);
-    P.cv_f = (float)(vs - vi);
-    if (P.cu_f >= 1.0f) P.cu_f = 0.99999994f;
-    if (P.cv_f >= 1.0f) P.cv_f = 0.99999994f;
-    P.cu = ui + (double)P.cu_f;
-    P.cv = vi + (double)P.cv_f;
-    for (int k = 0; k < 3; ++k) P.ystar[k] = c[k] + P.cu * P.a[k] + P.cv * P.b[k];
-    P.qmin = P.ystar[0] * P.ystar[0] + P.ystar[1] * P.ystar[1] +
-             P.ystar[2] * P.ystar[2];
+    P.ui = (int)fmin(fmax(rint(us), (double)w.iu0), (double)w.iu1);
+    P.vi = (int)fmin(fmax(rint(vs), (double)w.iv0), (double)w.iv1);
     return P;
+}
+
+// Linear and constant exponent terms (log2 domain, kq = -log2(e)/2, log2
+// alpha folded into F) around pixel (pu, pv).
+__device__ __forceinline__ void expansion(const PlaneForm &P, int pu, int pv, double kq,
+                                          double log2a, double &D, double &E, double &F) {
+    double y[3];
+    for (int k = 0; k < 3; ++k) y[k] = P.c[k] + (double)pu * P.a[k] + (double)pv * P.b[k];
+    D = 2.0 * kq * (P.a[0] * y[0] + P.a[1] * y[1] + P.a[2] * y[2]);
+    E = 2.0 * kq * (P.b[0] * y[0] + P.b[1] * y[1] + P.b[2] * y[2]);
+    F = kq * (y[0] * y[0] + y[1] * y[1] + y[2] * y[2]) + log2a;
+}
+
+// Clipped rectangle of window w in the tile whose pixel origin is (tu0, tv0),
+// and that rectangle's expansion pixel (ui, vi) clamped into it.
+struct TileRect {
+    int x0, x1, y0, y1;    // absolute pixel coordinates, inclusive
+    int pu, pv;
+};
+
+__device__ __forceinline__ TileRect tile_rect(int iu0, int iu1, int iv0, int iv1,
+                                              int tu0, int tv0, int ui, int vi) {
+    TileRect t;
+    t.x0 = max(iu0, tu0);
+    t.x1 = min(iu1, tu0 + kTile - 1);
+    t.y0 = max(iv0, tv0);
+    t.y1 = min(iv1, tv0 + kTile - 1);
+    t.pu = min(max(ui, t.x0), t.x1);
+    t.pv = min(max(vi, t.y0), t.y1);
+    return t;
 }
 
 }  // namespace ugs

@@ -19,15 +19,24 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-// Per accepted (slice, Gaussian) record: three float4 = 48 B.
-//   r0 = (cu_int, cv_int, cu_frac, cv_frac)   in-plane conditional centre in
-//        pixel units, split into an exact integer part and a [0,1) fraction
-//   r1 = (A, B2, C, E0): exponent (log2 domain) of the plane-conditioned
-//        Gaussian: log2(w) = A dx^2 + B2 dx dy + C dy^2 + E0, dx = u - cu
-//   r2 = (color, bits(iu0 | iu1 << 16), bits(iv0 | iv1 << 16), alpha)
+// Per accepted (slice, Gaussian) record: two float4 = 32 B.
+//   r0 = (A, B2, C, color): quadratic part of the plane-conditioned exponent
+//        (log2 domain, ugs_geometry.cuh PlaneForm), pixel units
+//   r1 = (bits(iu0 | iu1 << 16), bits(iv0 | iv1 << 16), alpha,
+//         bits(ui | vi << 16)): inclusive pixel window and the record's
+//        reference pixel (rounded in-plane centre clamped to the window)
 struct Rec {
-    float4 r0, r1, r2;
+    float4 r0, r1;
 };
+
+// Per tile instance (16 B): the exponent re-expanded EXACTLY (float64) around
+// the instance's own expansion pixel (pu, pv) = (ui, vi) clamped to the
+// instance's clipped tile rectangle:
+//   log2 w = A x^2 + B2 x y + C y^2 + D x + E y + F,  x = u - pu, y = v - pv
+// so pixel offsets never exceed the tile (|x|, |y| <= 15) whatever the
+// Gaussian's extent; inside the tile holding (ui, vi) the expansion is the
+// record's own.  (D, E, F, bits(record index)).
+using Inst = float4;
 
 // Per-batch binning state (device pointers are owned by the plan).
 struct PlanBuffers {
@@ -56,7 +65,7 @@ struct PlanBuffers {
     size_t chunk_lo_cap = 0;
     double2 *bg_sums = nullptr;     // [64] per-slice background gradient sums
     // instances
-    uint32_t *owner = nullptr;      // [K] record of each (unsorted) instance
+    Inst *idata = nullptr;          // [K] (D, E, F, record) of each (unsorted) instance
     uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)
     uint32_t *keys2 = nullptr, *vals2 = nullptr;   // ping-pong
     float *partial = nullptr;       // [K][8] backward per-instance partial sums
@@ -144,7 +153,7 @@ int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nb
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        uint32_t *owner, uint32_t *keys, int64_t m_total,
+                        Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
                         cudaStream_t st);
 

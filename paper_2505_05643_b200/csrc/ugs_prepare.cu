@@ -160,7 +160,7 @@ prepare_emit_kernel(const float *__restrict__ means,
                     const uint2 *__restrict__ blk_off, int nblk,
                     const int64_t *__restrict__ slice_base,
                     Rec *__restrict__ rec, int32_t *__restrict__ rec_gid,
-                    int32_t *__restrict__ rec_inst, uint32_t *__restrict__ owner,
+                    int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
                     uint32_t *__restrict__ keys, int64_t m_total,
                     int64_t k_total, const uint2 *__restrict__ win_sparse,
                     const uint32_t *__restrict__ amask) {
@@ -207,8 +207,9 @@ prepare_emit_kernel(const float *__restrict__ means,
         int64_t inst = slice_base[2 * s + 1] + bo.y + ot + xt - tiles;
         // the float64 plane conditioning and the tile expansion run in
         // build_records_kernel (one thread per record, full occupancy)
-        rec[r].r2 = make_float4(color, __int_as_float(w.iu0 | (w.iu1 << 16)),
-                                __int_as_float(w.iv0 | (w.iv1 << 16)), alpha);
+        rec[r].r0 = make_float4(0.f, 0.f, 0.f, color);
+        rec[r].r1 = make_float4(__int_as_float(w.iu0 | (w.iu1 << 16)),
+                                __int_as_float(w.iv0 | (w.iv1 << 16)), alpha, 0.f);
         rec_gid[r] = (int32_t)g;
         rec_inst[r] = (int32_t)inst;
     }
@@ -216,13 +217,13 @@ prepare_emit_kernel(const float *__restrict__ means,
 
 // One thread per accepted (slice, Gaussian) record: plane-conditioned
 // exponent (float64, ugs_geometry.cuh PlaneForm) and the record's tile
-// instances in row-major tile order.
+// instances in row-major tile order, each with its exact re-expansion.
 __global__ void __launch_bounds__(128)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
                      float beta, const ugs_slice *__restrict__ slices, int S,
                      const int64_t *__restrict__ slice_base, int64_t m_total,
                      Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
-                     const int32_t *__restrict__ rec_inst, uint32_t *__restrict__ owner,
+                     const int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
                      uint32_t *__restrict__ keys) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m_total) return;
@@ -233,20 +234,25 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const Factor f = make_factor(l_raw, g, beta);
     const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
                          __ldg(means + 3 * g + 2)};
-    const float4 r2 = rec[r].r2;
-    const PlaneForm P = plane_form(mu, f, L);
+    const float4 r0 = rec[r].r0, r1 = rec[r].r1;
+    const int wu = __float_as_int(r1.x), wv = __float_as_int(r1.y);
+    const Window w{wu & 0xffff, wu >> 16, wv & 0xffff, wv >> 16};
+    const PlaneForm P = plane_form(mu, f, L, w);
     const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
-    rec[r].r0 = make_float4(P.cu_i, P.cv_i, P.cu_f, P.cv_f);
-    rec[r].r1 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
-                            (float)(kq * P.H11),
-                            (float)(kq * P.qmin + log2((double)r2.w)));
-    const int wu = __float_as_int(r2.y), wv = __float_as_int(r2.z);
-    const int tx0 = (wu & 0xffff) >> 4, tx1 = (wu >> 16) >> 4;
-    const int ty0 = (wv & 0xffff) >> 4, ty1 = (wv >> 16) >> 4;
+    const double log2a = log2((double)r1.z);
+    rec[r].r0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
+                            (float)(kq * P.H11), r0.w);
+    rec[r].r1.w = __int_as_float(P.ui | (P.vi << 16));
+    const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
+    const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
     int64_t inst = rec_inst[r];
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
-            owner[inst] = (uint32_t)r;
+            const TileRect t = tile_rect(w.iu0, w.iu1, w.iv0, w.iv1, tx * kTile,
+                                         ty * kTile, P.ui, P.vi);
+            double D, E, F;
+            expansion(P, t.pu, t.pv, kq, log2a, D, E, F);
+            idata[inst] = make_float4((float)D, (float)E, (float)F, __int_as_float((int)r));
             keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
             ++inst;
         }
@@ -274,17 +280,17 @@ int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nb
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        uint32_t *owner, uint32_t *keys, int64_t m_total,
+                        Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
                         cudaStream_t st) {
     prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
-        S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, owner, keys,
+        S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, idata, keys,
         m_total, k_total, win_sparse, amask);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
         c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,
-        rec_inst, owner, keys);
+        rec_inst, idata, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;
 }

@@ -10,9 +10,9 @@
 //
 // Per pair the reference evaluates w = alpha exp(-q/2), q = |L^T(p - mu)|^2
 // (28 flops, float64).  Phase 1 has conditioned each Gaussian on the slice
-// plane (ugs_geometry.cuh, PlaneForm): log2 w is a 2-D quadratic in the pixel
-// offset from the in-plane centre, so a pair costs 4 FADD + 5 FMA + one MUFU
-// ex2, with the centre split into integer + fraction to avoid cancellation.
+// plane (ugs_geometry.cuh, PlaneForm): log2 w is a 2-D quadratic in the exact
+// integer pixel offset (x, y) from a reference pixel next to the in-plane
+// centre, so with x fixed per lane a pair costs 2 FMA + one MUFU ex2.
 //
 // Work split ("record per 8-lane group"): each warp holds 4 groups of 8 lanes;
 // a group sweeps one record's clipped rectangle 8 pixels at a time (k -> (x,y)
@@ -71,19 +71,19 @@ __device__ __forceinline__ float big_float(int x) {
     return __int_as_float(0x4B000000 | x);
 }
 
-__device__ __forceinline__ void load_rec(const Rec *__restrict__ rec,
-                                         const uint32_t *__restrict__ owner,
-                                         uint32_t inst, Rec &R) {
-    const uint32_t r = __ldg(owner + inst);
-    const float4 *src = reinterpret_cast<const float4 *>(rec + r);
+__device__ __forceinline__ void load_inst(const Rec *__restrict__ rec,
+                                          const Inst *__restrict__ idata,
+                                          uint32_t inst, float4 &I, Rec &R) {
+    I = __ldg(idata + inst);
+    const float4 *src = reinterpret_cast<const float4 *>(rec + __float_as_int(I.w));
     R.r0 = __ldg(src);
     R.r1 = __ldg(src + 1);
-    R.r2 = __ldg(src + 2);
 }
 
 // Shared-memory state of one staged batch.
-//   sA = (C1x, C1y, cu_frac, cv_frac)  dx = (big_float(x) - C1x) - cu_frac
-//   sB = (A, B2, C, E0)                log2 w = A dx^2 + B2 dx dy + C dy^2 + E0
+//   sA = (C1x, C1y, D, E)   x = big_float(lx) - C1x: exact integer offset of
+//                           the lane's pixel from the instance's expansion pixel
+//   sB = (A, B2, C, F)      log2 w = A x^2 + B2 x y + C y^2 + D x + E y + F
 //   sC = (color, base | (w-1) << 8, area, instance)   base = y0*16 + x0
 struct Batch {
     float4 sA[kBatch], sB[kBatch], sC[kBatch];
@@ -92,19 +92,24 @@ struct Batch {
     uint32_t base[kMaxTrips + 2];
 };
 
-__device__ __forceinline__ int stage_record(const Rec &R, int tu0, int tv0,
+__device__ __forceinline__ TileRect inst_rect(const Rec &R, int tu0, int tv0) {
+    const int wu = __float_as_int(R.r1.x), wv = __float_as_int(R.r1.y);
+    const int uv = __float_as_int(R.r1.w);
+    return tile_rect(wu & 0xffff, wu >> 16, wv & 0xffff, wv >> 16, tu0, tv0,
+                     uv & 0xffff, uv >> 16);
+}
+
+__device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int tu0, int tv0,
                                             uint32_t inst, int glen, float4 &a,
                                             float4 &b, float4 &c) {
-    const int wu = __float_as_int(R.r2.y), wv = __float_as_int(R.r2.z);
-    const int x0 = max((wu & 0xffff) - tu0, 0), x1 = min((wu >> 16) - tu0, kTile - 1);
-    const int y0 = max((wv & 0xffff) - tv0, 0), y1 = min((wv >> 16) - tv0, kTile - 1);
-    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
-    // integer offset of the rectangle origin from the integer centre (exact)
-    const float offx = (float)(tu0 + x0) - R.r0.x;
-    const float offy = (float)(tv0 + y0) - R.r0.y;
-    a = make_float4(8388608.0f - offx, 8388608.0f - offy, R.r0.z, R.r0.w);
-    b = R.r1;
-    c = make_float4(R.r2.x, __int_as_float((y0 * kTile + x0) | ((w - 1) << 8)),
+    const TileRect t = inst_rect(R, tu0, tv0);
+    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
+    const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
+    // rectangle origin relative to the expansion pixel (exact small integers)
+    a = make_float4(8388608.0f - (float)(t.x0 - t.pu), 8388608.0f - (float)(t.y0 - t.pv),
+                    I.x, I.y);
+    b = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+    c = make_float4(R.r0.w, __int_as_float((y0 * kTile + x0) | ((w - 1) << 8)),
                     __int_as_float(w * h), __int_as_float((int)inst));
     return (w * h + glen - 1) / glen;
 }
@@ -155,7 +160,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
 
 
 __global__ void __launch_bounds__(kRasterThreads)
-forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
+forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                const uint32_t *__restrict__ vals,
                const int2 *__restrict__ bin_range,
                const ugs_slice *__restrict__ slices,
@@ -178,10 +183,11 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
         __syncthreads();
         if (threadIdx.x < nb) {
             Rec R;
+            float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
-            load_rec(rec, owner, inst, R);
+            load_inst(rec, idata, inst, I, R);
             float4 c;
-            stage_record(R, tu0, tv0, inst, 32, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
+            stage_record(I, R, tu0, tv0, inst, 32, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
             // lane layout: cw = pow2 >= w columns x (32/cw) rows per sweep
             const int bw = __float_as_int(c.y);
             const int w = ((bw >> 8) & 15) + 1;
@@ -201,20 +207,19 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             const int R = 32 >> lcw;   // rows per sweep (even, so a lane's
                                        // row parity -- hence its swizzle -- is fixed)
             if (lx >= w || ly >= h) continue;
-            // per lane: dx fixed, log2 w = P + dy (Q + C dy)
-            const float dx = (big_float(lx) - a.x) - a.z;
-            const float P = fmaf(b.x * dx, dx, b.w), Q = b.y * dx;
-            float yo = big_float(ly) - a.y;          // exact integer offset
+            // per lane: x fixed, log2 w = P + y (Q + C y), x and y exact
+            const float dx = big_float(lx) - a.x;
+            const float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w), Q = fmaf(b.y, dx, a.w);
+            float dy = big_float(ly) - a.y;
             const int Y = y0 + ly, X = x0 + lx;
             float2 *ptr = my + (Y * kTile + (X ^ ((Y & 1) << 3)));
             for (int y = ly; y < h; y += R) {
-                const float dy = yo - a.w;
                 const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
                 float2 v = *ptr;
                 v.x = fmaf(wgt, c.x, v.x);
                 v.y += wgt;
                 *ptr = v;
-                yo += (float)R;
+                dy += (float)R;
                 ptr += R * kTile;
             }
         }
@@ -240,7 +245,7 @@ forward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
 // Strict-order variant: every pixel walks the tile's list in ascending
 // Gaussian order, one f32 add per pair (the reference's sequential loop).
 __global__ void __launch_bounds__(kRasterThreads)
-forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
+forward_ordered_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                        const uint32_t *__restrict__ vals,
                        const int2 *__restrict__ bin_range,
                        const ugs_slice *__restrict__ slices,
@@ -263,10 +268,13 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__
         __syncthreads();
         if (threadIdx.x < nb) {
             Rec R;
-            load_rec(rec, owner, __ldg(vals + b0 + threadIdx.x), R);
-            s0[threadIdx.x] = R.r0;
-            s1[threadIdx.x] = R.r1;
-            s2[threadIdx.x] = R.r2;
+            float4 I;
+            load_inst(rec, idata, __ldg(vals + b0 + threadIdx.x), I, R);
+            const TileRect tr = inst_rect(R, (t % sl.tiles_x) * kTile,
+                                          (t / sl.tiles_x) * kTile);
+            s0[threadIdx.x] = make_float4((float)tr.pu, (float)tr.pv, I.x, I.y);
+            s1[threadIdx.x] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+            s2[threadIdx.x] = make_float4(R.r0.w, R.r1.x, R.r1.y, 0.f);
         }
         __syncthreads();
         for (int j = 0; j < nb; ++j) {
@@ -275,9 +283,9 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__
             const int iu0 = wu & 0xffff, iu1 = wu >> 16, iv0 = wv & 0xffff, iv1 = wv >> 16;
             if (iu0 > wu0 + 7 || iu1 < wu0 || iv0 > wv0 + 3 || iv1 < wv0) continue;
             const float4 r0 = s0[j], r1 = s1[j];
-            const float dx = (fu - r0.x) - r0.z;
-            const float dy = (fv - r0.y) - r0.w;
-            const float e = fmaf(fmaf(r1.x, dx, r1.y * dy), dx, fmaf(r1.z * dy, dy, r1.w));
+            const float dx = fu - r0.x, dy = fv - r0.y;   // exact integers
+            const float e = fmaf(fmaf(r1.x, dx, fmaf(r1.y, dy, r0.z)), dx,
+                                 fmaf(fmaf(r1.z, dy, r0.w), dy, r1.w));
             float w = ex2_approx(e);
             const bool in = (unsigned)(u - iu0) <= (unsigned)(iu1 - iu0) &&
                             (unsigned)(v - iv0) <= (unsigned)(iv1 - iv0);
@@ -320,7 +328,7 @@ __device__ __forceinline__ float group_reduce16(const float a[8]) {
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
-backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
+backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 const uint32_t *__restrict__ vals,
                 const int2 *__restrict__ bin_range,
                 const ugs_slice *__restrict__ slices,
@@ -365,10 +373,11 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
         int trips = 0;
         if (threadIdx.x < nb) {
             Rec R;
+            float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
-            load_rec(rec, owner, inst, R);
+            load_inst(rec, idata, inst, I, R);
             float4 c;
-            stage_record(R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
+            stage_record(I, R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
             // 16-lane group layout: cw = pow2 >= w columns x (16/cw) rows per sweep
             const int bw = __float_as_int(c.y);
             const int w = ((bw >> 8) & 15) + 1;
@@ -396,14 +405,13 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
             // per lane dx is fixed: log2 w = P + dy (Q + C dy); the x moments
             // follow from the per-lane sums: sum t dx = dx S0, sum t dx^2 =
             // dx^2 S0, sum t dx dy = dx Sy
-            const float dx = (big_float(lx) - a.x) - a.z;
-            const float P = fmaf(b.x * dx, dx, b.w), Q = b.y * dx;
-            float yo = big_float(ly) - a.y;
+            const float dx = big_float(lx) - a.x;
+            const float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w), Q = fmaf(b.y, dx, a.w);
+            float dy = big_float(ly) - a.y;
             const float2 *gp = pix + (y0 + ly) * kTile + x0 + lx;
             float m0 = 0.f, S0 = 0.f, Sy = 0.f, Syy = 0.f;
             if (lx < w) {
                 for (int y = ly; y < h; y += rows) {
-                    const float dy = yo - a.w;
                     const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
                     const float2 g = *gp;
                     const float tq = fmaf(g.x, c.x, -g.y) * wgt;   // dw * w
@@ -412,7 +420,7 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
                     const float ty = tq * dy;
                     Sy += ty;
                     Syy = fmaf(ty, dy, Syy);
-                    yo += (float)rows;
+                    dy += (float)rows;
                     gp += rows * kTile;
                 }
             }
@@ -435,7 +443,8 @@ backward_kernel(const Rec *__restrict__ rec, const uint32_t *__restrict__ owner,
 }
 
 // Raw-parameter gradients of one record (ref gradients.py:84-103): sum its
-// instance partials in order, then with e* = e(centre),
+// instance partials in order (moments in the integer offsets from the
+// record's reference pixel), then with e* = e(reference pixel),
 // V = S0 e* + Sx du + Sy dv and
 // M = S0 e*e*^T + e* w^T + w e*^T + Sxx du du^T + Sxy (du dv^T + dv du^T)
 //     + Syy dv dv^T  (w = Sx du + Sy dv, dq = -t/2):
@@ -449,22 +458,37 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
                                             const float *__restrict__ means,
                                             const float *__restrict__ l_raw, float beta,
                                             float o[11]) {
+    // instance moments are about each instance's expansion pixel; shift them
+    // (float64, exact integer offsets) to the record's reference pixel
+    const Rec R = rec[r];
+    const int wub = __float_as_int(R.r1.x), wvb = __float_as_int(R.r1.y);
+    const int iu0 = wub & 0xffff, iu1 = wub >> 16, iv0 = wvb & 0xffff, iv1 = wvb >> 16;
+    const int uv = __float_as_int(R.r1.w), ui = uv & 0xffff, vi = uv >> 16;
+    const int tx0 = iu0 >> 4, tx1 = iu1 >> 4;
     double Sm[7] = {0, 0, 0, 0, 0, 0, 0};
     const int i0 = rec_inst[r], i1 = rec_inst[r + 1];
+    int tx = tx0, ty = iv0 >> 4;
     for (int i = i0; i < i1; ++i) {
+        const TileRect t = tile_rect(iu0, iu1, iv0, iv1, tx * kTile, ty * kTile, ui, vi);
+        const double ox = (double)(t.pu - ui), oy = (double)(t.pv - vi);
+        if (++tx > tx1) { tx = tx0; ++ty; }
         const float4 pa = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8);
         const float4 pb = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8 + 4);
-        Sm[0] += pa.x; Sm[1] += pa.y; Sm[2] += pa.z; Sm[3] += pa.w;
-        Sm[4] += pb.x; Sm[5] += pb.y; Sm[6] += pb.z;
+        const double s0 = pa.y, sx = pa.z, sy = pa.w;
+        Sm[0] += pa.x;
+        Sm[1] += s0;
+        Sm[2] += sx + ox * s0;
+        Sm[3] += sy + oy * s0;
+        Sm[4] += (double)pb.x + ox * (2.0 * sx + ox * s0);
+        Sm[5] += (double)pb.y + ox * sy + oy * sx + ox * oy * s0;
+        Sm[6] += (double)pb.z + oy * (2.0 * sy + oy * s0);
     }
     const int64_t g = rec_gid[r];
-    const Rec R = rec[r];
     const Factor f = make_factor(l_raw, g, beta);
     const double mu[3] = {means[3 * g], means[3 * g + 1], means[3 * g + 2]};
     const double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
     const double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
-    const double cu = (double)R.r0.x + (double)R.r0.z;
-    const double cv = (double)R.r0.y + (double)R.r0.w;
+    const double cu = (double)ui, cv = (double)vi;
     double es[3];
     for (int k = 0; k < 3; ++k)
         es[k] = ((double)sl.origin[k] - mu[k]) + cu * du[k] + cv * dv[k];
@@ -496,7 +520,7 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
     o[6] = (float)dL(1, 0);
     o[7] = (float)dL(2, 0);
     o[8] = (float)dL(2, 1);
-    const double c = R.r2.x, a = R.r2.w;
+    const double c = R.r0.w, a = R.r1.z;
     o[9] = (float)(Tc * c * (1.0 - c));
     o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
 }
@@ -750,11 +774,11 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     stage_begin(pm, kStageForward, st);
     if (p.ordered) {
         forward_ordered_kernel<<<grid, kRasterThreads, 0, st>>>(
-            p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
         forward_kernel<<<grid, kRasterThreads, kFwdSmem, st>>>(
-            p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
         UGS_LAUNCH_CHECK("forward_kernel");
     }
     stage_end(pm, kStageForward, st);
@@ -772,7 +796,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
     backward_kernel<<<grid, kRasterThreads, kBwdSmem, st>>>(
-        p.b.rec, p.b.owner, vals, p.b.bin_range, p.b.slices, num, den, dpix,
+        p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, num, den, dpix,
         c.bg_raw, p.b.partial, p.b.bin_bg);
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);

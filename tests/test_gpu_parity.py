@@ -289,3 +289,64 @@ def test_ordered_forward(case, rend):
     b0 = ug.rasterize(cloud, spec, p=p)
     np.testing.assert_allclose(b0.intensity_num.cpu().numpy(),
                                b1.intensity_num.cpu().numpy(), rtol=1e-5, atol=1e-6)
+
+
+def _needle_cloud(rng, n, R, t, beta=1e-6):
+    """Needles (sigma 60 mm x 0.4 x 0.4) whose long axis lies within ~1e-4 rad
+    of the slice plane, 1-3 mm off it: their in-plane conditional centre is
+    far outside the image while the ridge crosses it."""
+    means, l_raw = [], []
+    for _ in range(n):
+        phi = rng.uniform(0, np.pi)
+        eps = rng.uniform(-1e-4, 1e-4)
+        d_local = np.array([np.cos(phi) * np.cos(eps), np.sin(phi) * np.cos(eps), np.sin(eps)])
+        d = R @ d_local
+        q, _ = np.linalg.qr(np.column_stack([d, rng.standard_normal((3, 2))]))
+        sig = np.array([60.0, rng.uniform(0.3, 0.6), rng.uniform(0.3, 0.6)])
+        prec = q @ np.diag(1.0 / sig ** 2) @ q.T
+        # lower-triangular L with L L^T = prec: reverse-order Cholesky
+        J = np.eye(3)[::-1]
+        C = np.linalg.cholesky(J @ np.linalg.inv(prec) @ J)
+        L = np.linalg.inv(J @ C @ J).T
+        L = L * np.sign(np.diag(L))[None, :]
+        assert np.allclose(L @ L.T, prec, rtol=1e-8, atol=1e-10)
+        ld = np.sqrt(np.diag(L) - beta)
+        l_raw.append([ld[0], ld[1], ld[2], L[1, 0], L[2, 0], L[2, 1]])
+        off = R @ np.array([rng.uniform(-15, 15), rng.uniform(-15, 15), rng.uniform(-3, 3)])
+        means.append(t + off)
+    return dict(means=np.asarray(means, np.float32), l_raw=np.asarray(l_raw, np.float32),
+                intensity_raw=rng.normal(0, 1, n).astype(np.float32),
+                opacity_raw=rng.normal(0, 1, n).astype(np.float32),
+                bg_intensity_raw=0.3, bg_opacity_raw=-4.0, beta=beta)
+
+
+@pytest.mark.parametrize("kind", ["broad_lraw", "needles"])
+def test_degenerate_clouds_vs_oracle(kind):
+    """Training-state stress: l_raw components crossing zero (huge, strongly
+    anisotropic footprints) and near-in-plane needles (conditional centre far
+    outside the image).  Renders stay finite and within tolerance."""
+    rng = np.random.default_rng(17)
+    R, t = cases.random_pose(rng, 5.0)
+    if kind == "broad_lraw":
+        cloud_np = cases.uniform_cloud(3, 1500, [[-20] * 3, [20] * 3], -3.0, 3.0)
+    else:
+        cloud_np = _needle_cloud(rng, 300, R, t)
+    w = h = 128
+    spec = spec_of(R, t, w, h, 0.375)
+    sc = O.slice_constants(R, t, w, h, 0.375, 0.95)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    buf = ug.rasterize(cloud, spec)
+    num, den, acc, G = O.rasterize(*oracle_args(cloud_np, sc), workers=8)
+    assert np.array_equal(buf.accepted.cpu().numpy(), acc)
+    gn, gd = buf.intensity_num.cpu().numpy(), buf.opacity_sum.cpu().numpy()
+    assert np.isfinite(gn).all() and np.isfinite(gd).all()
+    np.testing.assert_allclose(gn, num, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(gd, den, rtol=RTOL, atol=ATOL)
+    dpix = np.random.default_rng(4).standard_normal((h, w)).astype(np.float32)
+    g = ug.backward(cloud, spec, buf, dpix)
+    ref = O.backward(*oracle_args(cloud_np, sc), num, den, dpix, workers=8, gathered=G)
+    for k in ("d_means", "d_l_raw", "d_intensity_raw", "d_opacity_raw"):
+        got = getattr(g, k).cpu().numpy()
+        assert np.isfinite(got).all(), k
+        np.testing.assert_allclose(got, ref[k], rtol=RTOL,
+                                   atol=ATOL * np.abs(ref[k]).max(), err_msg=k)
