@@ -47,9 +47,13 @@ __device__ __forceinline__ float adam_update(float g, float &m, float &v,
     vi = (float)__dadd_rn((double)vi, __dmul_rn(k.one_m_b2, __dmul_rn(gd, gd)));
     m = mi;
     v = vi;
-    const float mh = __fdiv_rn(mi, k.bc1);
-    const float vh = __fdiv_rn(vi, k.bc2);
-    return __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), k.eps));
+    // a zero numerator short-cuts the IEEE division exactly (0/x = 0 with
+    // the numerator's sign for x > 0); rows that have never seen a gradient
+    // (m = v = 0) would otherwise take the division's slow path (x = eps)
+    const float mh = mi == 0.f ? mi : __fdiv_rn(mi, k.bc1);
+    const float vh = vi == 0.f ? vi : __fdiv_rn(vi, k.bc2);
+    const float num = __fmul_rn(lr, mh);
+    return num == 0.f ? num : __fdiv_rn(num, __fadd_rn(__fsqrt_rn(vh), k.eps));
 }
 
 // ||d_means|| as numpy computes it for float32 rows: sqrt((x^2 + y^2) + z^2)

@@ -126,10 +126,10 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.win_sparse, b.slice_tot,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.warp_rec, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.rgrad, b.slice_m, b.chunk_lo, b.bg_sums,
+                    b.vals2, b.partial, b.rgrad, b.slice_m, b.bg_sums,
                     b.hist,
                     b.scan_tmp, b.bin_range,
                     b.bin_bg};
@@ -200,6 +200,10 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.amask, &b.amask_cap,
                      (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc amask")))
         return rc;
+    if ((rc = ensure(&b.warp_rec, &b.warp_rec_cap,
+                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
+                     "alloc warp_rec")))
+        return rc;
     if ((rc = ensure(&b.win_sparse, &b.win_sparse_cap,
                      (size_t)S * (c->n > 0 ? c->n : 1), "alloc win_sparse")))
         return rc;
@@ -251,9 +255,6 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
-    if ((rc = ensure(&b.chunk_lo, &b.chunk_lo_cap, chunk_lo_entries(S, c->n) + 1,
-                     "alloc chunk_lo")))
-        return rc;
     {
         size_t cap = b.slice_m ? 64 : 0;
         if ((rc = ensure(&b.slice_m, &cap, (size_t)64, "alloc slice_m"))) return rc;
@@ -291,7 +292,8 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if (c->n > 0 && m_total > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
-                                      m_total, k_total, b.win_sparse, b.amask, st)))
+                                      m_total, k_total, b.win_sparse, b.amask,
+                                      b.warp_rec, st)))
             return rc;
     } else {
         int32_t zero = 0;

@@ -47,6 +47,8 @@ struct PlanBuffers {
     size_t blk_pairs_cap = 0;
     uint32_t *amask = nullptr;      // [S][nblk*8] accept ballots of the count pass
     size_t amask_cap = 0;
+    int32_t *warp_rec = nullptr;    // [S][nblk*8] record index of each warp's first
+    size_t warp_rec_cap = 0;        //   accepted Gaussian (emit pass)
     uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
     size_t win_sparse_cap = 0;
     unsigned long long *slice_tot = nullptr; // [S][2] totals (accepted, tiles)
@@ -61,8 +63,6 @@ struct PlanBuffers {
     float *rgrad = nullptr;         // [M][12] per-record raw gradients (backward)
     size_t rgrad_cap = 0;
     int64_t *slice_m = nullptr;     // [S] accepted records per slice
-    int32_t *chunk_lo = nullptr;    // [S][nchunk+1] record bounds per Gaussian chunk
-    size_t chunk_lo_cap = 0;
     double2 *bg_sums = nullptr;     // [64] per-slice background gradient sums
     // instances
     Inst *idata = nullptr;          // [K] (D, E, F, record) of each (unsorted) instance
@@ -155,7 +155,7 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        cudaStream_t st);
+                        int32_t *warp_rec, cudaStream_t st);
 
 // radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
 // bits, stable.  On return *keys_out/*vals_out point at the sorted arrays
@@ -170,7 +170,6 @@ int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 
 // raster (ugs_raster.cu)
-size_t chunk_lo_entries(int S, int64_t n);
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st);
 struct AdamArgs;   // ugs_adam.cuh

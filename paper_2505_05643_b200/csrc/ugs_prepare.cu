@@ -163,7 +163,7 @@ prepare_emit_kernel(const float *__restrict__ means,
                     int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
                     uint32_t *__restrict__ keys, int64_t m_total,
                     int64_t k_total, const uint2 *__restrict__ win_sparse,
-                    const uint32_t *__restrict__ amask) {
+                    const uint32_t *__restrict__ amask, int32_t *__restrict__ warp_rec) {
     __shared__ uint2 wpre[kPrepThreads / 32];
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
     const bool valid = g < n;
@@ -201,8 +201,12 @@ prepare_emit_kernel(const float *__restrict__ means,
         __syncthreads();
         unsigned oa = 0, ot = 0;
         for (int k = 0; k < warp; ++k) { oa += wpre[k].x; ot += wpre[k].y; }
-        if (!acc) continue;
         const uint2 bo = blk_off[(size_t)s * nblk + blockIdx.x];
+        // record of this warp's first accepted Gaussian: the update pass maps
+        // (slice, Gaussian) -> record with one popcount
+        if (lane == 0)
+            warp_rec[(size_t)s * nwarp_all + gwarp] = (int32_t)(slice_base[2 * s] + bo.x + oa);
+        if (!acc) continue;
         const int64_t r = slice_base[2 * s] + bo.x + oa + xa - acc;
         int64_t inst = slice_base[2 * s + 1] + bo.y + ot + xt - tiles;
         // the float64 plane conditioning and the tile expansion run in
@@ -282,11 +286,11 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        cudaStream_t st) {
+                        int32_t *warp_rec, cudaStream_t st) {
     prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
         S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, idata, keys,
-        m_total, k_total, win_sparse, amask);
+        m_total, k_total, win_sparse, amask, warp_rec);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
         c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,

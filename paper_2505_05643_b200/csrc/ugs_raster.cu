@@ -45,8 +45,8 @@ constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
 constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
-constexpr int kAccStride = kTile * kTile;    // forward: one record per warp,
-                                             // one private buffer per warp
+constexpr int kAccStride = kTile * kTile;    // forward: one private tile
+constexpr int kGroups = kRasterThreads / 16; //   buffer per 16-lane group
 
 // Private-buffer slot of tile pixel p = 16*Y + X (float2 slots: a 64-bit
 // access is served 16 lanes at a time, bank pair = slot mod 16).  The forward
@@ -168,51 +168,64 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                float *__restrict__ den_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     Batch &B = *reinterpret_cast<Batch *>(smem);
-    float2 *acc = reinterpret_cast<float2 *>(smem + sizeof(Batch));   // [warp][256]
+    // one private (num, den) tile buffer per 16-lane group
+    float2 *acc = reinterpret_cast<float2 *>(smem + sizeof(Batch));   // [group][256]
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
-    for (int i = threadIdx.x; i < kWarps * kAccStride; i += kRasterThreads)
+    for (int i = threadIdx.x; i < kGroups * kAccStride; i += kRasterThreads)
         acc[i] = make_float2(0.f, 0.f);
-    float2 *my = acc + warp * kAccStride;
+    float2 *my = acc + (threadIdx.x >> 4) * kAccStride;
+    const int gl16 = lane & 15;
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
+        int trips = 0;
         if (threadIdx.x < nb) {
             Rec R;
             float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_inst(rec, idata, inst, I, R);
             float4 c;
-            stage_record(I, R, tu0, tv0, inst, 32, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
-            // lane layout: cw = pow2 >= w columns x (32/cw) rows per sweep
+            stage_record(I, R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
+            // 16-lane group layout: cw = pow2 >= w columns x (16/cw) rows per sweep
             const int bw = __float_as_int(c.y);
             const int w = ((bw >> 8) & 15) + 1;
             const int h = __float_as_int(c.z) / w;
             const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
+            const int rows = 16 >> lcw;
+            trips = (h + rows - 1) / rows;
             c.y = __int_as_float((bw & 255) | ((w - 1) << 8) | ((h - 1) << 12) | (lcw << 16));
             B.sC[threadIdx.x] = c;
         }
-        __syncthreads();
-        for (int j = warp; j < nb; j += kWarps) {
+        // records with equal sweep counts share a warp (two per warp)
+        sort_batch(B, trips, threadIdx.x < nb);
+        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
+            const int slot = s0 + (lane >> 4);
+            if (slot >= nb) continue;
+            const int j = B.order[slot];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
             const int pk = __float_as_int(c.y);
             const int x0 = pk & 15, y0 = (pk >> 4) & 15;
             const int w = ((pk >> 8) & 15) + 1, h = ((pk >> 12) & 15) + 1;
             const int lcw = (pk >> 16) & 7;
-            const int lx = lane & ((1 << lcw) - 1), ly = lane >> lcw;
-            const int R = 32 >> lcw;   // rows per sweep (even, so a lane's
-                                       // row parity -- hence its swizzle -- is fixed)
-            if (lx >= w || ly >= h) continue;
+            const int lx = gl16 & ((1 << lcw) - 1), ly = gl16 >> lcw;
+            const int R = 16 >> lcw;   // rows per sweep
+            if (lx >= w) continue;
             // per lane: x fixed, log2 w = P + y (Q + C y), x and y exact
             const float dx = big_float(lx) - a.x;
             const float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w), Q = fmaf(b.y, dx, a.w);
             float dy = big_float(ly) - a.y;
             const int Y = y0 + ly, X = x0 + lx;
             float2 *ptr = my + (Y * kTile + (X ^ ((Y & 1) << 3)));
+            // swizzled slot of row Y is 16 Y + (X ^ 8 (Y & 1)): an even R keeps
+            // the lane's row parity, R == 1 flips it every sweep (16 +- 8)
+            const int sx = (X ^ 8) - X;
+            int step = (R == 1) ? (kTile + ((Y & 1) ? -sx : sx)) : R * kTile;
+            const int flip = (R == 1) ? 2 * kTile : 2 * step;
             for (int y = ly; y < h; y += R) {
                 const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
                 float2 v = *ptr;
@@ -220,7 +233,8 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 v.y += wgt;
                 *ptr = v;
                 dy += (float)R;
-                ptr += R * kTile;
+                ptr += step;
+                step = flip - step;
             }
         }
     }
@@ -230,7 +244,7 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
         float n = 0.f, d = 0.f;
         const int sp = acc_swizzle(threadIdx.x);
 #pragma unroll
-        for (int g = 0; g < kWarps; ++g) {
+        for (int g = 0; g < kGroups; ++g) {
             const float2 q = acc[g * kAccStride + sp];
             n += q.x;
             d += q.y;
@@ -525,28 +539,6 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
     o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
 }
 
-constexpr int kChunk = 512;   // Gaussians per accumulate block
-
-// chunk_lo[s][c] = first record of slice s whose Gaussian index >= c*kChunk
-// (records of a slice are sorted by Gaussian index).
-__global__ void chunk_bounds_kernel(const int32_t *__restrict__ rec_gid,
-                                    const int64_t *__restrict__ slice_base,
-                                    const int64_t *__restrict__ slice_m, int S,
-                                    int nchunk, int64_t m_total,
-                                    int32_t *__restrict__ chunk_lo) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m_total) return;
-    int s = 0;
-    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
-    const int64_t r0 = slice_base[2 * s], r1 = r0 + slice_m[s];
-    const int c = rec_gid[r] / kChunk;
-    const int cprev = (r == r0) ? -1 : rec_gid[r - 1] / kChunk;
-    int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
-    for (int k = cprev + 1; k <= c; ++k) lo[k] = (int32_t)r;
-    if (r == r1 - 1)
-        for (int k = c + 1; k <= nchunk; ++k) lo[k] = (int32_t)r1;
-}
-
 // One thread per record: its raw-parameter gradient (float64 chain) into
 // rgrad[r][0..10] (AoS-12 row), for the staged update below.
 __global__ void __launch_bounds__(128)
@@ -569,129 +561,80 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
     dst[2] = make_float4(o[8], o[9], o[10], 0.f);
 }
 
-constexpr int kStageCap = 1024;   // staged record gradients per pass
-constexpr int kGroupSlices = 16;  // slices per pass (slot-map rows)
-constexpr int kFinThreads = 256;
+constexpr int kUpdThreads = 256;
 
-struct FinSmem {
-    float stage[kStageCap][11];
-    int16_t slot[kGroupSlices][kChunk];
-    int32_t lo[kGroupSlices + 1];
-};
-
-// Block c owns Gaussians [c*kChunk, (c+1)*kChunk).  In passes over groups of
-// slices whose records fit the staging area it
-//   A) computes every (slice, record) gradient of its range in parallel
-//      (record_grad, float64) into shared memory, noting each record's slot
-//      in a per-slice map, then
-//   B) lets the owner thread of each Gaussian add its slots in SLICE ORDER,
-// so every gradient sums its slices in a fixed order (deterministic, no
-// atomics).  Finally (adam != 0, single GPU) densify statistics and Adam run
-// for EVERY Gaussian of the range -- zero-gradient rows still move
-// (trainer.py:182-199) -- and the dense gradient never touches HBM; or
-// (adam == 0) the gradient rows are added into the dense AoS-12 buffer.
-template <bool kPre>
-__global__ void __launch_bounds__(kFinThreads)
-finalize_update_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
-                       const int32_t *__restrict__ rec_inst,
-                       const float *__restrict__ partial, const float *__restrict__ rgrad,
-                       const int32_t *__restrict__ chunk_lo,
-                       const int64_t *__restrict__ slice_m,
-                       const ugs_slice *__restrict__ slices, int S, int nchunk, int64_t n,
-                       const float *__restrict__ means, const float *__restrict__ l_raw,
-                       float beta, float scale, int adam, float *__restrict__ grad,
-                       uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
-                       float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
-                       int32_t *__restrict__ grad_cnt) {
-    extern __shared__ __align__(16) unsigned char fsm[];
-    FinSmem &F = *reinterpret_cast<FinSmem *>(fsm);
-    constexpr int kOwn = kChunk / kFinThreads;   // Gaussians per thread
-    const int c = blockIdx.x;
-    const int64_t g0 = (int64_t)c * kChunk;
-    float acc[kOwn][11];
-    bool hit[kOwn];
+// One thread per Gaussian g (the count pass's warp -> Gaussian mapping): for
+// every slice of the batch, in SLICE ORDER, the accept ballot says whether
+// (slice, g) has a record, and the record index is the warp's first record
+// plus a popcount -- no search, no staging, no atomics.  The record
+// gradients (finalize_records) are accumulated as acc = fma(scale, rg, acc),
+// so every gradient sums its slices in a fixed order (deterministic).  Then
+// (adam != 0, single GPU) densify statistics and Adam run for EVERY Gaussian
+// -- zero-gradient rows still move (trainer.py:182-199) -- and the dense
+// gradient never touches HBM; or (adam == 0) the rows are added into the
+// dense AoS-12 buffer.
+__global__ void __launch_bounds__(kUpdThreads)
+update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restrict__ warp_rec,
+                     const float *__restrict__ rgrad, int S, int64_t nwarp_all, int64_t n,
+                     float scale, int adam, float *__restrict__ grad,
+                     uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
+                     float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
+                     int32_t *__restrict__ grad_cnt) {
+    const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
+    const int64_t gwarp = g >> 5;
+    if (gwarp >= nwarp_all) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    float acc[11];
 #pragma unroll
-    for (int q = 0; q < kOwn; ++q) {
-        hit[q] = false;
+    for (int j = 0; j < 11; ++j) acc[j] = 0.f;
+    bool hit = false;
+    // four slices at a time: the ballot / base loads, then the record-row
+    // loads, are independent -> issued together (memory-level parallelism)
+    for (int s0 = 0; s0 < S; s0 += 4) {
+        uint32_t wd[4];
+        int32_t wb[4];
 #pragma unroll
-        for (int j = 0; j < 11; ++j) acc[q][j] = 0.f;
-    }
-    int s0 = 0;
-    while (s0 < S) {
-        // next group of slices whose records of this range fit the stage
-        int s1 = s0, tot = 0;
-        while (s1 < S && s1 - s0 < kGroupSlices) {
-            const int32_t *lo = chunk_lo + (size_t)s1 * (nchunk + 1);
-            const int cnt = slice_m[s1] ? lo[c + 1] - lo[c] : 0;
-            if (s1 > s0 && tot + cnt > kStageCap) break;
-            tot += cnt;
-            ++s1;
+        for (int q = 0; q < 4; ++q) {
+            const bool in = s0 + q < S;
+            const size_t o = (size_t)(in ? s0 + q : 0) * nwarp_all + gwarp;
+            wd[q] = in ? __ldg(amask + o) : 0u;
+            wb[q] = __ldg(warp_rec + o);
         }
-        __syncthreads();   // previous pass done with stage / slot
-        if (threadIdx.x <= s1 - s0) {
-            int pre = 0;
-            for (int s = s0; s < s0 + (int)threadIdx.x; ++s) {
-                const int32_t *lo = chunk_lo + (size_t)s * (nchunk + 1);
-                pre += slice_m[s] ? lo[c + 1] - lo[c] : 0;
-            }
-            F.lo[threadIdx.x] = pre;
-        }
-        for (int i = threadIdx.x; i < kGroupSlices * kChunk; i += kFinThreads)
-            (&F.slot[0][0])[i] = -1;
-        __syncthreads();
-        // A) all (slice, record) gradients of the pass, in parallel
-        for (int i = threadIdx.x; i < tot; i += kFinThreads) {
-            int sg = 0;
-            while (sg + 1 < s1 - s0 && F.lo[sg + 1] <= i) ++sg;
-            const int s = s0 + sg;
-            const int64_t r = chunk_lo[(size_t)s * (nchunk + 1) + c] + (i - F.lo[sg]);
-            float o[12];
-            if (kPre) {   // per-record gradients precomputed by finalize_records
+        float4 t[4][3];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((wd[q] >> lane) & 1u) {
+                const int64_t r = (int64_t)wb[q] + __popc(wd[q] & lt);
                 const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float4 t = src[q];
-                    o[4 * q] = t.x; o[4 * q + 1] = t.y; o[4 * q + 2] = t.z; o[4 * q + 3] = t.w;
-                }
-            } else {
-                record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw,
-                            beta, o);
-            }
-#pragma unroll
-            for (int j = 0; j < 11; ++j) F.stage[i][j] = o[j];
-            F.slot[sg][rec_gid[r] - g0] = (int16_t)i;
-        }
-        __syncthreads();
-        // B) owner threads add their Gaussians' slots in slice order
-#pragma unroll
-        for (int q = 0; q < kOwn; ++q) {
-            const int gl = threadIdx.x + q * kFinThreads;
-            for (int sg = 0; sg < s1 - s0; ++sg) {
-                const int sl = F.slot[sg][gl];
-                if (sl < 0) continue;
-                hit[q] = true;
-#pragma unroll
-                for (int j = 0; j < 11; ++j) acc[q][j] = fmaf(scale, F.stage[sl][j], acc[q][j]);
+                t[q][0] = __ldg(src);
+                t[q][1] = __ldg(src + 1);
+                t[q][2] = __ldg(src + 2);
             }
         }
-        s0 = s1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!((wd[q] >> lane) & 1u)) continue;
+            const float o[11] = {t[q][0].x, t[q][0].y, t[q][0].z, t[q][0].w, t[q][1].x,
+                                 t[q][1].y, t[q][1].z, t[q][1].w, t[q][2].x, t[q][2].y,
+                                 t[q][2].z};
+#pragma unroll
+            for (int j = 0; j < 11; ++j) acc[j] = fmaf(scale, o[j], acc[j]);
+            hit = true;
+        }
     }
+    if (g >= n) return;
+    if (adam) {
+        float gr[kG];
 #pragma unroll
-    for (int q = 0; q < kOwn; ++q) {
-        const int64_t g = g0 + threadIdx.x + q * kFinThreads;
-        if (g >= n) continue;
-        if (adam) {
-            float gr[kG];
+        for (int j = 0; j < 11; ++j) gr[j] = acc[j];
+        gr[11] = 0.f;
+        adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit, grad_sum, grad_cnt);
+    } else if (hit) {
+        float *row = grad + kG * g;
 #pragma unroll
-            for (int j = 0; j < 11; ++j) gr[j] = acc[q][j];
-            gr[11] = 0.f;
-            adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit[q], grad_sum, grad_cnt);
-        } else if (hit[q]) {
-            float *row = grad + kG * g;
-#pragma unroll
-            for (int j = 0; j < 11; ++j) row[j] += acc[q][j];
-            if (touched) touched[g] = 1;
-        }
+        for (int j = 0; j < 11; ++j) row[j] += acc[j];
+        if (touched) touched[g] = 1;
     }
 }
 
@@ -746,7 +689,7 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
     }
 }
 
-constexpr size_t kFwdSmem = sizeof(Batch) + sizeof(float2) * kWarps * kAccStride;
+constexpr size_t kFwdSmem = sizeof(Batch) + sizeof(float2) * kGroups * kAccStride;
 constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(float2) * (kTile * kTile + kWarps);
 
 int set_smem_attrs() {
@@ -801,46 +744,28 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
     stage_begin(pm, kStageFinalize, st);
-    const int nchunk = (int)((c.n + kChunk - 1) / kChunk);
     const CloudMut cm{const_cast<float *>(c.means), const_cast<float *>(c.l_raw),
                       const_cast<float *>(c.intensity_raw),
                       const_cast<float *>(c.opacity_raw)};
-    if (p.m_total > 0) {
-        chunk_bounds_kernel<<<(unsigned)((p.m_total + 255) / 256), 256, 0, st>>>(
-            p.b.rec_gid, p.b.slice_base, p.b.slice_m, p.S, nchunk, p.m_total,
-            p.b.chunk_lo);
-        UGS_LAUNCH_CHECK("chunk_bounds_kernel");
-    } else {
-        // every slice is skipped through slice_m == 0; the fused update still
-        // runs for all rows
-        UGS_CUDA(cudaMemsetAsync(p.b.slice_m, 0, sizeof(int64_t) * p.S, st));
-    }
     bg_slice_kernel<<<p.S, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
     UGS_LAUNCH_CHECK("bg_slice_kernel");
-    if (adam || p.m_total > 0) {
-        static bool attr = false;
-        if (!attr) {
-            UGS_CUDA(cudaFuncSetAttribute(finalize_update_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(FinSmem)));
-            attr = true;
-        }
-        if (p.m_total > 0) {
-            const int th = 128;
-            finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
-                p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total,
-                p.b.slice_base, p.S, p.b.slices, c.means, c.l_raw, (float)c.beta,
-                p.b.rgrad);
-            UGS_LAUNCH_CHECK("finalize_records_kernel");
-        }
-        finalize_update_kernel<true><<<nchunk, kFinThreads, sizeof(FinSmem), st>>>(
-            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.b.rgrad, p.b.chunk_lo,
-            p.b.slice_m,
-            p.b.slices, p.S, nchunk, c.n, c.means, c.l_raw, (float)c.beta, scale,
-            adam ? 1 : 0, grad, touched, cm, adam ? adam->m : nullptr,
-            adam ? adam->v : nullptr, adam ? adam->k : AdamConst{},
-            adam ? adam->grad_sum : nullptr, adam ? adam->grad_cnt : nullptr);
-        UGS_LAUNCH_CHECK("finalize_update_kernel");
+    if (p.m_total > 0) {
+        const int th = 128;
+        finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
+            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base, p.S,
+            p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
+        UGS_LAUNCH_CHECK("finalize_records_kernel");
+    }
+    if (c.n > 0 && (adam || p.m_total > 0)) {
+        const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
+        const int64_t nwarp_all = nblk * (kPrepThreads / 32);
+        update_gather_kernel<<<(unsigned)((nwarp_all * 32 + kUpdThreads - 1) / kUpdThreads),
+                               kUpdThreads, 0, st>>>(
+            p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale, adam ? 1 : 0,
+            grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
+            adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,
+            adam ? adam->grad_cnt : nullptr);
+        UGS_LAUNCH_CHECK("update_gather_kernel");
     }
     if (adam) {
         bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
@@ -854,10 +779,6 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageFinalize, st);
     return UGS_OK;
-}
-
-size_t chunk_lo_entries(int S, int64_t n) {
-    return (size_t)S * ((n + kChunk - 1) / kChunk + 1);
 }
 
 }  // namespace ugs
