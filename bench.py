@@ -55,6 +55,9 @@ def parse():
                     help="slices in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tts", action="store_true",
+                    help="skip the time-to-0.99-SSIM run (C2, N=1 only)")
+    ap.add_argument("--tts-budget", type=float, default=120.0)
     return ap.parse_args()
 
 
@@ -421,6 +424,18 @@ def run_ours(a):
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_cores(),
                                     "kind": "port", "sample": f"failed: {exc!r}"}
+    if rank == 0 and world == 1 and not a.no_tts:
+        # BASELINE metric part 2: time to 0.99 held-out SSIM (config C2, 1 GPU)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import time_to_ssim
+        del eng
+        torch.cuda.empty_cache()
+        r = time_to_ssim.run(budget=a.tts_budget, log=lambda m: None)
+        line["time_to_ssim"] = {k: r[k] for k in ("target", "reached_s", "best_ssim",
+                                                  "iterations", "slices_trained")}
+        line["time_to_ssim"]["config"] = ("C2: 200k Gaussians, 160^3 shells phantom, "
+                                          "256x256 @0.375 mm, 2048 train / 64 held-out "
+                                          "random-pose slices, batch 16, 1 GPU")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
