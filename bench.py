@@ -267,14 +267,36 @@ def run_ours(a):
     init = [t.clone() for t in (cloud.means, cloud.l_raw, cloud.intensity_raw,
                                 cloud.opacity_raw, cloud.bg_raw)]
 
+    # the step's loss goes device -> pinned host memory asynchronously; the
+    # host reads (and checks) step i's loss while step i+1 runs, so no step
+    # waits for its own loss (the reference aborts on a non-finite loss,
+    # trainer.py:392-396; here a non-finite loss fails the bench)
+    loss_host = torch.empty(1 << 12, dtype=torch.float64).pin_memory()
+    loss_ev = [None] * loss_host.numel()
+
+    def read_loss(i):
+        if i < 0 or loss_ev[i % len(loss_ev)] is None:
+            return None
+        loss_ev[i % len(loss_ev)].synchronize()
+        v = float(loss_host[i % len(loss_ev)])
+        if not np.isfinite(v):
+            raise RuntimeError(f"non-finite loss at step {i}")
+        return v
+
     def step(targets_batch=None, idx=None):
         it[0] += 1
         c = eng.cloud
         for dst, src in zip((c.means, c.l_raw, c.intensity_raw, c.opacity_raw,
                              c.bg_raw), init):
             dst.copy_(src)
-        return eng.step(idx if idx is not None else next_batch(), it[0],
-                        targets_batch=targets_batch)
+        lt = eng.step(idx if idx is not None else next_batch(), it[0],
+                      targets_batch=targets_batch, check_finite=False)
+        k = it[0] % len(loss_ev)
+        loss_host[k].copy_(lt, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        loss_ev[k] = ev
+        return read_loss(it[0] - 1)       # the previous step's loss
 
     def barrier():
         if world > 1:
@@ -305,6 +327,7 @@ def run_ours(a):
     e0.record()
     for _ in range(a.steps):
         step()
+    read_loss(it[0])
     e1.record()
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -323,18 +346,28 @@ def run_ours(a):
     e2e = None
     if not a.no_e2e:
         host_t = targets.cpu().pin_memory()
-        staging = torch.empty((B, a.size, a.size), dtype=torch.float32).pin_memory()
+        # double-buffered pinned staging: a buffer is refilled only after the
+        # H2D copy that read it has completed (its event)
+        staging = [torch.empty((B, a.size, a.size), dtype=torch.float32).pin_memory()
+                   for _ in range(2)]
+        st_ev = [None, None]
         dev_t = torch.empty((B, a.size, a.size), dtype=torch.float32, device="cuda")
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
         f0.record()
-        for _ in range(a.steps):
+        for i in range(a.steps):
             idx = next_batch()
-            torch.index_select(host_t, 0, torch.as_tensor(idx), out=staging)
-            dev_t.copy_(staging, non_blocking=True)
-            step(targets_batch=dev_t, idx=idx)     # loss .item() = the D2H read
+            b = i & 1
+            if st_ev[b] is not None:
+                st_ev[b].synchronize()
+            torch.index_select(host_t, 0, torch.as_tensor(idx), out=staging[b])
+            dev_t.copy_(staging[b], non_blocking=True)
+            st_ev[b] = torch.cuda.Event()
+            st_ev[b].record()
+            step(targets_batch=dev_t, idx=idx)     # + D2H read of the previous loss
+        read_loss(it[0])                           # ... and of the last one
         f1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0

@@ -68,14 +68,20 @@ __device__ __forceinline__ void box_axis(int i, const float mu[3], const Factor 
     bmax = __fadd_rn(mp, half);
 }
 
-__device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
-                                            const ugs_slice &sl, Window &w) {
-    float bmin[3], bmax[3];
-    // the plane-straddle test (axis z) rejects most Gaussians: evaluate it
-    // first; every axis is computed exactly as the reference does, so the
-    // early exit cannot change the (AND-ed) outcome
-    box_axis(2, mu, f, sl, bmin[2], bmax[2]);
-    if (!((bmin[2] <= 0.0f) && (bmax[2] >= 0.0f))) return false;
+// The plane-straddle test (axis z) rejects most Gaussians; it is evaluated
+// on its own first.  Every axis is computed exactly as the reference does,
+// so splitting the AND-ed test cannot change the outcome.
+__device__ __forceinline__ bool straddles(const float mu[3], const Factor &f,
+                                          const ugs_slice &sl) {
+    float bmin, bmax;
+    box_axis(2, mu, f, sl, bmin, bmax);
+    return (bmin <= 0.0f) && (bmax >= 0.0f);
+}
+
+// In-plane overlap + clamped window of a Gaussian that straddles the plane.
+__device__ __forceinline__ bool cull_window_xy(const float mu[3], const Factor &f,
+                                               const ugs_slice &sl, Window &w) {
+    float bmin[2], bmax[2];
     box_axis(0, mu, f, sl, bmin[0], bmax[0]);
     box_axis(1, mu, f, sl, bmin[1], bmax[1]);
     bool keep = (bmax[0] >= -sl.x1h) && (bmin[0] <= sl.x1h) &&
@@ -95,6 +101,11 @@ __device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
     w.iv0 = (int)fv0;
     w.iv1 = (int)fv1;
     return (w.iu0 <= w.iu1) && (w.iv0 <= w.iv1);
+}
+
+__device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
+                                            const ugs_slice &sl, Window &w) {
+    return straddles(mu, f, sl) && cull_window_xy(mu, f, sl, w);
 }
 
 __device__ __forceinline__ int window_tiles(const Window &w) {

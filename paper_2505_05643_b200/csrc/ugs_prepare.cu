@@ -33,9 +33,14 @@ prepare_count_kernel(const float *__restrict__ means,
                      int nblk, uint2 *__restrict__ win_sparse,
                      uint32_t *__restrict__ amask) {
     __shared__ ugs_slice sl[kMaxSlicesSmem];
-    __shared__ uint2 wsum[kMaxSlicesSmem][kPrepThreads / 32];
-    __shared__ unsigned wpairs[kMaxSlicesSmem][kPrepThreads / 32];
+    __shared__ unsigned s_acc[kMaxSlicesSmem], s_tiles[kMaxSlicesSmem],
+        s_pairs[kMaxSlicesSmem];
     load_slices_smem(sl, slices, S);
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+        s_acc[s] = 0;
+        s_tiles[s] = 0;
+        s_pairs[s] = 0;
+    }
     __syncthreads();
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
     const bool valid = g < n;
@@ -47,42 +52,43 @@ prepare_count_kernel(const float *__restrict__ means,
         mu[1] = __ldg(means + 3 * g + 1);
         mu[2] = __ldg(means + 3 * g + 2);
     }
+    // 1) the cheap plane-straddle test for every slice
+    uint64_t zmask = 0;
+    if (valid)
+        for (int s = 0; s < S; ++s)
+            if (straddles(mu, f, sl[s])) zmask |= 1ull << s;
+    // 2) the in-plane test and window only for the straddled slices: a lane
+    //    loops over ITS slices, so the warp runs max-over-lanes (~4 of 16)
+    //    iterations instead of every slice any lane straddles
+    uint64_t accmask = 0;
+    while (zmask) {
+        const int s = __ffsll((long long)zmask) - 1;
+        zmask &= zmask - 1;
+        Window w;
+        if (cull_window_xy(mu, f, sl[s], w)) {
+            accmask |= 1ull << s;
+            // the emit pass reads the window back instead of recomputing
+            win_sparse[(size_t)s * n + g] =
+                make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
+            // integer sums: shared atomics give exact (order-free) totals
+            atomicAdd(&s_tiles[s], (unsigned)window_tiles(w));
+            atomicAdd(&s_pairs[s], (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1)));
+        }
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
     for (int s = 0; s < S; ++s) {
-        unsigned acc = 0, tiles = 0, pairs = 0;
-        Window w;
-        if (valid && cull_window(mu, f, sl[s], w)) {
-            acc = 1;
-            tiles = (unsigned)window_tiles(w);
-            pairs = (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1));
-            // the emit pass reads the window back instead of recomputing
-            win_sparse[(size_t)s * n + g] =
-                make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, acc);
-        if (lane == 0) amask[(size_t)s * nwarp_all + gwarp] = bal;
-        acc = __reduce_add_sync(0xffffffffu, acc);
-        tiles = __reduce_add_sync(0xffffffffu, tiles);
-        pairs = __reduce_add_sync(0xffffffffu, pairs);
+        const unsigned bal = __ballot_sync(0xffffffffu, (unsigned)(accmask >> s) & 1u);
         if (lane == 0) {
-            wsum[s][warp] = make_uint2(acc, tiles);
-            wpairs[s][warp] = pairs;
+            amask[(size_t)s * nwarp_all + gwarp] = bal;
+            if (bal) atomicAdd(&s_acc[s], (unsigned)__popc(bal));
         }
     }
     __syncthreads();
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
-        uint2 t = make_uint2(0, 0);
-        unsigned pr = 0;
-#pragma unroll
-        for (int w = 0; w < kPrepThreads / 32; ++w) {
-            t.x += wsum[s][w].x;
-            t.y += wsum[s][w].y;
-            pr += wpairs[s][w];
-        }
-        blk_cnt[(size_t)s * nblk + blockIdx.x] = t;
-        blk_pairs[(size_t)s * nblk + blockIdx.x] = pr;
+        blk_cnt[(size_t)s * nblk + blockIdx.x] = make_uint2(s_acc[s], s_tiles[s]);
+        blk_pairs[(size_t)s * nblk + blockIdx.x] = s_pairs[s];
     }
 }
 

@@ -317,28 +317,27 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ ida
 }
 
 
-// Transpose-reduce of 8 values across a 16-lane half warp: on return lanes
-// with even group lane g hold the group total of value g >> 1.
-__device__ __forceinline__ float group_reduce16(const float a[8]) {
-    const int gl = threadIdx.x & 15;
-    const bool h8 = gl & 8, h4 = gl & 4, h2 = gl & 2;
+// Transpose-reduce of 8 values across an 8-lane group (3 levels, 7
+// shuffles): on return group lane g holds the group total of value g.
+__device__ __forceinline__ float group_reduce8(const float a[8]) {
+    const int gl = threadIdx.x & 7;
+    const bool h4 = gl & 4, h2 = gl & 2, h1 = gl & 1;
     float b[4], c[2];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float send = h8 ? a[k] : a[k + 4];
-        const float keep = h8 ? a[k + 4] : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        const float send = h4 ? a[k] : a[k + 4];
+        const float keep = h4 ? a[k + 4] : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float send = h4 ? b[k] : b[k + 2];
-        const float keep = h4 ? b[k + 2] : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        const float send = h2 ? b[k] : b[k + 2];
+        const float keep = h2 ? b[k + 2] : b[k];
+        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
-    const float send = h2 ? c[0] : c[1];
-    const float keep = h2 ? c[1] : c[0];
-    float d = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    return d + __shfl_xor_sync(0xffffffffu, d, 1);
+    const float send = h1 ? c[0] : c[1];
+    const float keep = h1 ? c[1] : c[0];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
@@ -391,21 +390,22 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_inst(rec, idata, inst, I, R);
             float4 c;
-            stage_record(I, R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
-            // 16-lane group layout: cw = pow2 >= w columns x (16/cw) rows per sweep
+            stage_record(I, R, tu0, tv0, inst, 8, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
+            // 8-lane group layout: w <= 8 -> cw = pow2 >= w columns x (8/cw)
+            // rows per sweep, two sweeps per iteration; w > 8 ("wide") -> one
+            // row per iteration, each lane takes columns gl and gl + 8
             const int bw = __float_as_int(c.y);
             const int w = ((bw >> 8) & 15) + 1;
             const int h = __float_as_int(c.z) / w;
             const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
-            const int rows = 16 >> lcw;
-            trips = (h + rows - 1) / rows;
+            trips = (lcw == 4) ? h : (h + (16 >> lcw) - 1) / (16 >> lcw);
             c.y = __int_as_float((bw & 255) | ((w - 1) << 8) | ((h - 1) << 12) | (lcw << 16));
             B.sC[threadIdx.x] = c;
         }
         sort_batch(B, trips, threadIdx.x < nb);
-        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
+        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
             // every lane takes part in the shuffles; empty lanes carry zeros
-            const int slot = s0 + (lane >> 4);
+            const int slot = s0 + (lane >> 3);
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
@@ -413,35 +413,70 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             const int x0 = pk & 15, y0 = (pk >> 4) & 15;
             const int w = ((pk >> 8) & 15) + 1, h = live ? ((pk >> 12) & 15) + 1 : 0;
             const int lcw = (pk >> 16) & 7;
-            const int gl16 = lane & 15;
-            const int lx = gl16 & ((1 << lcw) - 1), ly = gl16 >> lcw;
-            const int rows = 16 >> lcw;
-            // per lane dx is fixed: log2 w = P + dy (Q + C dy); the x moments
-            // follow from the per-lane sums: sum t dx = dx S0, sum t dx^2 =
-            // dx^2 S0, sum t dx dy = dx Sy
-            const float dx = big_float(lx) - a.x;
-            const float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w), Q = fmaf(b.y, dx, a.w);
-            float dy = big_float(ly) - a.y;
-            const float2 *gp = pix + (y0 + ly) * kTile + x0 + lx;
-            float m0 = 0.f, S0 = 0.f, Sy = 0.f, Syy = 0.f;
-            if (lx < w) {
-                for (int y = ly; y < h; y += rows) {
-                    const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
-                    const float2 g = *gp;
-                    const float tq = fmaf(g.x, c.x, -g.y) * wgt;   // dw * w
-                    m0 = fmaf(g.x, wgt, m0);
-                    S0 += tq;
-                    const float ty = tq * dy;
-                    Sy += ty;
-                    Syy = fmaf(ty, dy, Syy);
-                    dy += (float)rows;
-                    gp += rows * kTile;
-                }
+            const int gl = lane & 7;
+            // two pixel streams per lane, A and B, each with a fixed column:
+            //   wide (cw = 16): A = (gl, row 0), B = (gl + 8, row 0), +1 row
+            //   narrow:         A = (lx, ly),    B = (lx, ly + R),    +2R rows
+            // with R = 8 >> lcw, both are lx = gl & (cw-1), ly = gl >> lcw,
+            // B = A + (8 [wide] | 0, R), stride = 16 >> lcw
+            const int lxA = gl & ((1 << lcw) - 1), lyA = gl >> lcw;
+            const int wideoff = (lcw >> 2) << 3;
+            const int lxB = lxA + wideoff, lyB = lyA + (8 >> lcw);
+            const int ls = 4 - lcw;   // log2 of the row stride
+            const int stride = 1 << ls;
+            const bool okA = lxA < w && lyA < h, okB = lxB < w && lyB < h;
+            const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
+            // wide rows always pair A with B (B masked when out of the rectangle)
+            const int nB = okB ? (h - lyB + stride - 1) >> ls : (wideoff ? nA : 0);
+            // per lane dx is fixed per stream: log2 w = P + dy (Q + C dy); the x
+            // moments follow from the per-stream sums (sum t dx = dx S0, ...)
+            const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)wideoff;
+            const float PA = fmaf(fmaf(b.x, dxA, a.z), dxA, b.w), QA = fmaf(b.y, dxA, a.w);
+            const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
+            const float QB = fmaf(b.y, dxB, a.w);
+            float dyA = big_float(lyA) - a.y, dyB = dyA + (float)(8 >> lcw);
+            const float2 *gA = pix + (y0 + lyA) * kTile + x0 + lxA;
+            const float2 *gB = okB ? gA + ((8 >> lcw) * kTile + wideoff) : gA;
+            const int gstep = okB ? stride * kTile : 0;
+            const float fstride = (float)stride;
+            float m0 = 0.f, S0a = 0.f, Sya = 0.f, Syya = 0.f, S0b = 0.f, Syb = 0.f, Syyb = 0.f;
+            int i = 0;
+            for (; i < nB; ++i) {
+                const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
+                const float wb = ex2_approx(fmaf(dyB, fmaf(b.z, dyB, QB), PB));
+                const float2 ga = *gA, gb = *gB;
+                const float ta = fmaf(ga.x, c.x, -ga.y) * wa;   // dw * w
+                const float tb = fmaf(gb.x, c.x, -gb.y) * wb;
+                m0 = fmaf(ga.x, wa, m0);
+                m0 = fmaf(gb.x, wb, m0);
+                S0a += ta;
+                S0b += tb;
+                const float tya = ta * dyA, tyb = tb * dyB;
+                Sya += tya;
+                Syb += tyb;
+                Syya = fmaf(tya, dyA, Syya);
+                Syyb = fmaf(tyb, dyB, Syyb);
+                dyA += fstride;
+                dyB += fstride;
+                gA += stride * kTile;
+                gB += gstep;
             }
-            float m[8] = {m0, S0, dx * S0, Sy, dx * dx * S0, dx * Sy, Syy, 0.f};
-            const float red = group_reduce16(m);
-            if (live && (lane & 1) == 0)
-                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + (gl16 >> 1)] = red;
+            if (i < nA) {   // narrow tail: one more row of stream A
+                const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
+                const float2 ga = *gA;
+                const float ta = fmaf(ga.x, c.x, -ga.y) * wa;
+                m0 = fmaf(ga.x, wa, m0);
+                S0a += ta;
+                const float tya = ta * dyA;
+                Sya += tya;
+                Syya = fmaf(tya, dyA, Syya);
+            }
+            float m[8] = {m0, S0a + S0b, fmaf(dxA, S0a, dxB * S0b), Sya + Syb,
+                          fmaf(dxA * dxA, S0a, dxB * dxB * S0b), fmaf(dxA, Sya, dxB * Syb),
+                          Syya + Syyb, 0.f};
+            const float red = group_reduce8(m);
+            if (live)
+                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + gl] = red;
         }
     }
     __syncthreads();
