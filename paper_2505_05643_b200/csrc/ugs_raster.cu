@@ -84,12 +84,17 @@ __device__ __forceinline__ void load_inst(const Rec *__restrict__ rec,
 //   sA = (C1x, C1y, D, E)   x = big_float(lx) - C1x: exact integer offset of
 //                           the lane's pixel from the instance's expansion pixel
 //   sB = (A, B2, C, F)      log2 w = A x^2 + B2 x y + C y^2 + D x + E y + F
-//   sC = (color, base | (w-1) << 8, area, instance)   base = y0*16 + x0
+//   sC = (color, ls, -, instance)   ls = log2 of the stream's row stride
+//   sL = (cmaskA, lcwA, wideoff, lyoff), sM = (w, h, x0, y0): the record's
+//        two-stream lane layout (stage_layout)
 struct Batch {
     float4 sA[kBatch], sB[kBatch], sC[kBatch];
     uint16_t order[kBatch];            // staged slot of the j-th record by trips
     uint32_t wcnt[kWarps][kMaxTrips + 2];
     uint32_t base[kMaxTrips + 2];
+};
+struct Layout {   // two-stream layouts (backward), after the Batch
+    int4 sL[kBatch], sM[kBatch];
 };
 
 __device__ __forceinline__ TileRect inst_rect(const Rec &R, int tu0, int tv0) {
@@ -99,19 +104,55 @@ __device__ __forceinline__ TileRect inst_rect(const Rec &R, int tu0, int tv0) {
                      uv & 0xffff, uv >> 16);
 }
 
+// Stages one tile instance (one thread per record) for a group of G lanes
+// and returns its loop trip count.  Two pixel streams per lane, A and B, each
+// with a fixed column, so that x (hence P, Q) is per-lane constant:
+//   narrow (cw = pow2 >= w <= 8): A = (lx, ly), B = A + (0, R), R = G/cw,
+//                                 both advance 2R rows per iteration
+//   wide   (w > 8):               A = (gl & 7, gl >> 3), B = A + (8, 0),
+//                                 both advance G/8 rows per iteration
+// with lx = gl & (cw-1), ly = gl >> log2 cw.  Every row stride is even for
+// G = 16 (the forward), so a lane's row parity -- its swizzle -- is fixed.
+template <int G>
 __device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int tu0, int tv0,
-                                            uint32_t inst, int glen, float4 &a,
-                                            float4 &b, float4 &c) {
+                                            uint32_t inst, Batch &B, Layout &Ly,
+                                            int slot) {
+    constexpr int lg = (G == 16) ? 4 : 3;
     const TileRect t = inst_rect(R, tu0, tv0);
     const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
+    const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
+    const bool wide = lcw == 4;
+    const int lcwA = wide ? 3 : lcw;
+    const int ls = wide ? lg - 3 : lg + 1 - lcw;
     // rectangle origin relative to the expansion pixel (exact small integers)
-    a = make_float4(8388608.0f - (float)(t.x0 - t.pu), 8388608.0f - (float)(t.y0 - t.pv),
-                    I.x, I.y);
-    b = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
-    c = make_float4(R.r0.w, __int_as_float((y0 * kTile + x0) | ((w - 1) << 8)),
-                    __int_as_float(w * h), __int_as_float((int)inst));
-    return (w * h + glen - 1) / glen;
+    B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
+                             8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
+    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+    B.sC[slot] = make_float4(R.r0.w, __int_as_float(ls), 0.f, __int_as_float((int)inst));
+    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, wide ? 8 : 0, wide ? 0 : (G >> lcw));
+    Ly.sM[slot] = make_int4(w, h, x0, y0);
+    return (h + (1 << ls) - 1) >> ls;
+}
+
+// Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
+// columns x (16/cw) rows per sweep; sC.y packs base = y0*16 + x0, w-1, h-1
+// and log2 cw.  Returns the number of sweeps.
+__device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, int tu0,
+                                                 int tv0, uint32_t inst, Batch &B,
+                                                 int slot) {
+    const TileRect t = inst_rect(R, tu0, tv0);
+    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
+    const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
+    const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
+    B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
+                             8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
+    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+    B.sC[slot] = make_float4(R.r0.w,
+                             __int_as_float((y0 * kTile + x0) | ((w - 1) << 8) |
+                                            ((h - 1) << 12) | (lcw << 16)),
+                             0.f, __int_as_float((int)inst));
+    return (h + (16 >> lcw) - 1) >> (4 - lcw);
 }
 
 // Stable counting sort of the staged slots by trip count (warp match-any
@@ -189,17 +230,7 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_inst(rec, idata, inst, I, R);
-            float4 c;
-            stage_record(I, R, tu0, tv0, inst, 16, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
-            // 16-lane group layout: cw = pow2 >= w columns x (16/cw) rows per sweep
-            const int bw = __float_as_int(c.y);
-            const int w = ((bw >> 8) & 15) + 1;
-            const int h = __float_as_int(c.z) / w;
-            const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
-            const int rows = 16 >> lcw;
-            trips = (h + rows - 1) / rows;
-            c.y = __int_as_float((bw & 255) | ((w - 1) << 8) | ((h - 1) << 12) | (lcw << 16));
-            B.sC[threadIdx.x] = c;
+            trips = stage_record_rows(I, R, tu0, tv0, inst, B, threadIdx.x);
         }
         // records with equal sweep counts share a warp (two per warp)
         sort_batch(B, trips, threadIdx.x < nb);
@@ -350,7 +381,8 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg) {
     extern __shared__ __align__(16) unsigned char smem[];
     Batch &B = *reinterpret_cast<Batch *>(smem);
-    float2 *pix = reinterpret_cast<float2 *>(smem + sizeof(Batch));  // (G, G chat)
+    Layout &Ly = *reinterpret_cast<Layout *>(smem + sizeof(Batch));
+    float2 *pix = reinterpret_cast<float2 *>(smem + sizeof(Batch) + sizeof(Layout));  // (G, G chat)
     float2 *s_bg = pix + kTile * kTile;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
@@ -389,18 +421,7 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_inst(rec, idata, inst, I, R);
-            float4 c;
-            stage_record(I, R, tu0, tv0, inst, 8, B.sA[threadIdx.x], B.sB[threadIdx.x], c);
-            // 8-lane group layout: w <= 8 -> cw = pow2 >= w columns x (8/cw)
-            // rows per sweep, two sweeps per iteration; w > 8 ("wide") -> one
-            // row per iteration, each lane takes columns gl and gl + 8
-            const int bw = __float_as_int(c.y);
-            const int w = ((bw >> 8) & 15) + 1;
-            const int h = __float_as_int(c.z) / w;
-            const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
-            trips = (lcw == 4) ? h : (h + (16 >> lcw) - 1) / (16 >> lcw);
-            c.y = __int_as_float((bw & 255) | ((w - 1) << 8) | ((h - 1) << 12) | (lcw << 16));
-            B.sC[threadIdx.x] = c;
+            trips = stage_record<8>(I, R, tu0, tv0, inst, B, Ly, threadIdx.x);
         }
         sort_batch(B, trips, threadIdx.x < nb);
         for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
@@ -409,38 +430,31 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
-            const int pk = __float_as_int(c.y);
-            const int x0 = pk & 15, y0 = (pk >> 4) & 15;
-            const int w = ((pk >> 8) & 15) + 1, h = live ? ((pk >> 12) & 15) + 1 : 0;
-            const int lcw = (pk >> 16) & 7;
+            const int4 L = Ly.sL[j], M = Ly.sM[j];
             const int gl = lane & 7;
-            // two pixel streams per lane, A and B, each with a fixed column:
-            //   wide (cw = 16): A = (gl, row 0), B = (gl + 8, row 0), +1 row
-            //   narrow:         A = (lx, ly),    B = (lx, ly + R),    +2R rows
-            // with R = 8 >> lcw, both are lx = gl & (cw-1), ly = gl >> lcw,
-            // B = A + (8 [wide] | 0, R), stride = 16 >> lcw
-            const int lxA = gl & ((1 << lcw) - 1), lyA = gl >> lcw;
-            const int wideoff = (lcw >> 2) << 3;
-            const int lxB = lxA + wideoff, lyB = lyA + (8 >> lcw);
-            const int ls = 4 - lcw;   // log2 of the row stride
-            const int stride = 1 << ls;
-            const bool okA = lxA < w && lyA < h, okB = lxB < w && lyB < h;
+            const int h = live ? M.y : 0;
+            // the two pixel streams of stage_record<8>
+            const int lxA = gl & L.x, lyA = gl >> L.y;
+            const int lxB = lxA + L.z, lyB = lyA + L.w;
+            const int ls = __float_as_int(c.y), stride = 1 << ls;
+            const bool okA = lxA < M.x && lyA < h, okB = lxB < M.x && lyB < h;
             const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
             // wide rows always pair A with B (B masked when out of the rectangle)
-            const int nB = okB ? (h - lyB + stride - 1) >> ls : (wideoff ? nA : 0);
+            const int nB = okB ? (h - lyB + stride - 1) >> ls : (L.z ? nA : 0);
             // per lane dx is fixed per stream: log2 w = P + dy (Q + C dy); the x
             // moments follow from the per-stream sums (sum t dx = dx S0, ...)
-            const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)wideoff;
+            const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)L.z;
             const float PA = fmaf(fmaf(b.x, dxA, a.z), dxA, b.w), QA = fmaf(b.y, dxA, a.w);
             const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
             const float QB = fmaf(b.y, dxB, a.w);
-            float dyA = big_float(lyA) - a.y, dyB = dyA + (float)(8 >> lcw);
-            const float2 *gA = pix + (y0 + lyA) * kTile + x0 + lxA;
-            const float2 *gB = okB ? gA + ((8 >> lcw) * kTile + wideoff) : gA;
+            float dyA = big_float(lyA) - a.y, dyB = dyA + (float)L.w;
+            const float2 *gA = pix + (M.w + lyA) * kTile + M.z + lxA;
+            const float2 *gB = okB ? gA + (L.w * kTile + L.z) : gA;
             const int gstep = okB ? stride * kTile : 0;
             const float fstride = (float)stride;
             float m0 = 0.f, S0a = 0.f, Sya = 0.f, Syya = 0.f, S0b = 0.f, Syb = 0.f, Syyb = 0.f;
             int i = 0;
+#pragma unroll 1
             for (; i < nB; ++i) {
                 const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
                 const float wb = ex2_approx(fmaf(dyB, fmaf(b.z, dyB, QB), PB));
@@ -725,7 +739,8 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
 }
 
 constexpr size_t kFwdSmem = sizeof(Batch) + sizeof(float2) * kGroups * kAccStride;
-constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(float2) * (kTile * kTile + kWarps);
+constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(Layout) +
+                            sizeof(float2) * (kTile * kTile + kWarps);
 
 int set_smem_attrs() {
     static bool done = false;
