@@ -126,7 +126,7 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.warp_rec, b.win_sparse, b.slice_tot,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.slice_m, b.bg_sums,
@@ -200,6 +200,9 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.amask, &b.amask_cap,
                      (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc amask")))
         return rc;
+    if ((rc = ensure(&b.wcnt, &b.wcnt_cap,
+                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc wcnt")))
+        return rc;
     if ((rc = ensure(&b.warp_rec, &b.warp_rec_cap,
                      (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
                      "alloc warp_rec")))
@@ -218,7 +221,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     stage_begin(p, kStageCount, st);
     if (c->n > 0) {
         if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
-                                       b.win_sparse, b.amask, st)))
+                                       b.win_sparse, b.amask, b.wcnt, st)))
             return rc;
         if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
             return rc;
@@ -293,7 +296,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
                                       m_total, k_total, b.win_sparse, b.amask,
-                                      b.warp_rec, st)))
+                                      b.wcnt, b.warp_rec, st)))
             return rc;
     } else {
         int32_t zero = 0;

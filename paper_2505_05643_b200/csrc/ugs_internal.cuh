@@ -47,6 +47,8 @@ struct PlanBuffers {
     size_t blk_pairs_cap = 0;
     uint32_t *amask = nullptr;      // [S][nblk*8] accept ballots of the count pass
     size_t amask_cap = 0;
+    uint2 *wcnt = nullptr;          // [S][nblk*8] (accepted, tiles) per warp of Gaussians
+    size_t wcnt_cap = 0;
     int32_t *warp_rec = nullptr;    // [S][nblk*8] record index of each warp's first
     size_t warp_rec_cap = 0;        //   accepted Gaussian (emit pass)
     uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
@@ -147,7 +149,7 @@ void stage_end(ugs_plan *p, int stage, cudaStream_t st);
 // phase 1 (ugs_prepare.cu)
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
-                         uint2 *win_sparse, uint32_t *amask, cudaStream_t st);
+                         uint2 *win_sparse, uint32_t *amask, uint2 *wcnt, cudaStream_t st);
 int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st);
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
@@ -155,7 +157,7 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        int32_t *warp_rec, cudaStream_t st);
+                        const uint2 *wcnt, int32_t *warp_rec, cudaStream_t st);
 
 // radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
 // bits, stable.  On return *keys_out/*vals_out point at the sorted arrays

@@ -31,16 +31,17 @@ prepare_count_kernel(const float *__restrict__ means,
                      const ugs_slice *__restrict__ slices, int S,
                      uint2 *__restrict__ blk_cnt, unsigned *__restrict__ blk_pairs,
                      int nblk, uint2 *__restrict__ win_sparse,
-                     uint32_t *__restrict__ amask) {
+                     uint32_t *__restrict__ amask, uint2 *__restrict__ wcnt) {
+    constexpr int kW = kPrepThreads / 32;
     __shared__ ugs_slice sl[kMaxSlicesSmem];
-    __shared__ unsigned s_acc[kMaxSlicesSmem], s_tiles[kMaxSlicesSmem],
-        s_pairs[kMaxSlicesSmem];
+    __shared__ unsigned s_tiles[kMaxSlicesSmem], s_pairs[kMaxSlicesSmem];
+    __shared__ unsigned s_wt[kMaxSlicesSmem][kW], s_bal[kMaxSlicesSmem][kW];
     load_slices_smem(sl, slices, S);
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
-        s_acc[s] = 0;
         s_tiles[s] = 0;
         s_pairs[s] = 0;
     }
+    for (int i = threadIdx.x; i < S * kW; i += blockDim.x) (&s_wt[0][0])[i] = 0;
     __syncthreads();
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
     const bool valid = g < n;
@@ -71,7 +72,9 @@ prepare_count_kernel(const float *__restrict__ means,
             win_sparse[(size_t)s * n + g] =
                 make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
             // integer sums: shared atomics give exact (order-free) totals
-            atomicAdd(&s_tiles[s], (unsigned)window_tiles(w));
+            const unsigned nt = (unsigned)window_tiles(w);
+            atomicAdd(&s_tiles[s], nt);
+            atomicAdd(&s_wt[s][threadIdx.x >> 5], nt);
             atomicAdd(&s_pairs[s], (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1)));
         }
     }
@@ -82,12 +85,22 @@ prepare_count_kernel(const float *__restrict__ means,
         const unsigned bal = __ballot_sync(0xffffffffu, (unsigned)(accmask >> s) & 1u);
         if (lane == 0) {
             amask[(size_t)s * nwarp_all + gwarp] = bal;
-            if (bal) atomicAdd(&s_acc[s], (unsigned)__popc(bal));
+            s_bal[s][warp] = (unsigned)__popc(bal);
         }
     }
     __syncthreads();
+    // per-warp (accepted, tiles): the emit pass turns them into offsets
+    // without a block-wide scan
+    for (int i = threadIdx.x; i < S * kW; i += blockDim.x) {
+        const int s = i / kW, wp = i % kW;
+        wcnt[(size_t)s * nwarp_all + (int64_t)blockIdx.x * kW + wp] =
+            make_uint2(s_bal[s][wp], s_wt[s][wp]);
+    }
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
-        blk_cnt[(size_t)s * nblk + blockIdx.x] = make_uint2(s_acc[s], s_tiles[s]);
+        unsigned a = 0;
+#pragma unroll
+        for (int wp = 0; wp < kW; ++wp) a += s_bal[s][wp];
+        blk_cnt[(size_t)s * nblk + blockIdx.x] = make_uint2(a, s_tiles[s]);
         blk_pairs[(size_t)s * nblk + blockIdx.x] = s_pairs[s];
     }
 }
@@ -169,8 +182,8 @@ prepare_emit_kernel(const float *__restrict__ means,
                     int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
                     uint32_t *__restrict__ keys, int64_t m_total,
                     int64_t k_total, const uint2 *__restrict__ win_sparse,
-                    const uint32_t *__restrict__ amask, int32_t *__restrict__ warp_rec) {
-    __shared__ uint2 wpre[kPrepThreads / 32];
+                    const uint32_t *__restrict__ amask, const uint2 *__restrict__ wcnt,
+                    int32_t *__restrict__ warp_rec) {
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
     const bool valid = g < n;
     float color = 0.f, alpha = 0.f;
@@ -182,10 +195,14 @@ prepare_emit_kernel(const float *__restrict__ means,
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
     if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
+    const uint32_t lt = (1u << lane) - 1u;
     for (int s = 0; s < S; ++s) {
-        // the count pass left the accept bits and the windows of accepted
-        // (slice, Gaussian) pairs: no phase-1 recompute here
-        const unsigned acc = (__ldg(amask + (size_t)s * nwarp_all + gwarp) >> lane) & 1u;
+        // the count pass left the accept bits, the per-warp counts and the
+        // windows of accepted (slice, Gaussian) pairs: no phase-1 recompute
+        // and no block-wide scan (no barriers)
+        const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + gwarp);
+        if (word == 0) continue;   // warp-uniform
+        const unsigned acc = (word >> lane) & 1u;
         unsigned tiles = 0;
         Window w;
         if (acc) {
@@ -194,27 +211,29 @@ prepare_emit_kernel(const float *__restrict__ means,
             w.iv0 = pw.y & 0xffff; w.iv1 = pw.y >> 16;
             tiles = (unsigned)window_tiles(w);
         }
-        // block exclusive scan of (acc, tiles)
-        unsigned xa = acc, xt = tiles;
+        unsigned xt = tiles;   // inclusive warp scan of the tile counts
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            unsigned ta = __shfl_up_sync(0xffffffffu, xa, o);
-            unsigned tt = __shfl_up_sync(0xffffffffu, xt, o);
-            if (lane >= o) { xa += ta; xt += tt; }
+            const unsigned tt = __shfl_up_sync(0xffffffffu, xt, o);
+            if (lane >= o) xt += tt;
         }
-        __syncthreads();   // wpre reuse across slices
-        if (lane == 31) wpre[warp] = make_uint2(xa, xt);
-        __syncthreads();
-        unsigned oa = 0, ot = 0;
-        for (int k = 0; k < warp; ++k) { oa += wpre[k].x; ot += wpre[k].y; }
-        const uint2 bo = blk_off[(size_t)s * nblk + blockIdx.x];
+        // this warp's offset inside the slice: the block's offset plus the
+        // counts of the block's earlier warps
+        const uint2 bo = __ldg(blk_off + (size_t)s * nblk + blockIdx.x);
+        uint32_t oa = bo.x, ot = bo.y;
+        const uint2 *wc = wcnt + (size_t)s * nwarp_all + (int64_t)blockIdx.x * (kPrepThreads / 32);
+        for (int k = 0; k < warp; ++k) {
+            const uint2 c = __ldg(wc + k);
+            oa += c.x;
+            ot += c.y;
+        }
+        const int64_t r0 = slice_base[2 * s] + oa;
         // record of this warp's first accepted Gaussian: the update pass maps
         // (slice, Gaussian) -> record with one popcount
-        if (lane == 0)
-            warp_rec[(size_t)s * nwarp_all + gwarp] = (int32_t)(slice_base[2 * s] + bo.x + oa);
+        if (lane == 0) warp_rec[(size_t)s * nwarp_all + gwarp] = (int32_t)r0;
         if (!acc) continue;
-        const int64_t r = slice_base[2 * s] + bo.x + oa + xa - acc;
-        int64_t inst = slice_base[2 * s + 1] + bo.y + ot + xt - tiles;
+        const int64_t r = r0 + __popc(word & lt);
+        const int64_t inst = slice_base[2 * s + 1] + ot + xt - tiles;
         // the float64 plane conditioning and the tile expansion run in
         // build_records_kernel (one thread per record, full occupancy)
         rec[r].r0 = make_float4(0.f, 0.f, 0.f, color);
@@ -272,10 +291,10 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
 
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
-                         uint2 *win_sparse, uint32_t *amask, cudaStream_t st) {
+                         uint2 *win_sparse, uint32_t *amask, uint2 *wcnt, cudaStream_t st) {
     prepare_count_kernel<<<nblk, kPrepThreads, 0, st>>>(
         c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk,
-        win_sparse, amask);
+        win_sparse, amask, wcnt);
     UGS_LAUNCH_CHECK("prepare_count_kernel");
     return UGS_OK;
 }
@@ -292,11 +311,11 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        int32_t *warp_rec, cudaStream_t st) {
+                        const uint2 *wcnt, int32_t *warp_rec, cudaStream_t st) {
     prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
         S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, idata, keys,
-        m_total, k_total, win_sparse, amask, warp_rec);
+        m_total, k_total, win_sparse, amask, wcnt, warp_rec);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
         c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,
