@@ -611,13 +611,17 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
 }
 
 constexpr int kUpdThreads = 256;
+constexpr int kUpdWarps = kUpdThreads / 32;
+constexpr int kUpdRows = 512;   // staged record-gradient rows per pass
 
-// One thread per Gaussian g (the count pass's warp -> Gaussian mapping): for
-// every slice of the batch, in SLICE ORDER, the accept ballot says whether
-// (slice, g) has a record, and the record index is the warp's first record
-// plus a popcount -- no search, no staging, no atomics.  The record
-// gradients (finalize_records) are accumulated as acc = fma(scale, rg, acc),
-// so every gradient sums its slices in a fixed order (deterministic).  Then
+// One block per 256 Gaussians (the count pass's warp -> Gaussian mapping).
+// For every slice of the batch the accept ballots say which of the block's
+// Gaussians have a record; those records are consecutive, starting at the
+// first record of the block's first non-empty warp (warp_rec).  The block
+// stages all of its record-gradient rows (finalize_records) into shared
+// memory with fully parallel, coalesced loads -- one round trip instead of
+// one per slice per warp -- then each thread adds its Gaussian's rows in
+// SLICE ORDER, acc = fma(scale, row, acc): deterministic, no atomics.  Then
 // (adam != 0, single GPU) densify statistics and Adam run for EVERY Gaussian
 // -- zero-gradient rows still move (trainer.py:182-199) -- and the dense
 // gradient never touches HBM; or (adam == 0) the rows are added into the
@@ -629,48 +633,79 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
                      uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
                      int32_t *__restrict__ grad_cnt) {
+    __shared__ float4 rows[kUpdRows][3];
+    __shared__ uint32_t s_word[64][kUpdWarps];
+    __shared__ int s_wpre[64][kUpdWarps];   // records of earlier warps (block, slice)
+    __shared__ int s_cnt[64], s_base[64], s_off[65];
     const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
-    const int64_t gwarp = g >> 5;
-    if (gwarp >= nwarp_all) return;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gw0 = (int64_t)blockIdx.x * kUpdWarps;
     const uint32_t lt = (1u << lane) - 1u;
+    if (adam && g < n) {
+        // the update's streams (moments, parameters) start towards L2 while
+        // the gather runs: no registers held, the latency overlaps
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(m + kG * g));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(v + kG * g));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.l_raw + 6 * g));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.means + 3 * g));
+    }
+    for (int i = threadIdx.x; i < S * kUpdWarps; i += kUpdThreads) {
+        const int sl = i / kUpdWarps, w = i % kUpdWarps;
+        s_word[sl][w] = (gw0 + w < nwarp_all) ? __ldg(amask + (size_t)sl * nwarp_all + gw0 + w)
+                                              : 0u;
+    }
+    __syncthreads();
+    for (int sl = threadIdx.x; sl < S; sl += kUpdThreads) {
+        int c = 0, first = -1;
+        for (int w = 0; w < kUpdWarps; ++w) {
+            s_wpre[sl][w] = c;
+            const int pc = __popc(s_word[sl][w]);
+            if (pc && first < 0) first = w;
+            c += pc;
+        }
+        s_cnt[sl] = c;
+        s_base[sl] = first >= 0 ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw0 + first) : 0;
+    }
+    __syncthreads();
     float acc[11];
 #pragma unroll
     for (int j = 0; j < 11; ++j) acc[j] = 0.f;
     bool hit = false;
-    // four slices at a time: the ballot / base loads, then the record-row
-    // loads, are independent -> issued together (memory-level parallelism)
-    for (int s0 = 0; s0 < S; s0 += 4) {
-        uint32_t wd[4];
-        int32_t wb[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const bool in = s0 + q < S;
-            const size_t o = (size_t)(in ? s0 + q : 0) * nwarp_all + gwarp;
-            wd[q] = in ? __ldg(amask + o) : 0u;
-            wb[q] = __ldg(warp_rec + o);
+    int s0 = 0;
+    while (s0 < S) {
+        // next group of slices whose rows fit the stage (a slice alone always
+        // fits: <= 256 rows)
+        int s1 = s0, tot = 0;
+        while (s1 < S && tot + s_cnt[s1] <= kUpdRows) tot += s_cnt[s1++];
+        __syncthreads();   // previous group done with rows / s_off
+        if (threadIdx.x == 0) {
+            int o = 0;
+            for (int sl = s0; sl < s1; ++sl) { s_off[sl - s0] = o; o += s_cnt[sl]; }
+            s_off[s1 - s0] = o;
         }
-        float4 t[4][3];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((wd[q] >> lane) & 1u) {
-                const int64_t r = (int64_t)wb[q] + __popc(wd[q] & lt);
-                const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
-                t[q][0] = __ldg(src);
-                t[q][1] = __ldg(src + 1);
-                t[q][2] = __ldg(src + 2);
-            }
+        __syncthreads();
+        for (int i = threadIdx.x; i < tot; i += kUpdThreads) {
+            int sg = 0;
+            while (s_off[sg + 1] <= i) ++sg;
+            const int64_t r = (int64_t)s_base[s0 + sg] + (i - s_off[sg]);
+            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
+            rows[i][0] = __ldg(src);
+            rows[i][1] = __ldg(src + 1);
+            rows[i][2] = __ldg(src + 2);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!((wd[q] >> lane) & 1u)) continue;
-            const float o[11] = {t[q][0].x, t[q][0].y, t[q][0].z, t[q][0].w, t[q][1].x,
-                                 t[q][1].y, t[q][1].z, t[q][1].w, t[q][2].x, t[q][2].y,
-                                 t[q][2].z};
+        __syncthreads();
+        for (int sl = s0; sl < s1; ++sl) {
+            const uint32_t word = s_word[sl][warp];
+            if (!((word >> lane) & 1u)) continue;
+            const int slot = s_off[sl - s0] + s_wpre[sl][warp] + __popc(word & lt);
+            const float4 t0 = rows[slot][0], t1 = rows[slot][1], t2 = rows[slot][2];
+            const float o[11] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w,
+                                 t2.x, t2.y, t2.z};
 #pragma unroll
             for (int j = 0; j < 11; ++j) acc[j] = fmaf(scale, o[j], acc[j]);
             hit = true;
         }
+        s0 = s1;
     }
     if (g >= n) return;
     if (adam) {
@@ -809,8 +844,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     if (c.n > 0 && (adam || p.m_total > 0)) {
         const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
         const int64_t nwarp_all = nblk * (kPrepThreads / 32);
-        update_gather_kernel<<<(unsigned)((nwarp_all * 32 + kUpdThreads - 1) / kUpdThreads),
-                               kUpdThreads, 0, st>>>(
+        static_assert(kUpdThreads == kPrepThreads, "update blocks mirror count blocks");
+        update_gather_kernel<<<(unsigned)nblk, kUpdThreads, 0, st>>>(
             p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale, adam ? 1 : 0,
             grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
             adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,
