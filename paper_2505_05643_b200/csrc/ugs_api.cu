@@ -131,7 +131,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.slice_m, b.bg_sums,
                     b.hist,
-                    b.scan_tmp, b.bin_range,
+                    b.scan_tmp, b.sort_slices, b.bin_range,
                     b.bin_bg};
     for (void *q : bufs)
         if (q) cudaFree(q);
@@ -279,11 +279,40 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         UGS_CUDA(cudaMalloc(&b.vals2, sizeof(uint32_t) * b.inst_cap));
         UGS_CUDA(cudaMalloc(&b.partial, sizeof(float) * 8 * b.inst_cap));
     }
-    const size_t hn = radix_hist_entries(k_total) + 1;
+    // bin sort plan: single-pass per-slice counting sort when every slice has
+    // <= kSliceSortMaxTiles tiles and the tables fit the scan, else LSD radix
+    std::vector<SortSlice> ss(S);
+    int64_t hist_n = 0;
+    int nblk_sort = 0;
+    for (int s = 0; s < S; ++s) {
+        SortSlice &q = ss[s];
+        q.inst_base = (int)p->h_slice_base[2 * s + 1];
+        q.k = (int)tot[3 * s + 1];
+        q.tile_base = p->h_tile_base[s];
+        q.ntile = p->h_ntile[s];
+        q.nb = (q.k + kSortTile - 1) / kSortTile;
+        q.bpre = nblk_sort;
+        q.hoff = (int)hist_n;
+        q.pad = 0;
+        nblk_sort += q.nb;
+        hist_n += (int64_t)q.ntile * q.nb;
+    }
+    p->slice_sort = max_tiles <= kSliceSortMaxTiles && hist_n < ((int64_t)1 << 24);
+    const size_t hn = (p->slice_sort ? (size_t)hist_n : radix_hist_entries(k_total)) + 1;
     if ((rc = ensure(&b.hist, &b.hist_cap, hn, "alloc hist"))) return rc;
     if ((rc = ensure(&b.scan_tmp, &b.scan_tmp_cap, scan_tmp_entries(hn) + 1,
                      "alloc scan_tmp")))
         return rc;
+    {
+        size_t cap = (size_t)b.sort_slices_cap;
+        if ((rc = ensure(&b.sort_slices, &cap, (size_t)64, "alloc sort_slices"))) return rc;
+        b.sort_slices_cap = (int)cap;
+    }
+    if (p->slice_sort)
+        UGS_CUDA(cudaMemcpyAsync(b.sort_slices, ss.data(), sizeof(SortSlice) * S,
+                                 cudaMemcpyHostToDevice, st));
+    p->hist_n = hist_n;
+    p->nblk_sort = nblk_sort;
     if (b.bin_cap < (size_t)n_bins || !b.bin_range) {
         if (b.bin_range) cudaFree(b.bin_range);
         if (b.bin_bg) cudaFree(b.bin_bg);
@@ -305,15 +334,24 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     }
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);
-    if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, k_total,
-                               bits_for(n_bins), b.hist, b.scan_tmp, st,
-                               &p->sorted_keys, &p->sorted_vals)))
-        return rc;
-    stage_end(p, kStageSort, st);
-    stage_begin(p, kStageRanges, st);
-    if ((rc = launch_bin_ranges(p->sorted_keys, k_total, b.bin_range, n_bins, st)))
-        return rc;
-    stage_end(p, kStageRanges, st);
+    if (p->slice_sort) {
+        if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, p->hist_n, max_tiles, n_bins,
+                                  p->nblk_sort, b.hist, b.scan_tmp, b.vals, b.bin_range, st)))
+            return rc;
+        p->sorted_keys = nullptr;
+        p->sorted_vals = b.vals;
+        stage_end(p, kStageSort, st);
+    } else {
+        if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, k_total,
+                                   bits_for(n_bins), b.hist, b.scan_tmp, st,
+                                   &p->sorted_keys, &p->sorted_vals)))
+            return rc;
+        stage_end(p, kStageSort, st);
+        stage_begin(p, kStageRanges, st);
+        if ((rc = launch_bin_ranges(p->sorted_keys, k_total, b.bin_range, n_bins, st)))
+            return rc;
+        stage_end(p, kStageRanges, st);
+    }
     return UGS_OK;
 }
 

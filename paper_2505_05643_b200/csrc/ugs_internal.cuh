@@ -38,6 +38,14 @@ struct Rec {
 // record's own.  (D, E, F, bits(record index)).
 using Inst = float4;
 
+// Per-slice parameters of the single-pass bin sort (ugs_sort.cu).
+struct SortSlice {
+    int inst_base, k;        // the slice's instance segment
+    int tile_base, ntile;    // its bins
+    int nb, bpre;            // sort blocks of the segment, and of earlier slices
+    int hoff, pad;           // offset of its (tile-major) histogram table
+};
+
 // Per-batch binning state (device pointers are owned by the plan).
 struct PlanBuffers {
     // phase 1
@@ -76,6 +84,8 @@ struct PlanBuffers {
     uint32_t *hist = nullptr;       // [kRadix][nblk_sort]
     uint32_t *scan_tmp = nullptr;
     size_t hist_cap = 0, scan_tmp_cap = 0;
+    SortSlice *sort_slices = nullptr;   // [S] device copy
+    int sort_slices_cap = 0;
     // bins
     int2 *bin_range = nullptr;      // [n_bins] [start, end) into sorted arrays
     float2 *bin_bg = nullptr;       // [n_bins] per-tile (sum G, sum G*chat)
@@ -101,6 +111,9 @@ struct ugs_plan {
     uint32_t *sorted_keys = nullptr; // point into b.keys/b.keys2
     uint32_t *sorted_vals = nullptr;
     bool ordered = false;            // strict per-pixel ascending-index forward
+    bool slice_sort = false;         // single-pass per-slice bin sort in use
+    int64_t hist_n = 0;              // its histogram table entries
+    int nblk_sort = 0;               // and sort blocks
     // optional per-stage CUDA-event timing (ugs_plan_set_timing)
     bool timing = false;
     bool ev_ready = false;
@@ -168,6 +181,13 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
                      uint32_t **vals_out);
 size_t radix_hist_entries(int64_t n);
 size_t scan_tmp_entries(size_t n);
+// single-pass per-slice counting sort of slice-major instances; tiles per
+// slice <= 1024 (else the LSD radix sort above is used)
+constexpr int kSliceSortMaxTiles = 1024;
+int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, int64_t hist_n,
+                    int max_tiles, int n_bins, int nblk, uint32_t *hist,
+                    uint32_t *scan_tmp, uint32_t *vals_out, int2 *bin_range,
+                    cudaStream_t st);
 int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 
