@@ -89,12 +89,16 @@ prepare_count_kernel(const float *__restrict__ means,
         }
     }
     __syncthreads();
-    // per-warp (accepted, tiles): the emit pass turns them into offsets
-    // without a block-wide scan
+    // per warp: (accepted, tiles) of the block's EARLIER warps, so the emit
+    // pass gets its offsets with one load and no block-wide scan
     for (int i = threadIdx.x; i < S * kW; i += blockDim.x) {
         const int s = i / kW, wp = i % kW;
-        wcnt[(size_t)s * nwarp_all + (int64_t)blockIdx.x * kW + wp] =
-            make_uint2(s_bal[s][wp], s_wt[s][wp]);
+        unsigned a = 0, t = 0;
+        for (int k = 0; k < wp; ++k) {
+            a += s_bal[s][k];
+            t += s_wt[s][k];
+        }
+        wcnt[(size_t)s * nwarp_all + (int64_t)blockIdx.x * kW + wp] = make_uint2(a, t);
     }
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
         unsigned a = 0;
@@ -185,31 +189,31 @@ prepare_emit_kernel(const float *__restrict__ means,
                     const uint32_t *__restrict__ amask, const uint2 *__restrict__ wcnt,
                     int32_t *__restrict__ warp_rec) {
     const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
-    const bool valid = g < n;
-    float color = 0.f, alpha = 0.f;
-    if (valid) {
-        color = sigmoid_f32(__ldg(intensity_raw + g));
-        alpha = sigmoid_f32(__ldg(opacity_raw + g));
-    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
     if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
     const uint32_t lt = (1u << lane) - 1u;
-    for (int s = 0; s < S; ++s) {
-        // the count pass left the accept bits, the per-warp counts and the
+    // per-slice cursors (pointer increments, no 64-bit index products)
+    const uint32_t *am = amask + gwarp;
+    const uint2 *wc = wcnt + gwarp;
+    const uint2 *bo_p = blk_off + blockIdx.x;
+    const uint2 *ws = win_sparse + g;
+    int32_t *wr = warp_rec + gwarp;
+    for (int s = 0; s < S; ++s, am += nwarp_all, wc += nwarp_all, bo_p += nblk, ws += n,
+             wr += nwarp_all) {
+        // the count pass left the accept bits, the per-warp offsets and the
         // windows of accepted (slice, Gaussian) pairs: no phase-1 recompute
         // and no block-wide scan (no barriers)
-        const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + gwarp);
+        const uint32_t word = __ldg(am);
         if (word == 0) continue;   // warp-uniform
         const unsigned acc = (word >> lane) & 1u;
         unsigned tiles = 0;
-        Window w;
+        uint2 pw = make_uint2(0u, 0u);
         if (acc) {
-            const uint2 pw = __ldg(win_sparse + (size_t)s * n + g);
-            w.iu0 = pw.x & 0xffff; w.iu1 = pw.x >> 16;
-            w.iv0 = pw.y & 0xffff; w.iv1 = pw.y >> 16;
-            tiles = (unsigned)window_tiles(w);
+            pw = __ldg(ws);
+            tiles = (unsigned)((((pw.x >> 16) >> 4) - ((pw.x & 0xffff) >> 4) + 1) *
+                               (((pw.y >> 16) >> 4) - ((pw.y & 0xffff) >> 4) + 1));
         }
         unsigned xt = tiles;   // inclusive warp scan of the tile counts
 #pragma unroll
@@ -219,26 +223,17 @@ prepare_emit_kernel(const float *__restrict__ means,
         }
         // this warp's offset inside the slice: the block's offset plus the
         // counts of the block's earlier warps
-        const uint2 bo = __ldg(blk_off + (size_t)s * nblk + blockIdx.x);
-        uint32_t oa = bo.x, ot = bo.y;
-        const uint2 *wc = wcnt + (size_t)s * nwarp_all + (int64_t)blockIdx.x * (kPrepThreads / 32);
-        for (int k = 0; k < warp; ++k) {
-            const uint2 c = __ldg(wc + k);
-            oa += c.x;
-            ot += c.y;
-        }
-        const int64_t r0 = slice_base[2 * s] + oa;
+        const uint2 bo = __ldg(bo_p), c = __ldg(wc);
+        const int64_t r0 = slice_base[2 * s] + bo.x + c.x;
         // record of this warp's first accepted Gaussian: the update pass maps
         // (slice, Gaussian) -> record with one popcount
-        if (lane == 0) warp_rec[(size_t)s * nwarp_all + gwarp] = (int32_t)r0;
+        if (lane == 0) *wr = (int32_t)r0;
         if (!acc) continue;
         const int64_t r = r0 + __popc(word & lt);
-        const int64_t inst = slice_base[2 * s + 1] + ot + xt - tiles;
-        // the float64 plane conditioning and the tile expansion run in
-        // build_records_kernel (one thread per record, full occupancy)
-        rec[r].r0 = make_float4(0.f, 0.f, 0.f, color);
-        rec[r].r1 = make_float4(__int_as_float(w.iu0 | (w.iu1 << 16)),
-                                __int_as_float(w.iv0 | (w.iv1 << 16)), alpha, 0.f);
+        const int64_t inst = slice_base[2 * s + 1] + bo.y + c.y + xt - tiles;
+        // colour, alpha, the float64 plane conditioning and the tile
+        // expansion run in build_records_kernel (one thread per record)
+        *reinterpret_cast<uint2 *>(&rec[r].r1) = pw;
         rec_gid[r] = (int32_t)g;
         rec_inst[r] = (int32_t)inst;
     }
@@ -249,7 +244,8 @@ prepare_emit_kernel(const float *__restrict__ means,
 // instances in row-major tile order, each with its exact re-expansion.
 __global__ void __launch_bounds__(128)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
-                     float beta, const ugs_slice *__restrict__ slices, int S,
+                     const float *__restrict__ intensity_raw,
+                     const float *__restrict__ opacity_raw, float beta, const ugs_slice *__restrict__ slices, int S,
                      const int64_t *__restrict__ slice_base, int64_t m_total,
                      Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                      const int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
@@ -263,15 +259,17 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const Factor f = make_factor(l_raw, g, beta);
     const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
                          __ldg(means + 3 * g + 2)};
-    const float4 r0 = rec[r].r0, r1 = rec[r].r1;
+    const float2 r1 = *reinterpret_cast<const float2 *>(&rec[r].r1);   // window (emit)
+    const float color = sigmoid_f32(__ldg(intensity_raw + g));
+    const float alpha = sigmoid_f32(__ldg(opacity_raw + g));
     const int wu = __float_as_int(r1.x), wv = __float_as_int(r1.y);
     const Window w{wu & 0xffff, wu >> 16, wv & 0xffff, wv >> 16};
     const PlaneForm P = plane_form(mu, f, L, w);
     const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
-    const double log2a = log2((double)r1.z);
+    const double log2a = log2((double)alpha);
     rec[r].r0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
-                            (float)(kq * P.H11), r0.w);
-    rec[r].r1.w = __int_as_float(P.ui | (P.vi << 16));
+                            (float)(kq * P.H11), color);
+    rec[r].r1 = make_float4(r1.x, r1.y, alpha, __int_as_float(P.ui | (P.vi << 16)));
     const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
     const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
     int64_t inst = rec_inst[r];
@@ -318,7 +316,8 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
         m_total, k_total, win_sparse, amask, wcnt, warp_rec);
     UGS_LAUNCH_CHECK("prepare_emit_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
-        c.means, c.l_raw, (float)c.beta, slices, S, slice_base, m_total, rec, rec_gid,
+        c.means, c.l_raw, c.intensity_raw, c.opacity_raw, (float)c.beta, slices, S,
+        slice_base, m_total, rec, rec_gid,
         rec_inst, idata, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;
