@@ -9,7 +9,8 @@
 // valid filter).  One CTA owns a 32x32 output tile: it loads the 52x52 input
 // neighbourhood, filters the five moments (x, y, x^2, y^2, xy) separably onto
 // the 42x42 valid points it needs, forms A, B, C there, applies the adjoint
-// separably back onto its 32x32 pixels and writes d_pixels (float32, what
+// separably back onto its 32x32 pixels (register-blocked runs of outputs per
+// thread) and writes d_pixels (float32, what
 // the backward consumes -- gradients.py:62 casts the same way).  Per-tile
 // sums (sum|diff| over owned pixels, sum SSIM over owned valid points) are
 // reduced per slice in fixed order by a second tiny kernel: deterministic.
@@ -22,13 +23,21 @@ constexpr int kLT = 32;              // output tile
 constexpr int kPad = 5;              // window radius
 constexpr int kF = kLT + 2 * kPad;   // 42: valid points needed
 constexpr int kI = kF + 2 * kPad;    // 52: input points needed
-constexpr int kLossThreads = 1024;   // one 173 KB CTA per SM: all warps it can hold
+constexpr int kLossThreads = 384;    // 12 warps, one 147 KB CTA per SM
 
 __constant__ double c_win[11];
 
+// Register blocking: every pass gives a thread a run of consecutive outputs
+// (6 or 8) of one row/column, so each shared-memory value it loads feeds up
+// to 11 outputs from registers (the earlier one-output-per-thread passes were
+// shared-memory bound).  Per output the taps are still added in increasing
+// order with the same expressions, so the sums are unchanged.
+constexpr int kHB = 6;               // horizontal / vertical moment run
+constexpr int kAB = 4;               // adjoint run
+
 struct LossSmem {
-    double X[kI][kI];                 // prediction (f64 of f32 num/den)
-    double Y[kI][kI];                 // target
+    float X[kI][kI];                  // prediction (f32 num/den, exact in float)
+    float Y[kI][kI];                  // target
     union {
         double h[5][kI][kF];          // horizontal moment pass
         double ha[3][kF][kLT];        // horizontal adjoint pass
@@ -37,7 +46,7 @@ struct LossSmem {
     double red[2][kLossThreads / 32];
 };
 
-__global__ void __launch_bounds__(kLossThreads)
+__global__ void __launch_bounds__(kLossThreads, 1)
 loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                  const float *__restrict__ target, int H, int W, double lam,
                  int l2, float *__restrict__ dpix, double *__restrict__ tile_sums,
@@ -51,117 +60,189 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
     const int tid = threadIdx.x;
     const int HV = H - 2 * kPad, WV = W - 2 * kPad;   // valid grid
     const double npx = (double)H * W, nv = (double)HV * WV;
-    // load the 52x52 neighbourhood (rows p0-10 .., cols q0-10 ..)
-    for (int i = tid; i < kI * kI; i += kLossThreads) {
+    // load the 52x52 neighbourhood (rows p0-10 .., cols q0-10 ..): all of a
+    // thread's global loads are issued before any is consumed
+    constexpr int kLd = (kI * kI + kLossThreads - 1) / kLossThreads;
+    float ln[kLd], ld[kLd], lt[kLd];
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+        const int i = tid + j * kLossThreads;
         const int r = i / kI, c = i % kI;
         const int P = p0 - 2 * kPad + r, Q = q0 - 2 * kPad + c;
-        double x = 0.0, y = 0.0;
-        if (P >= 0 && P < H && Q >= 0 && Q < W) {
+        ln[j] = 0.f;
+        ld[j] = 1.f;
+        lt[j] = 0.f;
+        if (i < kI * kI && P >= 0 && P < H && Q >= 0 && Q < W) {
             const size_t o = base + (size_t)P * W + Q;
-            x = (double)__fdiv_rn(num[o], den[o]);   // pred = num / den (float32)
-            y = (double)target[o];
+            ln[j] = __ldg(num + o);
+            ld[j] = __ldg(den + o);
+            lt[j] = __ldg(target + o);
         }
-        sm.X[r][c] = x;
-        sm.Y[r][c] = y;
+    }
+#pragma unroll
+    for (int j = 0; j < kLd; ++j) {
+        const int i = tid + j * kLossThreads;
+        if (i >= kI * kI) continue;
+        const int r = i / kI, c = i % kI;
+        sm.X[r][c] = __fdiv_rn(ln[j], ld[j]);   // pred = num / den (float32); 0 outside
+        sm.Y[r][c] = lt[j];
     }
     __syncthreads();
     double ssim_sum = 0.0;
     const bool ssim = !l2 && lam > 0.0;
     if (ssim) {
         // horizontal pass: h[f][r][c] = sum_b w[b] f(r, c+b), c in [0,42)
-        for (int i = tid; i < kI * kF; i += kLossThreads) {
-            const int r = i / kF, c = i % kF;
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+        constexpr int kCh = kF / kHB;   // 7 runs per row
+        for (int it = tid; it < kI * kCh; it += kLossThreads) {
+            const int r = it / kCh, c0 = (it % kCh) * kHB;
+            double a[5][kHB];
 #pragma unroll
-            for (int b = 0; b < 11; ++b) {
-                const double w = c_win[b], x = sm.X[r][c + b], y = sm.Y[r][c + b];
-                a0 += w * x;
-                a1 += w * y;
-                a2 += w * x * x;
-                a3 += w * y * y;
-                a4 += w * x * y;
+            for (int f = 0; f < 5; ++f)
+#pragma unroll
+                for (int o = 0; o < kHB; ++o) a[f][o] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < kHB + 10; ++kk) {
+                const double x = sm.X[r][c0 + kk], y = sm.Y[r][c0 + kk];
+#pragma unroll
+                for (int o = 0; o < kHB; ++o) {
+                    const int b = kk - o;
+                    if (b < 0 || b > 10) continue;
+                    const double w = c_win[b];
+                    a[0][o] += w * x;
+                    a[1][o] += w * y;
+                    a[2][o] += w * x * x;
+                    a[3][o] += w * y * y;
+                    a[4][o] += w * x * y;
+                }
             }
-            sm.u.h[0][r][c] = a0;
-            sm.u.h[1][r][c] = a1;
-            sm.u.h[2][r][c] = a2;
-            sm.u.h[3][r][c] = a3;
-            sm.u.h[4][r][c] = a4;
+#pragma unroll
+            for (int f = 0; f < 5; ++f)
+#pragma unroll
+                for (int o = 0; o < kHB; ++o) sm.u.h[f][r][c0 + o] = a[f][o];
         }
         __syncthreads();
         // vertical pass -> moments at valid point (i, j) = (p0-10+r, q0-10+c)
-        for (int k = tid; k < kF * kF; k += kLossThreads) {
-            const int r = k / kF, c = k % kF;
-            const int i = p0 - 2 * kPad + r, j = q0 - 2 * kPad + c;
-            double A = 0, B = 0, C = 0;
-            if (i >= 0 && i < HV && j >= 0 && j < WV) {
-                double m[5] = {0, 0, 0, 0, 0};
+        for (int it = tid; it < kF * kCh; it += kLossThreads) {
+            const int c = it % kF, r0 = (it / kF) * kHB;
+            double m[5][kHB];
 #pragma unroll
-                for (int a = 0; a < 11; ++a) {
+            for (int f = 0; f < 5; ++f)
+#pragma unroll
+                for (int o = 0; o < kHB; ++o) m[f][o] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < kHB + 10; ++kk) {
+                double v[5];
+#pragma unroll
+                for (int f = 0; f < 5; ++f) v[f] = sm.u.h[f][r0 + kk][c];
+#pragma unroll
+                for (int o = 0; o < kHB; ++o) {
+                    const int a = kk - o;
+                    if (a < 0 || a > 10) continue;
                     const double w = c_win[a];
 #pragma unroll
-                    for (int f = 0; f < 5; ++f) m[f] += w * sm.u.h[f][r + a][c];
+                    for (int f = 0; f < 5; ++f) m[f][o] += w * v[f];
                 }
-                const double mx = m[0], my = m[1];
-                const double sxx = m[2] - mx * mx, syy = m[3] - my * my;
-                const double sxy = m[4] - mx * my;
-                const double C1 = 1e-4, C2 = 9e-4;
-                const double a1 = 2.0 * mx * my + C1, a2 = 2.0 * sxy + C2;
-                const double b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
-                const double sv = (a1 * a2) / (b1 * b2);
-                const double d_mu = (2.0 * my * a2) / (b1 * b2) -
-                                    (2.0 * mx * a1 * a2) / (b1 * b1 * b2);
-                const double d_sxx = -sv / b2, d_sxy = 2.0 * a1 / (b1 * b2);
-                A = d_mu - 2.0 * mx * d_sxx - my * d_sxy;
-                B = d_sxx;
-                C = d_sxy;
-                if (r >= 2 * kPad && c >= 2 * kPad) ssim_sum += sv;   // owned point
             }
-            sm.F[0][r][c] = A;
-            sm.F[1][r][c] = B;
-            sm.F[2][r][c] = C;
+#pragma unroll
+            for (int o = 0; o < kHB; ++o) {
+                const int r = r0 + o;
+                const int i = p0 - 2 * kPad + r, j = q0 - 2 * kPad + c;
+                double A = 0, B = 0, C = 0;
+                if (i >= 0 && i < HV && j >= 0 && j < WV) {
+                    const double mx = m[0][o], my = m[1][o];
+                    const double sxx = m[2][o] - mx * mx, syy = m[3][o] - my * my;
+                    const double sxy = m[4][o] - mx * my;
+                    const double C1 = 1e-4, C2 = 9e-4;
+                    const double a1 = 2.0 * mx * my + C1, a2 = 2.0 * sxy + C2;
+                    const double b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
+                    const double sv = (a1 * a2) / (b1 * b2);
+                    const double d_mu = (2.0 * my * a2) / (b1 * b2) -
+                                        (2.0 * mx * a1 * a2) / (b1 * b1 * b2);
+                    const double d_sxx = -sv / b2, d_sxy = 2.0 * a1 / (b1 * b2);
+                    A = d_mu - 2.0 * mx * d_sxx - my * d_sxy;
+                    B = d_sxx;
+                    C = d_sxy;
+                    if (r >= 2 * kPad && c >= 2 * kPad) ssim_sum += sv;   // owned point
+                }
+                sm.F[0][r][c] = A;
+                sm.F[1][r][c] = B;
+                sm.F[2][r][c] = C;
+            }
         }
         __syncthreads();
         // adjoint horizontal: ha[f][r][q] = sum_b w[b] F[f][r][q+b], q in [0,32)
-        for (int i = tid; i < 3 * kF * kLT; i += kLossThreads) {
-            const int f = i / (kF * kLT), rem = i % (kF * kLT);
-            const int r = rem / kLT, q = rem % kLT;
-            double a = 0;
+        constexpr int kAq = kLT / kAB;   // 4 runs per row
+        for (int it = tid; it < kF * kAq; it += kLossThreads) {
+            const int r = it / kAq, q0r = (it % kAq) * kAB;
+            double a[3][kAB];
 #pragma unroll
-            for (int b = 0; b < 11; ++b) a += c_win[b] * sm.F[f][r][q + b];
-            sm.u.ha[f][r][q] = a;
+            for (int f = 0; f < 3; ++f)
+#pragma unroll
+                for (int o = 0; o < kAB; ++o) a[f][o] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < kAB + 10; ++kk) {
+                double v[3];
+#pragma unroll
+                for (int f = 0; f < 3; ++f) v[f] = sm.F[f][r][q0r + kk];
+#pragma unroll
+                for (int o = 0; o < kAB; ++o) {
+                    const int b = kk - o;
+                    if (b < 0 || b > 10) continue;
+#pragma unroll
+                    for (int f = 0; f < 3; ++f) a[f][o] += c_win[b] * v[f];
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 3; ++f)
+#pragma unroll
+                for (int o = 0; o < kAB; ++o) sm.u.ha[f][r][q0r + o] = a[f][o];
         }
         __syncthreads();
     }
-    // pixels of this tile: gradient and L1 term
+    // pixels of this tile: gradient and L1 term (column q, a run of rows)
     double l1_sum = 0.0;
-    for (int k = tid; k < kLT * kLT; k += kLossThreads) {
-        const int p = k / kLT, q = k % kLT;
-        const int P = p0 + p, Q = q0 + q;
-        if (P >= H || Q >= W) continue;
-        const double x = sm.X[p + 2 * kPad][q + 2 * kPad];
-        const double y = sm.Y[p + 2 * kPad][q + 2 * kPad];
-        const double diff = x - y;
-        double g;
-        if (l2) {
-            l1_sum += diff * diff;
-            g = 2.0 * diff / npx;
-        } else {
-            l1_sum += fabs(diff);
-            const double sg = (diff > 0.0) ? 1.0 : ((diff < 0.0) ? -1.0 : 0.0);
-            g = (1.0 - lam) * sg / npx;
-            if (ssim) {
-                double aA = 0, aB = 0, aC = 0;
+    constexpr int kAp = kLT / kAB;
+    for (int it = tid; it < kLT * kAp; it += kLossThreads) {
+        const int q = it % kLT, pr0 = (it / kLT) * kAB;
+        double aA[kAB], aB[kAB], aC[kAB];
 #pragma unroll
-                for (int a = 0; a < 11; ++a) {
+        for (int o = 0; o < kAB; ++o) aA[o] = aB[o] = aC[o] = 0.0;
+        if (ssim) {
+#pragma unroll
+            for (int kk = 0; kk < kAB + 10; ++kk) {
+                const double vA = sm.u.ha[0][pr0 + kk][q], vB = sm.u.ha[1][pr0 + kk][q],
+                             vC = sm.u.ha[2][pr0 + kk][q];
+#pragma unroll
+                for (int o = 0; o < kAB; ++o) {
+                    const int a = kk - o;
+                    if (a < 0 || a > 10) continue;
                     const double w = c_win[a];
-                    aA += w * sm.u.ha[0][p + a][q];
-                    aB += w * sm.u.ha[1][p + a][q];
-                    aC += w * sm.u.ha[2][p + a][q];
+                    aA[o] += w * vA;
+                    aB[o] += w * vB;
+                    aC[o] += w * vC;
                 }
-                g -= lam * (aA + 2.0 * x * aB + y * aC) / nv;
             }
         }
-        dpix[base + (size_t)P * W + Q] = (float)g;
+#pragma unroll
+        for (int o = 0; o < kAB; ++o) {
+            const int p = pr0 + o;
+            const int P = p0 + p, Q = q0 + q;
+            if (P >= H || Q >= W) continue;
+            const double x = sm.X[p + 2 * kPad][q + 2 * kPad];
+            const double y = sm.Y[p + 2 * kPad][q + 2 * kPad];
+            const double diff = x - y;
+            double g;
+            if (l2) {
+                l1_sum += diff * diff;
+                g = 2.0 * diff / npx;
+            } else {
+                l1_sum += fabs(diff);
+                const double sg = (diff > 0.0) ? 1.0 : ((diff < 0.0) ? -1.0 : 0.0);
+                g = (1.0 - lam) * sg / npx;
+                if (ssim) g -= lam * (aA[o] + 2.0 * x * aB[o] + y * aC[o]) / nv;
+            }
+            dpix[base + (size_t)P * W + Q] = (float)g;
+        }
     }
     // block sums in fixed order
     const int lane = tid & 31, warp = tid >> 5;
