@@ -74,6 +74,10 @@ int ensure(T **ptr, size_t *cap, size_t need, const char *what) {
 }
 
 int ensure_host(ugs_plan *p, int S) {
+    if (!p->h_plan) {
+        cudaError_t e = cudaMallocHost((void **)&p->h_plan, sizeof(unsigned long long) * kPlanWords);
+        if (e != cudaSuccess) { p->h_plan = nullptr; return cuda_fail(e, "alloc h_plan"); }
+    }
     if (S <= p->h_cap) return UGS_OK;
     delete[] p->h_slice_base;
     delete[] p->h_m;
@@ -129,7 +133,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.rgrad, b.slice_m, b.bg_sums,
+                    b.vals2, b.partial, b.rgrad, b.bg_sums,
                     b.hist,
                     b.scan_tmp, b.sort_slices, b.bin_range,
                     b.bin_bg};
@@ -139,6 +143,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     delete[] p->h_m;
     delete[] p->h_tile_base;
     delete[] p->h_ntile;
+    if (p->h_plan) cudaFreeHost(p->h_plan);
     if (p->ev_ready)
         for (int i = 0; i < kNumStages; ++i)
             for (int j = 0; j < 2; ++j) cudaEventDestroy(p->ev[i][j]);
@@ -212,12 +217,14 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     {
         static_assert(sizeof(unsigned long long) == 8, "");
-        size_t cap = b.slice_tot ? 192 : 0;
-        if ((rc = ensure(&b.slice_tot, &cap, (size_t)192, "alloc slice_tot"))) return rc;
+        size_t cap = b.slice_tot ? (size_t)kPlanWords : 0;
+        if ((rc = ensure(&b.slice_tot, &cap, (size_t)kPlanWords, "alloc slice_tot"))) return rc;
         size_t cap2 = b.slice_base ? 128 : 0;
         if ((rc = ensure(&b.slice_base, &cap2, (size_t)128, "alloc slice_base"))) return rc;
+        size_t cap3 = (size_t)b.sort_slices_cap;
+        if ((rc = ensure(&b.sort_slices, &cap3, (size_t)64, "alloc sort_slices"))) return rc;
+        b.sort_slices_cap = (int)cap3;
     }
-    std::vector<unsigned long long> tot(3 * S, 0ull);
     stage_begin(p, kStageCount, st);
     if (c->n > 0) {
         if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
@@ -225,32 +232,31 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
             return rc;
         if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
             return rc;
-        UGS_CUDA(cudaMemcpyAsync(tot.data(), b.slice_tot, sizeof(unsigned long long) * 3 * S,
-                                 cudaMemcpyDeviceToHost, st));
+    } else {
+        UGS_CUDA(cudaMemsetAsync(b.slice_tot, 0, sizeof(unsigned long long) * 3 * S, st));
     }
+    // bases and sort tables on the device; one small pinned D2H of the totals
+    if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices, st)))
+        return rc;
+    UGS_CUDA(cudaMemcpyAsync(p->h_plan, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                             cudaMemcpyDeviceToHost, st));
     stage_end(p, kStageCount, st);
     UGS_CUDA(cudaStreamSynchronize(st));
-    int64_t m_total = 0, k_total = 0, p_total = 0;
+    const unsigned long long *tot = p->h_plan;
+    const unsigned long long *tt = p->h_plan + 3 * 64;
     for (int s = 0; s < S; ++s) {
-        p->h_slice_base[2 * s] = m_total;
-        p->h_slice_base[2 * s + 1] = k_total;
-        p->h_m[s] = (int64_t)tot[3 * s];
         if (m_out) m_out[s] = (int64_t)tot[3 * s];
         if (k_out) k_out[s] = (int64_t)tot[3 * s + 1];
         if (p_out) p_out[s] = (int64_t)tot[3 * s + 2];
-        m_total += (int64_t)tot[3 * s];
-        k_total += (int64_t)tot[3 * s + 1];
-        p_total += (int64_t)tot[3 * s + 2];
     }
-    p->p_total = p_total;
+    const int64_t m_total = (int64_t)tt[0], k_total = (int64_t)tt[1];
+    p->p_total = (int64_t)tt[2];
     if (k_total >= 0x7fffffffLL || m_total >= 0x7fffffffLL) {
         set_error("ugs_bin: batch exceeds 2^31 tile instances; use fewer slices");
         return UGS_ERR_RANGE;
     }
     p->m_total = m_total;
     p->k_total = k_total;
-    UGS_CUDA(cudaMemcpyAsync(b.slice_base, p->h_slice_base, sizeof(int64_t) * 2 * S,
-                             cudaMemcpyHostToDevice, st));
     if ((rc = ensure(&b.rec, &b.rec_cap, (size_t)m_total + 1, "alloc rec"))) return rc;
     if ((rc = ensure(&b.rec_gid, &b.rec_gid_cap, (size_t)m_total + 2, "alloc rec_gid")))
         return rc;
@@ -259,13 +265,9 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
     {
-        size_t cap = b.slice_m ? 64 : 0;
-        if ((rc = ensure(&b.slice_m, &cap, (size_t)64, "alloc slice_m"))) return rc;
         size_t cap2 = b.bg_sums ? 64 : 0;
         if ((rc = ensure(&b.bg_sums, &cap2, (size_t)64, "alloc bg_sums"))) return rc;
     }
-    UGS_CUDA(cudaMemcpyAsync(b.slice_m, p->h_m, sizeof(int64_t) * S,
-                             cudaMemcpyHostToDevice, st));
     const size_t kneed = (size_t)k_total + 1;
     if (kneed > b.inst_cap || !b.idata) {
         void *olds[] = {b.idata, b.keys, b.vals, b.keys2, b.vals2, b.partial};
@@ -281,36 +283,14 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     }
     // bin sort plan: single-pass per-slice counting sort when every slice has
     // <= kSliceSortMaxTiles tiles and the tables fit the scan, else LSD radix
-    std::vector<SortSlice> ss(S);
-    int64_t hist_n = 0;
-    int nblk_sort = 0;
-    for (int s = 0; s < S; ++s) {
-        SortSlice &q = ss[s];
-        q.inst_base = (int)p->h_slice_base[2 * s + 1];
-        q.k = (int)tot[3 * s + 1];
-        q.tile_base = p->h_tile_base[s];
-        q.ntile = p->h_ntile[s];
-        q.nb = (q.k + kSortTile - 1) / kSortTile;
-        q.bpre = nblk_sort;
-        q.hoff = (int)hist_n;
-        q.pad = 0;
-        nblk_sort += q.nb;
-        hist_n += (int64_t)q.ntile * q.nb;
-    }
+    const int64_t hist_n = (int64_t)tt[3];
+    const int nblk_sort = (int)tt[4];
     p->slice_sort = max_tiles <= kSliceSortMaxTiles && hist_n < ((int64_t)1 << 24);
     const size_t hn = (p->slice_sort ? (size_t)hist_n : radix_hist_entries(k_total)) + 1;
     if ((rc = ensure(&b.hist, &b.hist_cap, hn, "alloc hist"))) return rc;
     if ((rc = ensure(&b.scan_tmp, &b.scan_tmp_cap, scan_tmp_entries(hn) + 1,
                      "alloc scan_tmp")))
         return rc;
-    {
-        size_t cap = (size_t)b.sort_slices_cap;
-        if ((rc = ensure(&b.sort_slices, &cap, (size_t)64, "alloc sort_slices"))) return rc;
-        b.sort_slices_cap = (int)cap;
-    }
-    if (p->slice_sort)
-        UGS_CUDA(cudaMemcpyAsync(b.sort_slices, ss.data(), sizeof(SortSlice) * S,
-                                 cudaMemcpyHostToDevice, st));
     p->hist_n = hist_n;
     p->nblk_sort = nblk_sort;
     if (b.bin_cap < (size_t)n_bins || !b.bin_range) {
@@ -328,9 +308,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
                                       b.wcnt, b.warp_rec, st)))
             return rc;
     } else {
-        int32_t zero = 0;
-        UGS_CUDA(cudaMemcpyAsync(b.rec_inst, &zero, sizeof(int32_t),
-                                 cudaMemcpyHostToDevice, st));
+        UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));
     }
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);

@@ -72,7 +72,6 @@ struct PlanBuffers {
     size_t rec_cap = 0, rec_gid_cap = 0, rec_inst_cap = 0;
     float *rgrad = nullptr;         // [M][12] per-record raw gradients (backward)
     size_t rgrad_cap = 0;
-    int64_t *slice_m = nullptr;     // [S] accepted records per slice
     double2 *bg_sums = nullptr;     // [64] per-slice background gradient sums
     // instances
     Inst *idata = nullptr;          // [K] (D, E, F, record) of each (unsorted) instance
@@ -104,6 +103,7 @@ struct ugs_plan {
     int max_tiles = 0;
     int64_t *h_slice_base = nullptr; // host copy [S][2]
     int64_t *h_m = nullptr;          // host [S]
+    unsigned long long *h_plan = nullptr;   // pinned [kPlanWords] (slice_tot D2H)
     int64_t p_total = 0;             // (Gaussian, pixel) pairs of the batch
     int32_t *h_tile_base = nullptr;  // host [S]
     int32_t *h_ntile = nullptr;      // host [S]
@@ -163,6 +163,11 @@ void stage_end(ugs_plan *p, int stage, cudaStream_t st);
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
                          uint2 *win_sparse, uint32_t *amask, uint2 *wcnt, cudaStream_t st);
+// per-slice bases + sort tables on the device; slice_tot holds [3*64] per-slice
+// (accepted, tiles, pairs) then 5 totals (m, k, pairs, sort entries, blocks)
+constexpr int kPlanWords = 3 * 64 + 8;
+int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
+                       int64_t *slice_base, SortSlice *ss, cudaStream_t st);
 int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st);
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,

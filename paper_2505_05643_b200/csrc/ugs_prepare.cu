@@ -285,6 +285,43 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
         }
 }
 
+// One thread: per-slice record / instance bases and the bin-sort tables from
+// the per-slice totals, on the device -- the host only reads the totals back
+// (one pinned D2H copy) to size buffers and grids.  totals = (m, k, pairs,
+// sort-table entries, sort blocks).
+__global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
+                                   const ugs_slice *__restrict__ slices, int S,
+                                   int64_t *__restrict__ slice_base,
+                                   SortSlice *__restrict__ ss) {
+    if (threadIdx.x != 0) return;
+    unsigned long long m = 0, k = 0, pr = 0, hn = 0, nbs = 0;
+    for (int s = 0; s < S; ++s) {
+        slice_base[2 * s] = (int64_t)m;
+        slice_base[2 * s + 1] = (int64_t)k;
+        SortSlice q;
+        q.inst_base = (int)k;
+        q.k = (int)tot[3 * s + 1];
+        q.tile_base = slices[s].tile_base;
+        q.ntile = slices[s].tiles_x * slices[s].tiles_y;
+        q.nb = (q.k + kSortTile - 1) / kSortTile;
+        q.bpre = (int)nbs;
+        q.hoff = (int)hn;
+        q.pad = 0;
+        ss[s] = q;
+        m += tot[3 * s];
+        k += tot[3 * s + 1];
+        pr += tot[3 * s + 2];
+        nbs += (unsigned long long)q.nb;
+        hn += (unsigned long long)q.ntile * q.nb;
+    }
+    unsigned long long *t = tot + 3 * kMaxSlicesSmem;
+    t[0] = m;
+    t[1] = k;
+    t[2] = pr;
+    t[3] = hn;
+    t[4] = nbs;
+}
+
 }  // namespace
 
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
@@ -294,6 +331,13 @@ int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
         c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk,
         win_sparse, amask, wcnt);
     UGS_LAUNCH_CHECK("prepare_count_kernel");
+    return UGS_OK;
+}
+
+int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
+                       int64_t *slice_base, SortSlice *ss, cudaStream_t st) {
+    plan_slices_kernel<<<1, 32, 0, st>>>(slice_tot, slices, S, slice_base, ss);
+    UGS_LAUNCH_CHECK("plan_slices_kernel");
     return UGS_OK;
 }
 
