@@ -397,11 +397,13 @@ def run_ours(a):
     except (OSError, ValueError):
         pass
     n = eng.cloud.n
-    # parameter update: N=1 fuses accumulate + stats + Adam into the finalize
-    # stage (params 44 B + m, v 96 B read and written per Gaussian); N>1 runs
-    # a separate Adam over the dense AoS-12 gradient (+ gradient r/w 96 B)
-    upd_stage = "finalize" if world == 1 else "adam"
-    upd_bytes = (280 if world == 1 else 376) * n
+    # parameter update (update_gather_kernel): N=1 fuses accumulate + stats +
+    # Adam -- reads params 44 B + m, v 96 B and writes them back (280 B per
+    # Gaussian) plus 48 B per record gradient row; N>1 adds the dense AoS-12
+    # gradient row write (48 B) and a separate Adam (ugs_adam_step, +96 B)
+    m_per_step = float(np.sum(eng.renderer.m)) if hasattr(eng.renderer, "m") else 0.0
+    upd_stage = "update" if world == 1 else "adam"
+    upd_bytes = (280 * n + 48 * m_per_step) if world == 1 else (376 + 48) * n + 48 * m_per_step
     upd_ms = stage_ms.get(upd_stage, float("nan"))
 
     def tflops(fpp, k):

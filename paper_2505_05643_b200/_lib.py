@@ -88,7 +88,7 @@ EXPORTS = {
 }
 
 STAGES = ("prepare_count", "prepare_emit", "sort", "bin_ranges", "forward",
-          "backward", "finalize")
+          "backward", "finalize", "update")
 
 
 def load(path: str = LIB_PATH):

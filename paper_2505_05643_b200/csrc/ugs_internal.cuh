@@ -153,7 +153,8 @@ enum Stage {
     kStageRanges,      // bin ranges
     kStageForward,     // forward_kernel
     kStageBackward,    // backward_kernel
-    kStageFinalize,    // finalize + bg_finalize (all slices)
+    kStageFinalize,    // bg_slice + finalize_records (all slices)
+    kStageUpdate,      // update_gather (accumulate + stats + Adam) + bg_finalize
     kNumStages
 };
 void stage_begin(ugs_plan *p, int stage, cudaStream_t st);

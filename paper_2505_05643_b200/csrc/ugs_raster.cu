@@ -841,6 +841,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
     }
+    stage_end(pm, kStageFinalize, st);
+    stage_begin(pm, kStageUpdate, st);
     if (c.n > 0 && (adam || p.m_total > 0)) {
         const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
         const int64_t nwarp_all = nblk * (kPrepThreads / 32);
@@ -862,7 +864,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                                              AdamConst{});
     }
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
-    stage_end(pm, kStageFinalize, st);
+    stage_end(pm, kStageUpdate, st);
     return UGS_OK;
 }
 
