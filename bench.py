@@ -232,10 +232,19 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # UGS_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to
+    # exercise the N > 1 code path on a one-GPU box (NCCL refuses that)
+    one_dev = os.environ.get("UGS_BENCH_ONE_DEVICE", "0") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl",
+                                                 device_id=torch.device("cuda", local))
     import paper_2505_05643_b200 as ug
     from paper_2505_05643_b200 import _lib
     from paper_2505_05643_b200.trainer import TrainEngine
@@ -427,10 +436,14 @@ def run_ours(a):
         "dtype": "f32", "data": "synthetic (160^3 shells phantom, random-pose GT slices, random-init cloud)",
         "config": {"workload": workload_desc(a), "n_gaussians": a.n_gaussians,
                    "slice": [a.size, a.size], "batch_per_gpu": B, "global_batch": B * world,
-                   "parallelism": f"dp{world}",
+                   "parallelism": f"dp{world}" + (
+                       "" if world == 1 else
+                       " (fused reduce-scatter+Adam+all-gather over NVLink peer memory)"
+                       if eng.peer else " (NCCL all-reduce + replicated Adam)"),
                    "step": "param reset to the fixed C3 cloud (device copy)+ugs_bin+forward+"
                            "loss(L1+0.2*SSIM, f64)+backward+"
-                           + ("allreduce+" if world > 1 else "") + "grad_stats+Adam",
+                           + ("" if world == 1 else "peer update (reduce-scatter+Adam+all-gather)+"
+                              if eng.peer else "allreduce+") + "grad_stats+Adam",
                    "l2": "inputs larger than L2: params+Adam moments+grads = "
                          f"{(44 + 88 + 44) * n / 1e6:.0f} MB streamed per step",
                    "pairs_per_slice": pairs_per_step / B},

@@ -131,8 +131,8 @@ UGS_API int ugs_forward(ugs_plan *plan, const ugs_cloud *cloud, float *num, floa
 
 /* Backward for every slice of the last ugs_bin.  d_pixels (dev, same layout
  * as num).  Accumulates `scale` x (raw-parameter gradients) into grad (dev,
- * AoS-12) and sets touched[g] = 1 for every accepted Gaussian (touched may
- * be NULL).  Slices are reduced in order, without atomics: deterministic. */
+ * AoS-12), sets the pad slot of every accepted Gaussian's row to 1 and
+ * touched[g] = 1 (touched may be NULL).  Slices are reduced in order, without atomics: deterministic. */
 UGS_API int ugs_backward(ugs_plan *plan, const ugs_cloud *cloud, const float *num,
                  const float *den, const float *d_pixels, float *grad,
                  uint8_t *touched, float scale, void *stream);
@@ -201,6 +201,44 @@ UGS_API int ugs_loss(const float *num, const float *den, const float *target,
  * ascending index, the reference's sequential workers=1 order
  * (_kernels.py:23-47).  Both are deterministic. */
 UGS_API int ugs_plan_set_ordered(ugs_plan *plan, int ordered);
+
+/* ---- multi-GPU update over peer memory (the reference
+ * is single-process) -------------------------------------------------------
+ * Each rank owns an "arena" (ugs_ipc_alloc: device memory + a 64-byte CUDA
+ * IPC handle) holding its parameters, AoS-12 gradient and moments and the
+ * densify statistics; every process maps each peer's arena (ugs_ipc_open)
+ * and describes all of them, as mapped locally, with ugs_peer_view. */
+typedef struct ugs_peer_view {
+    float *means, *l_raw, *intensity_raw, *opacity_raw; /* SoA, n rows */
+    float *grad, *m, *v;   /* AoS-12 (12 n + 2), 16-byte aligned */
+    float *grad_sum;       /* densify statistics, n */
+    int32_t *grad_cnt;
+    double *bg_raw;        /* the rank's background pair */
+} ugs_peer_view;
+
+UGS_API int ugs_ipc_alloc(size_t bytes, void **ptr, void *handle64);
+UGS_API int ugs_ipc_open(const void *handle64, void **ptr);
+UGS_API int ugs_ipc_close(void *ptr);
+UGS_API int ugs_ipc_free(void *ptr);
+
+/* Fused reduce-scatter + Adam + all-gather (replaces the all-reduce of the
+ * gradient and the replicated adam_step, trainer.py:170-200): for g in the
+ * rank's shard [lo, hi) sums the W ranks' gradient rows in rank order (pad
+ * slot > 0 marks a Gaussian some rank's slice accepted: densify statistics,
+ * trainer.py:399-401, when stats != 0), applies the bit-compatible Adam to
+ * the owned rows of this rank's arena and writes the new parameter rows into
+ * every peer's arena; every rank updates the background pair identically.
+ * The caller brackets it with barriers (all gradients written before; all
+ * parameter rows stored after). */
+UGS_API int ugs_peer_update(const ugs_peer_view *views, int world, int rank, int64_t n,
+                            int64_t lo, int64_t hi, int64_t t, const double *lr,
+                            double beta1, double beta2, double eps, int stats,
+                            void *stream);
+
+/* Before densify: copies the m, v, grad_sum, grad_cnt rows owned by other
+ * ranks (shard q = [n q / W, n (q+1) / W)) into this rank's arena. */
+UGS_API int ugs_peer_gather(const ugs_peer_view *views, int world, int rank, int64_t n,
+                            void *stream);
 
 /* ---- diagnostics (no counterpart in the reference, which has no tracing:
  * SURVEY section 5) --------------------------------------------------- */

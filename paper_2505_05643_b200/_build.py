@@ -25,7 +25,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
 # densify float64 math follow numpy's unfused rounding)
 NO_FMAD = {"ugs_adam.cu"}
 SOURCES = ["ugs_api.cu", "ugs_prepare.cu", "ugs_sort.cu", "ugs_raster.cu",
-           "ugs_adam.cu", "ugs_diag.cu", "ugs_loss.cu"]
+           "ugs_adam.cu", "ugs_diag.cu", "ugs_loss.cu", "ugs_peer.cu"]
 
 
 def nvcc() -> str:

@@ -44,6 +44,13 @@ class Cloud(ctypes.Structure):
                 ("beta", ctypes.c_double)]
 
 
+class PeerView(ctypes.Structure):
+    """struct ugs_peer_view (include/ugs.h): one rank's arena, as mapped here."""
+    _fields_ = [("means", c_vp), ("l_raw", c_vp), ("intensity_raw", c_vp),
+                ("opacity_raw", c_vp), ("grad", c_vp), ("m", c_vp), ("v", c_vp),
+                ("grad_sum", c_vp), ("grad_cnt", c_vp), ("bg_raw", c_vp)]
+
+
 EXPORTS = {
     "ugs_last_error": (ctypes.c_char_p, []),
     "ugs_abi_version": (ctypes.c_int, []),
@@ -85,6 +92,17 @@ EXPORTS = {
     "ugs_plan_timings": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(c_i64), ctypes.c_int,
                                         ctypes.c_int]),
+    "ugs_ipc_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(c_vp), c_vp]),
+    "ugs_ipc_open": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "ugs_ipc_close": (ctypes.c_int, [c_vp]),
+    "ugs_ipc_free": (ctypes.c_int, [c_vp]),
+    "ugs_peer_update": (ctypes.c_int, [ctypes.POINTER(PeerView), ctypes.c_int, ctypes.c_int,
+                                       c_i64, c_i64, c_i64, c_i64,
+                                       ctypes.POINTER(ctypes.c_double), ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                       c_vp]),
+    "ugs_peer_gather": (ctypes.c_int, [ctypes.POINTER(PeerView), ctypes.c_int, ctypes.c_int,
+                                       c_i64, c_vp]),
 }
 
 STAGES = ("prepare_count", "prepare_emit", "sort", "bin_ranges", "forward",

@@ -718,6 +718,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         float *row = grad + kG * g;
 #pragma unroll
         for (int j = 0; j < 11; ++j) row[j] += acc[j];
+        row[11] = 1.f;   // accepted by a slice of this batch (peer update)
         if (touched) touched[g] = 1;
     }
 }

@@ -82,3 +82,95 @@ def allreduce_gradients(flat: torch.Tensor, touched: torch.Tensor | None = None,
     dist.all_reduce(flat, group=group)
     if touched is not None:
         dist.all_reduce(touched, op=dist.ReduceOp.MAX, group=group)
+
+
+# ---------------------------------------------------------------------------
+# Fused multi-GPU update over peer memory (ugs_peer_update, include/ugs.h)
+# ---------------------------------------------------------------------------
+
+class _CudaArray:
+    """A raw device range as a __cuda_array_interface__ object, so torch can
+    alias it without a copy."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _align(x: int, a: int = 256) -> int:
+    return (x + a - 1) // a * a
+
+
+class PeerArena:
+    """One rank's arena -- parameters, AoS-12 gradient and moments, densify
+    statistics and background -- in a single CUDA IPC-exportable allocation,
+    plus every peer's arena mapped into this process (cudaIpcOpenMemHandle;
+    over NVLink on an NVSwitch node).  ``views`` describes all of them for
+    ugs_peer_update / ugs_peer_gather.  Collective: every rank constructs
+    (and closes) its arena at the same point of the program."""
+
+    # (name, floats-or-ints per row, extra entries, typestr)
+    _FIELDS = (("means", 3, 0, "<f4"), ("l_raw", 6, 0, "<f4"),
+               ("intensity_raw", 1, 0, "<f4"), ("opacity_raw", 1, 0, "<f4"),
+               ("grad", 12, 4, "<f4"), ("m", 12, 4, "<f4"), ("v", 12, 4, "<f4"),
+               ("grad_sum", 1, 0, "<f4"), ("grad_cnt", 1, 0, "<i4"))
+
+    def __init__(self, n: int, world: int, rank: int, group=None):
+        import ctypes
+        import torch.distributed as dist
+        from . import _lib
+        self.n, self.world, self.rank, self.group = n, world, rank, group
+        L = _lib.lib()
+        off, self.offsets = 0, {}
+        for name, per, extra, _ in self._FIELDS:
+            self.offsets[name] = off
+            off = _align(off + 4 * (per * n + extra))
+        self.offsets["bg_raw"] = off
+        self.nbytes = off + 16
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_ubyte * 64)()
+        _lib.check(L.ugs_ipc_alloc(self.nbytes, ctypes.byref(ptr), handle), "ugs_ipc_alloc")
+        self.ptr = ptr.value
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.bases = []
+        for q in range(world):
+            if q == rank:
+                self.bases.append(self.ptr)
+                continue
+            h = (ctypes.c_ubyte * 64).from_buffer_copy(handles[q])
+            pp = ctypes.c_void_p()
+            _lib.check(L.ugs_ipc_open(h, ctypes.byref(pp)), "ugs_ipc_open")
+            self.bases.append(pp.value)
+        self.views = (_lib.PeerView * world)()
+        for q, b in enumerate(self.bases):
+            v = self.views[q]
+            for name in ("means", "l_raw", "intensity_raw", "opacity_raw", "grad", "m",
+                         "v", "grad_sum", "grad_cnt", "bg_raw"):
+                setattr(v, name, b + self.offsets[name])
+        # this rank's arena as torch tensors (aliases, no copies)
+        self.t = {}
+        for name, per, extra, ts in self._FIELDS:
+            shape = (n, per) if (per > 1 and extra == 0) else (per * n + extra,)
+            self.t[name] = torch.as_tensor(
+                _CudaArray(self.ptr + self.offsets[name], shape, ts), device="cuda")
+        self.t["bg_raw"] = torch.as_tensor(
+            _CudaArray(self.ptr + self.offsets["bg_raw"], (2,), "<f8"), device="cuda")
+
+    def shard(self):
+        """[lo, hi) of the Gaussians this rank updates."""
+        return (self.n * self.rank) // self.world, (self.n * (self.rank + 1)) // self.world
+
+    def close(self, barrier) -> None:
+        """Unmap the peers and free this arena once every rank is done with it."""
+        from . import _lib
+        barrier()
+        L = _lib.lib()
+        for q, b in enumerate(self.bases):
+            if q != self.rank:
+                _lib.check(L.ugs_ipc_close(b), "ugs_ipc_close")
+        self.t = {}
+        torch.cuda.synchronize()
+        _lib.check(L.ugs_ipc_free(self.ptr), "ugs_ipc_free")
+        self.bases = []

@@ -349,10 +349,18 @@ class TrainEngine:
     """Device-resident training state and the fused per-step pipeline."""
 
     def __init__(self, cloud: GaussianCloud, config: TrainConfig, specs, targets,
-                 world_size: int = 1, rank: int = 0, process_group=None):
+                 world_size: int = 1, rank: int = 0, process_group=None,
+                 peer_update: bool | None = None):
         self.cloud = cloud
         self.config = config
         self.state = AdamState.for_cloud(cloud)
+        # world > 1: fused reduce-scatter + Adam + all-gather over peer memory
+        # (ugs_peer_update) instead of the NCCL all-reduce + replicated Adam
+        # (default for world > 1; UGS_PEER_UPDATE=0 selects the NCCL path)
+        if peer_update is None:
+            peer_update = os.environ.get("UGS_PEER_UPDATE", "1") == "1"
+        self.peer = bool(peer_update) and world_size > 1
+        self.arena = None
         self.renderer = Renderer()
         self.specs = list(specs)
         self.targets = targets        # (n_slices, H, W) float32 on the device
@@ -369,6 +377,82 @@ class TrainEngine:
         self.grad = grad_buffer(cloud.n, cloud.device)
         self.last_loss = None
         self.last_pred = None
+        if self.peer:
+            self._bar = torch.zeros(1, dtype=torch.float32, device=cloud.device)
+            self.peer = self._try_adopt_arena()
+
+    # ---- peer-memory update (world > 1) ----
+    def barrier(self):
+        """All ranks' work enqueued so far is complete everywhere.  NCCL: a
+        1-element all-reduce, ordered on the stream (no host sync); gloo
+        (two ranks on one GPU in the tests): host-side."""
+        import torch.distributed as dist
+        if dist.get_backend(self.pg) == "nccl":
+            dist.all_reduce(self._bar, group=self.pg)
+        else:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.pg)
+
+    def _try_adopt_arena(self) -> bool:
+        """Set up the peer arenas; every rank agrees on the outcome, and any
+        failure (no CUDA IPC / peer access) falls back to the NCCL path."""
+        import torch.distributed as dist
+        from .parallel import PeerArena
+        arena, ok = None, 1.0
+        try:
+            arena = PeerArena(self.cloud.n, self.world_size, self.rank, self.pg)
+        except Exception as exc:  # pragma: no cover - depends on the node
+            ok = 0.0
+            self.peer_error = repr(exc)
+        flag = torch.tensor([ok], device=self.cloud.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.pg)
+        if flag.item() < 1.0:
+            if arena is not None:
+                try:
+                    arena.close(lambda: None)
+                except Exception:  # pragma: no cover
+                    pass
+            return False
+        self._adopt_arena(arena)
+        return True
+
+    def _adopt_arena(self, a=None):
+        """Move the cloud, moments and statistics into a (fresh) peer arena."""
+        from .parallel import PeerArena
+        old = self.arena
+        if a is None:
+            a = PeerArena(self.cloud.n, self.world_size, self.rank, self.pg)
+        c, st = self.cloud, self.state
+        a.t["means"].copy_(c.means)
+        a.t["l_raw"].copy_(c.l_raw)
+        a.t["intensity_raw"].copy_(c.intensity_raw)
+        a.t["opacity_raw"].copy_(c.opacity_raw)
+        a.t["bg_raw"].copy_(c.bg_raw)
+        a.t["m"][:st.m_flat.numel()].copy_(st.m_flat)
+        a.t["v"][:st.v_flat.numel()].copy_(st.v_flat)
+        a.t["grad_sum"].copy_(self.grad_sum)
+        a.t["grad_cnt"].copy_(self.grad_cnt)
+        c.means, c.l_raw = a.t["means"], a.t["l_raw"]
+        c.intensity_raw, c.opacity_raw = a.t["intensity_raw"], a.t["opacity_raw"]
+        c.bg_raw = a.t["bg_raw"]
+        n = c.n
+        st.m_flat, st.v_flat = a.t["m"][:12 * n + 2], a.t["v"][:12 * n + 2]
+        self.grad = a.t["grad"][:12 * n + 2]
+        self.grad_sum, self.grad_cnt = a.t["grad_sum"], a.t["grad_cnt"]
+        self.arena = a
+        if old is not None:
+            old.close(self.barrier)
+        self.barrier()
+
+    def _peer_step(self, lrs):
+        st = self.state
+        st.t += 1
+        lo, hi = self.arena.shard()
+        self.barrier()            # every rank's gradient is in its arena
+        _lib.check(_lib.lib().ugs_peer_update(
+            self.arena.views, self.world_size, self.rank, self.cloud.n, lo, hi, st.t,
+            _lr_array(lrs), st.beta1, st.beta2, st.eps, 1, _stream()), "ugs_peer_update")
+        self.barrier()            # every parameter row is stored everywhere
 
     def _alloc_stats(self):
         n, dev = self.cloud.n, self.cloud.device
@@ -462,6 +546,13 @@ class TrainEngine:
                 "ugs_backward_adam")
             self._mark("adam1")
             return loss_val if check_finite else loss_t
+        if self.peer:
+            self.grad.zero_()
+            self.renderer.backward(self.cloud, num, den, dpix, self.grad, None, scale)
+            self._mark("adam0")
+            self._peer_step(lrs)
+            self._mark("adam1")
+            return loss_val if check_finite else loss_t
         self.renderer.backward(self.cloud, num, den, dpix, self.grad, self.touched, scale)
         self._mark("allreduce0")
         allreduce_gradients(self.grad, self.touched, self.pg)
@@ -473,6 +564,13 @@ class TrainEngine:
         return loss_val if check_finite else loss_t
 
     def densify(self, rng, scene_extent, threshold, max_total):
+        if self.peer:
+            # the owners' rows of m, v and the statistics, so every rank
+            # densifies the same full state
+            self.barrier()
+            _lib.check(_lib.lib().ugs_peer_gather(self.arena.views, self.world_size,
+                                                  self.rank, self.cloud.n, _stream()),
+                       "ugs_peer_gather")
         avg = (self.grad_sum.double() / torch.clamp(self.grad_cnt, min=1).double()).cpu().numpy()
         if threshold is None:
             threshold = float(np.quantile(avg, 0.9))
@@ -481,6 +579,8 @@ class TrainEngine:
             max_total)
         self._alloc_stats()
         self.grad = grad_buffer(self.cloud.n, self.cloud.device)
+        if self.peer:
+            self._adopt_arena()
         return threshold
 
 

@@ -46,8 +46,9 @@ def _params(cloud):
         "bg": np.array([cloud.bg_intensity_raw, cloud.bg_opacity_raw])}
 
 
-def _worker(rank, world, port, densify, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, port, densify, q, peer=False):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      UGS_PEER_UPDATE="1" if peer else "0")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2505_05643_b200 as ug
@@ -66,11 +67,12 @@ def _free_port():
     return p
 
 
-def _run_two(densify):
+def _run_two(densify, peer=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, densify, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, densify, q, peer))
+             for r in range(2)]
     for p in procs:
         p.start()
     out = {}
@@ -99,3 +101,26 @@ def test_two_ranks_densify_in_lockstep():
     assert out[0]["means"].shape == out[1]["means"].shape
     for k in out[0]:
         assert np.array_equal(out[0][k], out[1][k]), k
+
+
+def test_peer_update_matches_single_process_global_batch():
+    """The fused reduce-scatter + Adam + all-gather over CUDA IPC peer memory
+    (ugs_peer_update): replicas identical, same trajectory as one process
+    with the global batch."""
+    import paper_2505_05643_b200 as ug
+    out = _run_two(densify=0, peer=True)
+    for k in out[0]:
+        assert np.array_equal(out[0][k], out[1][k]), k
+    ref, _ = ug.train(_dataset(), _config(2 * B, 0), device="cuda:0")
+    ref = _params(ref)
+    for k in ref:
+        np.testing.assert_allclose(out[0][k], ref[k], rtol=1e-3, atol=1e-4, err_msg=k)
+
+
+def test_peer_update_densify_in_lockstep():
+    out = _run_two(densify=5, peer=True)
+    ref = _run_two(densify=5, peer=False)
+    assert out[0]["means"].shape == out[1]["means"].shape == ref[0]["means"].shape
+    for k in out[0]:
+        assert np.array_equal(out[0][k], out[1][k]), k
+        np.testing.assert_allclose(out[0][k], ref[0][k], rtol=1e-3, atol=1e-4, err_msg=k)
