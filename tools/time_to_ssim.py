@@ -24,40 +24,29 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run(n=200_000, train_slices=2048, test_slices=64, batch=16, budget=600.0, target=0.99,
-        eval_every=100, iterations=20000, densify=0, l_lo=0.85, l_hi=1.05, log=print):
-    """Train on C2 until the mean held-out SSIM reaches `target` (or the
-    budget runs out); returns the result dict."""
+def train_to_target(bounds, train_specs, gt_train, test_specs, gt_test, n=200_000,
+                    batch=16, budget=600.0, target=0.99, eval_every=100, iterations=20000,
+                    densify=0, l_lo=0.85, l_hi=1.05, log=print):
+    """Train on (train_specs, gt_train) until the mean SSIM of the renders at
+    test_specs against gt_test reaches `target` or the budget runs out."""
     import torch
     import paper_2505_05643_b200 as ug
-    from paper_2505_05643_b200.dataset import random_pose_specs
     from paper_2505_05643_b200.metrics import ssim_batch
     from paper_2505_05643_b200.parallel import SliceScheduler
     from paper_2505_05643_b200.trainer import TrainEngine
 
-    cfg_in = dict(n=n, train_slices=train_slices, test_slices=test_slices, batch=batch,
-                  budget=budget, target=target, eval_every=eval_every,
-                  iterations=iterations, densify=densify, l_lo=l_lo, l_hi=l_hi)
-    t_setup = time.perf_counter()
-    vol = ug.make_phantom("shells", 160, 0.6, seed=1)
-    specs = random_pose_specs(train_slices + test_slices, 256, 256, 0.375, seed=11,
-                              translate=12.0)
-    train_specs, test_specs = specs[:train_slices], specs[train_slices:]
-    gt_train = ug.sample_slices(vol, train_specs)
-    gt_test = ug.sample_slices(vol, test_specs)
     cfg = ug.TrainConfig(n_gaussians=n, iterations=iterations, seed=0,
                          l_init_low=l_lo, l_init_high=l_hi, lr_means_start=0.016,
                          lr_means_final=1.6e-4, lr_general_final=0.005,
                          heuristic_interval=densify, batch=batch)
-    cloud = ug.init_cloud(cfg, vol.world_bounds(), device="cuda")
+    cloud = ug.init_cloud(cfg, bounds, device="cuda")
     eng = TrainEngine(cloud, cfg, train_specs, gt_train)
     renderer = ug.Renderer()
-    bounds = vol.world_bounds()
+    bounds = np.asarray(bounds, np.float64)
     scene_extent = float(np.linalg.norm(bounds[1] - bounds[0]))
     rng = np.random.default_rng(cfg.seed)
     sched = SliceScheduler(rng, len(train_specs), batch)
     threshold = cfg.densify_grad_threshold
-    setup_s = time.perf_counter() - t_setup
 
     def heldout():
         preds = ug.render_slices(eng.cloud, test_specs, cfg.p_mass, renderer)
@@ -91,14 +80,38 @@ def run(n=200_000, train_slices=2048, test_slices=64, batch=16, budget=600.0, ta
                 reached = el
             if reached is not None or el >= budget:
                 break
-    return {"metric": "time to held-out SSIM target", "target": target,
-            "reached_s": reached, "best_ssim": max(e["ssim"] for e in entries),
-            "iterations": it, "slices_trained": it * batch,
-            "config": cfg_in, "setup_s": setup_s, "log": entries,
-            "note": "C2: 160^3 shells phantom, init_cloud over its bounds, 256x256 "
-                    "@0.375 mm random-pose slices (train set + disjoint held-out "
-                    "set, trilinear GT); train_s is wall-clock training time on one "
-                    "GPU, held-out evaluations excluded"}
+    return {"target": target, "reached_s": reached,
+            "best_ssim": max(e["ssim"] for e in entries), "iterations": it,
+            "slices_trained": it * batch, "log": entries}
+
+
+def run(n=200_000, train_slices=2048, test_slices=64, batch=16, budget=600.0, target=0.99,
+        eval_every=100, iterations=20000, densify=0, l_lo=0.85, l_hi=1.05, log=print):
+    """Config C2: random-pose train / held-out slices of the 160^3 phantom."""
+    import paper_2505_05643_b200 as ug
+    from paper_2505_05643_b200.dataset import random_pose_specs
+
+    cfg_in = dict(n=n, train_slices=train_slices, test_slices=test_slices, batch=batch,
+                  budget=budget, target=target, eval_every=eval_every,
+                  iterations=iterations, densify=densify, l_lo=l_lo, l_hi=l_hi)
+    t_setup = time.perf_counter()
+    vol = ug.make_phantom("shells", 160, 0.6, seed=1)
+    specs = random_pose_specs(train_slices + test_slices, 256, 256, 0.375, seed=11,
+                              translate=12.0)
+    train_specs, test_specs = specs[:train_slices], specs[train_slices:]
+    gt_train = ug.sample_slices(vol, train_specs)
+    gt_test = ug.sample_slices(vol, test_specs)
+    setup_s = time.perf_counter() - t_setup
+    out = train_to_target(vol.world_bounds(), train_specs, gt_train, test_specs, gt_test, n,
+                          batch, budget, target, eval_every, iterations, densify, l_lo,
+                          l_hi, log)
+    out.update({"metric": "time to held-out SSIM target", "config": cfg_in,
+                "setup_s": setup_s,
+                "note": "C2: 160^3 shells phantom, init_cloud over its bounds, 256x256 "
+                        "@0.375 mm random-pose slices (train set + disjoint held-out "
+                        "set, trilinear GT); train_s is wall-clock training time on one "
+                        "GPU, held-out evaluations excluded"})
+    return out
 
 
 def main():
