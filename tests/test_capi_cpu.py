@@ -38,6 +38,9 @@ def test_struct_layout():
     assert ctypes.sizeof(_lib.Slice) == 144
     assert _lib.Slice.pix_base.offset == 136
     assert ctypes.sizeof(_lib.Cloud) == 56
+    # ugs_peer_view: 10 device pointers
+    assert ctypes.sizeof(_lib.PeerView) == 80
+    assert _lib.PeerView.bg_raw.offset == 72
 
 
 def test_error_path_without_gpu():
