@@ -295,9 +295,9 @@ def run_ours(a):
     def step(targets_batch=None, idx=None):
         it[0] += 1
         c = eng.cloud
-        for dst, src in zip((c.means, c.l_raw, c.intensity_raw, c.opacity_raw,
-                             c.bg_raw), init):
-            dst.copy_(src)
+        # one multi-tensor copy kernel (5 separate DtoD memcpys cost ~36 us)
+        torch._foreach_copy_([c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.bg_raw],
+                             init)
         lt = eng.step(idx if idx is not None else next_batch(), it[0],
                       targets_batch=targets_batch, check_finite=False)
         k = it[0] % len(loss_ev)

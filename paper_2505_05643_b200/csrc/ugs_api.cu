@@ -77,6 +77,8 @@ int ensure_host(ugs_plan *p, int S) {
     if (!p->h_plan) {
         cudaError_t e = cudaMallocHost((void **)&p->h_plan, sizeof(unsigned long long) * kPlanWords);
         if (e != cudaSuccess) { p->h_plan = nullptr; return cuda_fail(e, "alloc h_plan"); }
+        e = cudaMallocHost((void **)&p->h_slices, sizeof(ugs_slice) * 64);
+        if (e != cudaSuccess) { p->h_slices = nullptr; return cuda_fail(e, "alloc h_slices"); }
     }
     if (S <= p->h_cap) return UGS_OK;
     delete[] p->h_slice_base;
@@ -144,6 +146,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     delete[] p->h_tile_base;
     delete[] p->h_ntile;
     if (p->h_plan) cudaFreeHost(p->h_plan);
+    if (p->h_slices) cudaFreeHost(p->h_slices);
     if (p->ev_ready)
         for (int i = 0; i < kNumStages; ++i)
             for (int j = 0; j < 2; ++j) cudaEventDestroy(p->ev[i][j]);
@@ -191,7 +194,11 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     size_t cap_sl = (size_t)b.slices_cap;
     if ((rc = ensure(&b.slices, &cap_sl, (size_t)S, "alloc slices"))) return rc;
     b.slices_cap = (int)cap_sl;
-    UGS_CUDA(cudaMemcpyAsync(b.slices, slices, sizeof(ugs_slice) * S,
+    // through pinned staging: an async DMA (a pageable copy would block the
+    // host until the stream drains, i.e. until the previous step finished);
+    // the previous call's copy from it completed at that call's sync
+    std::memcpy(p->h_slices, slices, sizeof(ugs_slice) * S);
+    UGS_CUDA(cudaMemcpyAsync(b.slices, p->h_slices, sizeof(ugs_slice) * S,
                              cudaMemcpyHostToDevice, st));
     const int nblk = (int)((c->n + kPrepThreads - 1) / kPrepThreads);
     if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, (size_t)S * (nblk > 0 ? nblk : 1),

@@ -104,6 +104,7 @@ struct ugs_plan {
     int64_t *h_slice_base = nullptr; // host copy [S][2]
     int64_t *h_m = nullptr;          // host [S]
     unsigned long long *h_plan = nullptr;   // pinned [kPlanWords] (slice_tot D2H)
+    ugs_slice *h_slices = nullptr;          // pinned [64] staging of the slice structs
     int64_t p_total = 0;             // (Gaussian, pixel) pairs of the batch
     int32_t *h_tile_base = nullptr;  // host [S]
     int32_t *h_ntile = nullptr;      // host [S]

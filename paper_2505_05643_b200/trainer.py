@@ -496,6 +496,11 @@ class TrainEngine:
         """bin + forward + loss for the slices `idx` (this rank's batch)."""
         cfg = self.config
         B = len(idx)
+        if targets_batch is None:
+            # slice ids via pinned memory: an async copy (a pageable one would
+            # block the host until the stream drains)
+            ids = torch.tensor(np.asarray(idx, np.int64)).pin_memory()
+            ids = ids.to(self.cloud.device, non_blocking=True)
         structs = self.batch_structs(idx)
         self.renderer.bin(self.cloud, [self.specs[i] for i in idx], cfg.p_mass, structs)
         self.pairs_total += int(self.renderer.pairs.sum())
@@ -504,7 +509,7 @@ class TrainEngine:
         self.renderer.forward(self.cloud, num, den)
         self._mark("loss0")
         if targets_batch is None:
-            tgt = self.targets[torch.as_tensor(np.asarray(idx), device=self.cloud.device)]
+            tgt = self.targets.index_select(0, ids)
         else:
             tgt = targets_batch
         lv, dpix, _ = fused_loss(num, den, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
