@@ -36,6 +36,9 @@ prepare_count_kernel(const float *__restrict__ means,
     __shared__ ugs_slice sl[kMaxSlicesSmem];
     __shared__ unsigned s_tiles[kMaxSlicesSmem], s_pairs[kMaxSlicesSmem];
     __shared__ unsigned s_wt[kMaxSlicesSmem][kW], s_bal[kMaxSlicesSmem][kW];
+    __shared__ uint32_t s_acc[kMaxSlicesSmem][kW];   // accept bits per (slice, warp)
+    __shared__ float s_fac[kW][9][32];                // L^-T (6) + mean (3) per lane
+    __shared__ uint16_t s_list[kW][32 * 32];          // candidate (slice << 5 | lane)
     load_slices_smem(sl, slices, S);
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
         s_tiles[s] = 0;
@@ -58,35 +61,78 @@ prepare_count_kernel(const float *__restrict__ means,
     if (valid)
         for (int s = 0; s < S; ++s)
             if (straddles(mu, f, sl[s])) zmask |= 1ull << s;
-    // 2) the in-plane test and window only for the straddled slices: a lane
-    //    loops over ITS slices, so the warp runs max-over-lanes (~4 of 16)
-    //    iterations instead of every slice any lane straddles
-    uint64_t accmask = 0;
-    while (zmask) {
-        const int s = __ffsll((long long)zmask) - 1;
-        zmask &= zmask - 1;
-        Window w;
-        if (cull_window_xy(mu, f, sl[s], w)) {
-            accmask |= 1ull << s;
-            // the emit pass reads the window back instead of recomputing
-            win_sparse[(size_t)s * n + g] =
-                make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
-            // integer sums: shared atomics give exact (order-free) totals
-            const unsigned nt = (unsigned)window_tiles(w);
-            atomicAdd(&s_tiles[s], nt);
-            atomicAdd(&s_wt[s][threadIdx.x >> 5], nt);
-            atomicAdd(&s_pairs[s], (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1)));
-        }
-    }
+    // 2) the in-plane test and window for the straddled (slice, Gaussian)
+    //    pairs, COMPACTED across the warp: every lane publishes its Gaussian's
+    //    L^-T and mean, the warp lists its candidate pairs and each lane takes
+    //    every 32nd -- ~2 rounds of full lanes instead of max-over-lanes
+    //    (~5) rounds of mostly idle ones
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
-    for (int s = 0; s < S; ++s) {
-        const unsigned bal = __ballot_sync(0xffffffffu, (unsigned)(accmask >> s) & 1u);
-        if (lane == 0) {
-            amask[(size_t)s * nwarp_all + gwarp] = bal;
-            s_bal[s][warp] = (unsigned)__popc(bal);
+    {
+        float *fw = &s_fac[warp][0][0];
+        fw[0 * 32 + lane] = f.LT[0][0];
+        fw[1 * 32 + lane] = f.LT[0][1];
+        fw[2 * 32 + lane] = f.LT[0][2];
+        fw[3 * 32 + lane] = f.LT[1][1];
+        fw[4 * 32 + lane] = f.LT[1][2];
+        fw[5 * 32 + lane] = f.LT[2][2];
+        fw[6 * 32 + lane] = mu[0];
+        fw[7 * 32 + lane] = mu[1];
+        fw[8 * 32 + lane] = mu[2];
+    }
+    for (int s = lane; s < S; s += 32) s_acc[s][warp] = 0u;
+    __syncwarp();
+    for (int c0 = 0; c0 < S; c0 += 32) {
+        const uint32_t zc = (uint32_t)(zmask >> c0);
+        const unsigned cnt = __popc(zc);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
         }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned j = incl - cnt;
+        for (uint32_t m = zc; m; m &= m - 1)
+            s_list[warp][j++] = (uint16_t)(((c0 + __ffs(m) - 1) << 5) | lane);
+        __syncwarp();
+        for (unsigned k = lane; k < total; k += 32) {
+            const unsigned e = s_list[warp][k];
+            const int src = e & 31, sidx = e >> 5;
+            const float *fw = &s_fac[warp][0][0];
+            Factor fx;
+            fx.L00 = fx.L10 = fx.L11 = fx.L20 = fx.L21 = fx.L22 = 0.f;
+            fx.LT[0][0] = fw[0 * 32 + src];
+            fx.LT[0][1] = fw[1 * 32 + src];
+            fx.LT[0][2] = fw[2 * 32 + src];
+            fx.LT[1][0] = 0.f;
+            fx.LT[1][1] = fw[3 * 32 + src];
+            fx.LT[1][2] = fw[4 * 32 + src];
+            fx.LT[2][0] = 0.f;
+            fx.LT[2][1] = 0.f;
+            fx.LT[2][2] = fw[5 * 32 + src];
+            const float mx[3] = {fw[6 * 32 + src], fw[7 * 32 + src], fw[8 * 32 + src]};
+            Window w;
+            if (cull_window_xy(mx, fx, sl[sidx], w)) {
+                atomicOr(&s_acc[sidx][warp], 1u << src);
+                // the emit pass reads the window back instead of recomputing
+                win_sparse[(size_t)sidx * n + gwarp * 32 + src] =
+                    make_uint2(w.iu0 | (w.iu1 << 16), w.iv0 | (w.iv1 << 16));
+                // integer sums: shared atomics give exact (order-free) totals
+                const unsigned nt = (unsigned)window_tiles(w);
+                atomicAdd(&s_tiles[sidx], nt);
+                atomicAdd(&s_wt[sidx][warp], nt);
+                atomicAdd(&s_pairs[sidx],
+                          (unsigned)((w.iu1 - w.iu0 + 1) * (w.iv1 - w.iv0 + 1)));
+            }
+        }
+        __syncwarp();
+    }
+    for (int s = lane; s < S; s += 32) {
+        const unsigned bal = s_acc[s][warp];
+        amask[(size_t)s * nwarp_all + gwarp] = bal;
+        s_bal[s][warp] = (unsigned)__popc(bal);
     }
     __syncthreads();
     // per warp: (accepted, tiles) of the block's EARLIER warps, so the emit
