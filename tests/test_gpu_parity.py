@@ -350,3 +350,30 @@ def test_degenerate_clouds_vs_oracle(kind):
         assert np.isfinite(got).all(), k
         np.testing.assert_allclose(got, ref[k], rtol=RTOL,
                                    atol=ATOL * np.abs(ref[k]).max(), err_msg=k)
+
+
+@pytest.mark.parametrize("kind", ["shells", "blobs"])
+def test_gpu_sampler_matches_reference(kind):
+    """sample_slices (GPU trilinear ground truth) vs the reference's
+    sample_slice (ref volume.py:223-263) on its own fixtures."""
+    z = load_golden("io.npz")
+    v = ug.make_phantom(kind, 24, 0.6, seed=1)
+    specs = [ug.SliceSpec(20, 17, 0.45, ug.ProbePose(z[f"{kind}/slice{i}/R"],
+                                                     z[f"{kind}/slice{i}/t"]))
+             for i in range(3)]
+    got = ug.sample_slices(v, specs).cpu().numpy()
+    for i in range(3):
+        np.testing.assert_allclose(got[i], z[f"{kind}/slice{i}/pixels"], rtol=1e-5, atol=1e-6)
+
+
+def test_render_slices_matches_render_slice():
+    """The batched render-only path (C5, the /slice consumer) equals the
+    single-slice API on every slice."""
+    cloud_np = cases.uniform_cloud(4, 20000, [[-20] * 3, [20] * 3], 0.85, 1.05)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    specs = [spec_of(*cases.random_pose(np.random.default_rng(40 + i), 5.0), 64, 64, 0.5)
+             for i in range(5)]
+    batch = ug.render_slices(cloud, specs).cpu().numpy()
+    for i, sp in enumerate(specs):
+        one = ug.render_slice(cloud, sp).pixels
+        np.testing.assert_allclose(batch[i], one, rtol=0, atol=0)
