@@ -296,10 +296,16 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                      const int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
                      uint32_t *__restrict__ keys) {
+    // the slices' record bases in shared memory: the per-thread slice search
+    // runs on it instead of on dependent global loads
+    __shared__ int64_t s_rb[64];
+    for (int q = threadIdx.x; q < S; q += blockDim.x) s_rb[q] = slice_base[2 * q];
+    __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m_total) return;
     int s = 0;
-    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    for (int step = 32; step > 0; step >>= 1)   // last slice whose base <= r
+        if (s + step < S && s_rb[s + step] <= r) s += step;
     const ugs_slice &L = slices[s];
     const int64_t g = rec_gid[r];
     const Factor f = make_factor(l_raw, g, beta);

@@ -598,10 +598,16 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
                         const ugs_slice *__restrict__ slices,
                         const float *__restrict__ means, const float *__restrict__ l_raw,
                         float beta, float *__restrict__ rgrad) {
+    // the slices' record bases in shared memory: the per-thread slice search
+    // runs on it instead of on dependent global loads
+    __shared__ int64_t s_rb[64];
+    for (int q = threadIdx.x; q < S; q += blockDim.x) s_rb[q] = slice_base[2 * q];
+    __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m_total) return;
     int s = 0;
-    while (s + 1 < S && slice_base[2 * (s + 1)] <= r) ++s;
+    for (int step = 32; step > 0; step >>= 1)   // last slice whose base <= r
+        if (s + step < S && s_rb[s + step] <= r) s += step;
     float o[11];
     record_grad(r, slices[s], rec, rec_gid, rec_inst, partial, means, l_raw, beta, o);
     float4 *dst = reinterpret_cast<float4 *>(rgrad + (size_t)r * kG);
