@@ -5,7 +5,7 @@
 // both moments (3 x 48 B) and writes params, moments (and optionally zeroes
 // the gradient): ~380 B/Gaussian.  The single-GPU training step does not use
 // this kernel -- there the update is fused into the gradient accumulation
-// (ugs_raster.cu, accumulate_adam_kernel) and the dense gradient never exists.
+// (ugs_raster.cu, update_gather_kernel) and the dense gradient never exists.
 #include "ugs_adam.cuh"
 #include "ugs_geometry.cuh"
 

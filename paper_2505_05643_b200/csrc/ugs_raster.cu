@@ -1,39 +1,40 @@
 // Tile-resident forward accumulation and backward for a batch of slices.
 //
-// One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted Gaussian list
-// (ascending Gaussian index, from the stable radix sort) is staged through
-// shared memory in batches of 256 records.  While staging, one thread per
-// record clips the record's pixel window to the tile and precomputes what a
-// pixel needs (rectangle, centre offsets); the batch is then ordered by the
-// record's pixel count with a stable counting sort, so the records a warp
-// processes together need the same number of sweeps.
+// One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted instance list
+// (ascending Gaussian index, from the stable bin sort) is staged through
+// shared memory in batches of 256.  While staging, one thread per instance
+// clips the record's window to the tile and precomputes what the lanes need
+// (rectangle, offsets from the instance's expansion pixel, lane layout); the
+// batch is then ordered by loop trip count with a stable counting sort, so
+// the records processed together by a warp need the same number of sweeps.
 //
 // Per pair the reference evaluates w = alpha exp(-q/2), q = |L^T(p - mu)|^2
 // (28 flops, float64).  Phase 1 has conditioned each Gaussian on the slice
-// plane (ugs_geometry.cuh, PlaneForm): log2 w is a 2-D quadratic in the exact
-// integer pixel offset (x, y) from a reference pixel next to the in-plane
-// centre, so with x fixed per lane a pair costs 2 FMA + one MUFU ex2.
+// plane (ugs_geometry.cuh, PlaneForm) and re-expanded it exactly around each
+// instance's expansion pixel: log2 w is a 2-D quadratic in exact integer
+// offsets bounded by the tile, so with x fixed per lane a pair costs 2 FMA +
+// one MUFU ex2.
 //
-// Work split ("record per 8-lane group"): each warp holds 4 groups of 8 lanes;
-// a group sweeps one record's clipped rectangle 8 pixels at a time (k -> (x,y)
-// from a shared 16x256 lookup table).
-//   Forward: each group adds into its own PRIVATE (num, den) tile buffer in
-//   shared memory; the 32 buffers are summed in fixed order at the end -- the
-//   reference's multi-worker scheme (private accumulators summed,
-//   rasterizer.py:157-173), deterministic because the record -> group
-//   assignment is a stable sort.  `forward_ordered_kernel` keeps the strict
-//   sequential ascending-index order per pixel (ref _kernels.py:23-47),
+//   Forward: two records per warp (16-lane groups, cw = pow2 >= width
+//   columns x 16/cw rows per sweep); each group adds into its own PRIVATE
+//   (num, den) tile buffer (XOR-swizzled float2) and the 16 buffers are
+//   summed in fixed order -- the reference's multi-worker scheme (private
+//   accumulators summed, rasterizer.py:157-173), deterministic because the
+//   record -> group assignment is a stable sort.  `forward_ordered_kernel`
+//   keeps the strict ascending-index order per pixel (ref _kernels.py:23-47),
 //   selectable with ugs_plan_set_ordered.
-//   Backward: the per-Gaussian gradient needs only 7 weighted moments of the
-//   window (sum G w, sum t, sum t dx, sum t dy, sum t dx^2, sum t dx dy,
-//   sum t dy^2; G = dpix/ssum, t = dw w), accumulated in registers; one
-//   3-level transpose-reduce inside the group (7 shuffles for 8 values, shared
-//   by the warp's 4 records) leaves lane j of the group with moment j, and the
-//   group writes one 32-byte partial per tile instance.
-// A finalize pass sums a record's instance partials in order and applies the
-// closed-form chain to d_mu, d_L and the raw parameters (float64); slices are
-// then accumulated into the gradient in slice order by Gaussian-range blocks
-// -- no atomics anywhere, so gradients are bitwise reproducible.
+//   Backward: four records per warp (8-lane groups), two pixel streams per
+//   lane with fixed columns (stage_record<8>).  The per-Gaussian gradient
+//   needs only 7 weighted moments of the pixel offsets (sum G w, sum t,
+//   sum t dx, sum t dy, sum t dx^2, sum t dx dy, sum t dy^2; G = dpix/ssum,
+//   t = dw w), accumulated in registers; an 8-lane transpose-reduce leaves
+//   lane j with moment j and the group writes one 32-byte partial per tile
+//   instance.
+// finalize_records sums a record's instance partials in order (shifting each
+// to the record's reference pixel) and applies the closed-form float64 chain
+// to d_mu, d_L and the raw parameters; update_gather accumulates every
+// Gaussian's records in slice order and runs densify statistics + Adam -- no
+// atomics anywhere, so gradients are bitwise reproducible.
 #include "ugs_adam.cuh"
 #include "ugs_geometry.cuh"
 
