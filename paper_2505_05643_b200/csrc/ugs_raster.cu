@@ -619,18 +619,19 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
 
 constexpr int kUpdThreads = 256;
 constexpr int kUpdWarps = kUpdThreads / 32;
-constexpr int kUpdRows = 512;   // staged record-gradient rows per pass
+constexpr int kUpdRows = 64;    // staged record-gradient rows per warp and pass
 
-// One block per 256 Gaussians (the count pass's warp -> Gaussian mapping).
-// For every slice of the batch the accept ballots say which of the block's
-// Gaussians have a record; those records are consecutive, starting at the
-// first record of the block's first non-empty warp (warp_rec).  The block
-// stages all of its record-gradient rows (finalize_records) into shared
-// memory with fully parallel, coalesced loads -- one round trip instead of
-// one per slice per warp -- then each thread adds its Gaussian's rows in
-// SLICE ORDER, acc = fma(scale, row, acc): deterministic, no atomics.  Then
-// (adam != 0, single GPU) densify statistics and Adam run for EVERY Gaussian
-// -- zero-gradient rows still move (trainer.py:182-199) -- and the dense
+// Every WARP works alone on its 32 Gaussians (the count pass's warp ->
+// Gaussian mapping), synchronising only with __syncwarp, so one warp's
+// memory round trips overlap the others' instead of meeting at block
+// barriers.  For every slice of the batch the accept ballot says which of
+// the warp's Gaussians have a record; those records are consecutive from
+// warp_rec.  The warp stages its record-gradient rows (finalize_records) in
+// shared memory with parallel loads -- one round trip per pass of up to 64
+// rows -- then each lane adds its Gaussian's rows in SLICE ORDER,
+// acc = fma(scale, row, acc): deterministic, no atomics.  Then (adam != 0,
+// single GPU) densify statistics and Adam run for EVERY Gaussian --
+// zero-gradient rows still move (trainer.py:182-199) -- and the dense
 // gradient never touches HBM; or (adam == 0) the rows are added into the
 // dense AoS-12 buffer.
 __global__ void __launch_bounds__(kUpdThreads)
@@ -640,13 +641,16 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
                      uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
                      int32_t *__restrict__ grad_cnt) {
-    __shared__ float4 rows[kUpdRows][3];
-    __shared__ uint32_t s_word[64][kUpdWarps];
-    __shared__ int s_wpre[64][kUpdWarps];   // records of earlier warps (block, slice)
-    __shared__ int s_cnt[64], s_base[64], s_off[65];
+    __shared__ float4 rows_all[kUpdWarps][kUpdRows][3];
+    __shared__ uint32_t word_all[kUpdWarps][64];
+    __shared__ int off_all[kUpdWarps][65], base_all[kUpdWarps][64];
     const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t gw0 = (int64_t)blockIdx.x * kUpdWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + warp;
+    if (gw >= nwarp_all) return;   // whole warp
+    float4(*rows)[3] = rows_all[warp];
+    uint32_t *s_word = word_all[warp];
+    int *s_off = off_all[warp], *s_base = base_all[warp];
     const uint32_t lt = (1u << lane) - 1u;
     if (adam && g < n) {
         // the update's streams (moments, parameters) start towards L2 while
@@ -656,24 +660,13 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.l_raw + 6 * g));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.means + 3 * g));
     }
-    for (int i = threadIdx.x; i < S * kUpdWarps; i += kUpdThreads) {
-        const int sl = i / kUpdWarps, w = i % kUpdWarps;
-        s_word[sl][w] = (gw0 + w < nwarp_all) ? __ldg(amask + (size_t)sl * nwarp_all + gw0 + w)
-                                              : 0u;
+    // slice words and record bases: lane s handles slice s (S <= 64)
+    for (int sl = lane; sl < S; sl += 32) {
+        const uint32_t w = __ldg(amask + (size_t)sl * nwarp_all + gw);
+        s_word[sl] = w;
+        s_base[sl] = w ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw) : 0;
     }
-    __syncthreads();
-    for (int sl = threadIdx.x; sl < S; sl += kUpdThreads) {
-        int c = 0, first = -1;
-        for (int w = 0; w < kUpdWarps; ++w) {
-            s_wpre[sl][w] = c;
-            const int pc = __popc(s_word[sl][w]);
-            if (pc && first < 0) first = w;
-            c += pc;
-        }
-        s_cnt[sl] = c;
-        s_base[sl] = first >= 0 ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw0 + first) : 0;
-    }
-    __syncthreads();
+    __syncwarp();
     float acc[11];
 #pragma unroll
     for (int j = 0; j < 11; ++j) acc[j] = 0.f;
@@ -681,17 +674,15 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
     int s0 = 0;
     while (s0 < S) {
         // next group of slices whose rows fit the stage (a slice alone always
-        // fits: <= 256 rows)
+        // fits: <= 32 rows)
         int s1 = s0, tot = 0;
-        while (s1 < S && tot + s_cnt[s1] <= kUpdRows) tot += s_cnt[s1++];
-        __syncthreads();   // previous group done with rows / s_off
-        if (threadIdx.x == 0) {
-            int o = 0;
-            for (int sl = s0; sl < s1; ++sl) { s_off[sl - s0] = o; o += s_cnt[sl]; }
-            s_off[s1 - s0] = o;
+        while (s1 < S && tot + __popc(s_word[s1]) <= kUpdRows) {
+            s_off[s1 - s0] = tot;
+            tot += __popc(s_word[s1++]);
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < tot; i += kUpdThreads) {
+        s_off[s1 - s0] = tot;   // every lane writes the same values
+        __syncwarp();
+        for (int i = lane; i < tot; i += 32) {
             int sg = 0;
             while (s_off[sg + 1] <= i) ++sg;
             const int64_t r = (int64_t)s_base[s0 + sg] + (i - s_off[sg]);
@@ -700,11 +691,11 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
             rows[i][1] = __ldg(src + 1);
             rows[i][2] = __ldg(src + 2);
         }
-        __syncthreads();
+        __syncwarp();
         for (int sl = s0; sl < s1; ++sl) {
-            const uint32_t word = s_word[sl][warp];
+            const uint32_t word = s_word[sl];
             if (!((word >> lane) & 1u)) continue;
-            const int slot = s_off[sl - s0] + s_wpre[sl][warp] + __popc(word & lt);
+            const int slot = s_off[sl - s0] + __popc(word & lt);
             const float4 t0 = rows[slot][0], t1 = rows[slot][1], t2 = rows[slot][2];
             const float o[11] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w,
                                  t2.x, t2.y, t2.z};
@@ -712,6 +703,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
             for (int j = 0; j < 11; ++j) acc[j] = fmaf(scale, o[j], acc[j]);
             hit = true;
         }
+        __syncwarp();   // rows / s_off reused by the next group
         s0 = s1;
     }
     if (g >= n) return;
