@@ -82,6 +82,9 @@ peer_update_kernel(PeerViews pv, int world, int rank, int64_t n, int64_t lo, int
         d.intensity_raw[g] = row[9];
         d.opacity_raw[g] = row[10];
     }
+    // the remote (NVLink) stores are performed system-wide before the thread
+    // retires, so the barrier that follows the kernel publishes them
+    __threadfence_system();
 }
 
 // Before densify: the rows of m, v, grad_sum, grad_cnt this rank does not
