@@ -409,8 +409,9 @@ def run_ours(a):
     except OSError:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    stage_ms = {k: v[0] / max(v[1], 1) for k, v in stage.items()}
-    stage_ms.update({k: v[0] / max(v[1], 1) for k, v in extra.items()})
+    # per step (a stage may launch more than once per step)
+    stage_ms = {k: v[0] / a.steps for k, v in stage.items()}
+    stage_ms.update({k: v[0] / a.steps for k, v in extra.items()})
     dom = max(("forward", "backward"), key=lambda k: stage_ms.get(k, 0.0))
     flop_pp = FLOP_BWD_PER_PAIR if dom == "backward" else FLOP_FWD_PER_PAIR
     achieved = flop_pp * pairs_per_step / (stage_ms[dom] * 1e-3) / 1e12
