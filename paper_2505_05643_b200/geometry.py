@@ -140,6 +140,51 @@ def chi2_cutoff(p: float) -> float:
     return _CHI2_CACHE[p]
 
 
+# struct ugs_slice (include/ugs.h) as a numpy record: 27 float32, 6 int32,
+# padding, int64 pix_base = 144 bytes
+SLICE_DTYPE = np.dtype([("f", "<f4", (27,)), ("i", "<i4", (6,)), ("pad", "<i4"),
+                        ("pix_base", "<i8")])
+
+
+def fill_slices(dst, specs, p: float) -> None:
+    """Fill a ctypes array of ugs_slice structs for a batch (pix_base = the
+    running pixel offset) -- the same float32 constants as fill_slice
+    (byte-identical), vectorised over the batch and copied in one memmove
+    (the serving path renders many small batches)."""
+    import ctypes
+    f32 = np.float32
+    S = len(specs)
+    R = np.stack([sp.pose.rotation for sp in specs])            # (S,3,3) f64
+    t = np.stack([sp.pose.translation for sp in specs])         # (S,3)
+    sp_ = np.array([sp.spacing for sp in specs], np.float64)
+    W = np.array([sp.width for sp in specs], np.int64)
+    H = np.array([sp.height for sp in specs], np.int64)
+    Rinv = np.transpose(R, (0, 2, 1))                           # ProbePose.inverse
+    tw = np.stack([-Rinv[j] @ t[j] for j in range(S)])          # as the reference
+    du = R[:, :, 0] * sp_[:, None]                              # plane_axes
+    dv = R[:, :, 1] * sp_[:, None]
+    cxw = (W - 1) / 2.0
+    cyh = (H - 1) / 2.0
+    origin = t - cxw[:, None] * du - cyh[:, None] * dv
+    rec = np.zeros(S, SLICE_DTYPE)
+    f = rec["f"]
+    f[:, 0:9] = Rinv.astype(f32).reshape(S, 9)
+    f[:, 9:12] = tw.astype(f32)
+    f[:, 12:15] = origin.astype(f32)
+    f[:, 15:18] = du.astype(f32)
+    f[:, 18:21] = dv.astype(f32)
+    f[:, 21] = np.sqrt(f32(chi2_cutoff(p)))
+    f[:, 22] = sp_.astype(f32)
+    f[:, 23] = cxw.astype(f32)
+    f[:, 24] = cyh.astype(f32)
+    f[:, 25] = (cxw * sp_).astype(f32)
+    f[:, 26] = (cyh * sp_).astype(f32)
+    rec["i"][:, 0] = W
+    rec["i"][:, 1] = H
+    rec["pix_base"] = np.concatenate([[0], np.cumsum(W * H)[:-1]])
+    ctypes.memmove(dst, rec.ctypes.data, rec.nbytes)
+
+
 def fill_slice(dst, spec: SliceSpec, p: float, pix_base: int = 0) -> None:
     """Fill one ugs_slice struct with the reference's float32 constants."""
     f32 = np.float32

@@ -24,7 +24,7 @@ import torch
 
 from . import _lib
 from .geometry import (InvalidParameterError, SliceImage, SliceSpec,
-                       chi2_cutoff, fill_slice)
+                       chi2_cutoff, fill_slice, fill_slices)
 from .model import GaussianCloud, ProbeFrameGaussian
 
 DEFAULT_P_MASS = 0.95
@@ -71,10 +71,7 @@ class Renderer:
             raise InvalidParameterError("a batch holds 1..64 slices")
         if slices is None:
             slices = (_lib.Slice * S)()
-            pix = 0
-            for s, spec in enumerate(specs):
-                fill_slice(slices[s], spec, p, pix)
-                pix += spec.width * spec.height
+            fill_slices(slices, specs, p)
         m = (ctypes.c_int64 * S)()
         k = (ctypes.c_int64 * S)()
         pp = (ctypes.c_int64 * S)()

@@ -68,3 +68,20 @@ def test_slice_constants_match_oracle():
             assert np.array_equal(np.array(getattr(st, k), np.float32), sc[k])
         for k in ("sqrt_cut", "s", "cx", "cy", "x1h", "x2h"):
             assert np.float32(getattr(st, k)) == sc[k], k
+
+
+def test_batched_slice_constants_identical():
+    """fill_slices (vectorised, the serving path) writes byte-identical
+    structs to per-slice fill_slice (the reference's float32 constants)."""
+    from paper_2505_05643_b200 import _lib
+    from paper_2505_05643_b200.dataset import random_pose_specs
+    from paper_2505_05643_b200.geometry import fill_slice, fill_slices
+    for seed in range(3):
+        specs = random_pose_specs(20, 96 + seed, 80, 0.4 + 0.05 * seed, seed=seed)
+        a, b = (_lib.Slice * 20)(), (_lib.Slice * 20)()
+        pix = 0
+        for j, sp in enumerate(specs):
+            fill_slice(a[j], sp, 0.95, pix)
+            pix += sp.width * sp.height
+        fill_slices(b, specs, 0.95)
+        assert bytes(a) == bytes(b)
