@@ -132,7 +132,7 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.win_sparse, b.slice_tot,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.warp_inst, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.bg_sums,
@@ -214,6 +214,10 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     if ((rc = ensure(&b.wcnt, &b.wcnt_cap,
                      (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc wcnt")))
+        return rc;
+    if ((rc = ensure(&b.warp_inst, &b.warp_inst_cap,
+                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
+                     "alloc warp_inst")))
         return rc;
     if ((rc = ensure(&b.warp_rec, &b.warp_rec_cap,
                      (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
@@ -312,7 +316,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
                                       m_total, k_total, b.win_sparse, b.amask,
-                                      b.wcnt, b.warp_rec, st)))
+                                      b.wcnt, b.warp_rec, b.warp_inst, st)))
             return rc;
     } else {
         UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));

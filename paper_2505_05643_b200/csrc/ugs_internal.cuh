@@ -57,6 +57,8 @@ struct PlanBuffers {
     size_t amask_cap = 0;
     uint2 *wcnt = nullptr;          // [S][nblk*8] (accepted, tiles) per warp of Gaussians
     size_t wcnt_cap = 0;
+    int32_t *warp_inst = nullptr;   // [S][nblk*8] first instance of each warp
+    size_t warp_inst_cap = 0;
     int32_t *warp_rec = nullptr;    // [S][nblk*8] record index of each warp's first
     size_t warp_rec_cap = 0;        //   accepted Gaussian (emit pass)
     uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
@@ -177,7 +179,8 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        const uint2 *wcnt, int32_t *warp_rec, cudaStream_t st);
+                        const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
+                        cudaStream_t st);
 
 // radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
 // bits, stable.  On return *keys_out/*vals_out point at the sorted arrays

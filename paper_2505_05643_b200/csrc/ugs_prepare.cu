@@ -2,13 +2,15 @@
 // compact + clamped windows (ref rasterizer.py:109-137), fused with the
 // per-(slice, Gaussian) record build and the tile-instance expansion.
 //
-// Three passes over the parameter SoA (44 B/Gaussian, L2-resident after the
-// first pass for N <= ~2M):
-//   count : one thread per Gaussian, loops over the S slices of the batch,
-//           block-reduces (accepted, tiles) per slice      -> blk_cnt[S][nblk]
-//   scan  : exclusive scan of blk_cnt along blocks, per slice (keeps ascending
-//           Gaussian order = the reference's compact() order)
-//   emit  : recompute, block-scan, write records + instances in order.
+//   count        : one thread per Gaussian, loops over the S slices of the
+//                  batch: accept ballots, windows, per-warp and per-block
+//                  (accepted, tiles) counts
+//   scan, plan   : exclusive scan of the block counts per slice (ascending
+//                  Gaussian order = the reference's compact() order), slice
+//                  bases and bin-sort tables on the device
+//   warp_offsets : first record / instance of every (slice, warp)
+//   build        : one thread per record: finds its Gaussian from the record
+//                  index, float64 plane conditioning, tile instances
 #include "ugs_geometry.cuh"
 
 namespace ugs {
@@ -220,82 +222,54 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
     }
 }
 
-__global__ void __launch_bounds__(kPrepThreads)
-prepare_emit_kernel(const float *__restrict__ means,
-                    const float *__restrict__ l_raw,
-                    const float *__restrict__ intensity_raw,
-                    const float *__restrict__ opacity_raw, int64_t n,
-                    float beta, const ugs_slice *__restrict__ slices, int S,
-                    const uint2 *__restrict__ blk_off, int nblk,
-                    const int64_t *__restrict__ slice_base,
-                    Rec *__restrict__ rec, int32_t *__restrict__ rec_gid,
-                    int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
-                    uint32_t *__restrict__ keys, int64_t m_total,
-                    int64_t k_total, const uint2 *__restrict__ win_sparse,
-                    const uint32_t *__restrict__ amask, const uint2 *__restrict__ wcnt,
-                    int32_t *__restrict__ warp_rec) {
-    const int64_t g = (int64_t)blockIdx.x * kPrepThreads + threadIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
-    const int64_t gwarp = (int64_t)blockIdx.x * (kPrepThreads / 32) + warp;
-    if (blockIdx.x == 0 && threadIdx.x == 0) rec_inst[m_total] = (int32_t)k_total;
-    const uint32_t lt = (1u << lane) - 1u;
-    // per-slice cursors (pointer increments, no 64-bit index products)
-    const uint32_t *am = amask + gwarp;
-    const uint2 *wc = wcnt + gwarp;
-    const uint2 *bo_p = blk_off + blockIdx.x;
-    const uint2 *ws = win_sparse + g;
-    int32_t *wr = warp_rec + gwarp;
-    for (int s = 0; s < S; ++s, am += nwarp_all, wc += nwarp_all, bo_p += nblk, ws += n,
-             wr += nwarp_all) {
-        // the count pass left the accept bits, the per-warp offsets and the
-        // windows of accepted (slice, Gaussian) pairs: no phase-1 recompute
-        // and no block-wide scan (no barriers)
-        const uint32_t word = __ldg(am);
-        if (word == 0) continue;   // warp-uniform
-        const unsigned acc = (word >> lane) & 1u;
-        unsigned tiles = 0;
-        uint2 pw = make_uint2(0u, 0u);
-        if (acc) {
-            pw = __ldg(ws);
-            tiles = (unsigned)((((pw.x >> 16) >> 4) - ((pw.x & 0xffff) >> 4) + 1) *
-                               (((pw.y >> 16) >> 4) - ((pw.y & 0xffff) >> 4) + 1));
-        }
-        unsigned xt = tiles;   // inclusive warp scan of the tile counts
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned tt = __shfl_up_sync(0xffffffffu, xt, o);
-            if (lane >= o) xt += tt;
-        }
-        // this warp's offset inside the slice: the block's offset plus the
-        // counts of the block's earlier warps
-        const uint2 bo = __ldg(bo_p), c = __ldg(wc);
-        const int64_t r0 = slice_base[2 * s] + bo.x + c.x;
-        // record of this warp's first accepted Gaussian: the update pass maps
-        // (slice, Gaussian) -> record with one popcount
-        if (lane == 0) *wr = (int32_t)r0;
-        if (!acc) continue;
-        const int64_t r = r0 + __popc(word & lt);
-        const int64_t inst = slice_base[2 * s + 1] + bo.y + c.y + xt - tiles;
-        // colour, alpha, the float64 plane conditioning and the tile
-        // expansion run in build_records_kernel (one thread per record)
-        *reinterpret_cast<uint2 *>(&rec[r].r1) = pw;
-        rec_gid[r] = (int32_t)g;
-        rec_inst[r] = (int32_t)inst;
-    }
+// Per (slice, warp of 32 Gaussians): the warp's first record and first
+// instance, from the block offsets (scan) and the within-block warp offsets
+// (count pass).  Empty warps get the offset of the next record, so each
+// slice's row is non-decreasing -- build_records searches it.
+__global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
+                                    const uint2 *__restrict__ blk_off,
+                                    const uint2 *__restrict__ wcnt,
+                                    const int64_t *__restrict__ slice_base,
+                                    int32_t *__restrict__ warp_rec,
+                                    int32_t *__restrict__ warp_inst,
+                                    int32_t *__restrict__ rec_inst, int64_t m_total,
+                                    int64_t k_total) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx == 0) rec_inst[m_total] = (int32_t)k_total;
+    if (idx >= (int64_t)S * nwarp_all) return;
+    const int s = (int)(idx / nwarp_all);
+    const int64_t gw = idx - (int64_t)s * nwarp_all;
+    const uint2 bo = __ldg(blk_off + (size_t)s * nblk + gw / (kPrepThreads / 32));
+    const uint2 c = __ldg(wcnt + idx);
+    warp_rec[idx] = (int32_t)(slice_base[2 * s] + bo.x + c.x);
+    warp_inst[idx] = (int32_t)(slice_base[2 * s + 1] + bo.y + c.y);
 }
 
-// One thread per accepted (slice, Gaussian) record: plane-conditioned
-// exponent (float64, ugs_geometry.cuh PlaneForm) and the record's tile
-// instances in row-major tile order, each with its exact re-expansion.
+__device__ __forceinline__ unsigned packed_tiles(uint2 w) {
+    return (((w.x >> 16) >> 4) - ((w.x & 0xffff) >> 4) + 1) *
+           (((w.y >> 16) >> 4) - ((w.y & 0xffff) >> 4) + 1);
+}
+
+// One thread per accepted (slice, Gaussian) record.  It finds its Gaussian
+// from the record index alone -- slice by the slice bases, warp by a binary
+// search of the slice's warp_rec row, lane as the k-th set bit of the warp's
+// accept ballot -- and its first instance as the warp's plus the tile counts
+// of the warp's earlier accepted lanes (no separate emit pass).  Then the
+// plane-conditioned exponent (float64, ugs_geometry.cuh PlaneForm) and the
+// record's tile instances in row-major tile order, each with its exact
+// re-expansion.
 __global__ void __launch_bounds__(128)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
                      const float *__restrict__ intensity_raw,
-                     const float *__restrict__ opacity_raw, float beta, const ugs_slice *__restrict__ slices, int S,
+                     const float *__restrict__ opacity_raw, int64_t n, float beta,
+                     const ugs_slice *__restrict__ slices, int S,
                      const int64_t *__restrict__ slice_base, int64_t m_total,
-                     Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
-                     const int32_t *__restrict__ rec_inst, Inst *__restrict__ idata,
-                     uint32_t *__restrict__ keys) {
+                     int64_t nwarp_all, const uint32_t *__restrict__ amask,
+                     const int32_t *__restrict__ warp_rec,
+                     const int32_t *__restrict__ warp_inst,
+                     const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
+                     int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
+                     Inst *__restrict__ idata, uint32_t *__restrict__ keys) {
     // the slices' record bases in shared memory: the per-thread slice search
     // runs on it instead of on dependent global loads
     __shared__ int64_t s_rb[64];
@@ -306,25 +280,40 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     int s = 0;
     for (int step = 32; step > 0; step >>= 1)   // last slice whose base <= r
         if (s + step < S && s_rb[s + step] <= r) s += step;
+    const int32_t *wr = warp_rec + (size_t)s * nwarp_all;
+    int64_t lo = 0, hi = nwarp_all - 1;          // last warp whose first record <= r
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(wr + mid) <= r) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + lo);
+    const int k = (int)(r - __ldg(wr + lo));
+    const int lane = (int)__fns(word, 0, k + 1);
+    const int64_t g = lo * 32 + lane;
+    const uint2 *ws = win_sparse + (size_t)s * n + lo * 32;
+    int64_t inst = __ldg(warp_inst + (size_t)s * nwarp_all + lo);
+    for (uint32_t mk = word & ((1u << lane) - 1u); mk; mk &= mk - 1)
+        inst += packed_tiles(__ldg(ws + (__ffs(mk) - 1)));
+    const uint2 pw = __ldg(ws + lane);
+    rec_gid[r] = (int32_t)g;
+    rec_inst[r] = (int32_t)inst;
     const ugs_slice &L = slices[s];
-    const int64_t g = rec_gid[r];
     const Factor f = make_factor(l_raw, g, beta);
     const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
                          __ldg(means + 3 * g + 2)};
-    const float2 r1 = *reinterpret_cast<const float2 *>(&rec[r].r1);   // window (emit)
     const float color = sigmoid_f32(__ldg(intensity_raw + g));
     const float alpha = sigmoid_f32(__ldg(opacity_raw + g));
-    const int wu = __float_as_int(r1.x), wv = __float_as_int(r1.y);
-    const Window w{wu & 0xffff, wu >> 16, wv & 0xffff, wv >> 16};
+    const Window w{(int)(pw.x & 0xffff), (int)(pw.x >> 16), (int)(pw.y & 0xffff),
+                   (int)(pw.y >> 16)};
     const PlaneForm P = plane_form(mu, f, L, w);
     const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
     const double log2a = log2((double)alpha);
     rec[r].r0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
                             (float)(kq * P.H11), color);
-    rec[r].r1 = make_float4(r1.x, r1.y, alpha, __int_as_float(P.ui | (P.vi << 16)));
+    rec[r].r1 = make_float4(__uint_as_float(pw.x), __uint_as_float(pw.y), alpha,
+                            __int_as_float(P.ui | (P.vi << 16)));
     const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
     const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
-    int64_t inst = rec_inst[r];
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             const TileRect t = tile_rect(w.iu0, w.iu1, w.iv0, w.iv1, tx * kTile,
@@ -405,16 +394,18 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
-                        const uint2 *wcnt, int32_t *warp_rec, cudaStream_t st) {
-    prepare_emit_kernel<<<nblk, kPrepThreads, 0, st>>>(
-        c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices,
-        S, blk_off, nblk, slice_base, rec, rec_gid, rec_inst, idata, keys,
-        m_total, k_total, win_sparse, amask, wcnt, warp_rec);
-    UGS_LAUNCH_CHECK("prepare_emit_kernel");
+                        const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
+                        cudaStream_t st) {
+    const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
+    const int64_t nw = (int64_t)S * nwarp_all;
+    warp_offsets_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(
+        S, nwarp_all, nblk, blk_off, wcnt, slice_base, warp_rec, warp_inst, rec_inst,
+        m_total, k_total);
+    UGS_LAUNCH_CHECK("warp_offsets_kernel");
     build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
-        c.means, c.l_raw, c.intensity_raw, c.opacity_raw, (float)c.beta, slices, S,
-        slice_base, m_total, rec, rec_gid,
-        rec_inst, idata, keys);
+        c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices, S,
+        slice_base, m_total, nwarp_all, amask, warp_rec, warp_inst, win_sparse, rec,
+        rec_gid, rec_inst, idata, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;
 }
