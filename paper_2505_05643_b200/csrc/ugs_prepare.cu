@@ -281,10 +281,11 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     for (int step = 32; step > 0; step >>= 1)   // last slice whose base <= r
         if (s + step < S && s_rb[s + step] <= r) s += step;
     const int32_t *wr = warp_rec + (size_t)s * nwarp_all;
-    int64_t lo = 0, hi = nwarp_all - 1;          // last warp whose first record <= r
+    int lo = 0, hi = (int)nwarp_all - 1;         // last warp whose first record <= r
+    const int32_t r32 = (int32_t)r;
     while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(wr + mid) <= r) lo = mid; else hi = mid - 1;
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(wr + mid) <= r32) lo = mid; else hi = mid - 1;
     }
     const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + lo);
     const int k = (int)(r - __ldg(wr + lo));
