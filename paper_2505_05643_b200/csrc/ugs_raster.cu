@@ -256,17 +256,36 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             // swizzled slot of row Y is 16 Y + (X ^ 8 (Y & 1)): an even R keeps
             // the lane's row parity, R == 1 flips it every sweep (16 +- 8)
             const int sx = (X ^ 8) - X;
-            int step = (R == 1) ? (kTile + ((Y & 1) ? -sx : sx)) : R * kTile;
-            const int flip = (R == 1) ? 2 * kTile : 2 * step;
-            for (int y = ly; y < h; y += R) {
-                const float wgt = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
-                float2 v = *ptr;
-                v.x = fmaf(wgt, c.x, v.x);
-                v.y += wgt;
-                *ptr = v;
-                dy += (float)R;
-                ptr += step;
-                step = flip - step;
+            const int s1 = (R == 1) ? (kTile + ((Y & 1) ? -sx : sx)) : R * kTile;
+            const int s12 = 2 * R * kTile;   // two rows: the lane's parity again
+            // rows ly, ly + R, ... < h, two per iteration (same column: P, Q
+            // shared; both loads before both stores, the rows never alias)
+            const int nrow = (h - ly + R - 1) >> (4 - lcw);
+            float dyB = dy + (float)R;
+            const float R2 = (float)(2 * R);
+            int i = 0;
+#pragma unroll 1
+            for (; i + 1 < nrow; i += 2) {
+                float2 *qB = ptr + s1;
+                const float wa = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
+                const float wb = ex2_approx(fmaf(dyB, fmaf(b.z, dyB, Q), P));
+                float2 va = *ptr, vb = *qB;
+                va.x = fmaf(wa, c.x, va.x);
+                va.y += wa;
+                vb.x = fmaf(wb, c.x, vb.x);
+                vb.y += wb;
+                *ptr = va;
+                *qB = vb;
+                dy += R2;
+                dyB += R2;
+                ptr += s12;
+            }
+            if (i < nrow) {   // odd row count: the last row
+                const float wa = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
+                float2 va = *ptr;
+                va.x = fmaf(wa, c.x, va.x);
+                va.y += wa;
+                *ptr = va;
             }
         }
     }
