@@ -139,6 +139,12 @@ __device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int t
 // Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
 // columns x (16/cw) rows per sweep; sC.y packs base = y0*16 + x0, w-1, h-1
 // and log2 cw.  Returns the number of sweeps.
+// Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
+// columns x R = 16/cw rows per sweep.  The lane layout is precomputed in
+// byte fields so a lane decodes each with one byte permute:
+//   sC.y = cmask | lcw << 8 | (h + R - 1) << 16 | log2(R) << 24
+//   sC.z = x0 | y0 << 8 | w << 16 | R << 24
+// Returns the number of sweeps.
 __device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, int tu0,
                                                  int tv0, uint32_t inst, Batch &B,
                                                  int slot) {
@@ -146,14 +152,21 @@ __device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, 
     const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
     const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
+    const int rows = 16 >> lcw;
     B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
                              8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
     B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
-    B.sC[slot] = make_float4(R.r0.w,
-                             __int_as_float((y0 * kTile + x0) | ((w - 1) << 8) |
-                                            ((h - 1) << 12) | (lcw << 16)),
-                             0.f, __int_as_float((int)inst));
-    return (h + (16 >> lcw) - 1) >> (4 - lcw);
+    B.sC[slot] = make_float4(
+        R.r0.w,
+        __int_as_float(((1 << lcw) - 1) | (lcw << 8) | ((h + rows - 1) << 16) |
+                       ((4 - lcw) << 24)),
+        __int_as_float(x0 | (y0 << 8) | (w << 16) | (rows << 24)),
+        __int_as_float((int)inst));
+    return (h + rows - 1) >> (4 - lcw);
+}
+
+__device__ __forceinline__ int byte_of(int x, int k) {
+    return (int)__byte_perm((unsigned)x, 0u, 0x4440u | (unsigned)k);
 }
 
 // Stable counting sort of the staged slots by trip count (warp match-any
@@ -240,27 +253,24 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             if (slot >= nb) continue;
             const int j = B.order[slot];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
-            const int pk = __float_as_int(c.y);
-            const int x0 = pk & 15, y0 = (pk >> 4) & 15;
-            const int w = ((pk >> 8) & 15) + 1, h = ((pk >> 12) & 15) + 1;
-            const int lcw = (pk >> 16) & 7;
-            const int lx = gl16 & ((1 << lcw) - 1), ly = gl16 >> lcw;
-            const int R = 16 >> lcw;   // rows per sweep
-            if (lx >= w) continue;
+            const int k1 = __float_as_int(c.y), k2 = __float_as_int(c.z);
+            const int lx = gl16 & byte_of(k1, 0), ly = gl16 >> byte_of(k1, 1);
+            if (lx >= byte_of(k2, 2)) continue;
+            const int R = byte_of(k2, 3);   // rows per sweep
             // per lane: x fixed, log2 w = P + y (Q + C y), x and y exact
             const float dx = big_float(lx) - a.x;
             const float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w), Q = fmaf(b.y, dx, a.w);
             float dy = big_float(ly) - a.y;
-            const int Y = y0 + ly, X = x0 + lx;
-            float2 *ptr = my + (Y * kTile + (X ^ ((Y & 1) << 3)));
-            // swizzled slot of row Y is 16 Y + (X ^ 8 (Y & 1)): an even R keeps
-            // the lane's row parity, R == 1 flips it every sweep (16 +- 8)
-            const int sx = (X ^ 8) - X;
-            const int s1 = (R == 1) ? (kTile + ((Y & 1) ? -sx : sx)) : R * kTile;
+            const int Y = byte_of(k2, 1) + ly;
+            const int sX = (byte_of(k2, 0) + lx) ^ ((Y & 1) << 3);   // swizzled column
+            float2 *ptr = my + (Y * kTile + sX);
+            // the next row's slot: 16 R for even R; R == 1 flips the swizzle
+            // every row, so the step is 16 + 8 or 16 - 8 (bit 3 of sX)
+            const int s1 = (R == 1) ? 24 - ((sX & 8) << 1) : R * kTile;
             const int s12 = 2 * R * kTile;   // two rows: the lane's parity again
             // rows ly, ly + R, ... < h, two per iteration (same column: P, Q
             // shared; both loads before both stores, the rows never alias)
-            const int nrow = (h - ly + R - 1) >> (4 - lcw);
+            const int nrow = (byte_of(k1, 2) - ly) >> byte_of(k1, 3);
             float dyB = dy + (float)R;
             const float R2 = (float)(2 * R);
             int i = 0;
