@@ -194,6 +194,15 @@ UGS_API int ugs_loss(const float *num, const float *den, const float *target,
                      double *loss_out, double *ssim_out, void *workspace,
                      void *stream);
 
+/* ugs_loss with the targets gathered from a dataset -- slice s compares
+ * against target + target_index[s] * H * W (target_index: dev int64, NULL =
+ * slice s itself) -- and the batch-mean loss written to loss_mean_out (dev
+ * double, may be NULL).  S <= 64. */
+UGS_API int ugs_loss_ex(const float *num, const float *den, const float *target,
+                        const int64_t *target_index, int S, int H, int W, double lam,
+                        int l2, float *d_pixels, double *loss_out, double *ssim_out,
+                        double *loss_mean_out, void *workspace, void *stream);
+
 /* Forward accumulation order.  0 (default): each of the 8 warps of a tile
  * accumulates its share of the tile's records into a private buffer and the
  * buffers are summed in fixed order -- the reference's multi-worker scheme

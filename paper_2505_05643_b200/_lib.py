@@ -89,6 +89,9 @@ EXPORTS = {
     "ugs_loss": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ctypes.c_double, ctypes.c_int, c_vp,
                                 c_vp, c_vp, c_vp, c_vp]),
+    "ugs_loss_ex": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_double, ctypes.c_int, c_vp,
+                                   c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ugs_plan_timings": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(c_i64), ctypes.c_int,
                                         ctypes.c_int]),

@@ -48,7 +48,8 @@ struct LossSmem {
 
 __global__ void __launch_bounds__(kLossThreads, 1)
 loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
-                 const float *__restrict__ target, int H, int W, double lam,
+                 const float *__restrict__ target, const int64_t *__restrict__ target_index,
+                 int H, int W, double lam,
                  int l2, float *__restrict__ dpix, double *__restrict__ tile_sums,
                  int tiles_x, int tiles_per_slice) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -57,6 +58,8 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
     const int tile = blockIdx.x;
     const int p0 = (tile / tiles_x) * kLT, q0 = (tile % tiles_x) * kLT;
     const size_t base = (size_t)s * H * W;
+    // the targets may be gathered from a dataset: slice s reads target_index[s]
+    const size_t tbase = (target_index ? (size_t)target_index[s] : (size_t)s) * H * W;
     const int tid = threadIdx.x;
     const int HV = H - 2 * kPad, WV = W - 2 * kPad;   // valid grid
     const double npx = (double)H * W, nv = (double)HV * WV;
@@ -76,7 +79,7 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
             const size_t o = base + (size_t)P * W + Q;
             ln[j] = __ldg(num + o);
             ld[j] = __ldg(den + o);
-            lt[j] = __ldg(target + o);
+            lt[j] = __ldg(target + (tbase + (size_t)P * W + Q));
         }
     }
 #pragma unroll
@@ -267,40 +270,52 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
     }
 }
 
+// One block for the whole batch: per slice, the tile sums in fixed order,
+// then loss / SSIM per slice and the batch-mean loss (slice order) --
+// deterministic, one launch.
 __global__ void loss_reduce_kernel(const double *__restrict__ tile_sums,
-                                   int tiles_per_slice, int H, int W, double lam,
+                                   int tiles_per_slice, int S, int H, int W, double lam,
                                    int l2, double *__restrict__ loss_out,
-                                   double *__restrict__ ssim_out) {
-    const int s = blockIdx.x;
-    __shared__ double ra[256], rb[256];
-    double a = 0, b = 0;
-    for (int t = threadIdx.x; t < tiles_per_slice; t += blockDim.x) {
-        a += tile_sums[2 * ((size_t)s * tiles_per_slice + t)];
-        b += tile_sums[2 * ((size_t)s * tiles_per_slice + t) + 1];
-    }
-    ra[threadIdx.x] = a;
-    rb[threadIdx.x] = b;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            ra[threadIdx.x] += ra[threadIdx.x + o];
-            rb[threadIdx.x] += rb[threadIdx.x + o];
+                                   double *__restrict__ ssim_out,
+                                   double *__restrict__ mean_out) {
+    __shared__ double ra[256], rb[256], lv[64];
+    const double npx = (double)H * W;
+    const double nv = (double)(H - 2 * kPad) * (W - 2 * kPad);
+    for (int s = 0; s < S; ++s) {
+        double a = 0, b = 0;
+        for (int t = threadIdx.x; t < tiles_per_slice; t += blockDim.x) {
+            a += tile_sums[2 * ((size_t)s * tiles_per_slice + t)];
+            b += tile_sums[2 * ((size_t)s * tiles_per_slice + t) + 1];
+        }
+        ra[threadIdx.x] = a;
+        rb[threadIdx.x] = b;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+                ra[threadIdx.x] += ra[threadIdx.x + o];
+                rb[threadIdx.x] += rb[threadIdx.x + o];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            double v;
+            const double mean_s = rb[0] / nv;
+            if (l2) {
+                v = ra[0] / npx;
+            } else {
+                v = (1.0 - lam) * (ra[0] / npx);
+                if (lam > 0.0) v += lam * (1.0 - mean_s);
+            }
+            if (loss_out) loss_out[s] = v;
+            if (ssim_out) ssim_out[s] = mean_s;
+            lv[s] = v;
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        const double npx = (double)H * W;
-        const double nv = (double)(H - 2 * kPad) * (W - 2 * kPad);
-        double v;
-        const double mean_s = rb[0] / nv;
-        if (l2) {
-            v = ra[0] / npx;
-        } else {
-            v = (1.0 - lam) * (ra[0] / npx);
-            if (lam > 0.0) v += lam * (1.0 - mean_s);
-        }
-        if (loss_out) loss_out[s] = v;
-        if (ssim_out) ssim_out[s] = mean_s;
+    if (threadIdx.x == 0 && mean_out) {
+        double m = 0.0;
+        for (int s = 0; s < S; ++s) m += lv[s];
+        *mean_out = m / (double)S;
     }
 }
 
@@ -330,12 +345,13 @@ extern "C" size_t ugs_loss_workspace_bytes(int S, int H, int W) {
     return sizeof(double) * 2 * (size_t)S * tx * ty;
 }
 
-extern "C" int ugs_loss(const float *num, const float *den, const float *target,
-                        int S, int H, int W, double lam, int l2, float *d_pixels,
-                        double *loss_out, double *ssim_out, void *workspace,
-                        void *stream) {
-    if (!num || !den || !target || !d_pixels || !workspace || S < 1 || H < 1 || W < 1) {
-        set_error("ugs_loss: invalid arguments");
+extern "C" int ugs_loss_ex(const float *num, const float *den, const float *target,
+                           const int64_t *target_index, int S, int H, int W, double lam,
+                           int l2, float *d_pixels, double *loss_out, double *ssim_out,
+                           double *loss_mean_out, void *workspace, void *stream) {
+    if (!num || !den || !target || !d_pixels || !workspace || S < 1 || S > 64 || H < 1 ||
+        W < 1) {
+        set_error("ugs_loss: invalid arguments (1 <= S <= 64)");
         return UGS_ERR_INVALID;
     }
     if (!l2 && lam > 0.0 && (H < 11 || W < 11)) {
@@ -356,11 +372,19 @@ extern "C" int ugs_loss(const float *num, const float *den, const float *target,
     }
     dim3 grid(tx * ty, S);
     double *sums = static_cast<double *>(workspace);
-    loss_tile_kernel<<<grid, kLossThreads, smem, st>>>(num, den, target, H, W, lam, l2,
-                                                       d_pixels, sums, tx, tx * ty);
+    loss_tile_kernel<<<grid, kLossThreads, smem, st>>>(num, den, target, target_index, H, W,
+                                                       lam, l2, d_pixels, sums, tx, tx * ty);
     UGS_LAUNCH_CHECK("loss_tile_kernel");
-    loss_reduce_kernel<<<S, 256, 0, st>>>(sums, tx * ty, H, W, lam, l2, loss_out,
-                                          ssim_out);
+    loss_reduce_kernel<<<1, 256, 0, st>>>(sums, tx * ty, S, H, W, lam, l2, loss_out,
+                                          ssim_out, loss_mean_out);
     UGS_LAUNCH_CHECK("loss_reduce_kernel");
     return UGS_OK;
+}
+
+extern "C" int ugs_loss(const float *num, const float *den, const float *target,
+                        int S, int H, int W, double lam, int l2, float *d_pixels,
+                        double *loss_out, double *ssim_out, void *workspace,
+                        void *stream) {
+    return ugs_loss_ex(num, den, target, nullptr, S, H, W, lam, l2, d_pixels, loss_out,
+                       ssim_out, nullptr, workspace, stream);
 }

@@ -335,33 +335,50 @@ __global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
                                    const ugs_slice *__restrict__ slices, int S,
                                    int64_t *__restrict__ slice_base,
                                    SortSlice *__restrict__ ss) {
-    if (threadIdx.x != 0) return;
-    unsigned long long m = 0, k = 0, pr = 0, hn = 0, nbs = 0;
-    for (int s = 0; s < S; ++s) {
+    // one thread per slice: its bases are prefix sums over the earlier
+    // slices (S <= 64: a short loop, all slices in parallel)
+    __shared__ unsigned long long sm[64], sk[64], sp[64];
+    __shared__ int snb[64], snt[64];
+    const int s = threadIdx.x;
+    if (s < S) {
+        sm[s] = tot[3 * s];
+        sk[s] = tot[3 * s + 1];
+        sp[s] = tot[3 * s + 2];
+        snt[s] = slices[s].tiles_x * slices[s].tiles_y;
+        snb[s] = (int)((sk[s] + kSortTile - 1) / kSortTile);
+    }
+    __syncthreads();
+    if (s < S) {
+        unsigned long long m = 0, k = 0, hn = 0, nbs = 0;
+        for (int q = 0; q < s; ++q) {
+            m += sm[q];
+            k += sk[q];
+            nbs += (unsigned long long)snb[q];
+            hn += (unsigned long long)snt[q] * snb[q];
+        }
         slice_base[2 * s] = (int64_t)m;
         slice_base[2 * s + 1] = (int64_t)k;
         SortSlice q;
         q.inst_base = (int)k;
-        q.k = (int)tot[3 * s + 1];
+        q.k = (int)sk[s];
         q.tile_base = slices[s].tile_base;
-        q.ntile = slices[s].tiles_x * slices[s].tiles_y;
-        q.nb = (q.k + kSortTile - 1) / kSortTile;
+        q.ntile = snt[s];
+        q.nb = snb[s];
         q.bpre = (int)nbs;
         q.hoff = (int)hn;
         q.pad = 0;
         ss[s] = q;
-        m += tot[3 * s];
-        k += tot[3 * s + 1];
-        pr += tot[3 * s + 2];
-        nbs += (unsigned long long)q.nb;
-        hn += (unsigned long long)q.ntile * q.nb;
+        if (s == S - 1) {
+            unsigned long long pr = 0;
+            for (int q2 = 0; q2 < S; ++q2) pr += sp[q2];
+            unsigned long long *t = tot + 3 * kMaxSlicesSmem;
+            t[0] = m + sm[s];
+            t[1] = k + sk[s];
+            t[2] = pr;
+            t[3] = hn + (unsigned long long)snt[s] * snb[s];
+            t[4] = nbs + (unsigned long long)snb[s];
+        }
     }
-    unsigned long long *t = tot + 3 * kMaxSlicesSmem;
-    t[0] = m;
-    t[1] = k;
-    t[2] = pr;
-    t[3] = hn;
-    t[4] = nbs;
 }
 
 }  // namespace
@@ -378,7 +395,7 @@ int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
 
 int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
                        int64_t *slice_base, SortSlice *ss, cudaStream_t st) {
-    plan_slices_kernel<<<1, 32, 0, st>>>(slice_tot, slices, S, slice_base, ss);
+    plan_slices_kernel<<<1, 64, 0, st>>>(slice_tot, slices, S, slice_base, ss);
     UGS_LAUNCH_CHECK("plan_slices_kernel");
     return UGS_OK;
 }

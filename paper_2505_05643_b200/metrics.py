@@ -135,11 +135,15 @@ _WS: dict = {}
 
 
 def fused_loss(num: torch.Tensor, den: torch.Tensor, target: torch.Tensor,
-               lam: float, l2: bool = False):
+               lam: float, l2: bool = False, target_index: torch.Tensor | None = None,
+               mean_out: torch.Tensor | None = None):
     """Training loss straight from the render accumulators, one fused CUDA
-    pass (ugs_loss): pred = num/den, (1-lam)*L1 + lam*(1-SSIM) per slice.
+    pass (ugs_loss_ex): pred = num/den, (1-lam)*L1 + lam*(1-SSIM) per slice.
 
-    num, den, target: (S, H, W) float32 on the device.  Returns
+    num, den: (S, H, W) float32 on the device; target: (S, H, W), or -- with
+    target_index (S,) int64 on the device -- the whole dataset (N, H, W), slice
+    s comparing against target[target_index[s]] (no gather copy).  mean_out
+    (0-dim float64 on the device) receives the batch-mean loss.  Returns
     (loss (S,) float64, d_pixels (S, H, W) float32, ssim (S,) float64)."""
     import ctypes
     from . import _lib
@@ -154,11 +158,18 @@ def fused_loss(num: torch.Tensor, den: torch.Tensor, target: torch.Tensor,
     lv = torch.empty(S, dtype=torch.float64, device=num.device)
     sv = torch.empty(S, dtype=torch.float64, device=num.device)
     tgt = target.to(dtype=torch.float32).contiguous()
-    _lib.check(L.ugs_loss(num.data_ptr(), den.data_ptr(), tgt.data_ptr(), S, H, W,
-                          float(lam), int(bool(l2)), dpix.data_ptr(), lv.data_ptr(),
-                          sv.data_ptr(), ws.data_ptr(),
-                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-               "ugs_loss")
+    if target_index is not None:
+        target_index = target_index.to(dtype=torch.int64).contiguous()
+        if tgt.shape[-2:] != (H, W) or target_index.shape != (S,):
+            raise InvalidParameterError("target / target_index shapes do not match")
+    elif tgt.shape != (S, H, W):
+        raise InvalidParameterError("prediction/target dimensions differ")
+    _lib.check(L.ugs_loss_ex(num.data_ptr(), den.data_ptr(), tgt.data_ptr(),
+                             _lib.ptr(target_index), S, H, W, float(lam), int(bool(l2)),
+                             dpix.data_ptr(), lv.data_ptr(), sv.data_ptr(),
+                             _lib.ptr(mean_out), ws.data_ptr(),
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "ugs_loss_ex")
     return lv, dpix, sv
 
 

@@ -508,11 +508,16 @@ class TrainEngine:
         den = torch.empty_like(num)
         self.renderer.forward(self.cloud, num, den)
         self._mark("loss0")
+        self.loss_mean = torch.empty((), dtype=torch.float64, device=self.cloud.device)
         if targets_batch is None:
-            tgt = self.targets.index_select(0, ids)
+            # the loss kernel reads the dataset rows directly (no gather copy)
+            lv, dpix, _ = fused_loss(num, den, self.targets, cfg.ssim_loss_weight,
+                                     cfg.l2_loss, target_index=ids, mean_out=self.loss_mean)
+            tgt = self.targets[int(idx[0]):int(idx[0]) + 1]   # slice 0's target (a view)
         else:
             tgt = targets_batch
-        lv, dpix, _ = fused_loss(num, den, tgt, cfg.ssim_loss_weight, cfg.l2_loss)
+            lv, dpix, _ = fused_loss(num, den, tgt, cfg.ssim_loss_weight, cfg.l2_loss,
+                                     mean_out=self.loss_mean)
         self._mark("loss1")
         return num, den, None, tgt, lv, dpix
 
@@ -521,7 +526,7 @@ class TrainEngine:
         check_finite, else the device tensor."""
         cfg = self.config
         num, den, pred, tgt, lv, dpix = self.forward_loss(idx, targets_batch)
-        loss_t = lv.mean()
+        loss_t = self.loss_mean
         if self.world_size > 1:
             torch.distributed.all_reduce(loss_t, group=self.pg)
             loss_t = loss_t / self.world_size
