@@ -22,9 +22,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -85,51 +83,91 @@ def train_config(a):
                        heuristic_interval=0, batch=a.batch)
 
 
+_SAMPLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+bus, period = sys.argv[1], float(sys.argv[2])
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(0)
+print("max", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+while True:
+    t = time.monotonic()
+    print(t, nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+          nv.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    time.sleep(period)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.  A child
+    process polls NVML (the library nvidia-smi reads) every `period` seconds
+    and prints monotonic-clock timestamped samples; it is started before the
+    warm-up (so its start-up cost is outside the timed region -- a
+    `nvidia-smi -lms` child needs ~100 ms to start, longer than a 50-step
+    timed region), `mark(t0, t1)` names the timed window and `stop()`
+    summarises the samples inside it.  A separate process keeps the poll
+    off this process's GIL."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
-              "clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("hw_power_brake_slowdown", 0x80),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, gpu_index=0):
-        self.gpu = gpu_index
+    def __init__(self, device=0, period=0.002):
+        self.device = device
+        self.period = period
         self.proc = None
+        self.window = None
+        self.err = None
 
     def start(self):
-        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import subprocess
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=self.tmp, stderr=subprocess.DEVNULL)
-        except OSError:
+            import torch
+            p = torch.cuda.get_device_properties(self.device)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        except Exception:
+            bus = "none"
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, bus, str(self.period)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            first = self.proc.stdout.readline().split()   # blocks until NVML is up
+            self.sm_max = float(first[1])
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = f"nvml sampler unavailable: {e}"
+            if self.proc is not None:
+                self.proc.kill()
             self.proc = None
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.06)
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "not sampled"],
+                    "samples": 0}
+        time.sleep(2 * self.period)
         self.proc.terminate()
-        self.proc.wait()
-        self.tmp.seek(0)
-        rows = [r.split(",") for r in self.tmp.read().strip().splitlines() if r.strip()]
-        os.unlink(self.tmp.name)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
+        out, _ = self.proc.communicate()
+        rows = []
+        for line in out.splitlines():
+            f = line.split()
             try:
-                sm.append(float(r[1]))
-                smax = float(r[2])
+                rows.append((float(f[0]), float(f[1]), int(f[2])))
             except (ValueError, IndexError):
                 continue
-            for k, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
-                    reasons.add(k)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        scope = "all"
+        if self.window is not None:
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1]]
+            if inside:
+                rows, scope = inside, "timed"
+        reasons = sorted({name for _, _, rs in rows for name, bit in self.REASONS if rs & bit})
+        sm = [r[1] for r in rows]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.sm_max,
+                "reasons": reasons, "samples": len(sm), "window": scope, "source": "nvml"}
 
 
 # ------------------------------------------------------------------ CPU ---
@@ -318,14 +356,15 @@ def run_ours(a):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(a.warmup):
         step()
     # ---- timed region: device-resident inputs, no instrumentation ----
     eng.pairs_total = 0
-    sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    t_host0 = time.monotonic()
     l0 = _lib.lib().ugs_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")      # ncu --nvtx-include "timed/"
@@ -336,6 +375,7 @@ def run_ours(a):
     e1.record()
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
+    sampler.mark(t_host0, time.monotonic())
     launches = _lib.lib().ugs_launch_count() - l0
     clocks = sampler.stop()
     barrier()

@@ -544,7 +544,7 @@ class TrainEngine:
         if self.world_size == 1:
             # single GPU: backward + ordered accumulation + stats + Adam in one
             # call; the dense gradient is never materialised
-            self._mark("adam0")
+            self._mark("backward_adam0")
             st = self.state
             st.t += 1
             cs = self.cloud.c_struct()
@@ -554,7 +554,7 @@ class TrainEngine:
                 st.v_flat.data_ptr(), st.t, _lr_array(lrs), st.beta1, st.beta2, st.eps,
                 self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
                 "ugs_backward_adam")
-            self._mark("adam1")
+            self._mark("backward_adam1")
             return loss_val if check_finite else loss_t
         if self.peer:
             self.grad.zero_()
