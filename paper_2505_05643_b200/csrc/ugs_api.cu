@@ -132,7 +132,7 @@ extern "C" int ugs_plan_create(ugs_plan **out) {
 extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (!p) return UGS_OK;
     PlanBuffers &b = p->b;
-    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.warp_inst, b.win_sparse, b.slice_tot,
+    void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.warp_inst, b.rec_bucket, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.bg_sums,
@@ -201,6 +201,11 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     UGS_CUDA(cudaMemcpyAsync(b.slices, p->h_slices, sizeof(ugs_slice) * S,
                              cudaMemcpyHostToDevice, st));
     const int nblk = (int)((c->n + kPrepThreads - 1) / kPrepThreads);
+    if ((int64_t)S * nblk * (kPrepThreads / 32) >= 0x7fffffffLL) {
+        // the flattened (slice, warp) index of the record search is 32-bit
+        set_error("ugs_bin: slices x Gaussians exceeds the 2^36 plan budget; use fewer slices");
+        return UGS_ERR_RANGE;
+    }
     if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, (size_t)S * (nblk > 0 ? nblk : 1),
                      "alloc blk_cnt")))
         return rc;
@@ -275,6 +280,9 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
+    if ((rc = ensure(&b.rec_bucket, &b.rec_bucket_cap, (size_t)m_total / 128 + 2,
+                     "alloc rec_bucket")))
+        return rc;
     {
         size_t cap2 = b.bg_sums ? 64 : 0;
         if ((rc = ensure(&b.bg_sums, &cap2, (size_t)64, "alloc bg_sums"))) return rc;
@@ -316,7 +324,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
                                       b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
                                       m_total, k_total, b.win_sparse, b.amask,
-                                      b.wcnt, b.warp_rec, b.warp_inst, st)))
+                                      b.wcnt, b.warp_rec, b.warp_inst, b.rec_bucket, st)))
             return rc;
     } else {
         UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));

@@ -61,6 +61,8 @@ struct PlanBuffers {
     size_t warp_inst_cap = 0;
     int32_t *warp_rec = nullptr;    // [S][nblk*8] record index of each warp's first
     size_t warp_rec_cap = 0;        //   accepted Gaussian (emit pass)
+    int32_t *rec_bucket = nullptr;  // [m/128 + 1] flattened warp holding record 128 b
+    size_t rec_bucket_cap = 0;
     uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
     size_t win_sparse_cap = 0;
     unsigned long long *slice_tot = nullptr; // [S][2] totals (accepted, tiles)
@@ -180,7 +182,7 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
-                        cudaStream_t st);
+                        int32_t *rec_bucket, cudaStream_t st);
 
 // radix sort (ugs_sort.cu): sorts (keys, identity values) by the low `bits`
 // bits, stable.  On return *keys_out/*vals_out point at the sorted arrays

@@ -270,48 +270,47 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
     }
 }
 
-// One block for the whole batch: per slice, the tile sums in fixed order,
-// then loss / SSIM per slice and the batch-mean loss (slice order) --
-// deterministic, one launch.
-__global__ void loss_reduce_kernel(const double *__restrict__ tile_sums,
-                                   int tiles_per_slice, int S, int H, int W, double lam,
-                                   int l2, double *__restrict__ loss_out,
-                                   double *__restrict__ ssim_out,
-                                   double *__restrict__ mean_out) {
-    __shared__ double ra[256], rb[256], lv[64];
+// One block for the whole batch, one warp per slice (all slices in
+// parallel): lane-strided sums of the slice's tile partials, then a fixed
+// xor tree -- the same order on every call (deterministic) -- loss / SSIM
+// per slice, and the batch-mean loss in slice order.
+constexpr int kReduceWarps = 32;
+
+__global__ void __launch_bounds__(32 * kReduceWarps)
+loss_reduce_kernel(const double *__restrict__ tile_sums, int tiles_per_slice, int S, int H,
+                   int W, double lam, int l2, double *__restrict__ loss_out,
+                   double *__restrict__ ssim_out, double *__restrict__ mean_out) {
+    __shared__ double lv[64];
     const double npx = (double)H * W;
     const double nv = (double)(H - 2 * kPad) * (W - 2 * kPad);
-    for (int s = 0; s < S; ++s) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < S; s += kReduceWarps) {
+        const double *ts = tile_sums + 2 * (size_t)s * tiles_per_slice;
         double a = 0, b = 0;
-        for (int t = threadIdx.x; t < tiles_per_slice; t += blockDim.x) {
-            a += tile_sums[2 * ((size_t)s * tiles_per_slice + t)];
-            b += tile_sums[2 * ((size_t)s * tiles_per_slice + t) + 1];
+        for (int t = lane; t < tiles_per_slice; t += 32) {
+            a += ts[2 * t];
+            b += ts[2 * t + 1];
         }
-        ra[threadIdx.x] = a;
-        rb[threadIdx.x] = b;
-        __syncthreads();
-        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-            if (threadIdx.x < o) {
-                ra[threadIdx.x] += ra[threadIdx.x + o];
-                rb[threadIdx.x] += rb[threadIdx.x + o];
-            }
-            __syncthreads();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
         }
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             double v;
-            const double mean_s = rb[0] / nv;
+            const double mean_s = b / nv;
             if (l2) {
-                v = ra[0] / npx;
+                v = a / npx;
             } else {
-                v = (1.0 - lam) * (ra[0] / npx);
+                v = (1.0 - lam) * (a / npx);
                 if (lam > 0.0) v += lam * (1.0 - mean_s);
             }
             if (loss_out) loss_out[s] = v;
             if (ssim_out) ssim_out[s] = mean_s;
             lv[s] = v;
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (threadIdx.x == 0 && mean_out) {
         double m = 0.0;
         for (int s = 0; s < S; ++s) m += lv[s];
@@ -375,7 +374,7 @@ extern "C" int ugs_loss_ex(const float *num, const float *den, const float *targ
     loss_tile_kernel<<<grid, kLossThreads, smem, st>>>(num, den, target, target_index, H, W,
                                                        lam, l2, d_pixels, sums, tx, tx * ty);
     UGS_LAUNCH_CHECK("loss_tile_kernel");
-    loss_reduce_kernel<<<1, 256, 0, st>>>(sums, tx * ty, S, H, W, lam, l2, loss_out,
+    loss_reduce_kernel<<<1, 32 * kReduceWarps, 0, st>>>(sums, tx * ty, S, H, W, lam, l2, loss_out,
                                           ssim_out, loss_mean_out);
     UGS_LAUNCH_CHECK("loss_reduce_kernel");
     return UGS_OK;

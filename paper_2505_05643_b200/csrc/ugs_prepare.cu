@@ -18,6 +18,7 @@ namespace ugs {
 namespace {
 
 constexpr int kMaxSlicesSmem = 64;
+constexpr int kBuildThreads = 128;   // records per build block (= rec_bucket stride)
 
 __device__ __forceinline__ void load_slices_smem(ugs_slice *dst,
                                                  const ugs_slice *src, int S) {
@@ -224,25 +225,40 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
 
 // Per (slice, warp of 32 Gaussians): the warp's first record and first
 // instance, from the block offsets (scan) and the within-block warp offsets
-// (count pass).  Empty warps get the offset of the next record, so each
-// slice's row is non-decreasing -- build_records searches it.
+// (count pass).  Empty warps get the offset of the next record, so the
+// flattened [S][nwarp] row is non-decreasing -- build_records searches it.
+// Every non-empty warp also records itself as the owner of each multiple of
+// kBuildThreads among its records: rec_bucket[b] = the flattened warp that
+// holds record b * kBuildThreads, so a build block searches only between
+// rec_bucket[b] and rec_bucket[b + 1].
 __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
                                     const uint2 *__restrict__ blk_off,
                                     const uint2 *__restrict__ wcnt,
+                                    const uint32_t *__restrict__ amask,
                                     const int64_t *__restrict__ slice_base,
                                     int32_t *__restrict__ warp_rec,
                                     int32_t *__restrict__ warp_inst,
+                                    int32_t *__restrict__ rec_bucket,
                                     int32_t *__restrict__ rec_inst, int64_t m_total,
                                     int64_t k_total) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx == 0) rec_inst[m_total] = (int32_t)k_total;
-    if (idx >= (int64_t)S * nwarp_all) return;
+    const int64_t nw = (int64_t)S * nwarp_all;
+    if (idx == 0) {
+        rec_inst[m_total] = (int32_t)k_total;
+        rec_bucket[(m_total + kBuildThreads - 1) / kBuildThreads] = (int32_t)(nw - 1);
+    }
+    if (idx >= nw) return;
     const int s = (int)(idx / nwarp_all);
     const int64_t gw = idx - (int64_t)s * nwarp_all;
     const uint2 bo = __ldg(blk_off + (size_t)s * nblk + gw / (kPrepThreads / 32));
     const uint2 c = __ldg(wcnt + idx);
-    warp_rec[idx] = (int32_t)(slice_base[2 * s] + bo.x + c.x);
+    const int32_t r0 = (int32_t)(slice_base[2 * s] + bo.x + c.x);
+    warp_rec[idx] = r0;
     warp_inst[idx] = (int32_t)(slice_base[2 * s + 1] + bo.y + c.y);
+    const int32_t r1 = r0 + __popc(__ldg(amask + idx));
+    for (int32_t q = (r0 + kBuildThreads - 1) / kBuildThreads * kBuildThreads; q < r1;
+         q += kBuildThreads)
+        rec_bucket[q / kBuildThreads] = (int32_t)idx;
 }
 
 __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
@@ -251,14 +267,15 @@ __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
 }
 
 // One thread per accepted (slice, Gaussian) record.  It finds its Gaussian
-// from the record index alone -- slice by the slice bases, warp by a binary
-// search of the slice's warp_rec row, lane as the k-th set bit of the warp's
+// from the record index alone -- (slice, warp) by a binary search of the
+// flattened warp_rec row between the block's rec_bucket bounds (a few steps:
+// the block's 128 records span a few dozen warps), lane as the k-th set bit of the warp's
 // accept ballot -- and its first instance as the warp's plus the tile counts
 // of the warp's earlier accepted lanes (no separate emit pass).  Then the
 // plane-conditioned exponent (float64, ugs_geometry.cuh PlaneForm) and the
 // record's tile instances in row-major tile order, each with its exact
 // re-expansion.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kBuildThreads)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
                      const float *__restrict__ intensity_raw,
                      const float *__restrict__ opacity_raw, int64_t n, float beta,
@@ -267,26 +284,23 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      int64_t nwarp_all, const uint32_t *__restrict__ amask,
                      const int32_t *__restrict__ warp_rec,
                      const int32_t *__restrict__ warp_inst,
+                     const int32_t *__restrict__ rec_bucket,
                      const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
                      int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
                      Inst *__restrict__ idata, uint32_t *__restrict__ keys) {
-    // the slices' record bases in shared memory: the per-thread slice search
-    // runs on it instead of on dependent global loads
-    __shared__ int64_t s_rb[64];
-    for (int q = threadIdx.x; q < S; q += blockDim.x) s_rb[q] = slice_base[2 * q];
-    __syncthreads();
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
     if (r >= m_total) return;
-    int s = 0;
-    for (int step = 32; step > 0; step >>= 1)   // last slice whose base <= r
-        if (s + step < S && s_rb[s + step] <= r) s += step;
-    const int32_t *wr = warp_rec + (size_t)s * nwarp_all;
-    int lo = 0, hi = (int)nwarp_all - 1;         // last warp whose first record <= r
+    // last flattened (slice, warp) whose first record <= r, between the
+    // owners of this block's first record and the next block's
+    int lo = __ldg(rec_bucket + blockIdx.x), hi = __ldg(rec_bucket + blockIdx.x + 1);
     const int32_t r32 = (int32_t)r;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(wr + mid) <= r32) lo = mid; else hi = mid - 1;
+        if (__ldg(warp_rec + mid) <= r32) lo = mid; else hi = mid - 1;
     }
+    const int s = (int)((unsigned)lo / (unsigned)nwarp_all);
+    const int32_t *wr = warp_rec + (size_t)s * nwarp_all;
+    lo -= s * (int)nwarp_all;
     const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + lo);
     const int k = (int)(r - __ldg(wr + lo));
     const int lane = (int)__fns(word, 0, k + 1);
@@ -413,16 +427,17 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         Inst *idata, uint32_t *keys, int64_t m_total,
                         int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
-                        cudaStream_t st) {
+                        int32_t *rec_bucket, cudaStream_t st) {
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t nw = (int64_t)S * nwarp_all;
     warp_offsets_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(
-        S, nwarp_all, nblk, blk_off, wcnt, slice_base, warp_rec, warp_inst, rec_inst,
-        m_total, k_total);
+        S, nwarp_all, nblk, blk_off, wcnt, amask, slice_base, warp_rec, warp_inst,
+        rec_bucket, rec_inst, m_total, k_total);
     UGS_LAUNCH_CHECK("warp_offsets_kernel");
-    build_records_kernel<<<(unsigned)((m_total + 127) / 128), 128, 0, st>>>(
+    build_records_kernel<<<(unsigned)((m_total + kBuildThreads - 1) / kBuildThreads),
+                           kBuildThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices, S,
-        slice_base, m_total, nwarp_all, amask, warp_rec, warp_inst, win_sparse, rec,
+        slice_base, m_total, nwarp_all, amask, warp_rec, warp_inst, rec_bucket, win_sparse, rec,
         rec_gid, rec_inst, idata, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;

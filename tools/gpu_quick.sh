@@ -11,7 +11,7 @@ import json, sys
 l = [x for x in open(f"gpurun_out/bench_{sys.argv[1]}.log") if x.startswith("{")]
 if l:
     d = json.loads(l[-1])
-    print("value", round(d["value"], 1), "ms/step", round(d["ms_per_step"], 4), "e2e", round(d.get("e2e", {}).get("value", 0), 1))
+    print("value", round(d["value"], 1), "ms/step", round(d["ms_per_step"], 4), "e2e", round(d.get("e2e", {}).get("value", 0), 1), "clocks", d.get("clocks"))
     print({k: round(v, 4) for k, v in d["stage_ms_per_step"].items()})
 else:
     print(open(f"gpurun_out/bench_{sys.argv[1]}.log").read()[-3000:])
