@@ -67,6 +67,21 @@ __device__ __forceinline__ float sigmoid_bg(const double *bg_raw, int i) {
     return (float)sigmoid_f64(bg_raw[i]);
 }
 
+// Packed f32x2 helpers (sm_100 FFMA2/FADD2/FMUL2: two fp32 lanes per
+// register pair, each half rounded exactly like its scalar fma.rn).  A u64
+// holds a live register pair, so a loop-invariant operand is not re-packed.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pack2(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 // exact float of a small non-negative int: 2^23 + x
 __device__ __forceinline__ float big_float(int x) {
     return __int_as_float(0x4B000000 | x);
@@ -137,13 +152,11 @@ __device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int t
 }
 
 // Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
-// columns x (16/cw) rows per sweep; sC.y packs base = y0*16 + x0, w-1, h-1
-// and log2 cw.  Returns the number of sweeps.
-// Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
 // columns x R = 16/cw rows per sweep.  The lane layout is precomputed in
 // byte fields so a lane decodes each with one byte permute:
-//   sC.y = cmask | lcw << 8 | (h + R - 1) << 16 | log2(R) << 24
-//   sC.z = x0 | y0 << 8 | w << 16 | R << 24
+//   sC.z = cmask | lcw << 8 | (h + R - 1) << 16 | log2(R) << 24
+//   sC.w = x0 | y0 << 8 | w << 16 | R << 24
+// and sC.xy = (color, 1) is the FFMA2 operand of (num, den) += w (color, 1).
 // Returns the number of sweeps.
 __device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, int tu0,
                                                  int tv0, uint32_t inst, Batch &B,
@@ -157,11 +170,10 @@ __device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, 
                              8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
     B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
     B.sC[slot] = make_float4(
-        R.r0.w,
+        R.r0.w, 1.f,
         __int_as_float(((1 << lcw) - 1) | (lcw << 8) | ((h + rows - 1) << 16) |
                        ((4 - lcw) << 24)),
-        __int_as_float(x0 | (y0 << 8) | (w << 16) | (rows << 24)),
-        __int_as_float((int)inst));
+        __int_as_float(x0 | (y0 << 8) | (w << 16) | (rows << 24)));
     return (h + rows - 1) >> (4 - lcw);
 }
 
@@ -252,8 +264,10 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             const int slot = s0 + (lane >> 4);
             if (slot >= nb) continue;
             const int j = B.order[slot];
-            const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
-            const int k1 = __float_as_int(c.y), k2 = __float_as_int(c.z);
+            const float4 a = B.sA[j], b = B.sB[j];
+            const u64 c1 = *reinterpret_cast<const u64 *>(&B.sC[j]);   // (color, 1)
+            const int2 kk = *reinterpret_cast<const int2 *>(&B.sC[j].z);
+            const int k1 = kk.x, k2 = kk.y;
             const int lx = gl16 & byte_of(k1, 0), ly = gl16 >> byte_of(k1, 1);
             if (lx >= byte_of(k2, 2)) continue;
             const int R = byte_of(k2, 3);   // rows per sweep
@@ -271,31 +285,32 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             // rows ly, ly + R, ... < h, two per iteration (same column: P, Q
             // shared; both loads before both stores, the rows never alias)
             const int nrow = (byte_of(k1, 2) - ly) >> byte_of(k1, 3);
-            float dyB = dy + (float)R;
-            const float R2 = (float)(2 * R);
-            int i = 0;
+            // the two rows of an iteration in packed f32x2 arithmetic (FFMA2:
+            // same fma.rn rounding per half, half the issue slots); scalar
+            // operands broadcast, and (num, den) += w * (color, 1) is one
+            // FFMA2 per pixel
+            float2 dy2 = make_float2(dy, dy + (float)R);
+            const float2 C2 = make_float2(b.z, b.z), Q2 = make_float2(Q, Q),
+                         P2 = make_float2(P, P);
+            const float2 step2 = make_float2((float)(2 * R), (float)(2 * R));
+            u64 *pa = reinterpret_cast<u64 *>(ptr), *pb = reinterpret_cast<u64 *>(ptr + s1);
 #pragma unroll 1
-            for (; i + 1 < nrow; i += 2) {
-                float2 *qB = ptr + s1;
-                const float wa = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
-                const float wb = ex2_approx(fmaf(dyB, fmaf(b.z, dyB, Q), P));
-                float2 va = *ptr, vb = *qB;
-                va.x = fmaf(wa, c.x, va.x);
-                va.y += wa;
-                vb.x = fmaf(wb, c.x, vb.x);
-                vb.y += wb;
-                *ptr = va;
-                *qB = vb;
-                dy += R2;
-                dyB += R2;
-                ptr += s12;
+            for (int pairs = nrow >> 1; pairs > 0; --pairs) {
+                const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
+                const float wa = ex2_approx(e.x), wb = ex2_approx(e.y);
+                const u64 va = *pa, vb = *pb;
+                *pa = ffma2(c1, pack2(wa, wa), va);
+                *pb = ffma2(c1, pack2(wb, wb), vb);
+                dy2 = __fadd2_rn(dy2, step2);
+                pa += s12;
+                pb += s12;
             }
-            if (i < nrow) {   // odd row count: the last row
-                const float wa = ex2_approx(fmaf(dy, fmaf(b.z, dy, Q), P));
-                float2 va = *ptr;
-                va.x = fmaf(wa, c.x, va.x);
-                va.y += wa;
-                *ptr = va;
+            ptr = reinterpret_cast<float2 *>(pa);
+            if (nrow & 1) {   // odd row count: the last row
+                const float dyl = dy2.x;
+                const float wa = ex2_approx(fmaf(dyl, fmaf(b.z, dyl, Q), P));
+                u64 *pl = reinterpret_cast<u64 *>(ptr);
+                *pl = ffma2(c1, pack2(wa, wa), *pl);
             }
         }
     }
@@ -482,29 +497,34 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             const float2 *gB = okB ? gA + (L.w * kTile + L.z) : gA;
             const int gstep = okB ? stride * kTile : 0;
             const float fstride = (float)stride;
-            float m0 = 0.f, S0a = 0.f, Sya = 0.f, Syya = 0.f, S0b = 0.f, Syb = 0.f, Syyb = 0.f;
+            // streams A and B in packed f32x2 arithmetic (FFMA2 / FADD2 /
+            // FMUL2, per-half fma.rn rounding): lo = A, hi = B
+            float2 dy2 = make_float2(dyA, dyB);
+            const float2 P2 = make_float2(PA, PB), Q2 = make_float2(QA, QB);
+            const float2 C2 = make_float2(b.z, b.z), c2 = make_float2(c.x, c.x);
+            const float2 fs2 = make_float2((float)stride, (float)stride);
+            float2 m02 = make_float2(0.f, 0.f), S02 = m02, Sy2 = m02, Syy2 = m02;
             int i = 0;
 #pragma unroll 1
             for (; i < nB; ++i) {
-                const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
-                const float wb = ex2_approx(fmaf(dyB, fmaf(b.z, dyB, QB), PB));
+                const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
+                const float2 w2 = make_float2(ex2_approx(e.x), ex2_approx(e.y));
                 const float2 ga = *gA, gb = *gB;
-                const float ta = fmaf(ga.x, c.x, -ga.y) * wa;   // dw * w
-                const float tb = fmaf(gb.x, c.x, -gb.y) * wb;
-                m0 = fmaf(ga.x, wa, m0);
-                m0 = fmaf(gb.x, wb, m0);
-                S0a += ta;
-                S0b += tb;
-                const float tya = ta * dyA, tyb = tb * dyB;
-                Sya += tya;
-                Syb += tyb;
-                Syya = fmaf(tya, dyA, Syya);
-                Syyb = fmaf(tyb, dyB, Syyb);
-                dyA += fstride;
-                dyB += fstride;
+                const float2 gx = make_float2(ga.x, gb.x), gy = make_float2(-ga.y, -gb.y);
+                const float2 t2 = __fmul2_rn(__ffma2_rn(gx, c2, gy), w2);   // dw * w
+                m02 = __ffma2_rn(gx, w2, m02);
+                S02 = __fadd2_rn(S02, t2);
+                const float2 ty2 = __fmul2_rn(t2, dy2);
+                Sy2 = __fadd2_rn(Sy2, ty2);
+                Syy2 = __ffma2_rn(ty2, dy2, Syy2);
+                dy2 = __fadd2_rn(dy2, fs2);
                 gA += stride * kTile;
                 gB += gstep;
             }
+            float m0 = m02.x + m02.y;
+            float S0a = S02.x, Sya = Sy2.x, Syya = Syy2.x;
+            const float S0b = S02.y, Syb = Sy2.y, Syyb = Syy2.y;
+            dyA = dy2.x;
             if (i < nA) {   // narrow tail: one more row of stream A
                 const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
                 const float2 ga = *gA;
