@@ -105,7 +105,10 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                 for (int o = 0; o < kHB; ++o) a[f][o] = 0.0;
 #pragma unroll
             for (int kk = 0; kk < kHB + 10; ++kk) {
+                // the product images first (as the reference filters x*x,
+                // y*y, x*y), once per input point for all the run's outputs
                 const double x = sm.X[r][c0 + kk], y = sm.Y[r][c0 + kk];
+                const double xx = x * x, yy = y * y, xy = x * y;
 #pragma unroll
                 for (int o = 0; o < kHB; ++o) {
                     const int b = kk - o;
@@ -113,9 +116,9 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                     const double w = c_win[b];
                     a[0][o] += w * x;
                     a[1][o] += w * y;
-                    a[2][o] += w * x * x;
-                    a[3][o] += w * y * y;
-                    a[4][o] += w * x * y;
+                    a[2][o] += w * xx;
+                    a[3][o] += w * yy;
+                    a[4][o] += w * xy;
                 }
             }
 #pragma unroll
