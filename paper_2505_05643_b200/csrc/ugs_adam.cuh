@@ -74,18 +74,39 @@ struct AdamArgs {
     int32_t *grad_cnt;
 };
 
+// Adam on one Gaussian's row held in registers: parameters pr[11] in the
+// AoS-12 order, moments mm / vv.
+__device__ __forceinline__ void adam_row(const float gr[kG], float pr[11], float mm[kG],
+                                         float vv[kG], const AdamConst &k) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        pr[c] = __fsub_rn(pr[c], adam_update(gr[c], mm[c], vv[c], k, k.lr[0]));
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+        pr[3 + c] = __fsub_rn(pr[3 + c], adam_update(gr[3 + c], mm[3 + c], vv[3 + c], k,
+                                                     k.lr[1]));
+    pr[9] = __fsub_rn(pr[9], adam_update(gr[9], mm[9], vv[9], k, k.lr[2]));
+    pr[10] = __fsub_rn(pr[10], adam_update(gr[10], mm[10], vv[10], k, k.lr[3]));
+}
+
 // Adam on Gaussian g given its 11 gradient entries; m, v point at the
 // Gaussian's AoS-12 rows.  Optional densify statistics (trainer.py:399-401).
+// Every load first (parameters, moments, statistics), then the math, then
+// every store: the parameter arrays are distinct but not __restrict__, so an
+// interleaved load-update-store sequence would serialise the round trips.
 __device__ __forceinline__ void adam_gaussian(int64_t g, const float gr[kG],
                                               float *__restrict__ m,
                                               float *__restrict__ v,
                                               const CloudMut &p,
                                               const AdamConst &k, bool touched,
                                               float *grad_sum, int32_t *grad_cnt) {
-    if (touched && grad_sum) {
-        grad_sum[g] = __fadd_rn(grad_sum[g], norm3_f32(gr[0], gr[1], gr[2]));
-        grad_cnt[g] += 1;
-    }
+    float pr[11];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pr[c] = p.means[3 * g + c];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) pr[3 + c] = p.l_raw[6 * g + c];
+    pr[9] = p.intensity_raw[g];
+    pr[10] = p.opacity_raw[g];
     float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
     float mm[kG], vv[kG];
 #pragma unroll
@@ -94,19 +115,24 @@ __device__ __forceinline__ void adam_gaussian(int64_t g, const float gr[kG],
         mm[4 * q] = a.x; mm[4 * q + 1] = a.y; mm[4 * q + 2] = a.z; mm[4 * q + 3] = a.w;
         vv[4 * q] = b.x; vv[4 * q + 1] = b.y; vv[4 * q + 2] = b.z; vv[4 * q + 3] = b.w;
     }
+    const bool stats = touched && grad_sum;
+    float gs = 0.f;
+    int32_t gc = 0;
+    if (stats) {
+        gs = grad_sum[g];
+        gc = grad_cnt[g];
+    }
+    adam_row(gr, pr, mm, vv, k);
+    if (stats) {
+        grad_sum[g] = __fadd_rn(gs, norm3_f32(gr[0], gr[1], gr[2]));
+        grad_cnt[g] = gc + 1;
+    }
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-        p.means[3 * g + c] = __fsub_rn(p.means[3 * g + c],
-                                       adam_update(gr[c], mm[c], vv[c], k, k.lr[0]));
+    for (int c = 0; c < 3; ++c) p.means[3 * g + c] = pr[c];
 #pragma unroll
-    for (int c = 0; c < 6; ++c)
-        p.l_raw[6 * g + c] = __fsub_rn(p.l_raw[6 * g + c],
-                                       adam_update(gr[3 + c], mm[3 + c], vv[3 + c], k,
-                                                   k.lr[1]));
-    p.intensity_raw[g] = __fsub_rn(p.intensity_raw[g],
-                                   adam_update(gr[9], mm[9], vv[9], k, k.lr[2]));
-    p.opacity_raw[g] = __fsub_rn(p.opacity_raw[g],
-                                 adam_update(gr[10], mm[10], vv[10], k, k.lr[3]));
+    for (int c = 0; c < 6; ++c) p.l_raw[6 * g + c] = pr[3 + c];
+    p.intensity_raw[g] = pr[9];
+    p.opacity_raw[g] = pr[10];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         m4[q] = make_float4(mm[4 * q], mm[4 * q + 1], mm[4 * q + 2], mm[4 * q + 3]);

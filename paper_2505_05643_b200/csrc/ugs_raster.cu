@@ -683,14 +683,15 @@ constexpr int kUpdRows = 64;    // staged record-gradient rows per warp and pass
 // zero-gradient rows still move (trainer.py:182-199) -- and the dense
 // gradient never touches HBM; or (adam == 0) the rows are added into the
 // dense AoS-12 buffer.
-__global__ void __launch_bounds__(kUpdThreads)
+__global__ void __launch_bounds__(kUpdThreads, 4)
 update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restrict__ warp_rec,
                      const float *__restrict__ rgrad, int S, int64_t nwarp_all, int64_t n,
                      float scale, int adam, float *__restrict__ grad,
                      uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
-                     int32_t *__restrict__ grad_cnt) {
+                     int32_t *__restrict__ grad_cnt, int aligned) {
     __shared__ float4 rows_all[kUpdWarps][kUpdRows][3];
+    __shared__ float4 prm_all[kUpdWarps][24 + 48];   // means | l_raw rows of the warp
     __shared__ uint32_t word_all[kUpdWarps][64];
     __shared__ int off_all[kUpdWarps][65], base_all[kUpdWarps][64];
     const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
@@ -731,14 +732,28 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         }
         s_off[s1 - s0] = tot;   // every lane writes the same values
         __syncwarp();
-        for (int i = lane; i < tot; i += 32) {
-            int sg = 0;
-            while (s_off[sg + 1] <= i) ++sg;
-            const int64_t r = (int64_t)s_base[s0 + sg] + (i - s_off[sg]);
-            const float4 *src = reinterpret_cast<const float4 *>(rgrad + (size_t)r * kG);
-            rows[i][0] = __ldg(src);
-            rows[i][1] = __ldg(src + 1);
-            rows[i][2] = __ldg(src + 2);
+        {   // the rows as a flat float4 stream (each slice's rows are
+            // consecutive records): coalesced, all loads before the stores
+            constexpr int kPer = kUpdRows * 3 / 32;
+            const float4 *src4 = reinterpret_cast<const float4 *>(rgrad);
+            float4 *dst4 = &rows[0][0];
+            float4 t[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const int f = lane + 32 * j;
+                if (f < 3 * tot) {
+                    const int i = f / 3;
+                    int sg = 0;
+                    while (s_off[sg + 1] <= i) ++sg;
+                    const int64_t r = (int64_t)s_base[s0 + sg] + (i - s_off[sg]);
+                    t[j] = __ldg(src4 + 3 * (size_t)r + (f - 3 * i));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const int f = lane + 32 * j;
+                if (f < 3 * tot) dst4[f] = t[j];
+            }
         }
         __syncwarp();
         for (int sl = s0; sl < s1; ++sl) {
@@ -754,6 +769,94 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         }
         __syncwarp();   // rows / s_off reused by the next group
         s0 = s1;
+    }
+    const int64_t g0 = gw * 32;
+    if (adam && aligned && g0 + 32 <= n) {
+        // full warp: the warp's moment rows (2 x 1536 B) and parameter rows
+        // (means 384 B, l_raw 768 B) move as coalesced float4 streams through
+        // shared memory instead of 48 / 12 / 24-byte strided per-lane rows
+        float4 *mv = &rows[0][0];   // [0, 96) m, [96, 192) v
+        float4 *pm = prm_all[warp];  // [0, 24) means, [24, 72) l_raw
+        const float4 *gm = reinterpret_cast<const float4 *>(m + kG * g0);
+        const float4 *gv = reinterpret_cast<const float4 *>(v + kG * g0);
+        const float4 *gmu = reinterpret_cast<const float4 *>(p.means + 3 * g0);
+        const float4 *gl = reinterpret_cast<const float4 *>(p.l_raw + 6 * g0);
+        float4 a[3], b[3], c0, c1, c2 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            a[j] = gm[lane + 32 * j];
+            b[j] = gv[lane + 32 * j];
+        }
+        c0 = lane < 24 ? gmu[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        c1 = gl[lane];
+        if (lane < 16) c2 = gl[32 + lane];
+        float pr[11];
+        pr[9] = p.intensity_raw[g];
+        pr[10] = p.opacity_raw[g];
+        const bool stats = hit && grad_sum;
+        float gs = 0.f;
+        int32_t gc = 0;
+        if (stats) {
+            gs = grad_sum[g];
+            gc = grad_cnt[g];
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            mv[lane + 32 * j] = a[j];
+            mv[96 + lane + 32 * j] = b[j];
+        }
+        if (lane < 24) pm[lane] = c0;
+        pm[24 + lane] = c1;
+        if (lane < 16) pm[56 + lane] = c2;
+        __syncwarp();
+        float mm[kG], vv[kG];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float4 x = mv[3 * lane + q], y = mv[96 + 3 * lane + q];
+            mm[4 * q] = x.x; mm[4 * q + 1] = x.y; mm[4 * q + 2] = x.z; mm[4 * q + 3] = x.w;
+            vv[4 * q] = y.x; vv[4 * q + 1] = y.y; vv[4 * q + 2] = y.z; vv[4 * q + 3] = y.w;
+        }
+        float *pf = reinterpret_cast<float *>(pm);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) pr[q] = pf[3 * lane + q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) pr[3 + q] = pf[96 + 6 * lane + q];
+        float gr[kG];
+#pragma unroll
+        for (int j = 0; j < 11; ++j) gr[j] = acc[j];
+        gr[11] = 0.f;
+        adam_row(gr, pr, mm, vv, k);
+        __syncwarp();   // every lane has read its rows
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            mv[3 * lane + q] = make_float4(mm[4 * q], mm[4 * q + 1], mm[4 * q + 2], mm[4 * q + 3]);
+            mv[96 + 3 * lane + q] =
+                make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) pf[3 * lane + q] = pr[q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) pf[96 + 6 * lane + q] = pr[3 + q];
+        p.intensity_raw[g] = pr[9];
+        p.opacity_raw[g] = pr[10];
+        if (stats) {
+            grad_sum[g] = __fadd_rn(gs, norm3_f32(gr[0], gr[1], gr[2]));
+            grad_cnt[g] = gc + 1;
+        }
+        __syncwarp();
+        float4 *wm = reinterpret_cast<float4 *>(m + kG * g0);
+        float4 *wv = reinterpret_cast<float4 *>(v + kG * g0);
+        float4 *wmu = reinterpret_cast<float4 *>(p.means + 3 * g0);
+        float4 *wl = reinterpret_cast<float4 *>(p.l_raw + 6 * g0);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            wm[lane + 32 * j] = mv[lane + 32 * j];
+            wv[lane + 32 * j] = mv[96 + lane + 32 * j];
+        }
+        if (lane < 24) wmu[lane] = pm[lane];
+        wl[lane] = pm[24 + lane];
+        if (lane < 16) wl[32 + lane] = pm[56 + lane];
+        return;
     }
     if (g >= n) return;
     if (adam) {
@@ -896,11 +999,15 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
         const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
         const int64_t nwarp_all = nblk * (kPrepThreads / 32);
         static_assert(kUpdThreads == kPrepThreads, "update blocks mirror count blocks");
+        // the warp-coalesced Adam path moves rows as float4: 16-byte bases
+        const int aligned =
+            adam && ((((uintptr_t)c.means | (uintptr_t)c.l_raw | (uintptr_t)adam->m |
+                       (uintptr_t)adam->v) & 15) == 0);
         update_gather_kernel<<<(unsigned)nblk, kUpdThreads, 0, st>>>(
             p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale, adam ? 1 : 0,
             grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
             adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,
-            adam ? adam->grad_cnt : nullptr);
+            adam ? adam->grad_cnt : nullptr, aligned);
         UGS_LAUNCH_CHECK("update_gather_kernel");
     }
     if (adam) {
