@@ -280,7 +280,7 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         return rc;
     if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
         return rc;
-    if ((rc = ensure(&b.rec_bucket, &b.rec_bucket_cap, (size_t)m_total / 128 + 2,
+    if ((rc = ensure(&b.rec_bucket, &b.rec_bucket_cap, (size_t)m_total / 32 + 2,
                      "alloc rec_bucket")))
         return rc;
     {

@@ -61,7 +61,7 @@ struct PlanBuffers {
     size_t warp_inst_cap = 0;
     int32_t *warp_rec = nullptr;    // [S][nblk*8] record index of each warp's first
     size_t warp_rec_cap = 0;        //   accepted Gaussian (emit pass)
-    int32_t *rec_bucket = nullptr;  // [m/128 + 1] flattened warp holding record 128 b
+    int32_t *rec_bucket = nullptr;  // [m/32 + 1] flattened warp holding record 32 b
     size_t rec_bucket_cap = 0;
     uint2 *win_sparse = nullptr;    // [S][n] packed windows of accepted pairs
     size_t win_sparse_cap = 0;

@@ -18,7 +18,8 @@ namespace ugs {
 namespace {
 
 constexpr int kMaxSlicesSmem = 64;
-constexpr int kBuildThreads = 128;   // records per build block (= rec_bucket stride)
+constexpr int kBuildThreads = 128;   // records per build block
+constexpr int kBucket = 32;          // records per rec_bucket entry (one build warp)
 
 __device__ __forceinline__ void load_slices_smem(ugs_slice *dst,
                                                  const ugs_slice *src, int S) {
@@ -228,9 +229,9 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
 // (count pass).  Empty warps get the offset of the next record, so the
 // flattened [S][nwarp] row is non-decreasing -- build_records searches it.
 // Every non-empty warp also records itself as the owner of each multiple of
-// kBuildThreads among its records: rec_bucket[b] = the flattened warp that
-// holds record b * kBuildThreads, so a build block searches only between
-// rec_bucket[b] and rec_bucket[b + 1].
+// kBucket among its records: rec_bucket[b] = the flattened warp that holds
+// record b * kBucket, so a build warp searches only between rec_bucket[b]
+// and rec_bucket[b + 1].
 __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
                                     const uint2 *__restrict__ blk_off,
                                     const uint2 *__restrict__ wcnt,
@@ -245,7 +246,7 @@ __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
     const int64_t nw = (int64_t)S * nwarp_all;
     if (idx == 0) {
         rec_inst[m_total] = (int32_t)k_total;
-        rec_bucket[(m_total + kBuildThreads - 1) / kBuildThreads] = (int32_t)(nw - 1);
+        rec_bucket[(m_total + kBucket - 1) / kBucket] = (int32_t)(nw - 1);
     }
     if (idx >= nw) return;
     const int s = (int)(idx / nwarp_all);
@@ -256,9 +257,8 @@ __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
     warp_rec[idx] = r0;
     warp_inst[idx] = (int32_t)(slice_base[2 * s + 1] + bo.y + c.y);
     const int32_t r1 = r0 + __popc(__ldg(amask + idx));
-    for (int32_t q = (r0 + kBuildThreads - 1) / kBuildThreads * kBuildThreads; q < r1;
-         q += kBuildThreads)
-        rec_bucket[q / kBuildThreads] = (int32_t)idx;
+    for (int32_t q = (r0 + kBucket - 1) / kBucket * kBucket; q < r1; q += kBucket)
+        rec_bucket[q / kBucket] = (int32_t)idx;
 }
 
 __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
@@ -267,11 +267,12 @@ __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
 }
 
 // One thread per accepted (slice, Gaussian) record.  It finds its Gaussian
-// from the record index alone -- (slice, warp) by a binary search of the
-// flattened warp_rec row between the block's rec_bucket bounds (a few steps:
-// the block's 128 records span a few dozen warps), lane as the k-th set bit of the warp's
-// accept ballot -- and its first instance as the warp's plus the tile counts
-// of the warp's earlier accepted lanes (no separate emit pass).  Then the
+// from the record index alone -- (slice, Gaussian warp) by a register binary
+// search of the flattened warp_rec window that holds the build warp's 32
+// records, lane as the k-th set bit of the warp's accept ballot -- and its
+// first instance as the Gaussian warp's plus the tile counts of the warp's
+// earlier accepted lanes, by a segmented warp scan (no separate emit pass,
+// no serial dependent loads).  Then the
 // plane-conditioned exponent (float64, ugs_geometry.cuh PlaneForm) and the
 // record's tile instances in row-major tile order, each with its exact
 // re-expansion.
@@ -288,28 +289,75 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
                      int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
                      Inst *__restrict__ idata, uint32_t *__restrict__ keys) {
+    const int ln = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
-    if (r >= m_total) return;
-    // last flattened (slice, warp) whose first record <= r, between the
-    // owners of this block's first record and the next block's
-    int lo = __ldg(rec_bucket + blockIdx.x), hi = __ldg(rec_bucket + blockIdx.x + 1);
-    const int32_t r32 = (int32_t)r;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(warp_rec + mid) <= r32) lo = mid; else hi = mid - 1;
+    const int64_t rw0 = r - ln;                   // this warp's first record
+    if (rw0 >= m_total) return;                   // whole warp
+    const bool valid = r < m_total;
+    const int32_t r32 = (int32_t)min(r, m_total - 1);
+    // 1) (slice, Gaussian warp) of every lane's record: the flattened warps
+    //    holding this warp's 32 records lie between rec_bucket[b] and
+    //    rec_bucket[b + 1]; one coalesced load of that warp_rec window and a
+    //    register binary search (shuffles), no dependent global loads
+    const int64_t b = rw0 / kBucket;
+    const int blo = __ldg(rec_bucket + b), bhi = __ldg(rec_bucket + b + 1);
+    int flat;
+    int32_t first;                                // warp_rec[flat]
+    if (bhi - blo < 32) {
+        const int32_t e = ln <= bhi - blo ? __ldg(warp_rec + blo + ln) : INT32_MAX;
+        int pos = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int32_t v = __shfl_sync(0xffffffffu, e, pos + step);
+            if (v <= r32) pos += step;
+        }
+        flat = blo + pos;
+        first = __shfl_sync(0xffffffffu, e, pos);
+    } else {                                      // sparse slices: per-lane search
+        int lo = blo, hi = bhi;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(warp_rec + mid) <= r32) lo = mid; else hi = mid - 1;
+        }
+        flat = lo;
+        first = __ldg(warp_rec + lo);
     }
-    const int s = (int)((unsigned)lo / (unsigned)nwarp_all);
-    const int32_t *wr = warp_rec + (size_t)s * nwarp_all;
-    lo -= s * (int)nwarp_all;
-    const uint32_t word = __ldg(amask + (size_t)s * nwarp_all + lo);
-    const int k = (int)(r - __ldg(wr + lo));
+    const int s = (int)((unsigned)flat / (unsigned)nwarp_all);
+    const int lo = flat - s * (int)nwarp_all;
+    const uint32_t word = __ldg(amask + flat);
+    const int k = (int)(r32 - first);
     const int lane = (int)__fns(word, 0, k + 1);
-    const int64_t g = lo * 32 + lane;
-    const uint2 *ws = win_sparse + (size_t)s * n + lo * 32;
-    int64_t inst = __ldg(warp_inst + (size_t)s * nwarp_all + lo);
-    for (uint32_t mk = word & ((1u << lane) - 1u); mk; mk &= mk - 1)
-        inst += packed_tiles(__ldg(ws + (__ffs(mk) - 1)));
+    const int64_t g = (int64_t)lo * 32 + lane;
+    const uint2 *ws = win_sparse + (size_t)s * n + (int64_t)lo * 32;
     const uint2 pw = __ldg(ws + lane);
+    // 2) first instance: the Gaussian warp's plus the tiles of its earlier
+    //    accepted lanes -- a segmented warp scan over this warp's records
+    //    (consecutive records of one Gaussian warp are consecutive lanes),
+    //    plus, for the segment that began before this warp, the tiles of its
+    //    records in the previous warp (one parallel load per such record)
+    const unsigned nt = valid ? packed_tiles(pw) : 0u;
+    unsigned incl = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        const int kf = __shfl_up_sync(0xffffffffu, flat, o);
+        if (ln >= o && kf == flat) incl += t;
+    }
+    const int flat0 = __shfl_sync(0xffffffffu, flat, 0);
+    const int k0 = __shfl_sync(0xffffffffu, k, 0);   // records of segment 0 before rw0
+    unsigned pre = 0;
+    if (k0 > 0) {
+        const uint32_t word0 = __shfl_sync(0xffffffffu, word, 0);
+        const int s0 = (int)((unsigned)flat0 / (unsigned)nwarp_all);
+        const int lo0 = flat0 - s0 * (int)nwarp_all;
+        if (ln < k0)
+            pre = packed_tiles(__ldg(win_sparse + (size_t)s0 * n + (int64_t)lo0 * 32 +
+                                     __fns(word0, 0, ln + 1)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    }
+    if (!valid) return;
+    int64_t inst = (int64_t)__ldg(warp_inst + flat) + (incl - nt) + (flat == flat0 ? pre : 0u);
     rec_gid[r] = (int32_t)g;
     rec_inst[r] = (int32_t)inst;
     const ugs_slice &L = slices[s];
