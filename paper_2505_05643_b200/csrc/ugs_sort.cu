@@ -244,8 +244,16 @@ slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict
     __syncthreads();
     const int start = q.inst_base + lb * kSortTile;
     const int end = min(start + kSortTile, q.inst_base + q.k);
-    for (int i = start + threadIdx.x; i < end; i += kSortThreads)
-        atomicAdd(&sh[__ldg(keys + i) - q.tile_base], 1u);
+    // all of a thread's key loads are in flight before the first atomic
+    uint32_t d[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int i = start + j * kSortThreads + threadIdx.x;
+        d[j] = i < end ? __ldg(keys + i) - (uint32_t)q.tile_base : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j)
+        if (d[j] != 0xffffffffu) atomicAdd(&sh[d[j]], 1u);
     __syncthreads();
     for (int t = threadIdx.x; t < q.ntile; t += kSortThreads)
         hist[(size_t)q.hoff + (size_t)t * q.nb + lb] = sh[t];
@@ -291,9 +299,10 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
         dr[j] = ok ? ((d << 16) | (before + rank)) : 0xffffffffu;
     }
     __syncthreads();
-    // exclusive prefix of the per-warp tile counts across warps
+    // per tile: this block's global offset (scanned histogram, one load per
+    // tile) plus the exclusive prefix of the per-warp counts across warps
     for (int d = threadIdx.x; d < q.ntile; d += kSortThreads) {
-        uint32_t run = 0;
+        uint32_t run = __ldg(offs + (size_t)q.hoff + (size_t)d * q.nb + lb);
 #pragma unroll
         for (int w = 0; w < kWarpsS; ++w) {
             const uint32_t t = wcnt[w * kT + d];
@@ -306,8 +315,7 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
     for (int j = 0; j < kSortItems; ++j) {
         if (dr[j] == 0xffffffffu) continue;
         const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
-        const uint32_t pos = offs[(size_t)q.hoff + (size_t)d * q.nb + lb] + my[d] + r;
-        vals_out[pos] = (uint32_t)(start + j * 32 + lane);
+        vals_out[my[d] + r] = (uint32_t)(start + j * 32 + lane);
     }
 }
 
