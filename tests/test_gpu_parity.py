@@ -377,3 +377,61 @@ def test_render_slices_matches_render_slice():
     for i, sp in enumerate(specs):
         one = ug.render_slice(cloud, sp).pixels
         np.testing.assert_allclose(batch[i], one, rtol=0, atol=0)
+
+
+def test_sparse_acceptance_vs_oracle():
+    """Small Gaussians, few accepted per 32-Gaussian warp: a build warp's 32
+    records span more than 32 Gaussian warps, so build_records takes its
+    per-lane search path (the dense configs use the register search).
+    Accepted set bit-exact; render and gradients vs the oracle."""
+    cloud_np = cases.uniform_cloud(11, 300_000, [[-40] * 3, [40] * 3], 2.0, 3.0)
+    rng = np.random.default_rng(12)
+    R, t = cases.random_pose(rng, 8.0)
+    spec = spec_of(R, t, 128, 128, 0.6)
+    sc = O.slice_constants(R, t, 128, 128, 0.6, 0.95)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    buf = ug.rasterize(cloud, spec)
+    num, den, acc, G = O.rasterize(*oracle_args(cloud_np, sc), workers=8)
+    assert 0 < len(acc) < 300_000 // 64        # < one record per two warps
+    assert np.array_equal(buf.accepted.cpu().numpy(), acc)
+    np.testing.assert_allclose(buf.intensity_num.cpu().numpy(), num, rtol=RTOL, atol=ATOL)
+    np.testing.assert_allclose(buf.opacity_sum.cpu().numpy(), den, rtol=RTOL, atol=ATOL)
+    dpix = np.random.default_rng(3).standard_normal((128, 128)).astype(np.float32)
+    g = ug.backward(cloud, spec, buf, dpix)
+    ref = O.backward(*oracle_args(cloud_np, sc), num, den, dpix, workers=8, gathered=G)
+    for k in ("d_means", "d_l_raw", "d_intensity_raw", "d_opacity_raw"):
+        np.testing.assert_allclose(getattr(g, k).cpu().numpy(), ref[k], rtol=RTOL,
+                                   atol=ATOL * np.abs(ref[k]).max(), err_msg=k)
+
+
+def test_fused_step_misaligned_parameters_bitwise():
+    """The fused backward + Adam moves parameter rows as float4 streams when
+    the arrays are 16-byte aligned and falls back to per-Gaussian rows
+    otherwise: both give bitwise the same training trajectory."""
+    from paper_2505_05643_b200.trainer import TrainEngine
+    cloud_np = cases.uniform_cloud(13, 5000, [[-20] * 3, [20] * 3], 0.85, 1.05)
+    rng = np.random.default_rng(14)
+    specs = [spec_of(*cases.random_pose(rng, 6.0), 64, 64, 0.5) for _ in range(6)]
+    targets = torch.rand((6, 64, 64), generator=torch.Generator().manual_seed(1)).cuda()
+    cfg = ug.TrainConfig(n_gaussians=5000, iterations=100, seed=0, batch=3,
+                         heuristic_interval=0)
+
+    def run(misaligned):
+        n = 5000
+        arrs = {}
+        for k, w in (("means", 3), ("l_raw", 6)):
+            base = torch.empty(n * w + 1, device="cuda")
+            view = base[1:] if misaligned else base[:-1]
+            view.copy_(torch.as_tensor(cloud_np[k]).reshape(-1))
+            arrs[k] = view.view(n, w)
+        cloud = ug.GaussianCloud(arrs["means"], arrs["l_raw"], cloud_np["intensity_raw"],
+                                 cloud_np["opacity_raw"], device="cuda")
+        assert (cloud.means.data_ptr() % 16 != 0) == misaligned
+        eng = TrainEngine(cloud, cfg, specs, targets)
+        for it in range(1, 5):
+            eng.step([(2 * it) % 6, (2 * it + 1) % 6, (2 * it + 3) % 6], it)
+        return [getattr(eng.cloud, k).cpu().numpy() for k in
+                ("means", "l_raw", "intensity_raw", "opacity_raw")]
+
+    for a, b in zip(run(False), run(True)):
+        assert np.array_equal(a, b)
