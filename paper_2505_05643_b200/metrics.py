@@ -9,7 +9,9 @@ valid-window filter.  Batched over (B, H, W) with separable float64 conv2d.
 
 from __future__ import annotations
 
+import datetime
 import math
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -129,6 +131,81 @@ def psnr(a, b) -> float:
         raise InvalidParameterError("image dimensions differ")
     mse = float(torch.mean((x - y) ** 2))
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+
+
+@dataclass
+class EvalReport:
+    """Per-plane-family reconstruction quality (ref metrics.py:110-120)."""
+
+    families: dict  # family -> {ssim_mean, ssim_std, psnr_mean, psnr_std, count, psnr_inf_count}
+    timestamp: str
+
+    def to_json_dict(self) -> dict:
+        return {"families": {k: dict(sorted(v.items()))
+                             for k, v in sorted(self.families.items())},
+                "timestamp": self.timestamp}
+
+
+def family_poses(volume, family: str, n: int):
+    """n linearly spaced orthogonal planes of one family through the volume
+    (ref metrics.py:123-145): [(ProbePose, SliceSpec)].  axial: the stack's
+    axial_pose at plane i*d/n (w x h); coronal: plane axes world x and z,
+    normal -y, at y = (i*h/n - (h-1)/2)*s (w x d); sagittal: plane axes
+    world y and z, normal x, at x = (i*w/n - (w-1)/2)*s (h x d)."""
+    from .dataset import axial_pose
+    from .geometry import ProbePose, SliceSpec
+    d, h, w = volume.voxels.shape
+    s = volume.spacing
+    out = []
+    if family == "axial":
+        for i in range(n):
+            out.append((axial_pose(volume, i * d / n), w, h))
+    elif family == "coronal":
+        rot = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, -1.0], [0.0, 1.0, 0.0]])
+        for i in range(n):
+            out.append((ProbePose(rot, np.array([0.0, (i * h / n - (h - 1) / 2.0) * s, 0.0])),
+                        w, d))
+    elif family == "sagittal":
+        rot = np.array([[0.0, 0.0, 1.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+        for i in range(n):
+            out.append((ProbePose(rot, np.array([(i * w / n - (w - 1) / 2.0) * s, 0.0, 0.0])),
+                        h, d))
+    else:
+        raise InvalidParameterError(f"unknown family {family!r}")
+    return [(pose, SliceSpec(width=pw, height=ph, spacing=s, pose=pose))
+            for pose, pw, ph in out]
+
+
+def evaluate_views(cloud, volume, n_per_axis: int, p_mass: float = 0.95,
+                   workers: int = 1) -> EvalReport:
+    """Render linearly spaced axial / coronal / sagittal views and score them
+    against trilinear ground truth, SSIM and PSNR mean and std per family
+    (ref metrics.py:148-178).  Each family is ONE batched render
+    (render_slices) and one GPU sampling pass (sample_slices); SSIM float64
+    per view as ssim(), PSNR from the float64 per-view MSE (inf views are
+    counted, not averaged).  `workers` is accepted and ignored."""
+    from .rasterizer import as_cloud, render_slices
+    from .volume import sample_slices
+    cloud = as_cloud(cloud)
+    families = {}
+    for family in ("axial", "coronal", "sagittal"):
+        specs = [spec for _, spec in family_poses(volume, family, n_per_axis)]
+        pred = render_slices(cloud, specs, p_mass)
+        truth = sample_slices(volume, specs, device=cloud.device)
+        ssims = ssim_batch(pred, truth).cpu().numpy()
+        mse = torch.mean((pred.to(torch.float64) - truth.to(torch.float64)) ** 2,
+                         dim=(1, 2)).cpu().numpy()
+        psnrs = [10.0 * math.log10(1.0 / float(m)) for m in mse if m != 0.0]
+        families[family] = {
+            "count": n_per_axis,
+            "ssim_mean": float(np.mean(ssims)),
+            "ssim_std": float(np.std(ssims)),
+            "psnr_mean": float(np.mean(psnrs)) if psnrs else None,
+            "psnr_std": float(np.std(psnrs)) if psnrs else None,
+            "psnr_inf_count": int(np.sum(mse == 0.0)),
+        }
+    stamp = datetime.datetime.now(datetime.timezone.utc).isoformat()
+    return EvalReport(families=families, timestamp=stamp)
 
 
 _WS: dict = {}

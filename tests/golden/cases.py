@@ -98,3 +98,11 @@ def input_checksum(*arrays) -> float:
                                   (1.0 + np.arange(np.asarray(a).size).reshape(
                                       np.asarray(a).shape) % 7)))
                      for a in arrays))
+
+
+def eval_cloud(bounds):
+    """The seeded 3000-Gaussian cloud of the evaluate_views fixture
+    (make_golden_eval.py)."""
+    c = uniform_cloud(21, 3000, bounds, 1.2, 1.6)
+    c["intensity_raw"] = np.random.default_rng(3).normal(0, 1, 3000).astype(np.float32)
+    return c
