@@ -341,6 +341,80 @@ def load_checkpoint(path, device=None):
     return cloud, meta
 
 
+# ---- training-state extension (the reference has no
+# resume): the UGSC checkpoint stays bit-compatible and the optimiser /
+# scheduler state goes to a sidecar "<path>.adam":
+#   b"UGSA" | u32 version | u32 n | u64 t |
+#   f32 m[12n+2] | f32 v[12n+2]        (AoS-12 layout, include/ugs.h)
+#   f32 grad_sum[n] | i32 grad_cnt[n]  (densify statistics)
+#   u32 trailer length | JSON {beta1, beta2, eps, iteration, beta (exact),
+#                              threshold, rng (numpy bit-generator state),
+#                              order, cursor}
+STATE_MAGIC = b"UGSA"
+STATE_VERSION = 1
+
+
+def save_training_state(path, cloud: GaussianCloud, state: "AdamState", grad_sum, grad_cnt,
+                        config: TrainConfig | None, iteration: int, extra: dict) -> None:
+    """UGSC checkpoint at `path` + the resume sidecar `path + '.adam'`
+    (both written atomically)."""
+    save_checkpoint(cloud, path, config, iteration)
+    n = cloud.n
+    trailer = dict(extra)
+    trailer.update(beta1=state.beta1, beta2=state.beta2, eps=state.eps, iteration=iteration,
+                   beta=cloud.beta)   # exact (UGSC stores beta as float32)
+    tb = json.dumps(trailer).encode()
+    parts = [STATE_MAGIC, struct.pack("<IIQ", STATE_VERSION, n, state.t),
+             state.m_flat.detach().cpu().numpy().astype("<f4").tobytes(),
+             state.v_flat.detach().cpu().numpy().astype("<f4").tobytes(),
+             grad_sum.detach().cpu().numpy().astype("<f4").tobytes(),
+             grad_cnt.detach().cpu().numpy().astype("<i4").tobytes(),
+             struct.pack("<I", len(tb)), tb]
+    tmp = str(path) + ".adam.tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(b"".join(parts))
+    os.replace(tmp, str(path) + ".adam")
+
+
+def load_training_state(path, device=None):
+    """(cloud, AdamState, grad_sum, grad_cnt, meta) from save_training_state;
+    meta is the UGSC trailer merged with the sidecar's JSON."""
+    cloud, meta = load_checkpoint(path, device)
+    blob = open(str(path) + ".adam", "rb").read()
+    if blob[:4] != STATE_MAGIC or len(blob) < 20:
+        raise CheckpointFormatError(f"bad training-state sidecar for {path}")
+    version, n, t = struct.unpack_from("<IIQ", blob, 4)
+    if version != STATE_VERSION:
+        raise CheckpointFormatError(f"unsupported training-state version {version}")
+    if n != cloud.n:
+        raise CheckpointFormatError(f"sidecar has {n} Gaussians, checkpoint {cloud.n}")
+    k = 12 * n + 2
+    off = 20
+    need = off + 4 * (2 * k + 2 * n) + 4
+    if len(blob) < need:
+        raise CheckpointFormatError(f"truncated training-state sidecar for {path}")
+    m = np.frombuffer(blob, "<f4", count=k, offset=off).copy()
+    v = np.frombuffer(blob, "<f4", count=k, offset=off + 4 * k).copy()
+    off += 8 * k
+    gs = np.frombuffer(blob, "<f4", count=n, offset=off).copy()
+    gc = np.frombuffer(blob, "<i4", count=n, offset=off + 4 * n).copy()
+    off += 8 * n
+    (tlen,) = struct.unpack_from("<I", blob, off)
+    off += 4
+    if off + tlen != len(blob):
+        raise CheckpointFormatError(f"trailer size mismatch in {path}.adam")
+    extra = json.loads(blob[off:off + tlen].decode())
+    cloud.beta = float(extra.get("beta", cloud.beta))
+    dev = cloud.device
+    state = AdamState(n, dev, int(t), extra["beta1"], extra["beta2"], extra["eps"],
+                      m_flat=torch.as_tensor(m, device=dev),
+                      v_flat=torch.as_tensor(v, device=dev))
+    meta = dict(meta)
+    meta.update(extra)
+    return (cloud, state, torch.as_tensor(gs, device=dev), torch.as_tensor(gc, device=dev),
+            meta)
+
+
 # ---------------------------------------------------------------------------
 # the training step engine (shared by train() and bench.py)
 # ---------------------------------------------------------------------------
@@ -573,14 +647,29 @@ class TrainEngine:
         self._mark("adam1")
         return loss_val if check_finite else loss_t
 
-    def densify(self, rng, scene_extent, threshold, max_total):
+    def gather_state(self):
+        """Under the peer update every rank owns a shard of m, v and the
+        statistics; fetch the owners' rows so this rank holds the full state
+        (before densify or a training-state save)."""
         if self.peer:
-            # the owners' rows of m, v and the statistics, so every rank
-            # densifies the same full state
             self.barrier()
             _lib.check(_lib.lib().ugs_peer_gather(self.arena.views, self.world_size,
                                                   self.rank, self.cloud.n, _stream()),
                        "ugs_peer_gather")
+
+    def load_state(self, state: "AdamState", grad_sum, grad_cnt):
+        """Resume: adopt saved moments and statistics (same n as the cloud)."""
+        if state.n != self.cloud.n:
+            raise InvalidParameterError("training state does not match the cloud")
+        self.state = state
+        self.grad_sum = grad_sum.to(torch.float32).contiguous()
+        self.grad_cnt = grad_cnt.to(torch.int32).contiguous()
+        if self.peer:
+            self._adopt_arena()
+
+    def densify(self, rng, scene_extent, threshold, max_total):
+        # every rank densifies the same full state
+        self.gather_state()
         avg = (self.grad_sum.double() / torch.clamp(self.grad_cnt, min=1).double()).cpu().numpy()
         if threshold is None:
             threshold = float(np.quantile(avg, 0.9))
@@ -596,11 +685,19 @@ class TrainEngine:
 
 def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
           checkpoint_path=None, log_path=None, snapshot_path=None,
-          time_budget_s: float | None = None, device=None):
+          time_budget_s: float | None = None, device=None,
+          state_path=None, state_interval: int = 0, resume_from=None):
     """Full optimisation run (ref trainer.py:351-434) -> (cloud, log).
 
     Under torch.distributed (world_size > 1) every rank draws the same slice
-    order and takes its own `config.batch` slices of each global step."""
+    order and takes its own `config.batch` slices of each global step.
+
+    Extension (the reference has no resume): `state_path` saves the full
+    training state (UGSC checkpoint + the Adam / statistics / RNG / slice-
+    order sidecar, save_training_state) every `state_interval` iterations and
+    at the end (a "{iter}" field in the path keeps one file per save);
+    `resume_from` continues such a run -- bitwise the same trajectory as an
+    uninterrupted one."""
     train_slices = dataset.subset("train")
     if not train_slices:
         raise InvalidParameterError("dataset has no training slices")
@@ -611,7 +708,11 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
     if torch.distributed.is_available() and torch.distributed.is_initialized():
         world, rank = torch.distributed.get_world_size(), torch.distributed.get_rank()
     rng = np.random.default_rng(config.seed)
-    cloud = init_cloud(config, bounds, device)
+    start = 1
+    if resume_from is not None:
+        cloud, r_state, r_gs, r_gc, r_meta = load_training_state(resume_from, device)
+    else:
+        cloud = init_cloud(config, bounds, device)
     specs = [s.spec for s in train_slices]
     targets = torch.as_tensor(np.stack([np.asarray(s.pixels, np.float32)
                                         for s in train_slices]), device=cloud.device)
@@ -620,9 +721,29 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
     max_total = 2 * config.n_gaussians
     threshold = config.densify_grad_threshold
     sched = SliceScheduler(rng, len(train_slices), config.batch, world, rank)
+    if resume_from is not None:
+        eng.load_state(r_state, r_gs, r_gc)
+        rng.bit_generator.state = r_meta["rng"]
+        sched.order = np.asarray(r_meta["order"], dtype=np.int64)
+        sched.cursor = int(r_meta["cursor"])
+        threshold = r_meta["threshold"]
+        start = int(r_meta["iteration"]) + 1
+
+    def save_state(it):
+        eng.gather_state()
+        if rank == 0:
+            path = str(state_path)
+            path = path.format(iter=it) if "{iter" in path else path
+            save_training_state(path, eng.cloud, eng.state, eng.grad_sum, eng.grad_cnt,
+                                config, it, {"threshold": threshold,
+                                             "rng": rng.bit_generator.state,
+                                             "order": [int(x) for x in sched.order],
+                                             "cursor": sched.cursor})
+
     log = []
     t0 = time.perf_counter()
-    for it in range(1, config.iterations + 1):
+    it = start - 1
+    for it in range(start, config.iterations + 1):
         loss_val = eng.step(sched.next(), it)
         if not math.isfinite(loss_val):
             snap = snapshot_path or (str(checkpoint_path or "echosplat") + ".diverged")
@@ -641,8 +762,12 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
             if log_path is not None and rank == 0:
                 with open(log_path, "a") as fh:
                     fh.write(json.dumps(entry) + "\n")
+        if state_path is not None and state_interval > 0 and it % state_interval == 0:
+            save_state(it)
         if time_budget_s is not None and time.perf_counter() - t0 >= time_budget_s:
             break
+    if state_path is not None:
+        save_state(it)
     if checkpoint_path is not None and rank == 0:
         save_checkpoint(eng.cloud, checkpoint_path, config, config.iterations)
     return eng.cloud, log

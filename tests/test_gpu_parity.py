@@ -435,3 +435,24 @@ def test_fused_step_misaligned_parameters_bitwise():
 
     for a, b in zip(run(False), run(True)):
         assert np.array_equal(a, b)
+
+
+def test_resume_reproduces_uninterrupted_run(tmp_path):
+    """Training-state extension: a run resumed from its iteration-7 state
+    (Adam moments, densify statistics and threshold, RNG, slice order) ends
+    bitwise where the uninterrupted run ends, densify included."""
+    from conftest import load_golden as _lg
+    z = _lg("train.npz")
+    ds = ug.SliceDataset([ug.SliceImage(z["slices"][i], float(z["spacing"]),
+                                        ug.ProbePose(z["rot"][i], z["trans"][i]))
+                          for i in range(len(z["slices"]))])
+    cfg = ug.TrainConfig(n_gaussians=400, iterations=12, seed=3, batch=2,
+                         heuristic_interval=5, eval_interval=12)
+    full, _ = ug.train(ds, cfg, device="cuda:0",
+                       state_path=str(tmp_path / "s{iter}.ugsc"), state_interval=7)
+    assert (tmp_path / "s7.ugsc.adam").exists() and (tmp_path / "s12.ugsc.adam").exists()
+    resumed, _ = ug.train(ds, cfg, device="cuda:0", resume_from=str(tmp_path / "s7.ugsc"))
+    for k in ("means", "l_raw", "intensity_raw", "opacity_raw"):
+        assert torch.equal(getattr(full, k), getattr(resumed, k)), k
+    assert (full.bg_intensity_raw, full.bg_opacity_raw) == \
+        (resumed.bg_intensity_raw, resumed.bg_opacity_raw)

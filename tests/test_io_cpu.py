@@ -66,3 +66,41 @@ def test_phantom_and_sampler_match_reference(kind):
                                                        z[f"{kind}/slice{i}/t"]))
         px = ug.sample_slice(v, spec).pixels
         np.testing.assert_allclose(px, z[f"{kind}/slice{i}/pixels"], rtol=1e-6, atol=1e-7)
+
+
+def test_training_state_roundtrip(tmp_path):
+    """The resume sidecar (extension): the UGSC file stays byte-identical to
+    the reference's format and the moments / statistics / JSON state come
+    back exactly."""
+    c, cfg = _ref_inputs()
+    cloud = ug.GaussianCloud.from_numpy(c, device="cpu")
+    n = cloud.n
+    g = torch.Generator().manual_seed(5)
+    st = T.AdamState(n, "cpu", t=41, m_flat=torch.randn(12 * n + 2, generator=g),
+                     v_flat=torch.rand(12 * n + 2, generator=g))
+    gs = torch.rand(n, generator=g)
+    gc = torch.randint(0, 9, (n,), generator=g, dtype=torch.int32)
+    rng = np.random.default_rng(17)
+    rng.standard_normal(7)
+    extra = {"threshold": 0.125, "rng": rng.bit_generator.state, "order": [3, 1, 2],
+             "cursor": 2}
+    path = tmp_path / "run.ugsc"
+    ug.save_training_state(path, cloud, st, gs, gc, cfg, 77, extra)
+    assert path.read_bytes() == open(CKPT, "rb").read()      # UGSC unchanged
+    cloud2, st2, gs2, gc2, meta = ug.load_training_state(path, device="cpu")
+    assert st2.t == 41 and (st2.beta1, st2.beta2, st2.eps) == (0.9, 0.999, 1e-15)
+    assert torch.equal(st2.m_flat, st.m_flat) and torch.equal(st2.v_flat, st.v_flat)
+    assert torch.equal(gs2, gs) and torch.equal(gc2, gc)
+    assert meta["iteration"] == 77 and meta["threshold"] == 0.125
+    assert meta["order"] == [3, 1, 2] and meta["cursor"] == 2
+    r2 = np.random.default_rng()
+    r2.bit_generator.state = meta["rng"]
+    assert np.array_equal(r2.standard_normal(4), rng.standard_normal(4))
+    side = tmp_path / "run.ugsc.adam"
+    blob = side.read_bytes()
+    side.write_bytes(blob[:-5])
+    with pytest.raises(T.CheckpointFormatError):
+        ug.load_training_state(path, device="cpu")
+    side.write_bytes(b"XXXX" + blob[4:])
+    with pytest.raises(T.CheckpointFormatError):
+        ug.load_training_state(path, device="cpu")
