@@ -103,11 +103,6 @@ __device__ __forceinline__ bool cull_window_xy(const float mu[3], const Factor &
     return (w.iu0 <= w.iu1) && (w.iv0 <= w.iv1);
 }
 
-__device__ __forceinline__ bool cull_window(const float mu[3], const Factor &f,
-                                            const ugs_slice &sl, Window &w) {
-    return straddles(mu, f, sl) && cull_window_xy(mu, f, sl, w);
-}
-
 __device__ __forceinline__ int window_tiles(const Window &w) {
     return ((w.iu1 >> 4) - (w.iu0 >> 4) + 1) * ((w.iv1 >> 4) - (w.iv0 >> 4) + 1);
 }
