@@ -694,6 +694,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
     __shared__ float4 prm_all[kUpdWarps][24 + 48];   // means | l_raw rows of the warp
     __shared__ uint32_t word_all[kUpdWarps][64];
     __shared__ int off_all[kUpdWarps][65], base_all[kUpdWarps][64];
+    __shared__ uint8_t rs_all[kUpdWarps][kUpdRows];   // row -> slice of a pass
     const int64_t g = (int64_t)blockIdx.x * kUpdThreads + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kUpdWarps + warp;
@@ -701,6 +702,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
     float4(*rows)[3] = rows_all[warp];
     uint32_t *s_word = word_all[warp];
     int *s_off = off_all[warp], *s_base = base_all[warp];
+    uint8_t *s_rs = rs_all[warp];
     const uint32_t lt = (1u << lane) - 1u;
     if (adam && g < n) {
         // the update's streams (moments, parameters) start towards L2 while
@@ -710,27 +712,46 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.l_raw + 6 * g));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.means + 3 * g));
     }
-    // slice words and record bases: lane s handles slice s (S <= 64)
-    for (int sl = lane; sl < S; sl += 32) {
-        const uint32_t w = __ldg(amask + (size_t)sl * nwarp_all + gw);
-        s_word[sl] = w;
-        s_base[sl] = w ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw) : 0;
+    // slice words, record bases and the exclusive prefix of the warp's rows
+    // over the slices (lane s handles slice s; S <= 64: two rounds)
+    int total = 0;
+    for (int sw = 0; sw < S; sw += 32) {
+        const int sl = sw + lane;
+        uint32_t w = 0;
+        if (sl < S) {
+            w = __ldg(amask + (size_t)sl * nwarp_all + gw);
+            s_word[sl] = w;
+            s_base[sl] = w ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw) : 0;
+        }
+        const int c = __popc(w);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (sl < S) s_off[sl] = total + incl - c;
+        total += __shfl_sync(0xffffffffu, incl, 31);
     }
+    if (lane == 0) s_off[S] = total;
     __syncwarp();
     float acc[11];
 #pragma unroll
     for (int j = 0; j < 11; ++j) acc[j] = 0.f;
     bool hit = false;
-    int s0 = 0;
-    while (s0 < S) {
-        // next group of slices whose rows fit the stage (a slice alone always
-        // fits: <= 32 rows)
-        int s1 = s0, tot = 0;
-        while (s1 < S && tot + __popc(s_word[s1]) <= kUpdRows) {
-            s_off[s1 - s0] = tot;
-            tot += __popc(s_word[s1++]);
+    int sfirst = 0;   // first slice with rows at or after `base`
+    // passes of up to kUpdRows rows in slice order (a lane's rows ascend
+    // with the slice, so every lane still accumulates in slice order)
+    for (int base = 0; base < total; base += kUpdRows) {
+        const int nr = min(kUpdRows, total - base);
+        while (s_off[sfirst + 1] <= base) ++sfirst;
+        int slast = sfirst;   // last slice with rows before base + nr
+        while (slast + 1 < S && s_off[slast + 1] < base + nr) ++slast;
+        // row -> slice table of this pass (each slice's rows are one run)
+        for (int sl = sfirst + lane; sl <= slast; sl += 32) {
+            const int r0 = max(s_off[sl], base), r1 = min(s_off[sl + 1], base + nr);
+            for (int i = r0; i < r1; ++i) s_rs[i - base] = (uint8_t)sl;
         }
-        s_off[s1 - s0] = tot;   // every lane writes the same values
         __syncwarp();
         {   // the rows as a flat float4 stream (each slice's rows are
             // consecutive records): coalesced, all loads before the stores
@@ -741,25 +762,25 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const int f = lane + 32 * j;
-                if (f < 3 * tot) {
+                if (f < 3 * nr) {
                     const int i = f / 3;
-                    int sg = 0;
-                    while (s_off[sg + 1] <= i) ++sg;
-                    const int64_t r = (int64_t)s_base[s0 + sg] + (i - s_off[sg]);
+                    const int sl = s_rs[i];
+                    const int64_t r = (int64_t)s_base[sl] + (base + i - s_off[sl]);
                     t[j] = __ldg(src4 + 3 * (size_t)r + (f - 3 * i));
                 }
             }
 #pragma unroll
             for (int j = 0; j < kPer; ++j) {
                 const int f = lane + 32 * j;
-                if (f < 3 * tot) dst4[f] = t[j];
+                if (f < 3 * nr) dst4[f] = t[j];
             }
         }
         __syncwarp();
-        for (int sl = s0; sl < s1; ++sl) {
+        for (int sl = sfirst; sl <= slast; ++sl) {
             const uint32_t word = s_word[sl];
             if (!((word >> lane) & 1u)) continue;
-            const int slot = s_off[sl - s0] + __popc(word & lt);
+            const int slot = s_off[sl] + __popc(word & lt) - base;
+            if (slot < 0 || slot >= nr) continue;
             const float4 t0 = rows[slot][0], t1 = rows[slot][1], t2 = rows[slot][2];
             const float o[11] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w,
                                  t2.x, t2.y, t2.z};
@@ -767,8 +788,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
             for (int j = 0; j < 11; ++j) acc[j] = fmaf(scale, o[j], acc[j]);
             hit = true;
         }
-        __syncwarp();   // rows / s_off reused by the next group
-        s0 = s1;
+        __syncwarp();   // rows / s_rs reused by the next pass
     }
     const int64_t g0 = gw * 32;
     if (adam && aligned && g0 + 32 <= n) {
