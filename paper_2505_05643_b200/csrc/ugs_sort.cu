@@ -227,9 +227,17 @@ radix_scatter_kernel(const uint32_t *__restrict__ keys_in,
 // and a third of the launches of the two-pass LSD sort, and the per-tile
 // ranges fall out of the scan.
 
+// The slice of sort block b: the block stages the slices' first-block
+// indices in shared memory (one parallel load) and binary-searches them,
+// instead of a chain of dependent global loads per block.
 __device__ __forceinline__ int sort_slice_of(const SortSlice *__restrict__ ss, int S, int b) {
+    __shared__ int s_bpre[64];
+    for (int q = threadIdx.x; q < S; q += blockDim.x) s_bpre[q] = ss[q].bpre;
+    __syncthreads();
     int s = 0;
-    while (s + 1 < S && ss[s + 1].bpre <= b) ++s;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)   // last slice whose bpre <= b
+        if (s + step < S && s_bpre[s + step] <= b) s += step;
     return s;
 }
 
@@ -323,10 +331,15 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
 __global__ void slice_ranges_kernel(const SortSlice *__restrict__ ss, int S,
                                     const uint32_t *__restrict__ offs, int n_bins,
                                     int2 *__restrict__ range) {
+    __shared__ int s_tb[64];
+    for (int q = threadIdx.x; q < S; q += blockDim.x) s_tb[q] = ss[q].tile_base;
+    __syncthreads();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n_bins) return;
     int s = 0;
-    while (s + 1 < S && ss[s + 1].tile_base <= b) ++s;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)   // last slice whose tile_base <= b
+        if (s + step < S && s_tb[s + step] <= b) s += step;
     const SortSlice q = ss[s];
     const int t = b - q.tile_base;
     if (q.nb == 0) {
