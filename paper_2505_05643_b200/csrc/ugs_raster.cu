@@ -574,6 +574,14 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
     // instance moments are about each instance's expansion pixel; shift them
     // (float64, exact integer offsets) to the record's reference pixel
     const Rec R = rec[r];
+    // the Gaussian's parameters are loaded before the instance loop, so
+    // their round trip overlaps the partials' instead of following it
+    const int64_t g = rec_gid[r];
+    const float lr[6] = {__ldg(l_raw + 6 * g), __ldg(l_raw + 6 * g + 1),
+                         __ldg(l_raw + 6 * g + 2), __ldg(l_raw + 6 * g + 3),
+                         __ldg(l_raw + 6 * g + 4), __ldg(l_raw + 6 * g + 5)};
+    const float muf[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
+                          __ldg(means + 3 * g + 2)};
     const int wub = __float_as_int(R.r1.x), wvb = __float_as_int(R.r1.y);
     const int iu0 = wub & 0xffff, iu1 = wub >> 16, iv0 = wvb & 0xffff, iv1 = wvb >> 16;
     const int uv = __float_as_int(R.r1.w), ui = uv & 0xffff, vi = uv >> 16;
@@ -596,9 +604,11 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
         Sm[5] += (double)pb.y + ox * sy + oy * sx + ox * oy * s0;
         Sm[6] += (double)pb.z + oy * (2.0 * sy + oy * s0);
     }
-    const int64_t g = rec_gid[r];
-    const Factor f = make_factor(l_raw, g, beta);
-    const double mu[3] = {means[3 * g], means[3 * g + 1], means[3 * g + 2]};
+    // build_L (model.py:101-118): diagonal f32(l^2) + f32(beta)
+    const double L00 = __fadd_rn(__fmul_rn(lr[0], lr[0]), beta);
+    const double L11 = __fadd_rn(__fmul_rn(lr[1], lr[1]), beta);
+    const double L22 = __fadd_rn(__fmul_rn(lr[2], lr[2]), beta);
+    const double mu[3] = {muf[0], muf[1], muf[2]};
     const double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
     const double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
     const double cu = (double)ui, cv = (double)vi;
@@ -618,7 +628,9 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
             Mm[i][j] = S0 * es[i] * es[j] + es[i] * wv[j] + wv[i] * es[j] +
                        Sxx * du[i] * du[j] + Sxy * (du[i] * dv[j] + dv[i] * du[j]) +
                        Syy * dv[i] * dv[j];
-    const double L[3][3] = {{f.L00, 0.0, 0.0}, {f.L10, f.L11, 0.0}, {f.L20, f.L21, f.L22}};
+    const double L[3][3] = {{L00, 0.0, 0.0},
+                            {(double)lr[3], L11, 0.0},
+                            {(double)lr[4], (double)lr[5], L22}};
     double LtV[3];
     for (int k = 0; k < 3; ++k) LtV[k] = L[0][k] * V[0] + L[1][k] * V[1] + L[2][k] * V[2];
     for (int i = 0; i < 3; ++i)
@@ -626,7 +638,6 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
     auto dL = [&](int i, int j) {
         return -(Mm[i][0] * L[0][j] + Mm[i][1] * L[1][j] + Mm[i][2] * L[2][j]);
     };
-    const float *lr = l_raw + 6 * g;
     o[3] = (float)(dL(0, 0) * 2.0 * (double)lr[0]);   // L_jj = l_jj^2 + beta
     o[4] = (float)(dL(1, 1) * 2.0 * (double)lr[1]);
     o[5] = (float)(dL(2, 2) * 2.0 * (double)lr[2]);
