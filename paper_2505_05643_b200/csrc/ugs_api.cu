@@ -150,6 +150,9 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     if (p->ev_ready)
         for (int i = 0; i < kNumStages; ++i)
             for (int j = 0; j < 2; ++j) cudaEventDestroy(p->ev[i][j]);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->side) cudaStreamDestroy(p->side);
     delete p;
     return UGS_OK;
 }

@@ -119,6 +119,10 @@ struct ugs_plan {
     bool slice_sort = false;         // single-pass per-slice bin sort in use
     int64_t hist_n = 0;              // its histogram table entries
     int nblk_sort = 0;               // and sort blocks
+    // side stream for the background-gradient kernels, which overlap the
+    // per-record finalize + update (forked and joined with events)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // optional per-stage CUDA-event timing (ugs_plan_set_timing)
     bool timing = false;
     bool ev_ready = false;
@@ -158,7 +162,7 @@ enum Stage {
     kStageRanges,      // bin ranges
     kStageForward,     // forward_kernel
     kStageBackward,    // backward_kernel
-    kStageFinalize,    // bg_slice + finalize_records (all slices)
+    kStageFinalize,    // finalize_records (the bg kernels run on the side stream)
     kStageUpdate,      // update_gather (accumulate + stats + Adam) + bg_finalize
     kNumStages
 };

@@ -1011,12 +1011,34 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
         c.bg_raw, p.b.partial, p.b.bin_bg);
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
+    // the two background parameters (bg_slice -> bg_finalize) only need the
+    // backward's per-tile partials: they run on a side stream, overlapping
+    // the per-record finalize + update, and are joined before returning
+    if (!pm->side) {
+        UGS_CUDA(cudaStreamCreateWithFlags(&pm->side, cudaStreamNonBlocking));
+        UGS_CUDA(cudaEventCreateWithFlags(&pm->ev_fork, cudaEventDisableTiming));
+        UGS_CUDA(cudaEventCreateWithFlags(&pm->ev_join, cudaEventDisableTiming));
+    }
+    cudaStream_t side = pm->side;
+    UGS_CUDA(cudaEventRecord(pm->ev_fork, st));
+    UGS_CUDA(cudaStreamWaitEvent(side, pm->ev_fork, 0));
+    bg_slice_kernel<<<p.S, 256, 0, side>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
+    UGS_LAUNCH_CHECK("bg_slice_kernel");
+    if (adam) {
+        bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+                                               nullptr, scale, 1, adam->m + kG * c.n,
+                                               adam->v + kG * c.n, adam->k);
+    } else {
+        bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+                                               grad + kG * c.n, scale, 0, nullptr, nullptr,
+                                               AdamConst{});
+    }
+    UGS_LAUNCH_CHECK("bg_finalize_kernel");
+    UGS_CUDA(cudaEventRecord(pm->ev_join, side));
     stage_begin(pm, kStageFinalize, st);
     const CloudMut cm{const_cast<float *>(c.means), const_cast<float *>(c.l_raw),
                       const_cast<float *>(c.intensity_raw),
                       const_cast<float *>(c.opacity_raw)};
-    bg_slice_kernel<<<p.S, 256, 0, st>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
-    UGS_LAUNCH_CHECK("bg_slice_kernel");
     if (p.m_total > 0) {
         const int th = 128;
         finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
@@ -1041,17 +1063,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             adam ? adam->grad_cnt : nullptr, aligned);
         UGS_LAUNCH_CHECK("update_gather_kernel");
     }
-    if (adam) {
-        bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
-                                             nullptr, scale, 1, adam->m + kG * c.n,
-                                             adam->v + kG * c.n, adam->k);
-    } else {
-        bg_finalize_kernel<<<1, 32, 0, st>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
-                                             grad + kG * c.n, scale, 0, nullptr, nullptr,
-                                             AdamConst{});
-    }
-    UGS_LAUNCH_CHECK("bg_finalize_kernel");
     stage_end(pm, kStageUpdate, st);
+    UGS_CUDA(cudaStreamWaitEvent(st, pm->ev_join, 0));   // background joined
     return UGS_OK;
 }
 
