@@ -163,7 +163,7 @@ enum Stage {
     kStageForward,     // forward_kernel
     kStageBackward,    // backward_kernel
     kStageFinalize,    // finalize_records (the bg kernels run on the side stream)
-    kStageUpdate,      // update_gather (accumulate + stats + Adam) + bg_finalize
+    kStageUpdate,      // update_gather (accumulate + stats + Adam)
     kNumStages
 };
 void stage_begin(ugs_plan *p, int stage, cudaStream_t st);
