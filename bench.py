@@ -134,6 +134,8 @@ class ClockSampler:
             self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, bus, str(self.period)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                          text=True)
+            import atexit
+            atexit.register(self._kill)     # never outlive the bench
             first = self.proc.stdout.readline().split()   # blocks until NVML is up
             self.sm_max = float(first[1])
         except Exception as e:  # pragma: no cover - no NVML
@@ -141,6 +143,10 @@ class ClockSampler:
             if self.proc is not None:
                 self.proc.kill()
             self.proc = None
+
+    def _kill(self):
+        if self.proc is not None and self.proc.poll() is None:
+            self.proc.kill()
 
     def mark(self, t0, t1):
         self.window = (t0, t1)
