@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <string>
 
 #include "../../include/ugs.h"
@@ -136,6 +137,21 @@ struct ugs_plan {
 namespace ugs {
 
 void set_error(const std::string &msg);
+
+// Per-device one-time setup (function attributes, constant memory): one
+// process may drive several devices, so "done" is a bit per device.  The
+// setups are idempotent, so two threads racing on one device at most
+// repeat one.
+inline bool device_setup_done(const std::atomic<unsigned long long> &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (mask.load() >> (dev & 63)) & 1ull;
+}
+inline void mark_device_setup(std::atomic<unsigned long long> &mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    mask.fetch_or(1ull << (dev & 63));
+}
 int cuda_fail(cudaError_t e, const char *what);
 
 #define UGS_CUDA(call)                                              \

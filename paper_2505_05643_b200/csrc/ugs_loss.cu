@@ -321,10 +321,10 @@ loss_reduce_kernel(const double *__restrict__ tile_sums, int tiles_per_slice, in
     }
 }
 
-bool g_win_ready = false;
+std::atomic<unsigned long long> g_win_ready{0};
 
 int upload_window() {
-    if (g_win_ready) return UGS_OK;
+    if (device_setup_done(g_win_ready)) return UGS_OK;
     double w[11], sum = 0.0;
     for (int i = 0; i < 11; ++i) {
         const double x = (double)(i - kPad) / 1.5;
@@ -333,7 +333,7 @@ int upload_window() {
     }
     for (int i = 0; i < 11; ++i) w[i] /= sum;
     UGS_CUDA(cudaMemcpyToSymbol(c_win, w, sizeof(w)));
-    g_win_ready = true;
+    mark_device_setup(g_win_ready);
     return UGS_OK;
 }
 
@@ -365,12 +365,12 @@ extern "C" int ugs_loss_ex(const float *num, const float *den, const float *targ
     cudaStream_t st = (cudaStream_t)stream;
     const int tx = (W + kLT - 1) / kLT, ty = (H + kLT - 1) / kLT;
     const size_t smem = sizeof(LossSmem);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    if (!device_setup_done(attr)) {
         UGS_CUDA(cudaFuncSetAttribute(loss_tile_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-        attr = true;
+        mark_device_setup(attr);
     }
     dim3 grid(tx * ty, S);
     double *sums = static_cast<double *>(workspace);

@@ -961,15 +961,15 @@ constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(Layout) +
                             sizeof(float2) * (kTile * kTile + kWarps);
 
 int set_smem_attrs() {
-    static bool done = false;
-    if (done) return UGS_OK;
+    static std::atomic<unsigned long long> done{0};
+    if (device_setup_done(done)) return UGS_OK;
     UGS_CUDA(cudaFuncSetAttribute(forward_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kFwdSmem));
     UGS_CUDA(cudaFuncSetAttribute(backward_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kBwdSmem));
-    done = true;
+    mark_device_setup(done);
     return UGS_OK;
 }
 

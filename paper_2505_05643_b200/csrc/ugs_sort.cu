@@ -421,12 +421,12 @@ int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, int64_t 
     if (bits == 8) {
         slice_scatter_kernel<8><<<nblk, kSortThreads, ssm, st>>>(keys, d_ss, S, hist, vals_out);
     } else {
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (!device_setup_done(attr)) {
             UGS_CUDA(cudaFuncSetAttribute(slice_scatter_kernel<10>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)ssm));
-            attr = true;
+            mark_device_setup(attr);
         }
         slice_scatter_kernel<10><<<nblk, kSortThreads, ssm, st>>>(keys, d_ss, S, hist, vals_out);
     }
