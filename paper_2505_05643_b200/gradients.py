@@ -75,3 +75,64 @@ def backward(cloud, spec: SliceSpec, buffers: RenderBuffers, d_pixels,
     r.backward(cloud, buffers.intensity_num.contiguous(),
                buffers.opacity_sum.contiguous(), dpix, grad, None, 1.0)
     return ParamGradients.from_flat(grad, cloud.n)
+
+
+def grad_check(cloud, spec: SliceSpec, seed: int = 0,
+               h: float | tuple = (1e-3, 3e-3, 1e-2), p: float = 0.9999) -> dict:
+    """Finite-difference check of backward() (ref gradients.py:123-177).
+
+    Same protocol as the reference: scalar loss = sum of squared rendered
+    pixels, central differences at every step in `h` with the best agreement
+    kept per entry, entries with |analytic| + |numeric| <= 1e-8 skipped, and
+    the worst relative error per parameter group returned.  The renders here
+    are the float32 CUDA path (the loss is summed in float64), so agreement
+    is ~1e-3 rather than the reference's float64 ~1e-5; the default steps are
+    larger accordingly.  For small clouds (N <= 50)."""
+    from .rasterizer import rasterize
+    del seed   # deterministic; kept for signature parity
+    steps = (h,) if np.isscalar(h) else tuple(h)
+    base = as_cloud(cloud).copy()
+
+    def render_loss(c):
+        b = rasterize(c, spec, p=p)
+        pix = (b.intensity_num / b.opacity_sum).double()
+        return float(torch.sum(pix * pix)), b, pix
+
+    _, buf, pix = render_loss(base)
+    g = backward(base, spec, buf, (2.0 * pix).float())
+    groups = {"means": g.d_means, "l_raw": g.d_l_raw, "intensity_raw": g.d_intensity_raw,
+              "opacity_raw": g.d_opacity_raw}
+
+    def perturbed(name, idx, delta):
+        """(loss, parameter value actually set): float32 parameters round
+        the step, so the difference quotient uses the realised values."""
+        c = base.copy()
+        if name in ("bg_intensity_raw", "bg_opacity_raw"):
+            val = getattr(base, name) + delta
+            setattr(c, name, val)
+            val = getattr(c, name)
+        else:
+            t = getattr(c, name)
+            t[idx] = t[idx] + delta
+            val = float(t[idx])
+        return render_loss(c)[0], val
+
+    def entry_error(name, idx, ana):
+        best = None
+        for s in steps:
+            (lp, vp), (lm, vm) = perturbed(name, idx, s), perturbed(name, idx, -s)
+            num = (lp - lm) / (vp - vm)
+            den = abs(ana) + abs(num)
+            err = abs(ana - num) / den if den > 1e-8 else 0.0
+            best = err if best is None else min(best, err)
+        return best
+
+    report = {}
+    for name, ga in groups.items():
+        ga = ga.detach().cpu().numpy()
+        report[name] = max((entry_error(name, idx, float(ga[idx]))
+                            for idx in np.ndindex(ga.shape)), default=0.0)
+    report["bg_intensity_raw"] = entry_error("bg_intensity_raw", None,
+                                             float(g.d_bg_intensity_raw))
+    report["bg_opacity_raw"] = entry_error("bg_opacity_raw", None, float(g.d_bg_opacity_raw))
+    return report
