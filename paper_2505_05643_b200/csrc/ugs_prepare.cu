@@ -186,18 +186,28 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) { carry_x = 0; carry_y = 0; }
     __syncthreads();
-    for (int base = 0; base < nblk; base += 1024) {
-        const int i = base + threadIdx.x;
-        uint2 v = i < nblk ? row[i] : make_uint2(0, 0);
-        unsigned long long x = v.x, y = v.y;
-        // inclusive warp scan
+    // passes of 4 consecutive entries per thread: one block scan per 4096
+    // entries (one pass for up to 1M Gaussians) instead of one per 1024
+    constexpr int kPer = 4;
+    for (int base = 0; base < nblk; base += kPer * 1024) {
+        const int i0 = base + kPer * threadIdx.x;
+        uint2 v[kPer];
+        unsigned long long x = 0, y = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            v[k] = i0 + k < nblk ? row[i0 + k] : make_uint2(0, 0);
+            x += v[k].x;
+            y += v[k].y;
+        }
+        // inclusive warp scan of the thread totals
+        unsigned long long ix = x, iy = y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long tx = __shfl_up_sync(0xffffffffu, x, o);
-            unsigned long long ty = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) { x += tx; y += ty; }
+            unsigned long long tx = __shfl_up_sync(0xffffffffu, ix, o);
+            unsigned long long ty = __shfl_up_sync(0xffffffffu, iy, o);
+            if (lane >= o) { ix += tx; iy += ty; }
         }
-        if (lane == 31) { wx[warp] = x; wy[warp] = y; }
+        if (lane == 31) { wx[warp] = ix; wy[warp] = iy; }
         __syncthreads();
         if (warp == 0) {
             unsigned long long a = wx[lane], b = wy[lane];
@@ -211,9 +221,14 @@ prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
             wy[lane] = b;
         }
         __syncthreads();
-        unsigned long long px = (warp ? wx[warp - 1] : 0ull) + x - v.x + carry_x;
-        unsigned long long py = (warp ? wy[warp - 1] : 0ull) + y - v.y + carry_y;
-        if (i < nblk) row[i] = make_uint2((unsigned)px, (unsigned)py);
+        unsigned long long px = (warp ? wx[warp - 1] : 0ull) + ix - x + carry_x;
+        unsigned long long py = (warp ? wy[warp - 1] : 0ull) + iy - y + carry_y;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            if (i0 + k < nblk) row[i0 + k] = make_uint2((unsigned)px, (unsigned)py);
+            px += v[k].x;
+            py += v[k].y;
+        }
         __syncthreads();
         if (threadIdx.x == 0) { carry_x += wx[31]; carry_y += wy[31]; }
         __syncthreads();
