@@ -543,14 +543,14 @@ def run_ours(a):
         torch.cuda.empty_cache()
         # training batch 48 (the fastest of 8..64 to 0.99 on C2, measured:
         # 8: 28.6 s, 16: 11.9 s, 32: ~5 s, 48: 4.0 s, 64: 5.2 s)
-        r = time_to_ssim.run(budget=a.tts_budget, batch=48, eval_every=20,
+        r = time_to_ssim.run(budget=a.tts_budget, batch=48, eval_every=10,
                              log=lambda m: None)
         line["time_to_ssim"] = {k: r[k] for k in ("target", "reached_s", "best_ssim",
                                                   "iterations", "slices_trained")}
         line["time_to_ssim"]["config"] = ("C2: 200k Gaussians, 160^3 shells phantom, "
                                           "256x256 @0.375 mm, 2048 train / 64 held-out "
                                           "random-pose slices, batch 48, held-out SSIM "
-                                          "every 20 steps (not timed), 1 GPU")
+                                          "every 10 steps (not timed), 1 GPU")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
