@@ -24,7 +24,10 @@
  *   - every pointer marked (dev) is CUDA device memory, (host) host memory;
  *   - work is enqueued on the given cudaStream_t (passed as void*), nothing
  *     synchronizes except ugs_bin (one device->host read of the per-slice
- *     counts, needed to size the tile lists);
+ *     counts, needed to size the tile lists); ugs_backward /
+ *     ugs_backward_adam also run the two background-parameter kernels on the
+ *     plan's own side stream, forked from and joined back into the caller's
+ *     stream with events, so the call stays stream-ordered;
  *   - a ugs_plan owns the binning buffers of one batch; distinct plans may
  *     be used concurrently from different threads/streams;
  *   - no torch types: plain pointers and sizes, so ctypes / cffi / JNI /
