@@ -23,7 +23,7 @@ constexpr int kLT = 32;              // output tile
 constexpr int kPad = 5;              // window radius
 constexpr int kF = kLT + 2 * kPad;   // 42: valid points needed
 constexpr int kI = kF + 2 * kPad;    // 52: input points needed
-constexpr int kLossThreads = 384;    // 12 warps, one 147 KB CTA per SM
+constexpr int kLossThreads = 384;    // 12 warps, two 109 KB CTAs per SM
 
 __constant__ double c_win[11];
 
@@ -40,13 +40,19 @@ struct LossSmem {
     float Y[kI][kI];                  // target
     union {
         double h[5][kI][kF];          // horizontal moment pass
-        double ha[3][kF][kLT];        // horizontal adjoint pass
+        struct {                      // after the vertical pass (h dead):
+            double F[3][kF][kF];      //   A, B, C on the valid grid
+            double ha[3][kF][kLT];    //   horizontal adjoint pass
+        } a;
     } u;
-    double F[3][kF][kF];              // A, B, C on the valid grid
     double red[2][kLossThreads / 32];
 };
+// the vertical pass has at most one work item per thread, so its A, B, C
+// are held in registers across the barrier that retires h, and F reuses h's
+// storage: 109 KB per CTA, two CTAs per SM
+static_assert(kF * (kF / kHB) <= kLossThreads, "one vertical item per thread");
 
-__global__ void __launch_bounds__(kLossThreads, 1)
+__global__ void __launch_bounds__(kLossThreads, 2)
 loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                  const float *__restrict__ target, const int64_t *__restrict__ target_index,
                  int H, int W, double lam,
@@ -128,8 +134,10 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
         }
         __syncthreads();
         // vertical pass -> moments at valid point (i, j) = (p0-10+r, q0-10+c)
-        for (int it = tid; it < kF * kCh; it += kLossThreads) {
-            const int c = it % kF, r0 = (it / kF) * kHB;
+        double FA[kHB], FB[kHB], FC[kHB];
+        const int vit = tid;
+        if (vit < kF * kCh) {
+            const int c = vit % kF, r0 = (vit / kF) * kHB;
             double m[5][kHB];
 #pragma unroll
             for (int f = 0; f < 5; ++f)
@@ -170,9 +178,19 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                     C = d_sxy;
                     if (r >= 2 * kPad && c >= 2 * kPad) ssim_sum += sv;   // owned point
                 }
-                sm.F[0][r][c] = A;
-                sm.F[1][r][c] = B;
-                sm.F[2][r][c] = C;
+                FA[o] = A;
+                FB[o] = B;
+                FC[o] = C;
+            }
+        }
+        __syncthreads();   // every read of h is done: F may overwrite it
+        if (vit < kF * kCh) {
+            const int c = vit % kF, r0 = (vit / kF) * kHB;
+#pragma unroll
+            for (int o = 0; o < kHB; ++o) {
+                sm.u.a.F[0][r0 + o][c] = FA[o];
+                sm.u.a.F[1][r0 + o][c] = FB[o];
+                sm.u.a.F[2][r0 + o][c] = FC[o];
             }
         }
         __syncthreads();
@@ -189,7 +207,7 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
             for (int kk = 0; kk < kAB + 10; ++kk) {
                 double v[3];
 #pragma unroll
-                for (int f = 0; f < 3; ++f) v[f] = sm.F[f][r][q0r + kk];
+                for (int f = 0; f < 3; ++f) v[f] = sm.u.a.F[f][r][q0r + kk];
 #pragma unroll
                 for (int o = 0; o < kAB; ++o) {
                     const int b = kk - o;
@@ -201,7 +219,7 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
 #pragma unroll
             for (int f = 0; f < 3; ++f)
 #pragma unroll
-                for (int o = 0; o < kAB; ++o) sm.u.ha[f][r][q0r + o] = a[f][o];
+                for (int o = 0; o < kAB; ++o) sm.u.a.ha[f][r][q0r + o] = a[f][o];
         }
         __syncthreads();
     }
@@ -216,8 +234,8 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
         if (ssim) {
 #pragma unroll
             for (int kk = 0; kk < kAB + 10; ++kk) {
-                const double vA = sm.u.ha[0][pr0 + kk][q], vB = sm.u.ha[1][pr0 + kk][q],
-                             vC = sm.u.ha[2][pr0 + kk][q];
+                const double vA = sm.u.a.ha[0][pr0 + kk][q], vB = sm.u.a.ha[1][pr0 + kk][q],
+                             vC = sm.u.a.ha[2][pr0 + kk][q];
 #pragma unroll
                 for (int o = 0; o < kAB; ++o) {
                     const int a = kk - o;
