@@ -291,7 +291,7 @@ __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
 // plane-conditioned exponent (float64, ugs_geometry.cuh PlaneForm) and the
 // record's tile instances in row-major tile order, each with its exact
 // re-expansion.
-__global__ void __launch_bounds__(kBuildThreads)
+__global__ void __launch_bounds__(kBuildThreads, 8)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
                      const float *__restrict__ intensity_raw,
                      const float *__restrict__ opacity_raw, int64_t n, float beta,

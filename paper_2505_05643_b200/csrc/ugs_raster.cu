@@ -651,7 +651,7 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
 
 // One thread per record: its raw-parameter gradient (float64 chain) into
 // rgrad[r][0..10] (AoS-12 row), for the staged update below.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 8)
 finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                         const int32_t *__restrict__ rec_inst,
                         const float *__restrict__ partial, int64_t m_total,
