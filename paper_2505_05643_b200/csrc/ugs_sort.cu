@@ -268,7 +268,7 @@ slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict
 }
 
 template <int kBits>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 6)
 slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss,
                      int S, const uint32_t *__restrict__ offs, uint32_t *__restrict__ vals_out) {
     constexpr int kWarpsS = kSortThreads / 32;
