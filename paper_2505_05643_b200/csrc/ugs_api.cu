@@ -292,16 +292,30 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     }
     const size_t kneed = (size_t)k_total + 1;
     if (kneed > b.inst_cap || !b.idata) {
-        void *olds[] = {b.idata, b.keys, b.vals, b.keys2, b.vals2, b.partial};
-        for (void *q : olds)
-            if (q) cudaFree(q);
-        b.inst_cap = kneed + kneed / 4 + 64;
-        UGS_CUDA(cudaMalloc(&b.idata, sizeof(Inst) * b.inst_cap));
-        UGS_CUDA(cudaMalloc(&b.keys, sizeof(uint32_t) * b.inst_cap));
-        UGS_CUDA(cudaMalloc(&b.vals, sizeof(uint32_t) * b.inst_cap));
-        UGS_CUDA(cudaMalloc(&b.keys2, sizeof(uint32_t) * b.inst_cap));
-        UGS_CUDA(cudaMalloc(&b.vals2, sizeof(uint32_t) * b.inst_cap));
-        UGS_CUDA(cudaMalloc(&b.partial, sizeof(float) * 8 * b.inst_cap));
+        // all-or-nothing: every pointer is nulled when freed and the capacity
+        // is published only after every allocation succeeded, so a failed
+        // (OOM) grow leaves no dangling pointer and no stale capacity
+        void **bufs[] = {(void **)&b.idata, (void **)&b.keys, (void **)&b.vals,
+                         (void **)&b.keys2, (void **)&b.vals2, (void **)&b.partial};
+        const size_t elem[] = {sizeof(Inst), sizeof(uint32_t), sizeof(uint32_t),
+                               sizeof(uint32_t), sizeof(uint32_t), sizeof(float) * kPartial};
+        for (void **q : bufs) {
+            if (*q) cudaFree(*q);
+            *q = nullptr;
+        }
+        b.inst_cap = 0;
+        const size_t cap = kneed + kneed / 4 + 64;
+        for (int i = 0; i < 6; ++i) {
+            cudaError_t e = cudaMalloc(bufs[i], elem[i] * cap);
+            if (e != cudaSuccess) {
+                for (void **q : bufs) {
+                    if (*q) cudaFree(*q);
+                    *q = nullptr;
+                }
+                return cuda_fail(e, "alloc tile instances");
+            }
+        }
+        b.inst_cap = cap;
     }
     // bin sort plan: single-pass per-slice counting sort when every slice has
     // <= kSliceSortMaxTiles tiles and the tables fit the scan, else LSD radix
@@ -318,9 +332,19 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     if (b.bin_cap < (size_t)n_bins || !b.bin_range) {
         if (b.bin_range) cudaFree(b.bin_range);
         if (b.bin_bg) cudaFree(b.bin_bg);
-        b.bin_cap = (size_t)n_bins + 64;
-        UGS_CUDA(cudaMalloc(&b.bin_range, sizeof(int2) * b.bin_cap));
-        UGS_CUDA(cudaMalloc(&b.bin_bg, sizeof(float2) * b.bin_cap));
+        b.bin_range = nullptr;
+        b.bin_bg = nullptr;
+        b.bin_cap = 0;
+        const size_t cap = (size_t)n_bins + 64;
+        cudaError_t e = cudaMalloc(&b.bin_range, sizeof(int2) * cap);
+        if (e == cudaSuccess) e = cudaMalloc(&b.bin_bg, sizeof(float2) * cap);
+        if (e != cudaSuccess) {
+            if (b.bin_range) cudaFree(b.bin_range);
+            b.bin_range = nullptr;
+            b.bin_bg = nullptr;
+            return cuda_fail(e, "alloc bins");
+        }
+        b.bin_cap = cap;
     }
     stage_begin(p, kStageEmit, st);
     if (c->n > 0 && m_total > 0) {

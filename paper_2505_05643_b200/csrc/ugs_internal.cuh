@@ -19,6 +19,7 @@ constexpr int kRadix = 1 << kRadixBits;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kPartial = 8;          // floats per backward tile-instance partial
 
 // Per accepted (slice, Gaussian) record: two float4 = 32 B.
 //   r0 = (A, B2, C, color): quadratic part of the plane-conditioned exponent

@@ -78,6 +78,14 @@ class GaussianCloud:
                                         float(bg_opacity_raw)],
                                        dtype=torch.float64, device=dev)
         self.beta = float(beta)
+        # bumped by every library call that rewrites the parameters through
+        # raw pointers (Adam, the fused step, the peer update): those writes
+        # do not bump the tensors' torch _version, and the renderer's cached
+        # binning / records must not be reused across them
+        self.mutations = 0
+
+    def mark_mutated(self) -> None:
+        self.mutations += 1
 
     # --- reference-compatible accessors ----------------------------------
     @property

@@ -34,6 +34,14 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _device_index(device) -> int:
+    """An index-less 'cuda' means the current device (torch semantics)."""
+    d = torch.device(device) if device is not None else None
+    if d is None or d.index is None:
+        return torch.cuda.current_device()
+    return d.index
+
+
 class Renderer:
     """One libugs plan: the binning state of one batch of slices."""
 
@@ -49,6 +57,7 @@ class Renderer:
         self.p_mass = DEFAULT_P_MASS
         self._cloud_key = None
         self._slices = None
+        self.device_index = None
 
     def __del__(self):
         try:
@@ -61,11 +70,30 @@ class Renderer:
     @staticmethod
     def cloud_key(cloud: GaussianCloud):
         return (cloud.means.data_ptr(), cloud.l_raw.data_ptr(), cloud.n,
-                cloud.means._version, cloud.l_raw._version)
+                cloud.means._version, cloud.l_raw._version,
+                cloud.intensity_raw._version, cloud.opacity_raw._version,
+                getattr(cloud, "mutations", 0))
+
+    def _guard(self, device):
+        """Library calls run on the cloud's device (plan buffers, launches
+        and the current stream all follow the current device); a plan is
+        bound to the device of its first use."""
+        idx = _device_index(device)
+        if self.device_index is None:
+            self.device_index = idx
+        elif idx != self.device_index:
+            raise InvalidParameterError(
+                f"this Renderer's plan lives on cuda:{self.device_index}, "
+                f"the cloud on cuda:{idx}")
+        return torch.cuda.device(idx)
 
     def bin(self, cloud: GaussianCloud, specs, p: float = DEFAULT_P_MASS,
             slices=None):
         """Phase 1 + tile binning for a batch of slices (one host sync)."""
+        with self._guard(cloud.device):
+            return self._bin(cloud, specs, p, slices)
+
+    def _bin(self, cloud, specs, p, slices):
         S = len(specs)
         if S < 1 or S > 64:
             raise InvalidParameterError("a batch holds 1..64 slices")
@@ -91,20 +119,26 @@ class Renderer:
 
     def forward(self, cloud: GaussianCloud, num: torch.Tensor, den: torch.Tensor):
         cs = cloud.c_struct()
-        _lib.check(_lib.lib().ugs_forward(self._plan, ctypes.byref(cs),
-                                          num.data_ptr(), den.data_ptr(),
-                                          _stream()), "ugs_forward")
+        with self._guard(cloud.device):
+            _lib.check(_lib.lib().ugs_forward(self._plan, ctypes.byref(cs),
+                                              num.data_ptr(), den.data_ptr(),
+                                              _stream()), "ugs_forward")
 
     def backward(self, cloud: GaussianCloud, num, den, dpix, grad, touched=None,
                  scale: float = 1.0):
         cs = cloud.c_struct()
-        _lib.check(_lib.lib().ugs_backward(
-            self._plan, ctypes.byref(cs), num.data_ptr(), den.data_ptr(),
-            dpix.data_ptr(), grad.data_ptr(), _lib.ptr(touched), float(scale),
-            _stream()), "ugs_backward")
+        with self._guard(cloud.device):
+            _lib.check(_lib.lib().ugs_backward(
+                self._plan, ctypes.byref(cs), num.data_ptr(), den.data_ptr(),
+                dpix.data_ptr(), grad.data_ptr(), _lib.ptr(touched), float(scale),
+                _stream()), "ugs_backward")
 
     def accepted(self, device, windows: bool = False):
         """(accepted int64 per slice list, windows (M,4) int64 or None)."""
+        with self._guard(device):
+            return self._accepted(device, windows)
+
+    def _accepted(self, device, windows):
         M = int(self.m.sum())
         acc = torch.empty(max(M, 1), dtype=torch.int32, device=device)
         win = torch.empty((max(M, 1), 4), dtype=torch.int32, device=device) \
@@ -120,6 +154,10 @@ class Renderer:
 
     def bins(self, device):
         """(bin_range (n_bins,2) int32, sorted Gaussian ids (K,) int32)."""
+        with self._guard(device):
+            return self._bins(device)
+
+    def _bins(self, device):
         nb = ctypes.c_int32()
         kt = ctypes.c_int64()
         L = _lib.lib()
@@ -161,8 +199,7 @@ _DEFAULT: dict = {}
 
 
 def default_renderer(device=None) -> Renderer:
-    dev = torch.cuda.current_device() if device is None else \
-        torch.device(device).index or 0
+    dev = _device_index(device)
     r = _DEFAULT.get(dev)
     if r is None:
         r = _DEFAULT[dev] = Renderer()

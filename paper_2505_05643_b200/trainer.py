@@ -88,8 +88,6 @@ class TrainConfig:
         for name in ("lr_general", "lr_means_start", "lr_means_final"):
             if not getattr(self, name) > 0:
                 raise InvalidParameterError(f"{name} must be > 0")
-        if self.batch < 1 or self.batch > 64:
-            raise InvalidParameterError("batch must be in [1, 64]")
 
 
 # AoS-12 rows (include/ugs.h): column ranges of each group, plus background
@@ -183,6 +181,7 @@ def _adam_flat(state: AdamState, cloud: GaussianCloud, grad_flat: torch.Tensor,
         state.v_flat.data_ptr(), cloud.n, state.t, _lr_array(lrs), state.beta1,
         state.beta2, state.eps, 1 if zero_grad else 0, _lib.ptr(touched),
         _lib.ptr(gsum), _lib.ptr(gcnt), _stream()), "ugs_adam_step")
+    cloud.mark_mutated()
 
 
 def adam_step(state: AdamState, cloud: GaussianCloud, grads: ParamGradients,
@@ -437,10 +436,22 @@ class TrainEngine:
         self.arena = None
         self.renderer = Renderer()
         self.specs = list(specs)
-        self.targets = targets        # (n_slices, H, W) float32 on the device
-        h, w = self.targets.shape[-2:]
-        if any(s.height != h or s.width != w for s in self.specs):
-            raise InvalidParameterError("training slices must share width/height")
+        # (n_slices, H, W) float32 on the device, or -- slices of different
+        # sizes, which the reference also trains on (trainer.py:380-390) -- a
+        # list of (H_i, W_i) tensors; ugs_bin / forward / backward take
+        # per-slice sizes (pix_base offsets), only the loss runs per size
+        self.targets = targets
+        self.sizes = [(int(s.height), int(s.width)) for s in self.specs]
+        self.uniform = len(set(self.sizes)) <= 1 and isinstance(targets, torch.Tensor)
+        if self.uniform:
+            h, w = self.targets.shape[-2:]
+            if any(sz != (h, w) for sz in self.sizes):
+                raise InvalidParameterError("targets do not match the slice sizes")
+        else:
+            if len(targets) != len(self.specs) or any(
+                    tuple(t.shape[-2:]) != sz for t, sz in zip(targets, self.sizes)):
+                raise InvalidParameterError("targets do not match the slice sizes")
+            h, w = self.sizes[0]
         self.h, self.w = int(h), int(w)
         self.world_size, self.rank, self.pg = world_size, rank, process_group
         # per-slice constant structs, built once (host), copied per batch
@@ -526,6 +537,7 @@ class TrainEngine:
         _lib.check(_lib.lib().ugs_peer_update(
             self.arena.views, self.world_size, self.rank, self.cloud.n, lo, hi, st.t,
             _lr_array(lrs), st.beta1, st.beta2, st.eps, 1, _stream()), "ugs_peer_update")
+        self.cloud.mark_mutated()
         self.barrier()            # every parameter row is stored everywhere
 
     def _alloc_stats(self):
@@ -538,9 +550,12 @@ class TrainEngine:
         B = len(idx)
         arr = (_lib.Slice * B)()
         sz = ctypes.sizeof(_lib.Slice)
+        off = 0
         for j, i in enumerate(idx):
             ctypes.memmove(ctypes.byref(arr, j * sz), ctypes.byref(self._consts, int(i) * sz), sz)
-            arr[j].pix_base = j * self.h * self.w
+            arr[j].pix_base = off
+            h, w = self.sizes[int(i)]
+            off += h * w
         return arr
 
     # optional CUDA-event instrumentation of the non-library parts of a step
@@ -570,6 +585,11 @@ class TrainEngine:
         """bin + forward + loss for the slices `idx` (this rank's batch)."""
         cfg = self.config
         B = len(idx)
+        if B > 64:
+            raise InvalidParameterError("the GPU engine takes at most 64 slices per "
+                                        "step and rank (config.batch <= 64)")
+        if not self.uniform and targets_batch is None:
+            return self._forward_loss_mixed(idx)
         if targets_batch is None:
             # slice ids via pinned memory: an async copy (a pageable one would
             # block the host until the stream drains)
@@ -595,16 +615,56 @@ class TrainEngine:
         self._mark("loss1")
         return num, den, None, tgt, lv, dpix
 
+    def _forward_loss_mixed(self, idx):
+        """A batch whose slices differ in size: one flat (num, den, d_pixels)
+        buffer at the slices' pix_base offsets; the loss runs per slice."""
+        cfg = self.config
+        dev = self.cloud.device
+        structs = self.batch_structs(idx)
+        self.renderer.bin(self.cloud, [self.specs[i] for i in idx], cfg.p_mass, structs)
+        self.pairs_total += int(self.renderer.pairs.sum())
+        offs = [int(structs[j].pix_base) for j in range(len(idx))]
+        sizes = [self.sizes[int(i)] for i in idx]
+        total = offs[-1] + sizes[-1][0] * sizes[-1][1]
+        num = torch.empty(total, dtype=torch.float32, device=dev)
+        den = torch.empty_like(num)
+        dpix = torch.empty_like(num)
+        self.renderer.forward(self.cloud, num, den)
+        self._mark("loss0")
+        lvs = []
+        for j, i in enumerate(idx):
+            (h, w), o = sizes[j], offs[j]
+            view = (1, h, w)
+            lv, dp, _ = fused_loss(num[o:o + h * w].view(view), den[o:o + h * w].view(view),
+                                   self.targets[int(i)].view(view), cfg.ssim_loss_weight,
+                                   cfg.l2_loss)
+            dpix[o:o + h * w].copy_(dp.view(-1))
+            lvs.append(lv)
+        lv = torch.cat(lvs)
+        self.loss_mean = lv.mean()
+        self._mark("loss1")
+        h0, w0 = sizes[0]
+        first = (1, h0, w0)
+        return (num[:h0 * w0].view(first), den[:h0 * w0].view(first), None,
+                self.targets[int(idx[0])].view(first), lv, dpix, num, den)
+
     def step(self, idx, it: int, check_finite: bool = True, targets_batch=None):
         """One full training step; returns the mean loss (python float) when
-        check_finite, else the device tensor."""
+        check_finite, else the device tensor.  Runs on the cloud's device."""
+        with torch.cuda.device(self.cloud.device):
+            return self._step(idx, it, check_finite, targets_batch)
+
+    def _step(self, idx, it, check_finite, targets_batch):
         cfg = self.config
-        num, den, pred, tgt, lv, dpix = self.forward_loss(idx, targets_batch)
+        out = self.forward_loss(idx, targets_batch)
+        num, den, pred, tgt, lv, dpix = out[:6]
+        self.last_num, self.last_den, self.last_tgt = num, den, tgt
+        if len(out) > 6:
+            num, den = out[6], out[7]     # flat buffers of a mixed-size batch
         loss_t = self.loss_mean
         if self.world_size > 1:
             torch.distributed.all_reduce(loss_t, group=self.pg)
             loss_t = loss_t / self.world_size
-        self.last_num, self.last_den, self.last_tgt = num, den, tgt
         loss_val = None
         if check_finite:
             loss_val = float(loss_t.item())
@@ -628,6 +688,7 @@ class TrainEngine:
                 st.v_flat.data_ptr(), st.t, _lr_array(lrs), st.beta1, st.beta2, st.eps,
                 self.grad_sum.data_ptr(), self.grad_cnt.data_ptr(), _stream()),
                 "ugs_backward_adam")
+            self.cloud.mark_mutated()
             self._mark("backward_adam1")
             return loss_val if check_finite else loss_t
         if self.peer:
@@ -714,8 +775,14 @@ def train(dataset: SliceDataset, config: TrainConfig, bounds=None,
     else:
         cloud = init_cloud(config, bounds, device)
     specs = [s.spec for s in train_slices]
-    targets = torch.as_tensor(np.stack([np.asarray(s.pixels, np.float32)
-                                        for s in train_slices]), device=cloud.device)
+    if config.batch > 64:
+        raise InvalidParameterError("the GPU engine takes at most 64 slices per step "
+                                    "and rank: config.batch must be <= 64")
+    pix = [np.asarray(s.pixels, np.float32) for s in train_slices]
+    if len({p.shape for p in pix}) == 1:
+        targets = torch.as_tensor(np.stack(pix), device=cloud.device)
+    else:   # slices of different sizes (the reference trains on any slice)
+        targets = [torch.as_tensor(p, device=cloud.device) for p in pix]
     eng = TrainEngine(cloud, config, specs, targets, world, rank, pg)
     scene_extent = float(np.linalg.norm(bounds[1] - bounds[0]))
     max_total = 2 * config.n_gaussians
