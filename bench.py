@@ -336,6 +336,23 @@ def run_ours(a):
             raise RuntimeError(f"non-finite loss at step {i}")
         return v
 
+    pending = [None]      # (step number, device loss) of the last launched step
+
+    def flush_loss():
+        """Queue the D2H copy of the last launched step's loss.  Called once
+        that step is final: the engine settles a step (harvests its sync-free
+        binning counts, re-issues it if it overflowed the plan) at the start
+        of the next one, or in settle()."""
+        if pending[0] is None:
+            return
+        i, lt = pending[0]
+        k = i % len(loss_ev)
+        loss_host[k].copy_(lt, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        loss_ev[k] = ev
+        pending[0] = None
+
     def step(targets_batch=None, idx=None):
         it[0] += 1
         c = eng.cloud
@@ -344,12 +361,15 @@ def run_ours(a):
                              init)
         lt = eng.step(idx if idx is not None else next_batch(), it[0],
                       targets_batch=targets_batch, check_finite=False)
-        k = it[0] % len(loss_ev)
-        loss_host[k].copy_(lt, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        loss_ev[k] = ev
-        return read_loss(it[0] - 1)       # the previous step's loss
+        flush_loss()                      # the previous step (final now)
+        pending[0] = (it[0], lt)
+        return read_loss(it[0] - 2)       # two back: never waits on a running step
+
+    def finish():
+        eng.settle()
+        flush_loss()
+        read_loss(it[0] - 1)
+        read_loss(it[0])
 
     def barrier():
         if world > 1:
@@ -366,6 +386,7 @@ def run_ours(a):
     sampler.start()
     for _ in range(a.warmup):
         step()
+    finish()
     # ---- timed region: device-resident inputs, no instrumentation ----
     eng.pairs_total = 0
     barrier()
@@ -377,7 +398,7 @@ def run_ours(a):
     e0.record()
     for _ in range(a.steps):
         step()
-    read_loss(it[0])
+    finish()
     e1.record()
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -398,7 +419,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     for _ in range(a.steps):
         step()
-    read_loss(it[0])
+    finish()
     torch.cuda.synchronize()
     stage = eng.renderer.timings()
     extra = eng.event_times()
@@ -434,10 +455,14 @@ def run_ours(a):
                 st_ev[b] = torch.cuda.Event()
                 st_ev[b].record(copy_stream)
             torch.cuda.current_stream().wait_event(st_ev[b])
-            step(targets_batch=dev_t[b], idx=idx)     # + D2H read of the previous loss
-            used_ev[b] = torch.cuda.Event()
-            used_ev[b].record()
-        read_loss(it[0])                           # ... and of the last one
+            r0 = eng.reissued
+            step(targets_batch=dev_t[b], idx=idx)     # + D2H read of an earlier loss
+            # buffer b is read by this step -- and buffer 1-b again if the
+            # previous step was re-issued inside this call (binning overflow)
+            for q in ((b, 1 - b) if eng.reissued != r0 else (b,)):
+                used_ev[q] = torch.cuda.Event()
+                used_ev[q].record()
+        finish()                                   # ... and of the last one
         f1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0

@@ -24,7 +24,8 @@
  *   - every pointer marked (dev) is CUDA device memory, (host) host memory;
  *   - work is enqueued on the given cudaStream_t (passed as void*), nothing
  *     synchronizes except ugs_bin (one device->host read of the per-slice
- *     counts, needed to size the tile lists); ugs_backward /
+ *     counts, needed to size the tile lists; ugs_bin_async avoids it) and
+ *     ugs_plan_poll (waits for one event); ugs_backward /
  *     ugs_backward_adam also run the two background-parameter kernels on the
  *     plan's own side stream, forked from and joined back into the caller's
  *     stream with events, so the call stays stream-ordered;
@@ -107,6 +108,26 @@ UGS_API int ugs_plan_destroy(ugs_plan *plan);
  * Synchronizes `stream` once. */
 UGS_API int ugs_bin(ugs_plan *plan, const ugs_cloud *cloud, ugs_slice *slices, int S,
             void *stream, int64_t *m_out, int64_t *k_out, int64_t *p_out);
+
+/* ugs_bin without the host synchronisation (no reference counterpart: the
+ * reference sizes everything on the host).  The record / instance / sort
+ * buffers are used at the capacities the plan already has (an earlier
+ * ugs_bin sized them, with headroom; on a plan never binned synchronously,
+ * or with more than 1024 tiles per slice, this call IS ugs_bin).  The device
+ * compares the batch's totals with those capacities: if the batch does not
+ * fit, every later kernel of this plan (forward, backward, the fused update)
+ * returns at entry, leaving parameters and moments untouched.  The counts
+ * arrive with ugs_plan_poll. */
+UGS_API int ugs_bin_async(ugs_plan *plan, const ugs_cloud *cloud, ugs_slice *slices,
+                          int S, void *stream);
+
+/* Counts of the plan's last ugs_bin / ugs_bin_async (waits for that call's
+ * count stage only -- an event, not the stream).  *overflowed = 1 if that
+ * sync-free batch did not fit: its forward / backward / update did nothing,
+ * the plan has now grown to fit it, and the caller re-issues the step.
+ * Any output pointer may be NULL. */
+UGS_API int ugs_plan_poll(ugs_plan *plan, int *overflowed, int64_t *m_out, int64_t *k_out,
+                          int64_t *p_out);
 
 /* Accepted Gaussian indices (ascending per slice, slices concatenated) and
  * their inclusive pixel windows (iu0,iu1,iv0,iv1) -- the reference's

@@ -59,6 +59,11 @@ EXPORTS = {
     "ugs_bin": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), ctypes.POINTER(Slice),
                                ctypes.c_int, c_vp, ctypes.POINTER(c_i64),
                                ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "ugs_bin_async": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), ctypes.POINTER(Slice),
+                                     ctypes.c_int, c_vp]),
+    "ugs_plan_poll": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
+                                     ctypes.POINTER(c_i64)]),
     "ugs_export_accepted": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "ugs_export_bins": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_i32),
                                        ctypes.POINTER(c_i64), c_vp]),

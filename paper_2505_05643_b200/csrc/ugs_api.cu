@@ -4,6 +4,7 @@
 // its API layer for the same conditions (gradients.py:43-52).
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <vector>
 
@@ -75,10 +76,15 @@ int ensure(T **ptr, size_t *cap, size_t need, const char *what) {
 
 int ensure_host(ugs_plan *p, int S) {
     if (!p->h_plan) {
-        cudaError_t e = cudaMallocHost((void **)&p->h_plan, sizeof(unsigned long long) * kPlanWords);
+        cudaError_t e = cudaMallocHost((void **)&p->h_plan,
+                                       sizeof(unsigned long long) * kPlanWords * kRing);
         if (e != cudaSuccess) { p->h_plan = nullptr; return cuda_fail(e, "alloc h_plan"); }
-        e = cudaMallocHost((void **)&p->h_slices, sizeof(ugs_slice) * 64);
+        e = cudaMallocHost((void **)&p->h_slices, sizeof(ugs_slice) * 64 * kRing);
         if (e != cudaSuccess) { p->h_slices = nullptr; return cuda_fail(e, "alloc h_slices"); }
+        for (int i = 0; i < kRing; ++i) {
+            UGS_CUDA(cudaEventCreateWithFlags(&p->ev_slices[i], cudaEventDisableTiming));
+            UGS_CUDA(cudaEventCreateWithFlags(&p->ev_counts[i], cudaEventDisableTiming));
+        }
     }
     if (S <= p->h_cap) return UGS_OK;
     delete[] p->h_slice_base;
@@ -146,6 +152,10 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     delete[] p->h_tile_base;
     delete[] p->h_ntile;
     if (p->h_plan) cudaFreeHost(p->h_plan);
+    for (int i = 0; i < kRing; ++i) {
+        if (p->ev_slices[i]) cudaEventDestroy(p->ev_slices[i]);
+        if (p->ev_counts[i]) cudaEventDestroy(p->ev_counts[i]);
+    }
     if (p->h_slices) cudaFreeHost(p->h_slices);
     if (p->ev_ready)
         for (int i = 0; i < kNumStages; ++i)
@@ -157,140 +167,33 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     return UGS_OK;
 }
 
-extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
-                       int S, void *stream, int64_t *m_out, int64_t *k_out,
-                       int64_t *p_out) {
-    if (!p || !slices || S < 1 || S > 64) {
-        set_error("ugs_bin: need a plan and 1 <= S <= 64 slices");
-        return UGS_ERR_INVALID;
-    }
-    int rc = check_cloud(c);
-    if (rc) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
+namespace ugs {
+namespace {
+
+constexpr int64_t kHistCapMax = ((int64_t)1 << 24) - 1;   // one exclusive_scan
+
+PlanCaps caps_of(const ugs_plan *p) {
+    return PlanCaps{(unsigned long long)p->m_cap, (unsigned long long)p->k_cap,
+                    (unsigned long long)p->hist_cap, (unsigned long long)p->nblk_cap};
+}
+
+// Record / instance / sort-table buffers for m records and k instances (with
+// the headroom of ensure(): counts drift from batch to batch); the plan's
+// capacities are what later sync-free calls may use.
+int grow_to(ugs_plan *p, int64_t m_need, int64_t k_need, int max_tiles, int S) {
     PlanBuffers &b = p->b;
-    // tiles and bin ids
-    int tile_base = 0, max_tiles = 0;
-    for (int s = 0; s < S; ++s) {
-        ugs_slice &sl = slices[s];
-        if (sl.width < 1 || sl.height < 1 || sl.width > 32767 || sl.height > 32767 ||
-            !(sl.s > 0)) {
-            set_error("ugs_bin: slice width/height must be in [1, 32767], spacing > 0");
-            return UGS_ERR_INVALID;
-        }
-        sl.tiles_x = (sl.width + kTile - 1) / kTile;
-        sl.tiles_y = (sl.height + kTile - 1) / kTile;
-        sl.tile_base = tile_base;
-        const int nt = sl.tiles_x * sl.tiles_y;
-        tile_base += nt;
-        if (nt > max_tiles) max_tiles = nt;
-    }
-    const int n_bins = tile_base;
-    if ((rc = ensure_host(p, S))) return rc;
-    p->S = S;
-    p->n_bins = n_bins;
-    p->max_tiles = max_tiles;
-    p->n = c->n;
-    for (int s = 0; s < S; ++s) {
-        p->h_tile_base[s] = slices[s].tile_base;
-        p->h_ntile[s] = slices[s].tiles_x * slices[s].tiles_y;
-    }
-    size_t cap_sl = (size_t)b.slices_cap;
-    if ((rc = ensure(&b.slices, &cap_sl, (size_t)S, "alloc slices"))) return rc;
-    b.slices_cap = (int)cap_sl;
-    // through pinned staging: an async DMA (a pageable copy would block the
-    // host until the stream drains, i.e. until the previous step finished);
-    // the previous call's copy from it completed at that call's sync
-    std::memcpy(p->h_slices, slices, sizeof(ugs_slice) * S);
-    UGS_CUDA(cudaMemcpyAsync(b.slices, p->h_slices, sizeof(ugs_slice) * S,
-                             cudaMemcpyHostToDevice, st));
-    const int nblk = (int)((c->n + kPrepThreads - 1) / kPrepThreads);
-    if ((int64_t)S * nblk * (kPrepThreads / 32) >= 0x7fffffffLL) {
-        // the flattened (slice, warp) index of the record search is 32-bit
-        set_error("ugs_bin: slices x Gaussians exceeds the 2^36 plan budget; use fewer slices");
-        return UGS_ERR_RANGE;
-    }
-    if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, (size_t)S * (nblk > 0 ? nblk : 1),
-                     "alloc blk_cnt")))
+    int rc;
+    if ((rc = ensure(&b.rec, &b.rec_cap, (size_t)m_need + 1, "alloc rec"))) return rc;
+    if ((rc = ensure(&b.rec_gid, &b.rec_gid_cap, (size_t)m_need + 2, "alloc rec_gid")))
         return rc;
-    if ((rc = ensure(&b.blk_pairs, &b.blk_pairs_cap, (size_t)S * (nblk > 0 ? nblk : 1),
-                     "alloc blk_pairs")))
+    if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)m_need + 2, "alloc rec_inst")))
         return rc;
-    // accept bits per (slice, warp) and the windows of accepted pairs,
-    // written by the count pass and read back by the emit pass
-    if ((rc = ensure(&b.amask, &b.amask_cap,
-                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc amask")))
+    if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_need + 1), "alloc rgrad")))
         return rc;
-    if ((rc = ensure(&b.wcnt, &b.wcnt_cap,
-                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32), "alloc wcnt")))
-        return rc;
-    if ((rc = ensure(&b.warp_inst, &b.warp_inst_cap,
-                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
-                     "alloc warp_inst")))
-        return rc;
-    if ((rc = ensure(&b.warp_rec, &b.warp_rec_cap,
-                     (size_t)S * (nblk > 0 ? nblk : 1) * (kPrepThreads / 32),
-                     "alloc warp_rec")))
-        return rc;
-    if ((rc = ensure(&b.win_sparse, &b.win_sparse_cap,
-                     (size_t)S * (c->n > 0 ? c->n : 1), "alloc win_sparse")))
-        return rc;
-    {
-        static_assert(sizeof(unsigned long long) == 8, "");
-        size_t cap = b.slice_tot ? (size_t)kPlanWords : 0;
-        if ((rc = ensure(&b.slice_tot, &cap, (size_t)kPlanWords, "alloc slice_tot"))) return rc;
-        size_t cap2 = b.slice_base ? 128 : 0;
-        if ((rc = ensure(&b.slice_base, &cap2, (size_t)128, "alloc slice_base"))) return rc;
-        size_t cap3 = (size_t)b.sort_slices_cap;
-        if ((rc = ensure(&b.sort_slices, &cap3, (size_t)64, "alloc sort_slices"))) return rc;
-        b.sort_slices_cap = (int)cap3;
-    }
-    stage_begin(p, kStageCount, st);
-    if (c->n > 0) {
-        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
-                                       b.win_sparse, b.amask, b.wcnt, st)))
-            return rc;
-        if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
-            return rc;
-    } else {
-        UGS_CUDA(cudaMemsetAsync(b.slice_tot, 0, sizeof(unsigned long long) * 3 * S, st));
-    }
-    // bases and sort tables on the device; one small pinned D2H of the totals
-    if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices, st)))
-        return rc;
-    UGS_CUDA(cudaMemcpyAsync(p->h_plan, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
-                             cudaMemcpyDeviceToHost, st));
-    stage_end(p, kStageCount, st);
-    UGS_CUDA(cudaStreamSynchronize(st));
-    const unsigned long long *tot = p->h_plan;
-    const unsigned long long *tt = p->h_plan + 3 * 64;
-    for (int s = 0; s < S; ++s) {
-        if (m_out) m_out[s] = (int64_t)tot[3 * s];
-        if (k_out) k_out[s] = (int64_t)tot[3 * s + 1];
-        if (p_out) p_out[s] = (int64_t)tot[3 * s + 2];
-    }
-    const int64_t m_total = (int64_t)tt[0], k_total = (int64_t)tt[1];
-    p->p_total = (int64_t)tt[2];
-    if (k_total >= 0x7fffffffLL || m_total >= 0x7fffffffLL) {
-        set_error("ugs_bin: batch exceeds 2^31 tile instances; use fewer slices");
-        return UGS_ERR_RANGE;
-    }
-    p->m_total = m_total;
-    p->k_total = k_total;
-    if ((rc = ensure(&b.rec, &b.rec_cap, (size_t)m_total + 1, "alloc rec"))) return rc;
-    if ((rc = ensure(&b.rec_gid, &b.rec_gid_cap, (size_t)m_total + 2, "alloc rec_gid")))
-        return rc;
-    if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)m_total + 2, "alloc rec_inst")))
-        return rc;
-    if ((rc = ensure(&b.rgrad, &b.rgrad_cap, 12 * ((size_t)m_total + 1), "alloc rgrad")))
-        return rc;
-    if ((rc = ensure(&b.rec_bucket, &b.rec_bucket_cap, (size_t)m_total / 32 + 2,
+    if ((rc = ensure(&b.rec_bucket, &b.rec_bucket_cap, (size_t)m_need / 32 + 2,
                      "alloc rec_bucket")))
         return rc;
-    {
-        size_t cap2 = b.bg_sums ? 64 : 0;
-        if ((rc = ensure(&b.bg_sums, &cap2, (size_t)64, "alloc bg_sums"))) return rc;
-    }
-    const size_t kneed = (size_t)k_total + 1;
+    const size_t kneed = (size_t)k_need + 1;
     if (kneed > b.inst_cap || !b.idata) {
         // all-or-nothing: every pointer is nulled when freed and the capacity
         // is published only after every allocation succeeded, so a failed
@@ -317,18 +220,122 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         }
         b.inst_cap = cap;
     }
-    // bin sort plan: single-pass per-slice counting sort when every slice has
-    // <= kSliceSortMaxTiles tiles and the tables fit the scan, else LSD radix
-    const int64_t hist_n = (int64_t)tt[3];
-    const int nblk_sort = (int)tt[4];
-    p->slice_sort = max_tiles <= kSliceSortMaxTiles && hist_n < ((int64_t)1 << 24);
-    const size_t hn = (p->slice_sort ? (size_t)hist_n : radix_hist_entries(k_total)) + 1;
+    // capacities (each buffer's own, minus its +1/+2 sentinels)
+    int64_t mc = (int64_t)b.rec_cap - 1;
+    mc = std::min(mc, (int64_t)b.rec_gid_cap - 2);
+    mc = std::min(mc, (int64_t)b.rec_inst_cap - 2);
+    mc = std::min(mc, (int64_t)(b.rgrad_cap / 12) - 1);
+    mc = std::min(mc, ((int64_t)b.rec_bucket_cap - 2) * 32);
+    const int64_t kc = (int64_t)b.inst_cap - 1;
+    // sort tables: blocks <= k/kSortTile + S, entries <= tiles x blocks
+    const int64_t nb_cap = kc / kSortTile + S + 1;
+    int64_t hcap = std::min((int64_t)std::max(max_tiles, 1) * nb_cap, kHistCapMax);
+    const size_t hn = std::max((size_t)hcap, radix_hist_entries(kc)) + 1;
     if ((rc = ensure(&b.hist, &b.hist_cap, hn, "alloc hist"))) return rc;
-    if ((rc = ensure(&b.scan_tmp, &b.scan_tmp_cap, scan_tmp_entries(hn) + 1,
-                     "alloc scan_tmp")))
+    if ((rc = ensure(&b.scan_tmp, &b.scan_tmp_cap, scan_tmp_entries(hn) + 1, "alloc scan_tmp")))
         return rc;
-    p->hist_n = hist_n;
-    p->nblk_sort = nblk_sort;
+    p->m_cap = mc;
+    p->k_cap = kc;
+    p->hist_cap = hcap;
+    p->nblk_cap = nb_cap;
+    return UGS_OK;
+}
+
+// Harvests the counts of the last call (waits on its D2H event only).
+void read_counts(ugs_plan *p, int S, int64_t *m_out, int64_t *k_out, int64_t *p_out) {
+    const unsigned long long *tot = p->h_plan + (size_t)p->slot * kPlanWords;
+    const unsigned long long *tt = tot + kHdr;
+    for (int s = 0; s < S; ++s) {
+        if (m_out) m_out[s] = (int64_t)tot[3 * s];
+        if (k_out) k_out[s] = (int64_t)tot[3 * s + 1];
+        if (p_out) p_out[s] = (int64_t)tot[3 * s + 2];
+    }
+    p->m_total = (int64_t)tt[0];
+    p->k_total = (int64_t)tt[1];
+    p->p_total = (int64_t)tt[2];
+    p->hist_n = (int64_t)tt[3];
+    p->nblk_sort = (int)tt[4];
+}
+
+// ugs_bin / ugs_bin_async.  Synchronous: the per-slice totals come back to
+// the host before the record / instance buffers are sized, so the launches
+// are exact.  Sync-free (after one synchronous call sized the plan): the
+// launches cover the plan's capacities, the device compares the batch's
+// totals against them (plan_slices) and, if the batch does not fit, every
+// later kernel of the plan returns at entry; ugs_plan_poll reports it.
+int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,
+             bool async, int64_t *m_out, int64_t *k_out, int64_t *p_out) {
+    if (!p || !slices || S < 1 || S > 64) {
+        set_error("ugs_bin: need a plan and 1 <= S <= 64 slices");
+        return UGS_ERR_INVALID;
+    }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    PlanBuffers &b = p->b;
+    // tiles and bin ids
+    int tile_base = 0, max_tiles = 0;
+    for (int s = 0; s < S; ++s) {
+        ugs_slice &sl = slices[s];
+        if (sl.width < 1 || sl.height < 1 || sl.width > 32767 || sl.height > 32767 ||
+            !(sl.s > 0)) {
+            set_error("ugs_bin: slice width/height must be in [1, 32767], spacing > 0");
+            return UGS_ERR_INVALID;
+        }
+        sl.tiles_x = (sl.width + kTile - 1) / kTile;
+        sl.tiles_y = (sl.height + kTile - 1) / kTile;
+        sl.tile_base = tile_base;
+        const int nt = sl.tiles_x * sl.tiles_y;
+        tile_base += nt;
+        if (nt > max_tiles) max_tiles = nt;
+    }
+    const int n_bins = tile_base;
+    // sync-free only on a sized plan and with the single-pass bin sort
+    // (the LSD radix fallback for > 1024 tiles per slice sizes its passes
+    // on the host)
+    if (async && (!p->sized || max_tiles > kSliceSortMaxTiles)) async = false;
+    if ((rc = ensure_host(p, S))) return rc;
+    p->S = S;
+    p->n_bins = n_bins;
+    p->max_tiles = max_tiles;
+    p->n = c->n;
+    for (int s = 0; s < S; ++s) {
+        p->h_tile_base[s] = slices[s].tile_base;
+        p->h_ntile[s] = slices[s].tiles_x * slices[s].tiles_y;
+    }
+    size_t cap_sl = (size_t)b.slices_cap;
+    if ((rc = ensure(&b.slices, &cap_sl, (size_t)S, "alloc slices"))) return rc;
+    b.slices_cap = (int)cap_sl;
+    const int nblk = (int)((c->n + kPrepThreads - 1) / kPrepThreads);
+    if ((int64_t)S * nblk * (kPrepThreads / 32) >= 0x7fffffffLL) {
+        // the flattened (slice, warp) index of the record search is 32-bit
+        set_error("ugs_bin: slices x Gaussians exceeds the 2^36 plan budget; use fewer slices");
+        return UGS_ERR_RANGE;
+    }
+    const size_t nb1 = (size_t)S * (nblk > 0 ? nblk : 1);
+    if ((rc = ensure(&b.blk_cnt, &b.blk_cnt_cap, nb1, "alloc blk_cnt"))) return rc;
+    if ((rc = ensure(&b.blk_pairs, &b.blk_pairs_cap, nb1, "alloc blk_pairs"))) return rc;
+    // accept bits per (slice, warp) and the windows of accepted pairs,
+    // written by the count pass and read back by the emit pass
+    const size_t nw1 = nb1 * (kPrepThreads / 32);
+    if ((rc = ensure(&b.amask, &b.amask_cap, nw1, "alloc amask"))) return rc;
+    if ((rc = ensure(&b.wcnt, &b.wcnt_cap, nw1, "alloc wcnt"))) return rc;
+    if ((rc = ensure(&b.warp_inst, &b.warp_inst_cap, nw1, "alloc warp_inst"))) return rc;
+    if ((rc = ensure(&b.warp_rec, &b.warp_rec_cap, nw1, "alloc warp_rec"))) return rc;
+    if ((rc = ensure(&b.win_sparse, &b.win_sparse_cap, (size_t)S * (c->n > 0 ? c->n : 1),
+                     "alloc win_sparse")))
+        return rc;
+    {
+        static_assert(sizeof(unsigned long long) == 8, "");
+        size_t cap = b.slice_tot ? (size_t)kPlanWords : 0;
+        if ((rc = ensure(&b.slice_tot, &cap, (size_t)kPlanWords, "alloc slice_tot"))) return rc;
+        size_t cap2 = b.slice_base ? 128 : 0;
+        if ((rc = ensure(&b.slice_base, &cap2, (size_t)128, "alloc slice_base"))) return rc;
+        size_t cap3 = (size_t)b.sort_slices_cap;
+        if ((rc = ensure(&b.sort_slices, &cap3, (size_t)64, "alloc sort_slices"))) return rc;
+        b.sort_slices_cap = (int)cap3;
+        size_t cap4 = b.bg_sums ? 64 : 0;
+        if ((rc = ensure(&b.bg_sums, &cap4, (size_t)64, "alloc bg_sums"))) return rc;
+    }
     if (b.bin_cap < (size_t)n_bins || !b.bin_range) {
         if (b.bin_range) cudaFree(b.bin_range);
         if (b.bin_bg) cudaFree(b.bin_bg);
@@ -346,12 +353,77 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
         }
         b.bin_cap = cap;
     }
+    // the next ring slot: its previous copies (kRing calls ago) are done
+    p->slot = (p->slot + 1) % kRing;
+    const int slot = p->slot;
+    UGS_CUDA(cudaEventSynchronize(p->ev_slices[slot]));
+    UGS_CUDA(cudaEventSynchronize(p->ev_counts[slot]));
+    ugs_slice *hs = p->h_slices + (size_t)slot * 64;
+    unsigned long long *hp = p->h_plan + (size_t)slot * kPlanWords;
+    // through pinned staging: an async DMA (a pageable copy would block the
+    // host until the stream drains)
+    std::memcpy(hs, slices, sizeof(ugs_slice) * S);
+    UGS_CUDA(cudaMemcpyAsync(b.slices, hs, sizeof(ugs_slice) * S, cudaMemcpyHostToDevice, st));
+    UGS_CUDA(cudaEventRecord(p->ev_slices[slot], st));
+    stage_begin(p, kStageCount, st);
+    if (c->n > 0) {
+        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
+                                       b.win_sparse, b.amask, b.wcnt, st)))
+            return rc;
+        if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
+            return rc;
+    } else {
+        UGS_CUDA(cudaMemsetAsync(b.slice_tot, 0, sizeof(unsigned long long) * 3 * S, st));
+    }
+    // bases, sort tables and the overflow flag on the device; the totals go
+    // to pinned memory (read now, or by ugs_plan_poll)
+    if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices,
+                                 caps_of(p), st)))
+        return rc;
+    UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                             cudaMemcpyDeviceToHost, st));
+    UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
+    stage_end(p, kStageCount, st);
+    p->counts_pending = true;
+    if (!async) {
+        UGS_CUDA(cudaEventSynchronize(p->ev_counts[slot]));
+        read_counts(p, S, m_out, k_out, p_out);
+        p->counts_pending = false;
+        if (p->k_total >= 0x7fffffffLL || p->m_total >= 0x7fffffffLL) {
+            set_error("ugs_bin: batch exceeds 2^31 tile instances; use fewer slices");
+            return UGS_ERR_RANGE;
+        }
+        p->slice_sort = max_tiles <= kSliceSortMaxTiles && p->hist_n < kHistCapMax;
+        const bool fits = p->m_total <= p->m_cap && p->k_total <= p->k_cap &&
+                          (!p->slice_sort || (p->hist_n <= p->hist_cap &&
+                                              p->nblk_sort <= p->nblk_cap));
+        if (!fits && (rc = grow_to(p, p->m_total, p->k_total, max_tiles, S))) return rc;
+        if (hp[kHdr + 5] != 0ull) {
+            // re-derive the device flag against the new capacities (the
+            // radix fallback sizes its sort tables here, not from the caps)
+            PlanCaps caps = caps_of(p);
+            if (!p->slice_sort) caps.hist = caps.nblk = ~0ull;
+            if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base,
+                                         b.sort_slices, caps, st)))
+                return rc;
+        }
+        p->sized = true;
+        p->m_grid = p->m_total;
+        p->k_grid = p->k_total;
+        p->nblk_grid = p->nblk_sort;
+    } else {
+        p->slice_sort = true;
+        p->m_grid = p->m_cap;
+        p->k_grid = p->k_cap;
+        p->nblk_grid = p->nblk_cap;
+    }
+    const PlanHdr *hdr = plan_hdr(b);
     stage_begin(p, kStageEmit, st);
-    if (c->n > 0 && m_total > 0) {
+    if (c->n > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
-                                      b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys,
-                                      m_total, k_total, b.win_sparse, b.amask,
-                                      b.wcnt, b.warp_rec, b.warp_inst, b.rec_bucket, st)))
+                                      b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys, hdr,
+                                      p->m_grid, b.win_sparse, b.amask, b.wcnt, b.warp_rec,
+                                      b.warp_inst, b.rec_bucket, st)))
             return rc;
     } else {
         UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));
@@ -359,23 +431,62 @@ extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);
     if (p->slice_sort) {
-        if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, p->hist_n, max_tiles, n_bins,
-                                  p->nblk_sort, b.hist, b.scan_tmp, b.vals, b.bin_range, st)))
+        const int64_t hist_grid = async ? p->hist_cap : p->hist_n;
+        if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, hist_grid, max_tiles, n_bins,
+                                  (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals,
+                                  b.bin_range, st)))
             return rc;
         p->sorted_keys = nullptr;
         p->sorted_vals = b.vals;
         stage_end(p, kStageSort, st);
     } else {
-        if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, k_total,
+        if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, p->k_total,
                                    bits_for(n_bins), b.hist, b.scan_tmp, st,
                                    &p->sorted_keys, &p->sorted_vals)))
             return rc;
         stage_end(p, kStageSort, st);
         stage_begin(p, kStageRanges, st);
-        if ((rc = launch_bin_ranges(p->sorted_keys, k_total, b.bin_range, n_bins, st)))
+        if ((rc = launch_bin_ranges(p->sorted_keys, p->k_total, b.bin_range, n_bins, st)))
             return rc;
         stage_end(p, kStageRanges, st);
     }
+    return UGS_OK;
+}
+
+}  // namespace
+}  // namespace ugs
+
+extern "C" int ugs_bin(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices,
+                       int S, void *stream, int64_t *m_out, int64_t *k_out,
+                       int64_t *p_out) {
+    return bin_impl(p, c, slices, S, (cudaStream_t)stream, false, m_out, k_out, p_out);
+}
+
+extern "C" int ugs_bin_async(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S,
+                             void *stream) {
+    return bin_impl(p, c, slices, S, (cudaStream_t)stream, true, nullptr, nullptr, nullptr);
+}
+
+extern "C" int ugs_plan_poll(ugs_plan *p, int *overflowed, int64_t *m_out, int64_t *k_out,
+                             int64_t *p_out) {
+    if (!p) { set_error("ugs_plan_poll: NULL plan"); return UGS_ERR_INVALID; }
+    if (overflowed) *overflowed = 0;
+    if (!p->h_plan || p->S == 0) return UGS_OK;
+    UGS_CUDA(cudaEventSynchronize(p->ev_counts[p->slot]));
+    const unsigned long long *hp = p->h_plan + (size_t)p->slot * kPlanWords;
+    const bool ovf = hp[kHdr + 5] != 0ull;
+    read_counts(p, p->S, m_out, k_out, p_out);
+    if (p->counts_pending && ovf) {
+        if (p->k_total >= 0x7fffffffLL || p->m_total >= 0x7fffffffLL) {
+            set_error("ugs_bin_async: batch exceeds 2^31 tile instances; use fewer slices");
+            return UGS_ERR_RANGE;
+        }
+        // the batch's kernels were no-ops: grow so that a retry fits
+        int rc = grow_to(p, p->m_total, p->k_total, p->max_tiles, p->S);
+        if (rc) return rc;
+        if (overflowed) *overflowed = 1;
+    }
+    p->counts_pending = false;
     return UGS_OK;
 }
 

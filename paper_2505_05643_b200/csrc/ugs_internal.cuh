@@ -109,8 +109,20 @@ struct ugs_plan {
     int max_tiles = 0;
     int64_t *h_slice_base = nullptr; // host copy [S][2]
     int64_t *h_m = nullptr;          // host [S]
-    unsigned long long *h_plan = nullptr;   // pinned [kPlanWords] (slice_tot D2H)
-    ugs_slice *h_slices = nullptr;          // pinned [64] staging of the slice structs
+    // pinned staging, a ring of kRing slots so a sync-free call never
+    // overwrites a slot whose copy may still be queued: slice structs (H2D)
+    // and the per-slice totals + plan header (D2H), each with its event
+    unsigned long long *h_plan = nullptr;   // pinned [kRing][kPlanWords]
+    ugs_slice *h_slices = nullptr;          // pinned [kRing][64]
+    cudaEvent_t ev_slices[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_counts[4] = {nullptr, nullptr, nullptr, nullptr};
+    int slot = 0;                    // ring slot of the last ugs_bin / ugs_bin_async
+    bool counts_pending = false;     // the last call's counts not yet harvested
+    // capacities of the record / instance / sort-table buffers (what a
+    // sync-free call may use; the device flags an overflow against them)
+    int64_t m_cap = 0, k_cap = 0, hist_cap = 0, nblk_cap = 0;
+    bool sized = false;              // capacities set by a synchronous ugs_bin
+    int64_t m_grid = 0, k_grid = 0, nblk_grid = 0;   // launch extents of this batch
     int64_t p_total = 0;             // (Gaussian, pixel) pairs of the batch
     int32_t *h_tile_base = nullptr;  // host [S]
     int32_t *h_ntile = nullptr;      // host [S]
@@ -191,17 +203,37 @@ int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
                          uint2 *win_sparse, uint32_t *amask, uint2 *wcnt, cudaStream_t st);
 // per-slice bases + sort tables on the device; slice_tot holds [3*64] per-slice
-// (accepted, tiles, pairs) then 5 totals (m, k, pairs, sort entries, blocks)
+// (accepted, tiles, pairs) then the plan header: 5 totals (m, k, pairs, sort
+// entries, sort blocks) and the overflow flag
 constexpr int kPlanWords = 3 * 64 + 8;
+constexpr int kHdr = 3 * 64;
+constexpr int kRing = 4;
+struct PlanHdr {
+    unsigned long long m, k, pairs, hist_n, nblk, ovf;
+};
+// ovf != 0: the batch does not fit the plan's capacities (a sync-free call);
+// every later kernel of the plan returns at entry, the host grows and retries
+__device__ __forceinline__ bool plan_overflow(const PlanHdr *h) {
+    return h != nullptr && *(volatile const unsigned long long *)&h->ovf != 0ull;
+}
+inline const PlanHdr *plan_hdr(const PlanBuffers &b) {
+    return reinterpret_cast<const PlanHdr *>(b.slice_tot + kHdr);
+}
+struct PlanCaps {
+    unsigned long long m, k, hist, nblk;
+};
 int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
-                       int64_t *slice_base, SortSlice *ss, cudaStream_t st);
+                       int64_t *slice_base, SortSlice *ss, PlanCaps caps, cudaStream_t st);
 int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st);
+// m_grid: records the build grid covers (the exact count after a
+// synchronous plan, the capacity in a sync-free one); the kernels read the
+// batch's true totals from the plan header
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        Inst *idata, uint32_t *keys, int64_t m_total,
-                        int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
+                        Inst *idata, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
+                        const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
                         int32_t *rec_bucket, cudaStream_t st);
 
@@ -217,10 +249,12 @@ size_t scan_tmp_entries(size_t n);
 // single-pass per-slice counting sort of slice-major instances; tiles per
 // slice <= 1024 (else the LSD radix sort above is used)
 constexpr int kSliceSortMaxTiles = 1024;
-int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, int64_t hist_n,
-                    int max_tiles, int n_bins, int nblk, uint32_t *hist,
-                    uint32_t *scan_tmp, uint32_t *vals_out, int2 *bin_range,
-                    cudaStream_t st);
+// hist_grid / nblk_grid: table entries and sort blocks the launches cover
+// (exact, or capacities); the true counts come from the plan header
+int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const PlanHdr *hdr,
+                    int64_t hist_grid, int max_tiles, int n_bins, int nblk_grid,
+                    uint32_t *hist, uint32_t *scan_tmp, uint32_t *vals_out,
+                    int2 *bin_range, cudaStream_t st);
 int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 

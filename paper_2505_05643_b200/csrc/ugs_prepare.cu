@@ -255,8 +255,10 @@ __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
                                     int32_t *__restrict__ warp_rec,
                                     int32_t *__restrict__ warp_inst,
                                     int32_t *__restrict__ rec_bucket,
-                                    int32_t *__restrict__ rec_inst, int64_t m_total,
-                                    int64_t k_total) {
+                                    int32_t *__restrict__ rec_inst,
+                                    const PlanHdr *__restrict__ hdr) {
+    if (plan_overflow(hdr)) return;
+    const int64_t m_total = (int64_t)hdr->m, k_total = (int64_t)hdr->k;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nw = (int64_t)S * nwarp_all;
     if (idx == 0) {
@@ -296,14 +298,16 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      const float *__restrict__ intensity_raw,
                      const float *__restrict__ opacity_raw, int64_t n, float beta,
                      const ugs_slice *__restrict__ slices, int S,
-                     const int64_t *__restrict__ slice_base, int64_t m_total,
-                     int64_t nwarp_all, const uint32_t *__restrict__ amask,
+                     const int64_t *__restrict__ slice_base,
+                     const PlanHdr *__restrict__ hdr, int64_t nwarp_all, const uint32_t *__restrict__ amask,
                      const int32_t *__restrict__ warp_rec,
                      const int32_t *__restrict__ warp_inst,
                      const int32_t *__restrict__ rec_bucket,
                      const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
                      int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
                      Inst *__restrict__ idata, uint32_t *__restrict__ keys) {
+    if (plan_overflow(hdr)) return;
+    const int64_t m_total = (int64_t)hdr->m;
     const int ln = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kBuildThreads + threadIdx.x;
     const int64_t rw0 = r - ln;                   // this warp's first record
@@ -411,7 +415,7 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
 __global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
                                    const ugs_slice *__restrict__ slices, int S,
                                    int64_t *__restrict__ slice_base,
-                                   SortSlice *__restrict__ ss) {
+                                   SortSlice *__restrict__ ss, PlanCaps caps) {
     // one thread per slice: its bases are prefix sums over the earlier
     // slices (S <= 64: a short loop, all slices in parallel)
     __shared__ unsigned long long sm[64], sk[64], sp[64];
@@ -454,6 +458,12 @@ __global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
             t[2] = pr;
             t[3] = hn + (unsigned long long)snt[s] * snb[s];
             t[4] = nbs + (unsigned long long)snb[s];
+            // the batch must fit the buffers the launches were sized for
+            // (and the 31-bit index budget); else the plan's later kernels
+            // all return at entry and the host grows the buffers and retries
+            t[5] = (t[0] > caps.m || t[1] > caps.k || t[3] > caps.hist ||
+                    t[4] > caps.nblk || t[0] >= 0x7fffffffull || t[1] >= 0x7fffffffull)
+                       ? 1ull : 0ull;
         }
     }
 }
@@ -471,8 +481,8 @@ int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
 }
 
 int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
-                       int64_t *slice_base, SortSlice *ss, cudaStream_t st) {
-    plan_slices_kernel<<<1, 64, 0, st>>>(slice_tot, slices, S, slice_base, ss);
+                       int64_t *slice_base, SortSlice *ss, PlanCaps caps, cudaStream_t st) {
+    plan_slices_kernel<<<1, 64, 0, st>>>(slice_tot, slices, S, slice_base, ss, caps);
     UGS_LAUNCH_CHECK("plan_slices_kernel");
     return UGS_OK;
 }
@@ -487,20 +497,21 @@ int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nb
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        Inst *idata, uint32_t *keys, int64_t m_total,
-                        int64_t k_total, const uint2 *win_sparse, const uint32_t *amask,
+                        Inst *idata, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
+                        const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
                         int32_t *rec_bucket, cudaStream_t st) {
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t nw = (int64_t)S * nwarp_all;
     warp_offsets_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(
         S, nwarp_all, nblk, blk_off, wcnt, amask, slice_base, warp_rec, warp_inst,
-        rec_bucket, rec_inst, m_total, k_total);
+        rec_bucket, rec_inst, hdr);
     UGS_LAUNCH_CHECK("warp_offsets_kernel");
-    build_records_kernel<<<(unsigned)((m_total + kBuildThreads - 1) / kBuildThreads),
+    if (m_grid <= 0) return UGS_OK;
+    build_records_kernel<<<(unsigned)((m_grid + kBuildThreads - 1) / kBuildThreads),
                            kBuildThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices, S,
-        slice_base, m_total, nwarp_all, amask, warp_rec, warp_inst, rec_bucket, win_sparse, rec,
+        slice_base, hdr, nwarp_all, amask, warp_rec, warp_inst, rec_bucket, win_sparse, rec,
         rec_gid, rec_inst, idata, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;

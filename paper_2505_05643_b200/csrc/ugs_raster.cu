@@ -46,6 +46,11 @@ constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
 constexpr int kBatch = 256;
 constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
+constexpr int kKeyWide = kMaxTrips + 1;      // forward: warp-per-record class
+constexpr int kKeyInvalid = kMaxTrips + 2;   // unused staging slots
+constexpr int kKeys = kMaxTrips + 3;
+constexpr int kWideMin = 9;        // forward: clipped widths >= this take the
+                                   // register-tile path (one record per warp)
 constexpr int kAccStride = kTile * kTile;    // forward: one private tile
 constexpr int kGroups = kRasterThreads / 16; //   buffer per 16-lane group
 
@@ -106,8 +111,8 @@ __device__ __forceinline__ void load_inst(const Rec *__restrict__ rec,
 struct Batch {
     float4 sA[kBatch], sB[kBatch], sC[kBatch];
     uint16_t order[kBatch];            // staged slot of the j-th record by trips
-    uint32_t wcnt[kWarps][kMaxTrips + 2];
-    uint32_t base[kMaxTrips + 2];
+    uint32_t wcnt[kWarps][kKeys];
+    uint32_t base[kKeys];
 };
 struct Layout {   // two-stream layouts (backward), after the Batch
     int4 sL[kBatch], sM[kBatch];
@@ -181,12 +186,42 @@ __device__ __forceinline__ int byte_of(int x, int k) {
     return (int)__byte_perm((unsigned)x, 0u, 0x4440u | (unsigned)k);
 }
 
-// Stable counting sort of the staged slots by trip count (warp match-any
-// ranks + per-warp bucket counters): deterministic record -> group mapping.
-__device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
+// Forward staging of one tile instance (one thread per record).  Narrow
+// rectangles (< kWideMin columns) get stage_record_rows' 16-lane layout and
+// key = sweep count; wide ones the warp layout of the register-tile path:
+//   sA = (pu, pv, D, E)   the expansion pixel (tile-relative, exact floats)
+//   sB = (A, B2, C, F)
+//   sC = (color, bits(x0 | w << 8), bits(vm0 | vm1 << 8 | um << 16), -)
+// where lane (X, ph) owns rows 2m + ph, vm_ph = the m whose row lies in
+// [y0, y1], um = vm0 | vm1 (the warp-uniform row pairs).
+__device__ __forceinline__ uint32_t stage_forward(const float4 &I, const Rec &R, int tu0,
+                                                  int tv0, uint32_t inst, Batch &B, int slot) {
+    const TileRect t = inst_rect(R, tu0, tv0);
+    const int w = t.x1 - t.x0 + 1;
+    if (w < kWideMin) return (uint32_t)stage_record_rows(I, R, tu0, tv0, inst, B, slot);
+    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0, y1 = t.y1 - tv0;
+    unsigned vmask[2];
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph) {
+        const int mlo = (y0 - ph + 1) >> 1, mhi = (y1 - ph) >> 1;
+        vmask[ph] = (mhi >= mlo) ? ((2u << mhi) - (1u << mlo)) : 0u;
+    }
+    B.sA[slot] = make_float4((float)(t.pu - tu0), (float)(t.pv - tv0), I.x, I.y);
+    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+    B.sC[slot] = make_float4(R.r0.w, __int_as_float(x0 | (w << 8)),
+                             __int_as_float((int)(vmask[0] | (vmask[1] << 8) |
+                                                  ((vmask[0] | vmask[1]) << 16))),
+                             0.f);
+    return (uint32_t)kKeyWide;
+}
+
+// Stable counting sort of the staged slots by key (trip count, or the
+// forward's wide class; unused slots last) -- warp match-any ranks +
+// per-warp bucket counters: a deterministic record -> lane-group mapping.
+// Returns, in B.base, each key's first sorted position.
+__device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t key = valid ? (uint32_t)trips : (uint32_t)(kMaxTrips + 1);
-    for (int i = threadIdx.x; i < kWarps * (kMaxTrips + 2); i += kRasterThreads)
+    for (int i = threadIdx.x; i < kWarps * kKeys; i += kRasterThreads)
         (&B.wcnt[0][0])[i] = 0;
     __syncthreads();
     const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -195,7 +230,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
     __syncthreads();
     if (threadIdx.x < 32) {   // bucket bases (exclusive over keys), then per warp
         uint32_t tot = 0;
-        for (int k = lane; k < kMaxTrips + 2; k += 32) {
+        for (int k = lane; k < kKeys; k += 32) {
             uint32_t col = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) col += B.wcnt[w][k];
@@ -203,7 +238,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
         }
         __syncwarp();
         if (lane == 0) {
-            for (int k = 0; k < kMaxTrips + 2; ++k) {
+            for (int k = 0; k < kKeys; ++k) {
                 const uint32_t c = B.base[k];
                 B.base[k] = tot;
                 tot += c;
@@ -211,8 +246,9 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
         }
     }
     __syncthreads();
-    if (threadIdx.x < kMaxTrips + 2) {
-        uint32_t run = B.base[threadIdx.x];
+    uint32_t run = 0;
+    if (threadIdx.x < kKeys) {
+        run = B.base[threadIdx.x];
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = B.wcnt[w][threadIdx.x];
@@ -221,19 +257,32 @@ __device__ __forceinline__ void sort_batch(Batch &B, int trips, bool valid) {
         }
     }
     __syncthreads();
-    if (valid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
+    if (key != (uint32_t)kKeyInvalid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
     __syncthreads();
 }
 
 
+// Forward.  Records are split by clipped width:
+//   narrow (< kWideMin columns): two records per warp, each 16-lane group
+//     sweeps its record's rectangle and read-modify-writes its own PRIVATE
+//     (num, den) tile buffer in shared memory (XOR-swizzled float2);
+//   wide (>= kWideMin columns, ~3/4 of the pixel updates at C3): one record
+//     per warp, lane = (tile column X, row parity); every lane keeps the
+//     (num, den) of its 8 pixels (X, 2m + parity) in REGISTERS across all of
+//     the tile's wide records -- no shared-memory traffic per pair, which is
+//     what bounds the narrow path.
+// At the end each lane adds its register tile into its group's private
+// buffer and the 16 buffers are summed in fixed order -- deterministic,
+// because the record -> group / warp assignment is a stable sort.
 __global__ void __launch_bounds__(kRasterThreads)
 forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                const uint32_t *__restrict__ vals,
                const int2 *__restrict__ bin_range,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
-               float *__restrict__ den_out) {
+               float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
     // one private (num, den) tile buffer per 16-lane group
     float2 *acc = reinterpret_cast<float2 *>(smem + sizeof(Batch));   // [group][256]
@@ -247,22 +296,35 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
         acc[i] = make_float2(0.f, 0.f);
     float2 *my = acc + (threadIdx.x >> 4) * kAccStride;
     const int gl16 = lane & 15;
+    // wide path: this lane's column and row parity, and its register tile:
+    // (num, den) of pixels (X, 2m + ph), m = 2qq + {0, 1} in the two halves
+    const int X = lane & 15, ph = lane >> 4;
+    const float Xf = (float)X, phf = (float)ph;
+    float2 an2[4], ad2[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+        an2[qq] = make_float2(0.f, 0.f);
+        ad2[qq] = make_float2(0.f, 0.f);
+    }
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
-        int trips = 0;
+        uint32_t key = kKeyInvalid;
         if (threadIdx.x < nb) {
             Rec R;
             float4 I;
             const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
             load_inst(rec, idata, inst, I, R);
-            trips = stage_record_rows(I, R, tu0, tv0, inst, B, threadIdx.x);
+            key = stage_forward(I, R, tu0, tv0, inst, B, threadIdx.x);
         }
-        // records with equal sweep counts share a warp (two per warp)
-        sort_batch(B, trips, threadIdx.x < nb);
-        for (int s0 = warp * 2; s0 < nb; s0 += kWarps * 2) {
+        // narrow records with equal sweep counts share a warp (two per
+        // warp); the wide records follow them
+        sort_batch(B, key);
+        const int n_narrow = (int)B.base[kKeyWide];
+        const int n_valid = (int)B.base[kKeyInvalid];
+        for (int s0 = warp * 2; s0 < n_narrow; s0 += kWarps * 2) {
             const int slot = s0 + (lane >> 4);
-            if (slot >= nb) continue;
+            if (slot >= n_narrow) continue;
             const int j = B.order[slot];
             const float4 a = B.sA[j], b = B.sB[j];
             const u64 c1 = *reinterpret_cast<const u64 *>(&B.sC[j]);   // (color, 1)
@@ -313,6 +375,49 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 *pl = ffma2(c1, pack2(wa, wa), *pl);
             }
         }
+        // wide records: one per warp, all 32 lanes, register accumulation;
+        // rows 2m + ph in packed pairs (m = 2q, 2q + 1): FFMA2 / FADD2
+        for (int q = n_narrow + warp; q < n_valid; q += kWarps) {
+            const int j = B.order[q];
+            const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
+            const int xw = __float_as_int(c.y), masks = __float_as_int(c.z);
+            const float dx = Xf - a.x;                    // exact small integers
+            float P = fmaf(fmaf(b.x, dx, a.z), dx, b.w);
+            const float Q = fmaf(b.y, dx, a.w);
+            P = (unsigned)(X - (xw & 0xff)) < (unsigned)(xw >> 8) ? P : -INFINITY;
+            const unsigned vm = (unsigned)byte_of(masks, ph);
+            // provably warp-uniform (a lane-0 broadcast), so the row-pair
+            // skips compile to uniform branches without reconvergence barriers
+            const unsigned um = (unsigned)__shfl_sync(0xffffffffu, masks, 0) >> 16;
+            const float dyb = phf - a.y;                  // row ph (m = 0)
+            float2 dy2 = make_float2(dyb, dyb + 2.0f);
+            const float2 P2 = make_float2(P, P), Q2 = make_float2(Q, Q),
+                         C2 = make_float2(b.z, b.z), col2 = make_float2(c.x, c.x);
+            const float2 four = make_float2(4.0f, 4.0f);
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                if (um & (3u << (2 * qq))) {                 // warp-uniform
+                    const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
+                    float2 wv = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+                    wv.x = (vm & (1u << (2 * qq))) ? wv.x : 0.f;
+                    wv.y = (vm & (2u << (2 * qq))) ? wv.y : 0.f;
+                    an2[qq] = __ffma2_rn(wv, col2, an2[qq]);
+                    ad2[qq] = __fadd2_rn(ad2[qq], wv);
+                }
+                dy2 = __fadd2_rn(dy2, four);
+            }
+        }
+    }
+    __syncthreads();
+    // the register tiles join the group buffers (each lane owns distinct
+    // pixels of its group's buffer), then the fixed-order sum
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int p = acc_swizzle((2 * m + ph) * kTile + X);
+        float2 v = my[p];
+        v.x += (m & 1) ? an2[m >> 1].y : an2[m >> 1].x;
+        v.y += (m & 1) ? ad2[m >> 1].y : ad2[m >> 1].x;
+        my[p] = v;
     }
     __syncthreads();
     const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
@@ -340,8 +445,9 @@ forward_ordered_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ ida
                        const int2 *__restrict__ bin_range,
                        const ugs_slice *__restrict__ slices,
                        const double *__restrict__ bg_raw, float *__restrict__ num_out,
-                       float *__restrict__ den_out) {
+                       float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
     __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
+    if (plan_overflow(hdr)) return;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
@@ -423,8 +529,10 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 const ugs_slice *__restrict__ slices,
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
-                float *__restrict__ partial, float2 *__restrict__ bin_bg) {
+                float *__restrict__ partial, float2 *__restrict__ bin_bg,
+                const PlanHdr *__restrict__ hdr) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
     Layout &Ly = *reinterpret_cast<Layout *>(smem + sizeof(Batch));
     float2 *pix = reinterpret_cast<float2 *>(smem + sizeof(Batch) + sizeof(Layout));  // (G, G chat)
@@ -468,7 +576,7 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
             load_inst(rec, idata, inst, I, R);
             trips = stage_record<8>(I, R, tu0, tv0, inst, B, Ly, threadIdx.x);
         }
-        sort_batch(B, trips, threadIdx.x < nb);
+        sort_batch(B, threadIdx.x < nb ? (uint32_t)trips : (uint32_t)kKeyInvalid);
         for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
             // every lane takes part in the shuffles; empty lanes carry zeros
             const int slot = s0 + (lane >> 3);
@@ -654,7 +762,7 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
 __global__ void __launch_bounds__(128, 8)
 finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                         const int32_t *__restrict__ rec_inst,
-                        const float *__restrict__ partial, int64_t m_total,
+                        const float *__restrict__ partial, const PlanHdr *__restrict__ hdr,
                         const int64_t *__restrict__ slice_base, int S,
                         const ugs_slice *__restrict__ slices,
                         const float *__restrict__ means, const float *__restrict__ l_raw,
@@ -662,6 +770,9 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
     // the slices' record bases in shared memory: the per-thread slice search
     // runs on it instead of on dependent global loads
     __shared__ int64_t s_rb[64];
+    if (plan_overflow(hdr)) return;
+    const int64_t m_total = (int64_t)hdr->m;
+    if ((int64_t)blockIdx.x * blockDim.x >= m_total) return;   // whole block
     for (int q = threadIdx.x; q < S; q += blockDim.x) s_rb[q] = slice_base[2 * q];
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -700,8 +811,10 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
                      float scale, int adam, float *__restrict__ grad,
                      uint8_t *__restrict__ touched, CloudMut p, float *__restrict__ m,
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
-                     int32_t *__restrict__ grad_cnt, int aligned) {
+                     int32_t *__restrict__ grad_cnt, int aligned,
+                     const PlanHdr *__restrict__ hdr) {
     __shared__ float4 rows_all[kUpdWarps][kUpdRows][3];
+    if (plan_overflow(hdr)) return;
     __shared__ float4 prm_all[kUpdWarps][24 + 48];   // means | l_raw rows of the warp
     __shared__ uint32_t word_all[kUpdWarps][64];
     __shared__ int off_all[kUpdWarps][65], base_all[kUpdWarps][64];
@@ -909,8 +1022,9 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
 // s's tile partials in fixed order; the last step adds the slices in order.
 __global__ void bg_slice_kernel(const float2 *__restrict__ bin_bg,
                                 const ugs_slice *__restrict__ slices,
-                                double2 *__restrict__ out) {
+                                double2 *__restrict__ out, const PlanHdr *__restrict__ hdr) {
     __shared__ double sa[256], sc_[256];
+    if (plan_overflow(hdr)) return;
     const int s = blockIdx.x;
     const int tile_base = slices[s].tile_base;
     const int ntile = slices[s].tiles_x * slices[s].tiles_y;
@@ -938,8 +1052,8 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
                                    double *__restrict__ bg_raw,
                                    float *__restrict__ grad_bg, float scale, int adam,
                                    float *__restrict__ m_bg, float *__restrict__ v_bg,
-                                   AdamConst k) {
-    if (threadIdx.x != 0) return;
+                                   AdamConst k, const PlanHdr *__restrict__ hdr) {
+    if (threadIdx.x != 0 || plan_overflow(hdr)) return;
     const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
     float g[2] = {adam ? 0.f : grad_bg[0], adam ? 0.f : grad_bg[1]};
     for (int s = 0; s < S; ++s) {
@@ -985,11 +1099,13 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     stage_begin(pm, kStageForward, st);
     if (p.ordered) {
         forward_ordered_kernel<<<grid, kRasterThreads, 0, st>>>(
-            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den,
+            plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
         forward_kernel<<<grid, kRasterThreads, kFwdSmem, st>>>(
-            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den);
+            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den,
+            plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_kernel");
     }
     stage_end(pm, kStageForward, st);
@@ -1008,7 +1124,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     stage_begin(pm, kStageBackward, st);
     backward_kernel<<<grid, kRasterThreads, kBwdSmem, st>>>(
         p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, num, den, dpix,
-        c.bg_raw, p.b.partial, p.b.bin_bg);
+        c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
     // the two background parameters (bg_slice -> bg_finalize) only need the
@@ -1022,16 +1138,16 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     cudaStream_t side = pm->side;
     UGS_CUDA(cudaEventRecord(pm->ev_fork, st));
     UGS_CUDA(cudaStreamWaitEvent(side, pm->ev_fork, 0));
-    bg_slice_kernel<<<p.S, 256, 0, side>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums);
+    bg_slice_kernel<<<p.S, 256, 0, side>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("bg_slice_kernel");
     if (adam) {
         bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                                nullptr, scale, 1, adam->m + kG * c.n,
-                                               adam->v + kG * c.n, adam->k);
+                                               adam->v + kG * c.n, adam->k, plan_hdr(p.b));
     } else {
         bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                                grad + kG * c.n, scale, 0, nullptr, nullptr,
-                                               AdamConst{});
+                                               AdamConst{}, plan_hdr(p.b));
     }
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
     UGS_CUDA(cudaEventRecord(pm->ev_join, side));
@@ -1039,16 +1155,16 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     const CloudMut cm{const_cast<float *>(c.means), const_cast<float *>(c.l_raw),
                       const_cast<float *>(c.intensity_raw),
                       const_cast<float *>(c.opacity_raw)};
-    if (p.m_total > 0) {
+    if (p.m_grid > 0) {
         const int th = 128;
-        finalize_records_kernel<<<(unsigned)((p.m_total + th - 1) / th), th, 0, st>>>(
-            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, p.m_total, p.b.slice_base, p.S,
+        finalize_records_kernel<<<(unsigned)((p.m_grid + th - 1) / th), th, 0, st>>>(
+            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, plan_hdr(p.b), p.b.slice_base, p.S,
             p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
     }
     stage_end(pm, kStageFinalize, st);
     stage_begin(pm, kStageUpdate, st);
-    if (c.n > 0 && (adam || p.m_total > 0)) {
+    if (c.n > 0 && (adam || p.m_grid > 0)) {
         const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
         const int64_t nwarp_all = nblk * (kPrepThreads / 32);
         static_assert(kUpdThreads == kPrepThreads, "update blocks mirror count blocks");
@@ -1060,7 +1176,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale, adam ? 1 : 0,
             grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
             adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,
-            adam ? adam->grad_cnt : nullptr, aligned);
+            adam ? adam->grad_cnt : nullptr, aligned, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("update_gather_kernel");
     }
     stage_end(pm, kStageUpdate, st);

@@ -46,9 +46,17 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x,
     return pre;
 }
 
+// n_dev (optional): the true entry count on the device, clamped to the
+// launch extent n (a sync-free plan sizes the grid by capacity)
+__device__ __forceinline__ size_t scan_count(size_t n, const unsigned long long *n_dev) {
+    return n_dev ? (size_t)min((unsigned long long)n, *n_dev) : n;
+}
+
 __global__ void __launch_bounds__(kScanThreads)
 scan_reduce_kernel(const uint32_t *__restrict__ in, size_t n,
+                   const unsigned long long *__restrict__ n_dev,
                    uint32_t *__restrict__ sums) {
+    n = scan_count(n, n_dev);
     const size_t base = (size_t)blockIdx.x * kScanTile;
     uint32_t acc = 0;
 #pragma unroll
@@ -88,7 +96,9 @@ scan_sums_kernel(uint32_t *__restrict__ sums, int n) {
 
 __global__ void __launch_bounds__(kScanThreads)
 scan_down_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
-                 size_t n, const uint32_t *__restrict__ sums) {
+                 size_t n, const unsigned long long *__restrict__ n_dev,
+                 const uint32_t *__restrict__ sums) {
+    n = scan_count(n, n_dev);
     // each thread scans kScanItems consecutive entries (blocked layout)
     __shared__ uint32_t tile[kScanTile];
     const size_t base = (size_t)blockIdx.x * kScanTile;
@@ -119,18 +129,19 @@ scan_down_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
 }
 
 int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
-                   uint32_t *tmp, cudaStream_t st) {
+                   uint32_t *tmp, cudaStream_t st,
+                   const unsigned long long *n_dev = nullptr) {
     if (n == 0) return UGS_OK;
     const size_t nb = (n + kScanTile - 1) / kScanTile;
     if (nb > 8192) {
         set_error("exclusive_scan: input too large");
         return UGS_ERR_RANGE;
     }
-    scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, tmp);
+    scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_reduce_kernel");
     scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
     UGS_LAUNCH_CHECK("scan_sums_kernel");
-    scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, tmp);
+    scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_down_kernel");
     return UGS_OK;
 }
@@ -243,8 +254,9 @@ __device__ __forceinline__ int sort_slice_of(const SortSlice *__restrict__ ss, i
 
 __global__ void __launch_bounds__(kSortThreads)
 slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss, int S,
-                  uint32_t *__restrict__ hist) {
+                  const PlanHdr *__restrict__ hdr, uint32_t *__restrict__ hist) {
     extern __shared__ uint32_t sh[];
+    if (plan_overflow(hdr) || blockIdx.x >= hdr->nblk) return;   // whole block
     const int s = sort_slice_of(ss, S, blockIdx.x);
     const SortSlice q = ss[s];
     const int lb = blockIdx.x - q.bpre;
@@ -270,11 +282,13 @@ slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict
 template <int kBits>
 __global__ void __launch_bounds__(kSortThreads, 6)
 slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss,
-                     int S, const uint32_t *__restrict__ offs, uint32_t *__restrict__ vals_out) {
+                     int S, const PlanHdr *__restrict__ hdr, const uint32_t *__restrict__ offs,
+                     uint32_t *__restrict__ vals_out) {
     constexpr int kWarpsS = kSortThreads / 32;
     constexpr int kPerWarp = kSortItems * 32;
     constexpr int kT = 1 << kBits;
     extern __shared__ uint32_t wcnt[];   // [kWarpsS][kT]
+    if (plan_overflow(hdr) || blockIdx.x >= hdr->nblk) return;   // whole block
     const int s = sort_slice_of(ss, S, blockIdx.x);
     const SortSlice q = ss[s];
     const int lb = blockIdx.x - q.bpre;
@@ -329,9 +343,11 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
 
 // Per-(slice, tile) [start, end) straight from the scanned tables.
 __global__ void slice_ranges_kernel(const SortSlice *__restrict__ ss, int S,
+                                    const PlanHdr *__restrict__ hdr,
                                     const uint32_t *__restrict__ offs, int n_bins,
                                     int2 *__restrict__ range) {
     __shared__ int s_tb[64];
+    if (plan_overflow(hdr)) return;
     for (int q = threadIdx.x; q < S; q += blockDim.x) s_tb[q] = ss[q].tile_base;
     __syncthreads();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -402,38 +418,42 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
     return UGS_OK;
 }
 
-int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, int64_t hist_n,
-                    int max_tiles, int n_bins, int nblk, uint32_t *hist,
-                    uint32_t *scan_tmp, uint32_t *vals_out, int2 *bin_range,
-                    cudaStream_t st) {
-    if (n_bins > 0 && nblk == 0) {
-        // empty batch: every range is empty (slice bases are all 0 here)
-        UGS_CUDA(cudaMemsetAsync(bin_range, 0, sizeof(int2) * (size_t)n_bins, st));
-        return UGS_OK;
-    }
+int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const PlanHdr *hdr,
+                    int64_t hist_grid, int max_tiles, int n_bins, int nblk_grid,
+                    uint32_t *hist, uint32_t *scan_tmp, uint32_t *vals_out,
+                    int2 *bin_range, cudaStream_t st) {
+    // an empty batch (no sort blocks) still gets its ranges: slice_ranges
+    // writes [inst_base, inst_base) for every tile of a slice without blocks
     const size_t hsm = sizeof(uint32_t) * (size_t)max_tiles;
-    slice_hist_kernel<<<nblk, kSortThreads, hsm, st>>>(keys, d_ss, S, hist);
-    UGS_LAUNCH_CHECK("slice_hist_kernel");
-    int rc = exclusive_scan(hist, hist, (size_t)hist_n, scan_tmp, st);
-    if (rc) return rc;
-    const int bits = max_tiles <= 256 ? 8 : 10;
-    const size_t ssm = sizeof(uint32_t) * (kSortThreads / 32) * ((size_t)1 << bits);
-    if (bits == 8) {
-        slice_scatter_kernel<8><<<nblk, kSortThreads, ssm, st>>>(keys, d_ss, S, hist, vals_out);
-    } else {
-        static std::atomic<unsigned long long> attr{0};
-        if (!device_setup_done(attr)) {
-            UGS_CUDA(cudaFuncSetAttribute(slice_scatter_kernel<10>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)ssm));
-            mark_device_setup(attr);
+    if (nblk_grid > 0) {
+        slice_hist_kernel<<<nblk_grid, kSortThreads, hsm, st>>>(keys, d_ss, S, hdr, hist);
+        UGS_LAUNCH_CHECK("slice_hist_kernel");
+        int rc = exclusive_scan(hist, hist, (size_t)hist_grid, scan_tmp, st, &hdr->hist_n);
+        if (rc) return rc;
+        const int bits = max_tiles <= 256 ? 8 : 10;
+        const size_t ssm = sizeof(uint32_t) * (kSortThreads / 32) * ((size_t)1 << bits);
+        if (bits == 8) {
+            slice_scatter_kernel<8><<<nblk_grid, kSortThreads, ssm, st>>>(keys, d_ss, S, hdr,
+                                                                          hist, vals_out);
+        } else {
+            static std::atomic<unsigned long long> attr{0};
+            if (!device_setup_done(attr)) {
+                UGS_CUDA(cudaFuncSetAttribute(slice_scatter_kernel<10>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)ssm));
+                mark_device_setup(attr);
+            }
+            slice_scatter_kernel<10><<<nblk_grid, kSortThreads, ssm, st>>>(keys, d_ss, S, hdr,
+                                                                           hist, vals_out);
         }
-        slice_scatter_kernel<10><<<nblk, kSortThreads, ssm, st>>>(keys, d_ss, S, hist, vals_out);
+        UGS_LAUNCH_CHECK("slice_scatter_kernel");
     }
-    UGS_LAUNCH_CHECK("slice_scatter_kernel");
     const int th = 256;
-    slice_ranges_kernel<<<(n_bins + th - 1) / th, th, 0, st>>>(d_ss, S, hist, n_bins, bin_range);
-    UGS_LAUNCH_CHECK("slice_ranges_kernel");
+    if (n_bins > 0) {
+        slice_ranges_kernel<<<(n_bins + th - 1) / th, th, 0, st>>>(d_ss, S, hdr, hist, n_bins,
+                                                                   bin_range);
+        UGS_LAUNCH_CHECK("slice_ranges_kernel");
+    }
     return UGS_OK;
 }
 

@@ -58,6 +58,8 @@ class Renderer:
         self._cloud_key = None
         self._slices = None
         self.device_index = None
+        self.counts_pending = False
+        self.pairs = np.zeros(0, np.int64)
 
     def __del__(self):
         try:
@@ -117,6 +119,46 @@ class Renderer:
         self.generation += 1
         return self.m, self.k
 
+    def bin_async(self, cloud: GaussianCloud, specs, p: float = DEFAULT_P_MASS,
+                  slices=None):
+        """Phase 1 + binning without the host synchronisation
+        (ugs_bin_async): the counts arrive with poll(), which also reports
+        whether the batch overflowed the plan's buffers (then the forward /
+        backward / update launched on it did nothing and must be re-issued)."""
+        with self._guard(cloud.device):
+            S = len(specs)
+            if S < 1 or S > 64:
+                raise InvalidParameterError("a batch holds 1..64 slices")
+            if slices is None:
+                slices = (_lib.Slice * S)()
+                fill_slices(slices, specs, p)
+            cs = cloud.c_struct()
+            _lib.check(_lib.lib().ugs_bin_async(self._plan, ctypes.byref(cs), slices, S,
+                                                _stream()), "ugs_bin_async")
+            self._slices = slices
+            self.S = S
+            self.specs = list(specs)
+            self.p_mass = p
+            self._cloud_key = self.cloud_key(cloud)
+            self.generation += 1
+            self.counts_pending = True
+
+    def poll(self) -> bool:
+        """Counts of the last bin / bin_async (waits on one event); True if
+        that sync-free batch overflowed (the plan has grown: retry it)."""
+        S = max(self.S, 1)
+        m = (ctypes.c_int64 * S)()
+        k = (ctypes.c_int64 * S)()
+        pp = (ctypes.c_int64 * S)()
+        ovf = ctypes.c_int(0)
+        _lib.check(_lib.lib().ugs_plan_poll(self._plan, ctypes.byref(ovf), m, k, pp),
+                   "ugs_plan_poll")
+        self.m = np.frombuffer(m, np.int64)[:self.S].copy()
+        self.k = np.frombuffer(k, np.int64)[:self.S].copy()
+        self.pairs = np.frombuffer(pp, np.int64)[:self.S].copy()
+        self.counts_pending = False
+        return bool(ovf.value)
+
     def forward(self, cloud: GaussianCloud, num: torch.Tensor, den: torch.Tensor):
         cs = cloud.c_struct()
         with self._guard(cloud.device):
@@ -138,7 +180,13 @@ class Renderer:
         with self._guard(device):
             return self._accepted(device, windows)
 
+    def _settled(self):
+        if self.counts_pending and self.poll():
+            raise InvalidParameterError("the last sync-free batch overflowed the plan; "
+                                        "re-bin it before exporting")
+
     def _accepted(self, device, windows):
+        self._settled()
         M = int(self.m.sum())
         acc = torch.empty(max(M, 1), dtype=torch.int32, device=device)
         win = torch.empty((max(M, 1), 4), dtype=torch.int32, device=device) \
@@ -158,6 +206,7 @@ class Renderer:
             return self._bins(device)
 
     def _bins(self, device):
+        self._settled()
         nb = ctypes.c_int32()
         kt = ctypes.c_int64()
         L = _lib.lib()

@@ -581,7 +581,40 @@ class TrainEngine:
             self._events = {}
         return out
 
-    def forward_loss(self, idx, targets_batch=None):
+    # sync-free binning (ugs_bin_async) on one GPU: the step never waits for
+    # the host; its counts are harvested at the start of the next step (or by
+    # settle()), and a batch that overflowed the plan's buffers -- its
+    # forward / backward / Adam were device-side no-ops -- is re-issued then
+    async_bin = os.environ.get("UGS_ASYNC_BIN", "1") == "1"
+    reissued = 0          # steps re-issued after a sync-free binning overflow
+
+    def _harvest(self):
+        """Counts of the last launched step; True if it must be re-issued."""
+        r = self.renderer
+        if not r.counts_pending:
+            return False
+        ovf = r.poll()
+        if not ovf:
+            self.pairs_total += int(r.pairs.sum())
+        return ovf
+
+    def settle(self):
+        """Make the last launched step final: harvest its counts and re-issue
+        it if it overflowed (every later read of the cloud, the moments or
+        the statistics goes through here)."""
+        pend = getattr(self, "_pending", None)
+        self._pending = None
+        if pend is None:
+            self._harvest()
+            return
+        while self._harvest():
+            idx, it, targets_batch, loss_t, t0 = pend
+            self.reissued += 1
+            self.state.t = t0
+            with torch.cuda.device(self.cloud.device):
+                self._step(idx, it, False, targets_batch, loss_out=loss_t)
+
+    def forward_loss(self, idx, targets_batch=None, loss_out=None):
         """bin + forward + loss for the slices `idx` (this rank's batch)."""
         cfg = self.config
         B = len(idx)
@@ -596,13 +629,18 @@ class TrainEngine:
             ids = torch.tensor(np.asarray(idx, np.int64)).pin_memory()
             ids = ids.to(self.cloud.device, non_blocking=True)
         structs = self.batch_structs(idx)
-        self.renderer.bin(self.cloud, [self.specs[i] for i in idx], cfg.p_mass, structs)
-        self.pairs_total += int(self.renderer.pairs.sum())
+        specs = [self.specs[i] for i in idx]
+        if self.async_bin and self.world_size == 1:
+            self.renderer.bin_async(self.cloud, specs, cfg.p_mass, structs)
+        else:
+            self.renderer.bin(self.cloud, specs, cfg.p_mass, structs)
+            self.pairs_total += int(self.renderer.pairs.sum())
         num = torch.empty((B, self.h, self.w), dtype=torch.float32, device=self.cloud.device)
         den = torch.empty_like(num)
         self.renderer.forward(self.cloud, num, den)
         self._mark("loss0")
-        self.loss_mean = torch.empty((), dtype=torch.float64, device=self.cloud.device)
+        self.loss_mean = loss_out if loss_out is not None else \
+            torch.empty((), dtype=torch.float64, device=self.cloud.device)
         if targets_batch is None:
             # the loss kernel reads the dataset rows directly (no gather copy)
             lv, dpix, _ = fused_loss(num, den, self.targets, cfg.ssim_loss_weight,
@@ -652,11 +690,23 @@ class TrainEngine:
         """One full training step; returns the mean loss (python float) when
         check_finite, else the device tensor.  Runs on the cloud's device."""
         with torch.cuda.device(self.cloud.device):
-            return self._step(idx, it, check_finite, targets_batch)
+            self.settle()                    # the previous step is final
+            if check_finite:
+                return self._step(idx, it, True, targets_batch)
+            t0 = self.state.t
+            out = self._step(idx, it, False, targets_batch)
+            self._pending = (list(idx), it, targets_batch, out, t0)
+            return out
 
-    def _step(self, idx, it, check_finite, targets_batch):
+    def _step(self, idx, it, check_finite, targets_batch, loss_out=None):
         cfg = self.config
-        out = self.forward_loss(idx, targets_batch)
+        out = self.forward_loss(idx, targets_batch, loss_out)
+        if check_finite:
+            # the loss is read before the update (the reference aborts on a
+            # non-finite loss before it, trainer.py:392-396): a sync-free
+            # batch is made final first, re-binned if it overflowed
+            while self._harvest():
+                out = self.forward_loss(idx, targets_batch, self.loss_mean)
         num, den, pred, tgt, lv, dpix = out[:6]
         self.last_num, self.last_den, self.last_tgt = num, den, tgt
         if len(out) > 6:
@@ -712,6 +762,7 @@ class TrainEngine:
         """Under the peer update every rank owns a shard of m, v and the
         statistics; fetch the owners' rows so this rank holds the full state
         (before densify or a training-state save)."""
+        self.settle()
         if self.peer:
             self.barrier()
             _lib.check(_lib.lib().ugs_peer_gather(self.arena.views, self.world_size,
@@ -720,6 +771,7 @@ class TrainEngine:
 
     def load_state(self, state: "AdamState", grad_sum, grad_cnt):
         """Resume: adopt saved moments and statistics (same n as the cloud)."""
+        self.settle()
         if state.n != self.cloud.n:
             raise InvalidParameterError("training state does not match the cloud")
         self.state = state
@@ -729,6 +781,7 @@ class TrainEngine:
             self._adopt_arena()
 
     def densify(self, rng, scene_extent, threshold, max_total):
+        self.settle()
         # every rank densifies the same full state
         self.gather_state()
         avg = (self.grad_sum.double() / torch.clamp(self.grad_cnt, min=1).double()).cpu().numpy()

@@ -248,3 +248,39 @@ def test_c5_forward_4m_512():
     # the batched render-only path gives the same pixels
     pix = ug.render_slices(cloud, [spec, spec])
     assert torch.equal(pix[0], buf.pixels) and torch.equal(pix[1], buf.pixels)
+
+
+def test_async_bin_overflow_reissue():
+    """Sync-free binning (ugs_bin_async): a batch that overflows the plan's
+    capacities turns its forward / backward / Adam into device-side no-ops,
+    ugs_plan_poll reports it and the engine re-issues the step -- the
+    trajectory is bitwise the one of synchronous binning."""
+    cloud_np = cases.uniform_cloud(3, 200_000, [[-48] * 3, [48] * 3], 0.85, 1.05)
+    rng = np.random.default_rng(8)
+    poses = [cases.random_pose(rng, 12.0) for _ in range(8)]
+    specs = [ug.SliceSpec(256, 256, 0.375, ug.ProbePose(R, t)) for R, t in poses]
+    tg = torch.as_tensor(np.random.default_rng(1).random((8, 256, 256), np.float32),
+                         device="cuda")
+    cfg = ug.TrainConfig(n_gaussians=200_000, iterations=100, l_init_low=0.85,
+                         l_init_high=1.05, lr_means_start=0.016, lr_means_final=1.6e-4)
+    runs = []
+    for async_bin in (True, False):
+        eng = T.TrainEngine(ug.GaussianCloud.from_numpy(cloud_np), cfg, specs, tg)
+        eng.async_bin = async_bin
+        # size the plan on a tiny batch so the next batches overflow it
+        tiny = ug.SliceSpec(16, 16, 0.375, ug.ProbePose(np.eye(3), np.array([0, 0, 47.0])))
+        eng.renderer.bin(eng.cloud, [tiny], cfg.p_mass)
+        losses = []
+        for it, idx in enumerate(([0, 1, 2, 3], [4, 5, 6, 7], [0, 2, 4, 6]), start=1):
+            losses.append(eng.step(idx, it, check_finite=False))
+        eng.settle()
+        losses = [float(x) for x in losses]
+        runs.append((eng, losses))
+    (ea, la), (eb, lb) = runs
+    assert ea.reissued >= 1
+    assert la == lb
+    for k in ("means", "l_raw", "intensity_raw", "opacity_raw", "bg_raw"):
+        assert torch.equal(getattr(ea.cloud, k), getattr(eb.cloud, k)), k
+    assert torch.equal(ea.state.m_flat, eb.state.m_flat)
+    assert torch.equal(ea.grad_sum, eb.grad_sum) and torch.equal(ea.grad_cnt, eb.grad_cnt)
+    assert ea.pairs_total == eb.pairs_total
