@@ -148,6 +148,12 @@ UGS_API int ugs_export_bins(const ugs_plan *plan, int32_t *bin_range,
 UGS_API int ugs_forward(ugs_plan *plan, const ugs_cloud *cloud, float *num, float *den,
                 void *stream);
 
+/* Render-only forward (the serving path: rasterizer.py:182-186 render_slice,
+ * server.py:103-126): pixels (dev) float32 = clip(num / den, 0, 1) written
+ * directly, same layout as ugs_forward's outputs, bitwise equal to
+ * clip(num / den) of ugs_forward's num and den. */
+UGS_API int ugs_render(ugs_plan *plan, const ugs_cloud *cloud, float *pixels, void *stream);
+
 /* Gradient / Adam-moment layout ("AoS-12", float32, 12 n + 2 entries):
  * Gaussian g owns [12 g, 12 g + 12) = [d_means 0..2 | d_l_raw 3..8 |
  * d_intensity_raw 9 | d_opacity_raw 10 | pad 11]; [12 n, 12 n + 2) holds

@@ -40,18 +40,23 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = LIB,
+          build_dir: str = BUILD) -> str:
+    """Compile every source (stale ones only) and link ``out``; ``defines``
+    (e.g. ["UGS_WIDE_MIN=8"]) go to every translation unit -- used by
+    tools/build_variant.py for in-tree experiment variants."""
+    BUILD_ = build_dir
+    os.makedirs(BUILD_, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
     headers.append(os.path.join(ROOT, "include", "ugs.h"))
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(BUILD_, src.replace(".cu", ".o"))
         objs.append(obj)
         if not force and not _stale(obj, [path] + headers):
             continue
-        flags = list(COMMON)
+        flags = list(COMMON) + ["-D" + d for d in defines]
         if src in NO_FMAD:
             flags.append("-fmad=false")
         cmd = [nvcc()] + ARCH + flags + ["-Xptxas", "-v", "-c", path, "-o", obj]
@@ -61,13 +66,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(res.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs
+    if force or _stale(out, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", out] + objs
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc link failed")
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -12,7 +12,9 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libugs.so")
+# UGS_LIB overrides the path (experiments: tools/build_variant.py builds
+# in-tree variants with different compile-time constants)
+LIB_PATH = os.environ.get("UGS_LIB") or os.path.join(HERE, "libugs.so")
 
 _lock = threading.Lock()
 _LIB = None
@@ -68,6 +70,7 @@ EXPORTS = {
     "ugs_export_bins": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_i32),
                                        ctypes.POINTER(c_i64), c_vp]),
     "ugs_forward": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp]),
+    "ugs_render": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp]),
     "ugs_backward": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
                                     c_vp, c_vp, c_f, c_vp]),
     "ugs_grad_stats": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),

@@ -502,6 +502,21 @@ extern "C" int ugs_forward(ugs_plan *p, const ugs_cloud *c, float *num,
     return launch_forward(*p, *c, p->sorted_vals, num, den, (cudaStream_t)stream);
 }
 
+extern "C" int ugs_render(ugs_plan *p, const ugs_cloud *c, float *pixels, void *stream) {
+    if (!p || !pixels) { set_error("ugs_render: NULL argument"); return UGS_ERR_INVALID; }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (c->n != p->n) {
+        set_error("ugs_render: cloud size differs from the binned cloud");
+        return UGS_ERR_INVALID;
+    }
+    if (p->ordered) {
+        set_error("ugs_render: the strict-order forward has no render mode");
+        return UGS_ERR_INVALID;
+    }
+    return launch_forward(*p, *c, p->sorted_vals, pixels, nullptr, (cudaStream_t)stream);
+}
+
 extern "C" int ugs_backward(ugs_plan *p, const ugs_cloud *c, const float *num,
                             const float *den, const float *d_pixels, float *grad,
                             uint8_t *touched, float scale, void *stream) {

@@ -49,7 +49,10 @@ constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
 constexpr int kKeyWide = kMaxTrips + 1;      // forward: warp-per-record class
 constexpr int kKeyInvalid = kMaxTrips + 2;   // unused staging slots
 constexpr int kKeys = kMaxTrips + 3;
-constexpr int kWideMin = 9;        // forward: clipped widths >= this take the
+#ifndef UGS_WIDE_MIN
+#define UGS_WIDE_MIN 9
+#endif
+constexpr int kWideMin = UGS_WIDE_MIN;  // forward: clipped widths >= this take the
                                    // register-tile path (one record per warp)
 constexpr int kAccStride = kTile * kTile;    // forward: one private tile
 constexpr int kGroups = kRasterThreads / 16; //   buffer per 16-lane group
@@ -432,8 +435,14 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
         }
         const float abg = sigmoid_bg(bg_raw, 1), cbg = sigmoid_bg(bg_raw, 0);
         const int64_t p = sl.pix_base + (int64_t)v * sl.width + u;
-        num_out[p] = n + abg * cbg;
-        den_out[p] = d + abg;
+        const float nn = n + abg * cbg, dd = d + abg;
+        if (den_out) {
+            num_out[p] = nn;
+            den_out[p] = dd;
+        } else {   // render mode (ugs_render): clip(num / den, 0, 1), NaN kept
+            const float q = __fdiv_rn(nn, dd);
+            num_out[p] = q < 0.f ? 0.f : (q > 1.f ? 1.f : q);
+        }
     }
 }
 

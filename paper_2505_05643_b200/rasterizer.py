@@ -166,6 +166,13 @@ class Renderer:
                                               num.data_ptr(), den.data_ptr(),
                                               _stream()), "ugs_forward")
 
+    def render(self, cloud: GaussianCloud, pixels: torch.Tensor):
+        """clip(num / den, 0, 1) straight from the forward (ugs_render)."""
+        cs = cloud.c_struct()
+        with self._guard(cloud.device):
+            _lib.check(_lib.lib().ugs_render(self._plan, ctypes.byref(cs), pixels.data_ptr(),
+                                             _stream()), "ugs_render")
+
     def backward(self, cloud: GaussianCloud, num, den, dpix, grad, touched=None,
                  scale: float = 1.0):
         cs = cloud.c_struct()
@@ -318,23 +325,27 @@ def render_slice(cloud, spec: SliceSpec, p: float = DEFAULT_P_MASS,
 
 def render_slices(cloud, specs, p: float = DEFAULT_P_MASS,
                   renderer: Renderer | None = None) -> torch.Tensor:
-    """Batched render-only path: (S, H, W) clipped pixels on the device.
-    All specs must share width/height."""
+    """Batched render-only path (the serving consumer of the forward, config
+    C5): (S, H, W) clipped pixels on the device, written by the forward
+    itself (ugs_render).  Binning is sync-free once the plan is sized: the
+    host waits only for each chunk's count stage, to re-issue a chunk that
+    overflowed the plan's buffers.  All specs must share width/height."""
     cloud = as_cloud(cloud)
     h, w = specs[0].height, specs[0].width
     if any(s.height != h or s.width != w for s in specs):
         raise InvalidParameterError("render_slices needs equal slice sizes")
+    chi2_cutoff(p)
     r = renderer or default_renderer(cloud.device)
-    out = []
+    out = torch.empty((len(specs), h, w), dtype=torch.float32, device=cloud.device)
     for i in range(0, len(specs), 64):
         chunk = specs[i:i + 64]
-        r.bin(cloud, chunk, p)
-        num = torch.empty((len(chunk), h, w), dtype=torch.float32,
-                          device=cloud.device)
-        den = torch.empty_like(num)
-        r.forward(cloud, num, den)
-        out.append(torch.clamp(num / den, 0.0, 1.0))
-    return torch.cat(out)
+        view = out[i:i + len(chunk)]
+        r.bin_async(cloud, chunk, p)
+        r.render(cloud, view)
+        if r.poll():                  # overflowed: the plan has grown, retry
+            r.bin(cloud, chunk, p)
+            r.render(cloud, view)
+    return out
 
 
 # ---- host utilities with the reference signatures (rasterizer.py:33-106) --

@@ -284,3 +284,25 @@ def test_async_bin_overflow_reissue():
     assert torch.equal(ea.state.m_flat, eb.state.m_flat)
     assert torch.equal(ea.grad_sum, eb.grad_sum) and torch.equal(ea.grad_cnt, eb.grad_cnt)
     assert ea.pairs_total == eb.pairs_total
+
+
+def test_render_mode_and_overflow_retry():
+    """ugs_render writes clip(num/den) bitwise equal to the two-output
+    forward; render_slices re-issues a chunk that overflowed a small plan."""
+    cloud_np = cases.uniform_cloud(9, 300_000, [[-48] * 3, [48] * 3], 0.85, 1.05)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    rng = np.random.default_rng(21)
+    specs = [ug.SliceSpec(128, 128, 0.75, ug.ProbePose(*cases.random_pose(rng, 12.0)))
+             for _ in range(24)]
+    r = ug.Renderer()
+    # size the plan on a tiny batch: the 24-slice chunk must overflow it
+    r.bin(cloud, [ug.SliceSpec(16, 16, 0.75, ug.ProbePose(np.eye(3), np.array([0, 0, 47.0])))])
+    pix = ug.render_slices(cloud, specs, renderer=r)
+    r2 = ug.Renderer()
+    r2.bin(cloud, specs, 0.95)
+    num = torch.empty((24, 128, 128), device="cuda")
+    den = torch.empty_like(num)
+    r2.forward(cloud, num, den)
+    assert torch.equal(pix, torch.clamp(num / den, 0.0, 1.0))
+    # sized now: a second call is sync-free and identical
+    assert torch.equal(ug.render_slices(cloud, specs, renderer=r), pix)
