@@ -216,7 +216,8 @@ UGS_API int ugs_densify_apply(const ugs_cloud *src, const float *m_src,
  * metrics.py:23-98), float64 arithmetic: pred = f32(num/den);
  * loss[s] = (1-lam)*mean|pred-target| + lam*(1 - SSIM)  (or mean squared
  * error if l2 != 0) and d_pixels = d loss / d pred (float32, (S,H,W)).
- * loss_out / ssim_out (dev, S doubles) may be NULL.  `workspace` (dev) must
+ * loss_out / ssim_out (dev, S doubles) may be NULL; den may be NULL
+ * (pred = num: the public ssim / loss API on images).  `workspace` (dev) must
  * hold ugs_loss_workspace_bytes(S, H, W).  Deterministic. */
 UGS_API size_t ugs_loss_workspace_bytes(int S, int H, int W);
 UGS_API int ugs_loss(const float *num, const float *den, const float *target,

@@ -84,7 +84,7 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
         if (i < kI * kI && P >= 0 && P < H && Q >= 0 && Q < W) {
             const size_t o = base + (size_t)P * W + Q;
             ln[j] = __ldg(num + o);
-            ld[j] = __ldg(den + o);
+            ld[j] = den ? __ldg(den + o) : 1.f;   // den NULL: pred = num
             lt[j] = __ldg(target + (tbase + (size_t)P * W + Q));
         }
     }
@@ -369,7 +369,7 @@ extern "C" int ugs_loss_ex(const float *num, const float *den, const float *targ
                            const int64_t *target_index, int S, int H, int W, double lam,
                            int l2, float *d_pixels, double *loss_out, double *ssim_out,
                            double *loss_mean_out, void *workspace, void *stream) {
-    if (!num || !den || !target || !d_pixels || !workspace || S < 1 || S > 64 || H < 1 ||
+    if (!num || !target || !d_pixels || !workspace || S < 1 || S > 64 || H < 1 ||
         W < 1) {
         set_error("ugs_loss: invalid arguments (1 <= S <= 64)");
         return UGS_ERR_INVALID;

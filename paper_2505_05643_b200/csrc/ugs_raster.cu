@@ -326,15 +326,17 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
         const int n_narrow = (int)B.base[kKeyWide];
         const int n_valid = (int)B.base[kKeyInvalid];
         for (int s0 = warp * 2; s0 < n_narrow; s0 += kWarps * 2) {
+            // the group's next record may touch pixels another lane of the
+            // group still updates for this one: every iteration ends with a
+            // __syncwarp, so no lane leaves it early (no `continue`)
             const int slot = s0 + (lane >> 4);
-            if (slot >= n_narrow) continue;
-            const int j = B.order[slot];
+            const int j = B.order[slot < n_narrow ? slot : s0];
             const float4 a = B.sA[j], b = B.sB[j];
             const u64 c1 = *reinterpret_cast<const u64 *>(&B.sC[j]);   // (color, 1)
             const int2 kk = *reinterpret_cast<const int2 *>(&B.sC[j].z);
             const int k1 = kk.x, k2 = kk.y;
             const int lx = gl16 & byte_of(k1, 0), ly = gl16 >> byte_of(k1, 1);
-            if (lx >= byte_of(k2, 2)) continue;
+            if (slot < n_narrow && lx < byte_of(k2, 2)) {
             const int R = byte_of(k2, 3);   // rows per sweep
             // per lane: x fixed, log2 w = P + y (Q + C y), x and y exact
             const float dx = big_float(lx) - a.x;
@@ -377,6 +379,8 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
                 u64 *pl = reinterpret_cast<u64 *>(ptr);
                 *pl = ffma2(c1, pack2(wa, wa), *pl);
             }
+            }
+            __syncwarp();
         }
         // wide records: one per warp, all 32 lanes, register accumulation;
         // rows 2m + ph in packed pairs (m = 2q, 2q + 1): FFMA2 / FADD2

@@ -4,7 +4,13 @@ trainer.py:130-151).
 Same formulation as the reference: 11x11 Gaussian window (sigma 1.5),
 C1 = 1e-4, C2 = 9e-4, valid windows only, float64 arithmetic; the analytic
 gradient of mean SSIM uses the adjoint (zero-padded full correlation) of the
-valid-window filter.  Batched over (B, H, W) with separable float64 conv2d.
+valid-window filter.
+
+``ssim`` / ``ssim_with_grad`` / ``loss`` and their batched forms run on the
+hand-written CUDA kernel (ugs_loss: float64 filters over float32 images, the
+precision the training path feeds it).  The separable float64 conv2d
+formulation (``*_torch``) is kept only as an independent cross-check for the
+tests.
 """
 
 from __future__ import annotations
@@ -62,7 +68,7 @@ def _as4d(a, device=None):
     return t[:, None]
 
 
-def ssim_with_grad_batch(x, y):
+def ssim_with_grad_batch_torch(x, y):
     """x, y (B,H,W) -> (mean SSIM per image (B,), d meanSSIM/dx (B,H,W))."""
     x = _as4d(x)
     y = _as4d(y, x.device)
@@ -88,7 +94,7 @@ def ssim_with_grad_batch(x, y):
     return s.mean(dim=(1, 2, 3)), (grad / nv)[:, 0]
 
 
-def ssim_batch(x, y):
+def ssim_batch_torch(x, y):
     x = _as4d(x)
     y = _as4d(y, x.device)
     if x.shape != y.shape:
@@ -111,15 +117,61 @@ def _dev_for(a, b):
     return torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
 
 
+def _images(a, b):
+    """(S,H,W) float32 contiguous device tensors of two image stacks."""
+    dev = _dev_for(a, b)
+    if dev.type != "cuda":
+        raise RuntimeError("paper_2505_05643_b200 needs a CUDA device "
+                           "(there is no CPU fallback)")
+    x = (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a)))
+    y = (b if isinstance(b, torch.Tensor) else torch.as_tensor(np.asarray(b)))
+    x = x.to(device=dev, dtype=torch.float32)
+    y = y.to(device=dev, dtype=torch.float32)
+    if x.dim() == 2:
+        x = x[None]
+    if y.dim() == 2:
+        y = y[None]
+    if x.shape != y.shape:
+        raise InvalidParameterError("image dimensions differ")
+    return x.contiguous(), y.contiguous()
+
+
+def _kernel_loss(x, y, lam: float, l2: bool):
+    """ugs_loss over (S,H,W) stacks in chunks of 64: (loss (S,) float64,
+    d loss/d x (S,H,W) float32, SSIM (S,) float64)."""
+    if not l2 and lam > 0.0 and min(x.shape[-2:]) < WIN:
+        raise InvalidParameterError(f"images must be at least {WIN}x{WIN}")
+    lvs, dps, svs = [], [], []
+    for i in range(0, x.shape[0], 64):
+        lv, dp, sv = fused_loss(x[i:i + 64], None, y[i:i + 64], lam, l2)
+        lvs.append(lv)
+        dps.append(dp)
+        svs.append(sv)
+    return torch.cat(lvs), torch.cat(dps), torch.cat(svs)
+
+
+def ssim_batch(x, y):
+    """Mean SSIM per image of two (B,H,W) stacks (CUDA kernel)."""
+    x, y = _images(x, y)
+    return _kernel_loss(x, y, 1.0, False)[2]
+
+
+def ssim_with_grad_batch(x, y):
+    """(mean SSIM per image (B,), d meanSSIM/dx (B,H,W) float64): the loss
+    kernel at lam = 1 gives d(1 - SSIM)/dx."""
+    x, y = _images(x, y)
+    _, d, s = _kernel_loss(x, y, 1.0, False)
+    return s, -d.double()
+
+
 def ssim(a, b) -> float:
     """Mean SSIM of two [0,1] images (ref metrics.py:68-74)."""
-    dev = _dev_for(a, b)
-    return float(ssim_batch(_as4d(a, dev)[:, 0], _as4d(b, dev)[:, 0])[0])
+    return float(ssim_batch(a, b)[0])
 
 
 def ssim_with_grad(a, b):
-    dev = _dev_for(a, b)
-    s, g = ssim_with_grad_batch(_as4d(a, dev)[:, 0], _as4d(b, dev)[:, 0])
+    """(SSIM, dSSIM/da) (ref metrics.py:77-98)."""
+    s, g = ssim_with_grad_batch(a, b)
     return float(s[0]), g[0]
 
 
@@ -241,7 +293,7 @@ def fused_loss(num: torch.Tensor, den: torch.Tensor, target: torch.Tensor,
             raise InvalidParameterError("target / target_index shapes do not match")
     elif tgt.shape != (S, H, W):
         raise InvalidParameterError("prediction/target dimensions differ")
-    _lib.check(L.ugs_loss_ex(num.data_ptr(), den.data_ptr(), tgt.data_ptr(),
+    _lib.check(L.ugs_loss_ex(num.data_ptr(), _lib.ptr(den), tgt.data_ptr(),
                              _lib.ptr(target_index), S, H, W, float(lam), int(bool(l2)),
                              dpix.data_ptr(), lv.data_ptr(), sv.data_ptr(),
                              _lib.ptr(mean_out), ws.data_ptr(),
@@ -251,10 +303,16 @@ def fused_loss(num: torch.Tensor, den: torch.Tensor, target: torch.Tensor,
 
 
 def loss_batch(pred, target, lam: float, l2: bool = False):
-    """Per-image training loss and its pixel gradient (ref trainer.py:130-151).
+    """Per-image training loss and its pixel gradient (ref trainer.py:130-151)
+    on the CUDA kernel.  pred, target (B,H,W); returns (loss (B,) float64,
+    d_pixels (B,H,W) float64)."""
+    x, y = _images(pred, target)
+    lv, d, _ = _kernel_loss(x, y, lam, l2)
+    return lv, d.double()
 
-    pred, target (B,H,W); returns (loss (B,) float64, d_pixels (B,H,W) float64).
-    """
+
+def loss_batch_torch(pred, target, lam: float, l2: bool = False):
+    """The same in float64 torch ops (cross-check only)."""
     x = pred.to(torch.float64)
     y = target.to(device=x.device, dtype=torch.float64)
     if x.shape != y.shape:
@@ -266,7 +324,7 @@ def loss_batch(pred, target, lam: float, l2: bool = False):
     val = (1.0 - lam) * diff.abs().mean(dim=(1, 2))
     d = (1.0 - lam) * torch.sign(diff) / npx
     if lam > 0.0:
-        s, ds = ssim_with_grad_batch(x, y)
+        s, ds = ssim_with_grad_batch_torch(x, y)
         val = val + lam * (1.0 - s)
         d = d - lam * ds
     return val, d
@@ -274,8 +332,5 @@ def loss_batch(pred, target, lam: float, l2: bool = False):
 
 def loss(pred, target, lam: float, l2: bool = False):
     """Reference signature: (float, (H,W) gradient)."""
-    dev = _dev_for(pred, target)
-    x = _as4d(pred, dev)[:, 0]
-    y = _as4d(target, dev)[:, 0]
-    v, d = loss_batch(x, y, lam, l2)
+    v, d = loss_batch(pred, target, lam, l2)
     return float(v[0]), d[0]
