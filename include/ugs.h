@@ -50,7 +50,7 @@ extern "C" {
 #define UGS_API
 #endif
 
-#define UGS_ABI_VERSION 1
+#define UGS_ABI_VERSION 2
 #define UGS_TILE 16 /* pixels per tile side */
 
 typedef enum ugs_status {
@@ -167,6 +167,15 @@ UGS_API int ugs_backward(ugs_plan *plan, const ugs_cloud *cloud, const float *nu
                  const float *den, const float *d_pixels, float *grad,
                  uint8_t *touched, float scale, void *stream);
 
+/* ugs_backward that OVERWRITES grad instead of accumulating: every row of
+ * the AoS-12 buffer (all n Gaussians, zeros where no slice accepted g, pad
+ * slot = 1 where one did) and the two background entries -- the caller
+ * neither zeroes it nor has it read back (the multi-GPU step's per-rank
+ * gradient).  grad 16-byte aligned. */
+UGS_API int ugs_backward_dense(ugs_plan *plan, const ugs_cloud *cloud, const float *num,
+                               const float *den, const float *d_pixels, float *grad,
+                               float scale, void *stream);
+
 /* The single-GPU training step's backward half in one call: backward +
  * ordered accumulation + densify statistics (grad_sum/grad_cnt, may be NULL)
  * + Adam on every parameter (trainer.py:170-200, bit-compatible arithmetic),
@@ -254,6 +263,10 @@ typedef struct ugs_peer_view {
     float *grad_sum;       /* densify statistics, n */
     int32_t *grad_cnt;
     double *bg_raw;        /* the rank's background pair */
+    uint32_t *sync;        /* 64 words: ready[8], done[8], block counter --
+                              the device-side step barrier (ugs_peer_signal /
+                              ugs_peer_update / ugs_peer_wait), zeroed at
+                              allocation */
 } ugs_peer_view;
 
 UGS_API int ugs_ipc_alloc(size_t bytes, void **ptr, void *handle64);
@@ -267,16 +280,38 @@ UGS_API int ugs_ipc_free(void *ptr);
  * slot > 0 marks a Gaussian some rank's slice accepted: densify statistics,
  * trainer.py:399-401, when stats != 0), applies the bit-compatible Adam to
  * the owned rows of this rank's arena and writes the new parameter rows into
- * every peer's arena; every rank updates the background pair identically.
- * The caller brackets it with barriers (all gradients written before; all
- * parameter rows stored after). */
+ * every peer's arena (coalesced 16-byte stores over NVLink for full warps of
+ * 32 rows: shard bounds are multiples of 32, ugs_peer_shard); every rank
+ * updates the background pair identically.
+ * epoch > 0: the step barriers run on the device -- every block first waits
+ * until each rank's ready[] flag in this arena reaches `epoch` (set by the
+ * ranks' ugs_peer_signal after their gradients were written), and the last
+ * block to finish sets done[rank] = epoch in every peer's arena, which
+ * ugs_peer_wait awaits.  epoch = 0: the caller brackets the call with its
+ * own barriers (all gradients written before; all parameter rows stored
+ * after). */
 UGS_API int ugs_peer_update(const ugs_peer_view *views, int world, int rank, int64_t n,
                             int64_t lo, int64_t hi, int64_t t, const double *lr,
                             double beta1, double beta2, double eps, int stats,
+                            uint32_t epoch, void *stream);
+
+/* [lo, hi) of rank q's shard: multiples of 32 Gaussians (hi = n for the last
+ * rank), so a warp's rows move as whole 16-byte vectors. */
+UGS_API int ugs_peer_shard(int64_t n, int world, int q, int64_t *lo, int64_t *hi);
+
+/* Device-side step barrier halves (stream-ordered, no host involvement):
+ * signal stores ready[rank] = epoch into every peer's arena after a
+ * system-scope fence (this rank's gradient, written by earlier kernels on the
+ * stream, is then visible to the peers); wait spins until done[q] >= epoch
+ * for every rank q (all parameter rows of the step stored here).  Spins are
+ * bounded (~20 s): a missing peer traps the kernel instead of hanging. */
+UGS_API int ugs_peer_signal(const ugs_peer_view *views, int world, int rank, uint32_t epoch,
                             void *stream);
+UGS_API int ugs_peer_wait(const ugs_peer_view *views, int world, int rank, uint32_t epoch,
+                          void *stream);
 
 /* Before densify: copies the m, v, grad_sum, grad_cnt rows owned by other
- * ranks (shard q = [n q / W, n (q+1) / W)) into this rank's arena. */
+ * ranks (the ugs_peer_shard shards) into this rank's arena. */
 UGS_API int ugs_peer_gather(const ugs_peer_view *views, int world, int rank, int64_t n,
                             void *stream);
 

@@ -50,7 +50,7 @@ class PeerView(ctypes.Structure):
     """struct ugs_peer_view (include/ugs.h): one rank's arena, as mapped here."""
     _fields_ = [("means", c_vp), ("l_raw", c_vp), ("intensity_raw", c_vp),
                 ("opacity_raw", c_vp), ("grad", c_vp), ("m", c_vp), ("v", c_vp),
-                ("grad_sum", c_vp), ("grad_cnt", c_vp), ("bg_raw", c_vp)]
+                ("grad_sum", c_vp), ("grad_cnt", c_vp), ("bg_raw", c_vp), ("sync", c_vp)]
 
 
 EXPORTS = {
@@ -79,6 +79,8 @@ EXPORTS = {
                                      ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp,
                                      c_vp]),
+    "ugs_backward_dense": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
+                                          c_vp, c_f, c_vp]),
     "ugs_backward_adam": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
                                          c_f, c_vp, c_vp, c_i64,
                                          ctypes.POINTER(ctypes.c_double),
@@ -111,7 +113,13 @@ EXPORTS = {
                                        c_i64, c_i64, c_i64, c_i64,
                                        ctypes.POINTER(ctypes.c_double), ctypes.c_double,
                                        ctypes.c_double, ctypes.c_double, ctypes.c_int,
-                                       c_vp]),
+                                       ctypes.c_uint32, c_vp]),
+    "ugs_peer_shard": (ctypes.c_int, [c_i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_i64),
+                                      ctypes.POINTER(c_i64)]),
+    "ugs_peer_signal": (ctypes.c_int, [ctypes.POINTER(PeerView), ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_uint32, c_vp]),
+    "ugs_peer_wait": (ctypes.c_int, [ctypes.POINTER(PeerView), ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_uint32, c_vp]),
     "ugs_peer_gather": (ctypes.c_int, [ctypes.POINTER(PeerView), ctypes.c_int, ctypes.c_int,
                                        c_i64, c_vp]),
 }

@@ -534,6 +534,27 @@ extern "C" int ugs_backward(ugs_plan *p, const ugs_cloud *c, const float *num,
                            scale, nullptr, (cudaStream_t)stream);
 }
 
+extern "C" int ugs_backward_dense(ugs_plan *p, const ugs_cloud *c, const float *num,
+                                  const float *den, const float *d_pixels, float *grad,
+                                  float scale, void *stream) {
+    if (!p || !num || !den || !d_pixels || !grad) {
+        set_error("ugs_backward_dense: NULL argument");
+        return UGS_ERR_INVALID;
+    }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (c->n != p->n) {
+        set_error("ugs_backward_dense: buffers do not match this cloud");
+        return UGS_ERR_INVALID;
+    }
+    if (((uintptr_t)grad & 15) != 0) {
+        set_error("ugs_backward_dense: grad must be 16-byte aligned");
+        return UGS_ERR_INVALID;
+    }
+    return launch_backward(*p, *c, p->sorted_vals, num, den, d_pixels, grad, nullptr, scale,
+                           nullptr, (cudaStream_t)stream, true);
+}
+
 extern "C" int ugs_backward_adam(ugs_plan *p, const ugs_cloud *c, const float *num,
                                  const float *den, const float *d_pixels, float scale,
                                  float *m, float *v, int64_t t, const double *lr,

@@ -265,6 +265,6 @@ struct AdamArgs;   // ugs_adam.cuh
 int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     const float *num, const float *den, const float *dpix,
                     float *grad, uint8_t *touched, float scale, const AdamArgs *adam,
-                    cudaStream_t st);
+                    cudaStream_t st, bool dense = false);
 
 }  // namespace ugs

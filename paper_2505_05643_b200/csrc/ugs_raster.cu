@@ -817,7 +817,10 @@ constexpr int kUpdRows = 64;    // staged record-gradient rows per warp and pass
 // single GPU) densify statistics and Adam run for EVERY Gaussian --
 // zero-gradient rows still move (trainer.py:182-199) -- and the dense
 // gradient never touches HBM; or (adam == 0) the rows are added into the
-// dense AoS-12 buffer.
+// dense AoS-12 buffer; or (adam == 2, the multi-GPU step) every row of the
+// dense buffer is WRITTEN -- the scaled sum, zeros for Gaussians no slice
+// accepted, the pad slot = accepted -- so the caller neither zeroes nor
+// reads it first.
 __global__ void __launch_bounds__(kUpdThreads, 4)
 update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restrict__ warp_rec,
                      const float *__restrict__ rgrad, int S, int64_t nwarp_all, int64_t n,
@@ -841,6 +844,8 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
     int *s_off = off_all[warp], *s_base = base_all[warp];
     uint8_t *s_rs = rs_all[warp];
     const uint32_t lt = (1u << lane) - 1u;
+    const int mode = adam;
+    adam = mode == 1;
     if (adam && g < n) {
         // the update's streams (moments, parameters) start towards L2 while
         // the gather runs: no registers held, the latency overlaps
@@ -1022,6 +1027,12 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         for (int j = 0; j < 11; ++j) gr[j] = acc[j];
         gr[11] = 0.f;
         adam_gaussian(g, gr, m + kG * g, v + kG * g, p, k, hit, grad_sum, grad_cnt);
+    } else if (mode == 2) {
+        float4 *row = reinterpret_cast<float4 *>(grad + kG * g);
+        row[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        row[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        row[2] = make_float4(acc[8], acc[9], acc[10], hit ? 1.f : 0.f);
+        if (touched) touched[g] = hit ? 1 : 0;
     } else if (hit) {
         float *row = grad + kG * g;
 #pragma unroll
@@ -1068,6 +1079,7 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
                                    AdamConst k, const PlanHdr *__restrict__ hdr) {
     if (threadIdx.x != 0 || plan_overflow(hdr)) return;
     const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
+    // adam: 0 accumulate into grad_bg, 1 Adam step, 2 overwrite grad_bg
     float g[2] = {adam ? 0.f : grad_bg[0], adam ? 0.f : grad_bg[1]};
     for (int s = 0; s < S; ++s) {
         const double d_cbg = (double)(float)abg * sums[s].x;   // sum dpix*f32(a_bg)/ssum
@@ -1075,7 +1087,7 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
         g[0] += (float)((double)scale * d_cbg * cbg * (1.0 - cbg));
         g[1] += (float)((double)scale * d_abg * abg * (1.0 - abg));
     }
-    if (adam) {
+    if (adam == 1) {
         adam_bg(bg_raw, g, m_bg, v_bg, k);
     } else {
         grad_bg[0] = g[0];
@@ -1128,7 +1140,7 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
 int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                     const float *num, const float *den, const float *dpix,
                     float *grad, uint8_t *touched, float scale, const AdamArgs *adam,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool dense) {
     if (p.S == 0) return UGS_OK;
     int rc = set_smem_attrs();
     if (rc) return rc;
@@ -1159,7 +1171,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                                                adam->v + kG * c.n, adam->k, plan_hdr(p.b));
     } else {
         bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
-                                               grad + kG * c.n, scale, 0, nullptr, nullptr,
+                                               grad + kG * c.n, scale, dense ? 2 : 0,
+                                               nullptr, nullptr,
                                                AdamConst{}, plan_hdr(p.b));
     }
     UGS_LAUNCH_CHECK("bg_finalize_kernel");
@@ -1177,7 +1190,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     }
     stage_end(pm, kStageFinalize, st);
     stage_begin(pm, kStageUpdate, st);
-    if (c.n > 0 && (adam || p.m_grid > 0)) {
+    if (c.n > 0 && (adam || dense || p.m_grid > 0)) {
         const int64_t nblk = (c.n + kPrepThreads - 1) / kPrepThreads;
         const int64_t nwarp_all = nblk * (kPrepThreads / 32);
         static_assert(kUpdThreads == kPrepThreads, "update blocks mirror count blocks");
@@ -1186,7 +1199,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
             adam && ((((uintptr_t)c.means | (uintptr_t)c.l_raw | (uintptr_t)adam->m |
                        (uintptr_t)adam->v) & 15) == 0);
         update_gather_kernel<<<(unsigned)nblk, kUpdThreads, 0, st>>>(
-            p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale, adam ? 1 : 0,
+            p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale,
+            adam ? 1 : (dense ? 2 : 0),
             grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
             adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,
             adam ? adam->grad_cnt : nullptr, aligned, plan_hdr(p.b));

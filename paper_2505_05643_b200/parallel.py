@@ -114,7 +114,8 @@ class PeerArena:
     _FIELDS = (("means", 3, 0, "<f4"), ("l_raw", 6, 0, "<f4"),
                ("intensity_raw", 1, 0, "<f4"), ("opacity_raw", 1, 0, "<f4"),
                ("grad", 12, 4, "<f4"), ("m", 12, 4, "<f4"), ("v", 12, 4, "<f4"),
-               ("grad_sum", 1, 0, "<f4"), ("grad_cnt", 1, 0, "<i4"))
+               ("grad_sum", 1, 0, "<f4"), ("grad_cnt", 1, 0, "<i4"),
+               ("sync", 0, 64, "<u4"))   # device-side step barrier flags
 
     def __init__(self, n: int, world: int, rank: int, group=None):
         import ctypes
@@ -132,6 +133,12 @@ class PeerArena:
         handle = (ctypes.c_ubyte * 64)()
         _lib.check(L.ugs_ipc_alloc(self.nbytes, ctypes.byref(ptr), handle), "ugs_ipc_alloc")
         self.ptr = ptr.value
+        # the barrier flags start at 0 (epochs count from 1) before any peer
+        # can map and signal this arena
+        torch.as_tensor(_CudaArray(self.ptr + self.offsets["sync"], (64,), "<u4"),
+                        device="cuda").zero_()
+        torch.cuda.synchronize()
+        self.epoch = 0
         handles = [None] * world
         dist.all_gather_object(handles, bytes(handle), group=group)
         self.bases = []
@@ -147,11 +154,13 @@ class PeerArena:
         for q, b in enumerate(self.bases):
             v = self.views[q]
             for name in ("means", "l_raw", "intensity_raw", "opacity_raw", "grad", "m",
-                         "v", "grad_sum", "grad_cnt", "bg_raw"):
+                         "v", "grad_sum", "grad_cnt", "bg_raw", "sync"):
                 setattr(v, name, b + self.offsets[name])
         # this rank's arena as torch tensors (aliases, no copies)
         self.t = {}
         for name, per, extra, ts in self._FIELDS:
+            if name == "sync":
+                continue
             shape = (n, per) if (per > 1 and extra == 0) else (per * n + extra,)
             self.t[name] = torch.as_tensor(
                 _CudaArray(self.ptr + self.offsets[name], shape, ts), device="cuda")
@@ -159,8 +168,14 @@ class PeerArena:
             _CudaArray(self.ptr + self.offsets["bg_raw"], (2,), "<f8"), device="cuda")
 
     def shard(self):
-        """[lo, hi) of the Gaussians this rank updates."""
-        return (self.n * self.rank) // self.world, (self.n * (self.rank + 1)) // self.world
+        """[lo, hi) of the Gaussians this rank updates (ugs_peer_shard:
+        multiples of 32, so a warp's rows move as 16-byte vectors)."""
+        import ctypes
+        from . import _lib
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().ugs_peer_shard(self.n, self.world, self.rank, ctypes.byref(lo),
+                                             ctypes.byref(hi)), "ugs_peer_shard")
+        return lo.value, hi.value
 
     def close(self, barrier) -> None:
         """Unmap the peers and free this arena once every rank is done with it."""

@@ -182,6 +182,16 @@ class Renderer:
                 dpix.data_ptr(), grad.data_ptr(), _lib.ptr(touched), float(scale),
                 _stream()), "ugs_backward")
 
+    def backward_dense(self, cloud: GaussianCloud, num, den, dpix, grad, scale: float = 1.0):
+        """ugs_backward_dense: grad (AoS-12) OVERWRITTEN with scale x the
+        batch gradient, pad slot = accepted (no zeroing needed)."""
+        cs = cloud.c_struct()
+        with self._guard(cloud.device):
+            _lib.check(_lib.lib().ugs_backward_dense(
+                self._plan, ctypes.byref(cs), num.data_ptr(), den.data_ptr(),
+                dpix.data_ptr(), grad.data_ptr(), float(scale), _stream()),
+                "ugs_backward_dense")
+
     def accepted(self, device, windows: bool = False):
         """(accepted int64 per slice list, windows (M,4) int64 or None)."""
         with self._guard(device):

@@ -529,16 +529,35 @@ class TrainEngine:
             old.close(self.barrier)
         self.barrier()
 
+    # the step's two barriers as device flags in the peer arenas (signal /
+    # fused wait-and-signal inside ugs_peer_update / wait) instead of two
+    # 1-element NCCL all-reduces; UGS_PEER_FLAGS=0 keeps the collectives
+    device_barriers = os.environ.get("UGS_PEER_FLAGS", "1") == "1"
+
     def _peer_step(self, lrs):
         st = self.state
         st.t += 1
         lo, hi = self.arena.shard()
-        self.barrier()            # every rank's gradient is in its arena
-        _lib.check(_lib.lib().ugs_peer_update(
-            self.arena.views, self.world_size, self.rank, self.cloud.n, lo, hi, st.t,
-            _lr_array(lrs), st.beta1, st.beta2, st.eps, 1, _stream()), "ugs_peer_update")
+        L = _lib.lib()
+        a, W, r = self.arena, self.world_size, self.rank
+        if self.device_barriers:
+            a.epoch += 1
+            e = a.epoch
+            # ready: this rank's gradient is in its arena (peers wait on it
+            # inside their update kernels)
+            _lib.check(L.ugs_peer_signal(a.views, W, r, e, _stream()), "ugs_peer_signal")
+            _lib.check(L.ugs_peer_update(a.views, W, r, self.cloud.n, lo, hi, st.t,
+                                         _lr_array(lrs), st.beta1, st.beta2, st.eps, 1, e,
+                                         _stream()), "ugs_peer_update")
+            # done: every rank stored its shard's rows here
+            _lib.check(L.ugs_peer_wait(a.views, W, r, e, _stream()), "ugs_peer_wait")
+        else:
+            self.barrier()            # every rank's gradient is in its arena
+            _lib.check(L.ugs_peer_update(a.views, W, r, self.cloud.n, lo, hi, st.t,
+                                         _lr_array(lrs), st.beta1, st.beta2, st.eps, 1, 0,
+                                         _stream()), "ugs_peer_update")
+            self.barrier()            # every parameter row is stored everywhere
         self.cloud.mark_mutated()
-        self.barrier()            # every parameter row is stored everywhere
 
     def _alloc_stats(self):
         n, dev = self.cloud.n, self.cloud.device
@@ -742,8 +761,8 @@ class TrainEngine:
             self._mark("backward_adam1")
             return loss_val if check_finite else loss_t
         if self.peer:
-            self.grad.zero_()
-            self.renderer.backward(self.cloud, num, den, dpix, self.grad, None, scale)
+            # the rank's gradient rows are overwritten (no 48 B/Gaussian memset)
+            self.renderer.backward_dense(self.cloud, num, den, dpix, self.grad, scale)
             self._mark("adam0")
             self._peer_step(lrs)
             self._mark("adam1")

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for name in header_functions():
         assert hasattr(L, name), name
     assert set(header_functions()) == set(_lib.EXPORTS)
-    assert L.ugs_abi_version() == 1
+    assert L.ugs_abi_version() == 2
 
 
 def test_struct_layout():
@@ -38,9 +38,10 @@ def test_struct_layout():
     assert ctypes.sizeof(_lib.Slice) == 144
     assert _lib.Slice.pix_base.offset == 136
     assert ctypes.sizeof(_lib.Cloud) == 56
-    # ugs_peer_view: 10 device pointers
-    assert ctypes.sizeof(_lib.PeerView) == 80
+    # ugs_peer_view: 11 device pointers
+    assert ctypes.sizeof(_lib.PeerView) == 88
     assert _lib.PeerView.bg_raw.offset == 72
+    assert _lib.PeerView.sync.offset == 80
 
 
 def test_error_path_without_gpu():

@@ -46,9 +46,10 @@ def _params(cloud):
         "bg": np.array([cloud.bg_intensity_raw, cloud.bg_opacity_raw])}
 
 
-def _worker(rank, world, port, densify, q, peer=False):
+def _worker(rank, world, port, densify, q, peer=False, flags=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                      UGS_PEER_UPDATE="1" if peer else "0")
+                      UGS_PEER_UPDATE="1" if peer else "0",
+                      UGS_PEER_FLAGS="1" if flags else "0")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2505_05643_b200 as ug
@@ -67,11 +68,11 @@ def _free_port():
     return p
 
 
-def _run_two(densify, peer=False):
+def _run_two(densify, peer=False, flags=True):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, densify, q, peer))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, densify, q, peer, flags))
              for r in range(2)]
     for p in procs:
         p.start()
@@ -124,3 +125,38 @@ def test_peer_update_densify_in_lockstep():
     for k in out[0]:
         assert np.array_equal(out[0][k], out[1][k]), k
         np.testing.assert_allclose(out[0][k], ref[0][k], rtol=1e-3, atol=1e-4, err_msg=k)
+
+
+def test_peer_device_barriers_match_collective_barriers():
+    """The step barriers as device flags in the peer arenas (ugs_peer_signal
+    / ugs_peer_update(epoch) / ugs_peer_wait) give bitwise the trajectory of
+    the NCCL-style host barriers; n = 400 leaves the last rank a partial
+    warp (the shard tail path of the coalesced all-gather)."""
+    a = _run_two(densify=0, peer=True, flags=True)
+    b = _run_two(densify=0, peer=True, flags=False)
+    for k in a[0]:
+        assert np.array_equal(a[0][k], b[0][k]), k
+        assert np.array_equal(a[1][k], b[1][k]), k
+
+
+def test_bench_two_ranks_one_device():
+    """bench.py's N > 1 path end to end: two ranks on the one GPU over gloo
+    (UGS_BENCH_ONE_DEVICE=1), fused peer update with device barriers; one
+    JSON line from rank 0 with n_gpus = 2 (a functional check, not a
+    measurement)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, UGS_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--n-gaussians", "200000", "--no-tts", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2")
