@@ -185,7 +185,18 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def cpu_reference_rate(a, vol, specs, n_slices, cfg, warmup=1):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_reference_rate(a, vol, specs, n_slices, cfg, warmup=1, workers=None):
     """The reference's per-iteration path (oracle port, all host cores):
     rasterize -> loss -> backward -> adam_step per slice.  Returns
     (slices/s, seconds, cores)."""
@@ -200,7 +211,7 @@ def cpu_reference_rate(a, vol, specs, n_slices, cfg, warmup=1):
     v = {k: np.zeros_like(params[k]) for k in O.GROUPS}
     m["bg"] = np.zeros(2, np.float32)
     v["bg"] = np.zeros(2, np.float32)
-    cores = cpu_cores()
+    cores = workers or cpu_cores()
     targets = [sample_slice(vol, specs[i]).pixels for i in range(n_slices + warmup)]
     consts = [O.slice_constants(s.pose.rotation, s.pose.translation, s.width, s.height,
                                 s.spacing, cfg.p_mass) for s in specs[:n_slices + warmup]]
@@ -243,7 +254,7 @@ def run_reference(a):
                                             "batch_per_step": 1,
                                             "implementation": "oracle port of echosplat (C + numpy), host CPU"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -537,6 +548,10 @@ def run_ours(a):
         "roofline": {"bound": "fp32", "kernel": dom + "_kernel", "achieved": achieved,
                      "peak": peak_fp32, "unit": "TFLOP/s", "frac": achieved / peak_fp32,
                      "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum of this kernel from one ncu "
+                                       "--set full capture of the same command (not "
+                                       "measurable inside an uninstrumented run)",
                      "note": f"algorithmic {flop_pp} FLOP/pair (reference operator count, "
                              "SURVEY 8d) x pairs per launch / CUDA-event launch time (stage "
                              "events on the launch stream, a second pass of the same K steps); "
@@ -552,11 +567,18 @@ def run_ours(a):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             rate, dt, cores = cpu_reference_rate(a, vol, specs, a.cpu_sample, cfg, warmup=1)
+            # the reference's sequential mode too (workers=1, its
+            # deterministic default), on a smaller sample
+            n1 = max(2, a.cpu_sample // 8)
+            rate1, dt1, _ = cpu_reference_rate(a, vol, specs, n1, cfg, warmup=1, workers=1)
             line["cpu_baseline"] = {
                 "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                "cpu_model": cpu_model(),
                 "sample": f"{a.cpu_sample} slices of the same workload, one reference "
                           f"iteration each (rasterize->loss->backward->adam_step), "
-                          f"{dt:.1f} s, workers={cores}"}
+                          f"{dt:.1f} s, workers={cores}",
+                "workers_1": {"value": rate1, "unit": UNIT, "cores": 1,
+                              "sample": f"{n1} slices, {dt1:.1f} s, workers=1"}}
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_cores(),
                                     "kind": "port", "sample": f"failed: {exc!r}"}
