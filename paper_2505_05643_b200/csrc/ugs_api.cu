@@ -140,7 +140,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     PlanBuffers &b = p->b;
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.warp_inst, b.rec_bucket, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
-                    b.rec_gid, b.rec_inst, b.idata, b.keys, b.vals, b.keys2,
+                    b.rec_gid, b.rec_inst, b.frag, b.keys, b.vals, b.keys2,
                     b.vals2, b.partial, b.rgrad, b.bg_sums,
                     b.hist,
                     b.scan_tmp, b.sort_slices, b.bin_range,
@@ -194,13 +194,13 @@ int grow_to(ugs_plan *p, int64_t m_need, int64_t k_need, int max_tiles, int S) {
                      "alloc rec_bucket")))
         return rc;
     const size_t kneed = (size_t)k_need + 1;
-    if (kneed > b.inst_cap || !b.idata) {
+    if (kneed > b.inst_cap || !b.frag) {
         // all-or-nothing: every pointer is nulled when freed and the capacity
         // is published only after every allocation succeeded, so a failed
         // (OOM) grow leaves no dangling pointer and no stale capacity
-        void **bufs[] = {(void **)&b.idata, (void **)&b.keys, (void **)&b.vals,
+        void **bufs[] = {(void **)&b.frag, (void **)&b.keys, (void **)&b.vals,
                          (void **)&b.keys2, (void **)&b.vals2, (void **)&b.partial};
-        const size_t elem[] = {sizeof(Inst), sizeof(uint32_t), sizeof(uint32_t),
+        const size_t elem[] = {sizeof(Frag), sizeof(uint32_t), sizeof(uint32_t),
                                sizeof(uint32_t), sizeof(uint32_t), sizeof(float) * kPartial};
         for (void **q : bufs) {
             if (*q) cudaFree(*q);
@@ -421,7 +421,7 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
     stage_begin(p, kStageEmit, st);
     if (c->n > 0) {
         if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
-                                      b.rec, b.rec_gid, b.rec_inst, b.idata, b.keys, hdr,
+                                      b.rec, b.rec_gid, b.rec_inst, b.frag, b.keys, hdr,
                                       p->m_grid, b.win_sparse, b.amask, b.wcnt, b.warp_rec,
                                       b.warp_inst, b.rec_bucket, st)))
             return rc;
@@ -602,12 +602,19 @@ __global__ void export_accepted_kernel(const Rec *__restrict__ rec,
 }
 
 __global__ void export_sorted_kernel(const uint32_t *__restrict__ vals,
-                                     const Inst *__restrict__ idata,
+                                     const int32_t *__restrict__ rec_inst, int64_t m,
                                      const int32_t *__restrict__ gid, int64_t k,
                                      int32_t *__restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
-    out[i] = gid[__float_as_int(idata[vals[i]].w)];
+    // the instance's record: the last r with rec_inst[r] <= instance
+    const int32_t inst = (int32_t)vals[i];
+    int64_t lo = 0, hi = m - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (rec_inst[mid] <= inst) lo = mid; else hi = mid - 1;
+    }
+    out[i] = gid[lo];
 }
 }  // namespace
 }  // namespace ugs
@@ -637,7 +644,7 @@ extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
     if (sorted_gauss && p->k_total > 0) {
         const int th = 256;
         export_sorted_kernel<<<(unsigned)((p->k_total + th - 1) / th), th, 0, st>>>(
-            p->sorted_vals, p->b.idata, p->b.rec_gid, p->k_total, sorted_gauss);
+            p->sorted_vals, p->b.rec_inst, p->m_total, p->b.rec_gid, p->k_total, sorted_gauss);
         UGS_LAUNCH_CHECK("export_sorted_kernel");
     }
     return UGS_OK;

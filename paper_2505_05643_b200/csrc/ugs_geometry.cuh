@@ -204,4 +204,20 @@ __device__ __forceinline__ TileRect tile_rect(int iu0, int iu1, int iv0, int iv1
     return t;
 }
 
+// Decoded Frag rectangle (tile-relative, inclusive).
+struct FragRect {
+    int x0, x1, y0, y1, pu, pv;
+};
+__device__ __forceinline__ FragRect frag_rect(float bits_f) {
+    const unsigned b = (unsigned)__float_as_int(bits_f);
+    FragRect r;
+    r.x0 = b & 15;
+    r.x1 = (b >> 4) & 15;
+    r.y0 = (b >> 8) & 15;
+    r.y1 = (b >> 12) & 15;
+    r.pu = (b >> 16) & 15;
+    r.pv = (b >> 20) & 15;
+    return r;
+}
+
 }  // namespace ugs

@@ -40,6 +40,19 @@ struct Rec {
 // record's own.  (D, E, F, bits(record index)).
 using Inst = float4;
 
+// Per tile instance (32 B), written by the build in instance order (a
+// record's instances consecutive, row-major tiles): everything the raster
+// kernels need, so a tile's staging is one 32-byte gather per instance
+// (cp.async, sorted id -> Frag) instead of a dependent chain through the
+// record.
+//   q0 = (A, B2, C, color)   the record's quadratic and colour
+//   q1 = (D, E, F, bits)     the instance's exact re-expansion (Inst), and the
+//        clipped rectangle + expansion pixel relative to the tile origin:
+//        x0 | x1 << 4 | y0 << 8 | y1 << 12 | pu << 16 | pv << 20
+struct Frag {
+    float4 q0, q1;
+};
+
 // Per-slice parameters of the single-pass bin sort (ugs_sort.cu).
 struct SortSlice {
     int inst_base, k;        // the slice's instance segment
@@ -80,7 +93,7 @@ struct PlanBuffers {
     size_t rgrad_cap = 0;
     double2 *bg_sums = nullptr;     // [64] per-slice background gradient sums
     // instances
-    Inst *idata = nullptr;          // [K] (D, E, F, record) of each (unsorted) instance
+    Frag *frag = nullptr;           // [K] every (unsorted) instance's raster data
     uint32_t *keys = nullptr, *vals = nullptr;     // sorted (key, instance)
     uint32_t *keys2 = nullptr, *vals2 = nullptr;   // ping-pong
     float *partial = nullptr;       // [K][8] backward per-instance partial sums
@@ -232,7 +245,7 @@ int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nb
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        Inst *idata, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
+                        Frag *frag, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
                         const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
                         int32_t *rec_bucket, cudaStream_t st);

@@ -305,7 +305,7 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      const int32_t *__restrict__ rec_bucket,
                      const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
                      int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
-                     Inst *__restrict__ idata, uint32_t *__restrict__ keys) {
+                     Frag *__restrict__ frag, uint32_t *__restrict__ keys) {
     if (plan_overflow(hdr)) return;
     const int64_t m_total = (int64_t)hdr->m;
     const int ln = threadIdx.x & 31;
@@ -390,19 +390,25 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const PlaneForm P = plane_form(mu, f, L, w);
     const double kq = -0.72134752044448170368;   // -0.5 * log2(e)
     const double log2a = log2((double)alpha);
-    rec[r].r0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
-                            (float)(kq * P.H11), color);
+    const float4 q0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
+                                  (float)(kq * P.H11), color);
+    rec[r].r0 = q0;
     rec[r].r1 = make_float4(__uint_as_float(pw.x), __uint_as_float(pw.y), alpha,
                             __int_as_float(P.ui | (P.vi << 16)));
     const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
     const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
-            const TileRect t = tile_rect(w.iu0, w.iu1, w.iv0, w.iv1, tx * kTile,
-                                         ty * kTile, P.ui, P.vi);
+            const int tu0 = tx * kTile, tv0 = ty * kTile;
+            const TileRect t = tile_rect(w.iu0, w.iu1, w.iv0, w.iv1, tu0, tv0, P.ui, P.vi);
             double D, E, F;
             expansion(P, t.pu, t.pv, kq, log2a, D, E, F);
-            idata[inst] = make_float4((float)D, (float)E, (float)F, __int_as_float((int)r));
+            const int bits = (t.x0 - tu0) | ((t.x1 - tu0) << 4) | ((t.y0 - tv0) << 8) |
+                             ((t.y1 - tv0) << 12) | ((t.pu - tu0) << 16) |
+                             ((t.pv - tv0) << 20);
+            Frag *fp = frag + inst;
+            fp->q0 = q0;
+            fp->q1 = make_float4((float)D, (float)E, (float)F, __int_as_float(bits));
             keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
             ++inst;
         }
@@ -497,7 +503,7 @@ int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nb
 int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         const uint2 *blk_off, int nblk, const int64_t *slice_base,
                         Rec *rec, int32_t *rec_gid, int32_t *rec_inst,
-                        Inst *idata, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
+                        Frag *frag, uint32_t *keys, const PlanHdr *hdr, int64_t m_grid,
                         const uint2 *win_sparse, const uint32_t *amask,
                         const uint2 *wcnt, int32_t *warp_rec, int32_t *warp_inst,
                         int32_t *rec_bucket, cudaStream_t st) {
@@ -512,7 +518,7 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                            kBuildThreads, 0, st>>>(
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices, S,
         slice_base, hdr, nwarp_all, amask, warp_rec, warp_inst, rec_bucket, win_sparse, rec,
-        rec_gid, rec_inst, idata, keys);
+        rec_gid, rec_inst, frag, keys);
     UGS_LAUNCH_CHECK("build_records_kernel");
     return UGS_OK;
 }

@@ -2,7 +2,9 @@
 //
 // One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted instance list
 // (ascending Gaussian index, from the stable bin sort) is staged through
-// shared memory in batches of 256.  While staging, one thread per instance
+// shared memory in batches of 256: each instance's 32-byte Frag arrives by
+// cp.async (LDGSTS) issued one batch ahead, so the gathers overlap the
+// previous batch's accumulation.  While staging, one thread per instance
 // clips the record's window to the tile and precomputes what the lanes need
 // (rectangle, offsets from the instance's expansion pixel, lane layout); the
 // batch is then ordered by loop trip count with a stable counting sort, so
@@ -95,14 +97,49 @@ __device__ __forceinline__ float big_float(int x) {
     return __int_as_float(0x4B000000 | x);
 }
 
-__device__ __forceinline__ void load_inst(const Rec *__restrict__ rec,
-                                          const Inst *__restrict__ idata,
-                                          uint32_t inst, float4 &I, Rec &R) {
-    I = __ldg(idata + inst);
-    const float4 *src = reinterpret_cast<const float4 *>(rec + __float_as_int(I.w));
-    R.r0 = __ldg(src);
-    R.r1 = __ldg(src + 1);
+// Asynchronous staging of a tile's instances: each thread gathers the
+// 32-byte Frag of its slot of the NEXT batch with cp.async (LDGSTS, L2 only)
+// straight into shared memory while the CTA accumulates the current batch;
+// the sorted ids are prefetched a batch further ahead in a register.  A slot
+// is only ever written and read by its own thread, so the copy needs no
+// barrier: cp.async.wait_all makes it visible to that thread.
+__device__ __forceinline__ void stage_async(Frag *dst, const Frag *src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16),
+                 "l"(reinterpret_cast<const char *>(src) + 16)
+                 : "memory");
 }
+__device__ __forceinline__ void stage_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Per-thread staging pipeline over a tile's sorted range [lo, hi): `cur` is
+// the instance id whose Frag is in flight to raw[tid], `nxt` the next
+// batch's id (0 past the end).
+struct StagePipe {
+    uint32_t cur, nxt;
+    __device__ __forceinline__ void start(const uint32_t *__restrict__ vals,
+                                          const Frag *__restrict__ frag, Frag *raw, int lo,
+                                          int hi) {
+        const int i = lo + (int)threadIdx.x;
+        cur = i < hi ? __ldg(vals + i) : 0u;
+        if (i < hi) stage_async(raw + threadIdx.x, frag + cur);
+        stage_commit();
+        nxt = i + kBatch < hi ? __ldg(vals + i + kBatch) : 0u;
+    }
+    // after this thread staged batch b0 from raw: fetch batch b0 + kBatch
+    __device__ __forceinline__ void advance(const uint32_t *__restrict__ vals,
+                                            const Frag *__restrict__ frag, Frag *raw, int b0,
+                                            int hi) {
+        const int i = b0 + kBatch + (int)threadIdx.x;
+        cur = nxt;
+        if (i < hi) stage_async(raw + threadIdx.x, frag + cur);
+        stage_commit();
+        nxt = i + kBatch < hi ? __ldg(vals + i + kBatch) : 0u;
+    }
+};
 
 // Shared-memory state of one staged batch.
 //   sA = (C1x, C1y, D, E)   x = big_float(lx) - C1x: exact integer offset of
@@ -121,14 +158,17 @@ struct Layout {   // two-stream layouts (backward), after the Batch
     int4 sL[kBatch], sM[kBatch];
 };
 
-__device__ __forceinline__ TileRect inst_rect(const Rec &R, int tu0, int tv0) {
-    const int wu = __float_as_int(R.r1.x), wv = __float_as_int(R.r1.y);
-    const int uv = __float_as_int(R.r1.w);
-    return tile_rect(wu & 0xffff, wu >> 16, wv & 0xffff, wv >> 16, tu0, tv0,
-                     uv & 0xffff, uv >> 16);
-}
+constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+// forward shared memory: Batch | group accumulators | staged Frags
+constexpr size_t kFwdAccOff = align16(sizeof(Batch));
+constexpr size_t kFwdRawOff = align16(kFwdAccOff + sizeof(float2) * kGroups * kAccStride);
+// backward shared memory: Batch | Layout | pixel terms + bg partials |
+// staged Frags
+constexpr size_t kBwdLyOff = align16(sizeof(Batch));
+constexpr size_t kBwdPixOff = kBwdLyOff + sizeof(Layout);
+constexpr size_t kBwdRawOff = align16(kBwdPixOff + sizeof(float2) * (kTile * kTile + kWarps));
 
-// Stages one tile instance (one thread per record) for a group of G lanes
+// Stages one sorted instance (one thread per record) for a group of G lanes
 // and returns its loop trip count.  Two pixel streams per lane, A and B, each
 // with a fixed column, so that x (hence P, Q) is per-lane constant:
 //   narrow (cw = pow2 >= w <= 8): A = (lx, ly), B = A + (0, R), R = G/cw,
@@ -137,13 +177,12 @@ __device__ __forceinline__ TileRect inst_rect(const Rec &R, int tu0, int tv0) {
 //                                 both advance G/8 rows per iteration
 // with lx = gl & (cw-1), ly = gl >> log2 cw.  Every row stride is even for
 // G = 16 (the forward), so a lane's row parity -- its swizzle -- is fixed.
+// `inst` is the instance id (its backward partial's slot).
 template <int G>
-__device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int tu0, int tv0,
-                                            uint32_t inst, Batch &B, Layout &Ly,
+__device__ __forceinline__ int stage_record(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
                                             int slot) {
     constexpr int lg = (G == 16) ? 4 : 3;
-    const TileRect t = inst_rect(R, tu0, tv0);
-    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
+    const FragRect t = frag_rect(f.q1.w);
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
     const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
     const bool wide = lcw == 4;
@@ -151,11 +190,11 @@ __device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int t
     const int ls = wide ? lg - 3 : lg + 1 - lcw;
     // rectangle origin relative to the expansion pixel (exact small integers)
     B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
-                             8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
-    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
-    B.sC[slot] = make_float4(R.r0.w, __int_as_float(ls), 0.f, __int_as_float((int)inst));
+                             8388608.0f - (float)(t.y0 - t.pv), f.q1.x, f.q1.y);
+    B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
+    B.sC[slot] = make_float4(f.q0.w, __int_as_float(ls), 0.f, __int_as_float((int)inst));
     Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, wide ? 8 : 0, wide ? 0 : (G >> lcw));
-    Ly.sM[slot] = make_int4(w, h, x0, y0);
+    Ly.sM[slot] = make_int4(w, h, t.x0, t.y0);
     return (h + (1 << ls) - 1) >> ls;
 }
 
@@ -166,22 +205,19 @@ __device__ __forceinline__ int stage_record(const float4 &I, const Rec &R, int t
 //   sC.w = x0 | y0 << 8 | w << 16 | R << 24
 // and sC.xy = (color, 1) is the FFMA2 operand of (num, den) += w (color, 1).
 // Returns the number of sweeps.
-__device__ __forceinline__ int stage_record_rows(const float4 &I, const Rec &R, int tu0,
-                                                 int tv0, uint32_t inst, Batch &B,
+__device__ __forceinline__ int stage_record_rows(const Frag &f, const FragRect &t, Batch &B,
                                                  int slot) {
-    const TileRect t = inst_rect(R, tu0, tv0);
-    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0;
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
     const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
     const int rows = 16 >> lcw;
     B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
-                             8388608.0f - (float)(t.y0 - t.pv), I.x, I.y);
-    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
+                             8388608.0f - (float)(t.y0 - t.pv), f.q1.x, f.q1.y);
+    B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
     B.sC[slot] = make_float4(
-        R.r0.w, 1.f,
+        f.q0.w, 1.f,
         __int_as_float(((1 << lcw) - 1) | (lcw << 8) | ((h + rows - 1) << 16) |
                        ((4 - lcw) << 24)),
-        __int_as_float(x0 | (y0 << 8) | (w << 16) | (rows << 24)));
+        __int_as_float(t.x0 | (t.y0 << 8) | (w << 16) | (rows << 24)));
     return (h + rows - 1) >> (4 - lcw);
 }
 
@@ -197,21 +233,19 @@ __device__ __forceinline__ int byte_of(int x, int k) {
 //   sC = (color, bits(x0 | w << 8), bits(vm0 | vm1 << 8 | um << 16), -)
 // where lane (X, ph) owns rows 2m + ph, vm_ph = the m whose row lies in
 // [y0, y1], um = vm0 | vm1 (the warp-uniform row pairs).
-__device__ __forceinline__ uint32_t stage_forward(const float4 &I, const Rec &R, int tu0,
-                                                  int tv0, uint32_t inst, Batch &B, int slot) {
-    const TileRect t = inst_rect(R, tu0, tv0);
+__device__ __forceinline__ uint32_t stage_forward(const Frag &f, Batch &B, int slot) {
+    const FragRect t = frag_rect(f.q1.w);
     const int w = t.x1 - t.x0 + 1;
-    if (w < kWideMin) return (uint32_t)stage_record_rows(I, R, tu0, tv0, inst, B, slot);
-    const int x0 = t.x0 - tu0, y0 = t.y0 - tv0, y1 = t.y1 - tv0;
+    if (w < kWideMin) return (uint32_t)stage_record_rows(f, t, B, slot);
     unsigned vmask[2];
 #pragma unroll
     for (int ph = 0; ph < 2; ++ph) {
-        const int mlo = (y0 - ph + 1) >> 1, mhi = (y1 - ph) >> 1;
+        const int mlo = (t.y0 - ph + 1) >> 1, mhi = (t.y1 - ph) >> 1;
         vmask[ph] = (mhi >= mlo) ? ((2u << mhi) - (1u << mlo)) : 0u;
     }
-    B.sA[slot] = make_float4((float)(t.pu - tu0), (float)(t.pv - tv0), I.x, I.y);
-    B.sB[slot] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
-    B.sC[slot] = make_float4(R.r0.w, __int_as_float(x0 | (w << 8)),
+    B.sA[slot] = make_float4((float)t.pu, (float)t.pv, f.q1.x, f.q1.y);
+    B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
+    B.sC[slot] = make_float4(f.q0.w, __int_as_float(t.x0 | (w << 8)),
                              __int_as_float((int)(vmask[0] | (vmask[1] << 8) |
                                                   ((vmask[0] | vmask[1]) << 16))),
                              0.f);
@@ -278,8 +312,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
 // buffer and the 16 buffers are summed in fixed order -- deterministic,
 // because the record -> group / warp assignment is a stable sort.
 __global__ void __launch_bounds__(kRasterThreads)
-forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
-               const uint32_t *__restrict__ vals,
+forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                const int2 *__restrict__ bin_range,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
@@ -288,13 +321,16 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
     if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
     // one private (num, den) tile buffer per 16-lane group
-    float2 *acc = reinterpret_cast<float2 *>(smem + sizeof(Batch));   // [group][256]
+    float2 *acc = reinterpret_cast<float2 *>(smem + kFwdAccOff);   // [group][256]
+    Frag *raw = reinterpret_cast<Frag *>(smem + kFwdRawOff);      // async-staged batch
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
+    StagePipe pipe;
+    pipe.start(vals, frag, raw, rg.x, rg.y);
     for (int i = threadIdx.x; i < kGroups * kAccStride; i += kRasterThreads)
         acc[i] = make_float2(0.f, 0.f);
     float2 *my = acc + (threadIdx.x >> 4) * kAccStride;
@@ -312,14 +348,11 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
+        stage_wait();   // this thread's instance of the batch has landed
         uint32_t key = kKeyInvalid;
-        if (threadIdx.x < nb) {
-            Rec R;
-            float4 I;
-            const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
-            load_inst(rec, idata, inst, I, R);
-            key = stage_forward(I, R, tu0, tv0, inst, B, threadIdx.x);
-        }
+        if (threadIdx.x < nb) key = stage_forward(raw[threadIdx.x], B, threadIdx.x);
+        // the next batch's gathers overlap this batch's accumulation
+        pipe.advance(vals, frag, raw, b0, rg.y);
         // narrow records with equal sweep counts share a warp (two per
         // warp); the wide records follow them
         sort_batch(B, key);
@@ -453,53 +486,49 @@ forward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
 // Strict-order variant: every pixel walks the tile's list in ascending
 // Gaussian order, one f32 add per pair (the reference's sequential loop).
 __global__ void __launch_bounds__(kRasterThreads)
-forward_ordered_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
-                       const uint32_t *__restrict__ vals,
+forward_ordered_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                        const int2 *__restrict__ bin_range,
                        const ugs_slice *__restrict__ slices,
                        const double *__restrict__ bg_raw, float *__restrict__ num_out,
                        float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
-    __shared__ float4 s0[kBatch], s1[kBatch], s2[kBatch];
+    __shared__ float4 s0[kBatch], s1[kBatch];
+    __shared__ float2 s2[kBatch];   // (rectangle bits, colour)
     if (plan_overflow(hdr)) return;
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp owns an 8 x 4 block so whole warps skip records that miss it
-    const int wu0 = (t % sl.tiles_x) * kTile + (warp & 1) * 8;
-    const int wv0 = (t / sl.tiles_x) * kTile + (warp >> 1) * 4;
-    const int u = wu0 + (lane & 7), v = wv0 + (lane >> 3);
+    const int wx0 = (warp & 1) * 8, wy0 = (warp >> 1) * 4;   // tile-relative
+    const int x = wx0 + (lane & 7), y = wy0 + (lane >> 3);
+    const int u = (t % sl.tiles_x) * kTile + x, v = (t / sl.tiles_x) * kTile + y;
     const int2 rg = bin_range[sl.tile_base + t];
-    const float fu = (float)u, fv = (float)v;
+    const float fx = (float)x, fy = (float)y;
     float num = 0.f, den = 0.f;
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
         if (threadIdx.x < nb) {
-            Rec R;
-            float4 I;
-            load_inst(rec, idata, __ldg(vals + b0 + threadIdx.x), I, R);
-            const TileRect tr = inst_rect(R, (t % sl.tiles_x) * kTile,
-                                          (t / sl.tiles_x) * kTile);
-            s0[threadIdx.x] = make_float4((float)tr.pu, (float)tr.pv, I.x, I.y);
-            s1[threadIdx.x] = make_float4(R.r0.x, R.r0.y, R.r0.z, I.z);
-            s2[threadIdx.x] = make_float4(R.r0.w, R.r1.x, R.r1.y, 0.f);
+            const Frag f = frag[__ldg(vals + b0 + threadIdx.x)];
+            const FragRect r = frag_rect(f.q1.w);
+            s0[threadIdx.x] = make_float4((float)r.pu, (float)r.pv, f.q1.x, f.q1.y);
+            s1[threadIdx.x] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
+            s2[threadIdx.x] = make_float2(f.q1.w, f.q0.w);
         }
         __syncthreads();
         for (int j = 0; j < nb; ++j) {
-            const float4 r2 = s2[j];
-            const int wu = __float_as_int(r2.y), wv = __float_as_int(r2.z);
-            const int iu0 = wu & 0xffff, iu1 = wu >> 16, iv0 = wv & 0xffff, iv1 = wv >> 16;
-            if (iu0 > wu0 + 7 || iu1 < wu0 || iv0 > wv0 + 3 || iv1 < wv0) continue;
+            const float2 r2 = s2[j];
+            const FragRect r = frag_rect(r2.x);
+            if (r.x0 > wx0 + 7 || r.x1 < wx0 || r.y0 > wy0 + 3 || r.y1 < wy0) continue;
             const float4 r0 = s0[j], r1 = s1[j];
-            const float dx = fu - r0.x, dy = fv - r0.y;   // exact integers
+            const float dx = fx - r0.x, dy = fy - r0.y;   // exact integers
             const float e = fmaf(fmaf(r1.x, dx, fmaf(r1.y, dy, r0.z)), dx,
                                  fmaf(fmaf(r1.z, dy, r0.w), dy, r1.w));
             float w = ex2_approx(e);
-            const bool in = (unsigned)(u - iu0) <= (unsigned)(iu1 - iu0) &&
-                            (unsigned)(v - iv0) <= (unsigned)(iv1 - iv0);
+            const bool in = (unsigned)(x - r.x0) <= (unsigned)(r.x1 - r.x0) &&
+                            (unsigned)(y - r.y0) <= (unsigned)(r.y1 - r.y0);
             w = in ? w : 0.f;
-            num = fmaf(w, r2.x, num);
+            num = fmaf(w, r2.y, num);
             den += w;
         }
     }
@@ -536,8 +565,7 @@ __device__ __forceinline__ float group_reduce8(const float a[8]) {
 }
 
 __global__ void __launch_bounds__(kRasterThreads)
-backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
-                const uint32_t *__restrict__ vals,
+backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                 const int2 *__restrict__ bin_range,
                 const ugs_slice *__restrict__ slices,
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
@@ -547,15 +575,18 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
-    Layout &Ly = *reinterpret_cast<Layout *>(smem + sizeof(Batch));
-    float2 *pix = reinterpret_cast<float2 *>(smem + sizeof(Batch) + sizeof(Layout));  // (G, G chat)
+    Layout &Ly = *reinterpret_cast<Layout *>(smem + kBwdLyOff);
+    float2 *pix = reinterpret_cast<float2 *>(smem + kBwdPixOff);  // (G, G chat)
     float2 *s_bg = pix + kTile * kTile;
+    Frag *raw = reinterpret_cast<Frag *>(smem + kBwdRawOff);      // async-staged batch
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
+    StagePipe pipe;   // the first batch lands while the pixel terms load
+    pipe.start(vals, frag, raw, rg.x, rg.y);
     {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
         const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
         float G = 0.f, Gc = 0.f, Gb = 0.f;
@@ -581,14 +612,10 @@ backward_kernel(const Rec *__restrict__ rec, const Inst *__restrict__ idata,
     for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
+        stage_wait();   // this thread's instance of the batch has landed
         int trips = 0;
-        if (threadIdx.x < nb) {
-            Rec R;
-            float4 I;
-            const uint32_t inst = __ldg(vals + b0 + threadIdx.x);
-            load_inst(rec, idata, inst, I, R);
-            trips = stage_record<8>(I, R, tu0, tv0, inst, B, Ly, threadIdx.x);
-        }
+        if (threadIdx.x < nb) trips = stage_record<8>(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
+        pipe.advance(vals, frag, raw, b0, rg.y);   // next batch, during this one
         sort_batch(B, threadIdx.x < nb ? (uint32_t)trips : (uint32_t)kKeyInvalid);
         for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
             // every lane takes part in the shuffles; empty lanes carry zeros
@@ -1095,9 +1122,8 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
     }
 }
 
-constexpr size_t kFwdSmem = sizeof(Batch) + sizeof(float2) * kGroups * kAccStride;
-constexpr size_t kBwdSmem = sizeof(Batch) + sizeof(Layout) +
-                            sizeof(float2) * (kTile * kTile + kWarps);
+constexpr size_t kFwdSmem = kFwdRawOff + sizeof(Frag) * kBatch;
+constexpr size_t kBwdSmem = kBwdRawOff + sizeof(Frag) * kBatch;
 
 int set_smem_attrs() {
     static std::atomic<unsigned long long> done{0};
@@ -1124,13 +1150,11 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     stage_begin(pm, kStageForward, st);
     if (p.ordered) {
         forward_ordered_kernel<<<grid, kRasterThreads, 0, st>>>(
-            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den,
-            plan_hdr(p.b));
+            p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
         forward_kernel<<<grid, kRasterThreads, kFwdSmem, st>>>(
-            p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den,
-            plan_hdr(p.b));
+            p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_kernel");
     }
     stage_end(pm, kStageForward, st);
@@ -1148,7 +1172,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
     backward_kernel<<<grid, kRasterThreads, kBwdSmem, st>>>(
-        p.b.rec, p.b.idata, vals, p.b.bin_range, p.b.slices, num, den, dpix,
+        p.b.frag, vals, p.b.bin_range, p.b.slices, num, den, dpix,
         c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
