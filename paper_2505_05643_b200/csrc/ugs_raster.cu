@@ -51,6 +51,11 @@ constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
 constexpr int kKeyWide = kMaxTrips + 1;      // forward: warp-per-record class
 constexpr int kKeyInvalid = kMaxTrips + 2;   // unused staging slots
 constexpr int kKeys = kMaxTrips + 3;
+// backward (4-lane groups): trip counts 1..16 (narrow / medium records) and
+// 17..32 (wide records, two column passes of h rows: key 16 + h), invalid 33
+constexpr int kBwdKeyInvalid = 2 * kMaxTrips + 1;
+constexpr int kBwdKeys = 2 * kMaxTrips + 2;
+constexpr int kKeysMax = kBwdKeys;
 #ifndef UGS_WIDE_MIN
 #define UGS_WIDE_MIN 9
 #endif
@@ -151,8 +156,9 @@ struct StagePipe {
 struct Batch {
     float4 sA[kBatch], sB[kBatch], sC[kBatch];
     uint16_t order[kBatch];            // staged slot of the j-th record by trips
-    uint32_t wcnt[kWarps][kKeys];
-    uint32_t base[kKeys];
+    uint32_t wcnt[kWarps][kKeysMax];
+    uint32_t base[kKeysMax];
+    uint32_t next[2];                  // work-queue counters of the batch
 };
 struct Layout {   // two-stream layouts (backward), after the Batch
     int4 sL[kBatch], sM[kBatch];
@@ -168,34 +174,33 @@ constexpr size_t kBwdLyOff = align16(sizeof(Batch));
 constexpr size_t kBwdPixOff = kBwdLyOff + sizeof(Layout);
 constexpr size_t kBwdRawOff = align16(kBwdPixOff + sizeof(float2) * (kTile * kTile + kWarps));
 
-// Stages one sorted instance (one thread per record) for a group of G lanes
-// and returns its loop trip count.  Two pixel streams per lane, A and B, each
+// Backward staging of one instance (one thread per record) for a group of 4
+// lanes; returns its sort key.  Two pixel streams per lane, A and B, each
 // with a fixed column, so that x (hence P, Q) is per-lane constant:
-//   narrow (cw = pow2 >= w <= 8): A = (lx, ly), B = A + (0, R), R = G/cw,
-//                                 both advance 2R rows per iteration
-//   wide   (w > 8):               A = (gl & 7, gl >> 3), B = A + (8, 0),
-//                                 both advance G/8 rows per iteration
-// with lx = gl & (cw-1), ly = gl >> log2 cw.  Every row stride is even for
-// G = 16 (the forward), so a lane's row parity -- its swizzle -- is fixed.
-// `inst` is the instance id (its backward partial's slot).
-template <int G>
-__device__ __forceinline__ int stage_record(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
-                                            int slot) {
-    constexpr int lg = (G == 16) ? 4 : 3;
+//   narrow (w <= 4, cw = pow2 >= w): A = (lx, ly), B = A + (0, R), R = 4/cw,
+//                                    both advance 2R rows per iteration
+//   medium (w 5..8):                 A = (gl, 0), B = A + (4, 0), one row
+//                                    per iteration
+//   wide   (w 9..16):                the medium layout twice, over columns
+//                                    0-7 and 8-15 (two passes of h rows)
+// with lx = gl & (cw-1), ly = gl >> log2 cw.  Key: the loop trip count
+// (1..16), wide records 16 + h, so a warp's eight records share a loop shape.
+//   sL = (cmask, lcw, B column offset, B row offset), sM = (w, h, x0, y0)
+__device__ __forceinline__ int stage_record4(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
+                                             int slot) {
     const FragRect t = frag_rect(f.q1.w);
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
     const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
-    const bool wide = lcw == 4;
-    const int lcwA = wide ? 3 : lcw;
-    const int ls = wide ? lg - 3 : lg + 1 - lcw;
-    // rectangle origin relative to the expansion pixel (exact small integers)
+    const bool cols = lcw >= 3;                 // medium / wide: column-offset B
+    const int lcwA = cols ? 2 : lcw;
+    const int ls = cols ? 0 : 3 - lcw;          // log2 of the row stride
     B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
                              8388608.0f - (float)(t.y0 - t.pv), f.q1.x, f.q1.y);
     B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
     B.sC[slot] = make_float4(f.q0.w, __int_as_float(ls), 0.f, __int_as_float((int)inst));
-    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, wide ? 8 : 0, wide ? 0 : (G >> lcw));
+    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, cols ? 4 : 0, cols ? 0 : (4 >> lcw));
     Ly.sM[slot] = make_int4(w, h, t.x0, t.y0);
-    return (h + (1 << ls) - 1) >> ls;
+    return lcw == 4 ? kMaxTrips + h : (h + (1 << ls) - 1) >> ls;
 }
 
 // Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
@@ -252,14 +257,31 @@ __device__ __forceinline__ uint32_t stage_forward(const Frag &f, Batch &B, int s
     return (uint32_t)kKeyWide;
 }
 
+// Warp-level work queue over a batch's units, LARGEST first: the sorted
+// slots ascend by loop trip count, so unit n-1-k is the k-th largest and
+// warps that finish early take the remaining small ones (greedy
+// longest-first balance; the batch ends at a CTA barrier).  Returns the unit
+// index, or -1 when the queue is empty.  Only for work whose result does not
+// depend on which warp runs a unit (the backward's per-instance partials);
+// the forward's accumulation order must stay a fixed function of the batch.
+__device__ __forceinline__ int next_unit(uint32_t *ctr, int nunits) {
+    uint32_t k = 0;
+    if ((threadIdx.x & 31) == 0) k = atomicAdd(ctr, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    return (int)k < nunits ? nunits - 1 - (int)k : -1;
+}
+
 // Stable counting sort of the staged slots by key (trip count, or the
 // forward's wide class; unused slots last) -- warp match-any ranks +
 // per-warp bucket counters: a deterministic record -> lane-group mapping.
 // Returns, in B.base, each key's first sorted position.
+template <int NK>
 __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
+    constexpr int kInvalid = NK - 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * kKeys; i += kRasterThreads)
+    for (int i = threadIdx.x; i < kWarps * kKeysMax; i += kRasterThreads)
         (&B.wcnt[0][0])[i] = 0;
+    if (threadIdx.x < 2) B.next[threadIdx.x] = 0u;
     __syncthreads();
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
@@ -267,7 +289,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
     __syncthreads();
     if (threadIdx.x < 32) {   // bucket bases (exclusive over keys), then per warp
         uint32_t tot = 0;
-        for (int k = lane; k < kKeys; k += 32) {
+        for (int k = lane; k < NK; k += 32) {
             uint32_t col = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) col += B.wcnt[w][k];
@@ -275,7 +297,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
         }
         __syncwarp();
         if (lane == 0) {
-            for (int k = 0; k < kKeys; ++k) {
+            for (int k = 0; k < NK; ++k) {
                 const uint32_t c = B.base[k];
                 B.base[k] = tot;
                 tot += c;
@@ -284,7 +306,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
     }
     __syncthreads();
     uint32_t run = 0;
-    if (threadIdx.x < kKeys) {
+    if (threadIdx.x < NK) {
         run = B.base[threadIdx.x];
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
@@ -294,7 +316,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
         }
     }
     __syncthreads();
-    if (key != (uint32_t)kKeyInvalid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
+    if (key != (uint32_t)kInvalid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
     __syncthreads();
 }
 
@@ -355,7 +377,7 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
         pipe.advance(vals, frag, raw, b0, rg.y);
         // narrow records with equal sweep counts share a warp (two per
         // warp); the wide records follow them
-        sort_batch(B, key);
+        sort_batch<kKeys>(B, key);
         const int n_narrow = (int)B.base[kKeyWide];
         const int n_valid = (int)B.base[kKeyInvalid];
         for (int s0 = warp * 2; s0 < n_narrow; s0 += kWarps * 2) {
@@ -541,30 +563,30 @@ forward_ordered_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict
 }
 
 
-// Transpose-reduce of 8 values across an 8-lane group (3 levels, 7
-// shuffles): on return group lane g holds the group total of value g.
-__device__ __forceinline__ float group_reduce8(const float a[8]) {
-    const int gl = threadIdx.x & 7;
-    const bool h4 = gl & 4, h2 = gl & 2, h1 = gl & 1;
-    float b[4], c[2];
+// Transpose-reduce of 8 values across a 4-lane group (2 levels, 6
+// shuffles): on return group lane g holds the group totals of values 2g and
+// 2g + 1.
+__device__ __forceinline__ float2 group_reduce8x4(const float a[8]) {
+    const int gl = threadIdx.x & 3;
+    const bool h2 = gl & 2, h1 = gl & 1;
+    float b[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float send = h4 ? a[k] : a[k + 4];
-        const float keep = h4 ? a[k + 4] : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        const float send = h2 ? a[k] : a[k + 4];
+        const float keep = h2 ? a[k + 4] : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
     }
+    float c[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        const float send = h2 ? b[k] : b[k + 2];
-        const float keep = h2 ? b[k + 2] : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        const float send = h1 ? b[k] : b[k + 2];
+        const float keep = h1 ? b[k + 2] : b[k];
+        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
     }
-    const float send = h1 ? c[0] : c[1];
-    const float keep = h1 ? c[1] : c[0];
-    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    return make_float2(c[0], c[1]);
 }
 
-__global__ void __launch_bounds__(kRasterThreads)
+__global__ void __launch_bounds__(kRasterThreads, 4)
 backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                 const int2 *__restrict__ bin_range,
                 const ugs_slice *__restrict__ slices,
@@ -576,8 +598,11 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
     Layout &Ly = *reinterpret_cast<Layout *>(smem + kBwdLyOff);
-    float2 *pix = reinterpret_cast<float2 *>(smem + kBwdPixOff);  // (G, G chat)
-    float2 *s_bg = pix + kTile * kTile;
+    // per-pixel upstream terms as two planes (a lane's two streams load
+    // straight into a register pair): G, then G chat
+    float *pixG = reinterpret_cast<float *>(smem + kBwdPixOff);
+    float *pixGc = pixG + kTile * kTile;
+    float2 *s_bg = reinterpret_cast<float2 *>(pixGc + kTile * kTile);
     Frag *raw = reinterpret_cast<Frag *>(smem + kBwdRawOff);      // async-staged batch
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
@@ -600,7 +625,8 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
             // reference forms it (gradients.py:110), no cancellation
             Gb = G * (sigmoid_bg(bg_raw, 0) - chat);
         }
-        pix[threadIdx.x] = make_float2(G, Gc);
+        pixG[threadIdx.x] = G;
+        pixGc[threadIdx.x] = Gc;
         float a = G, c = Gb;   // background partials of this tile, fixed order
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -613,82 +639,96 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
         const int nb = min(kBatch, rg.y - b0);
         __syncthreads();
         stage_wait();   // this thread's instance of the batch has landed
-        int trips = 0;
-        if (threadIdx.x < nb) trips = stage_record<8>(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
+        int key = kBwdKeyInvalid;
+        if (threadIdx.x < nb) key = stage_record4(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
         pipe.advance(vals, frag, raw, b0, rg.y);   // next batch, during this one
-        sort_batch(B, threadIdx.x < nb ? (uint32_t)trips : (uint32_t)kKeyInvalid);
-        for (int s0 = warp * 4; s0 < nb; s0 += kWarps * 4) {
-            // every lane takes part in the shuffles; empty lanes carry zeros
-            const int slot = s0 + (lane >> 3);
+        sort_batch<kBwdKeys>(B, (uint32_t)key);
+        // eight records per warp (4-lane groups); every lane takes part in the
+        // shuffles, empty lanes carry zeros
+        const int nunits = (nb + 7) >> 3;
+        for (int u = next_unit(&B.next[0], nunits); u >= 0; u = next_unit(&B.next[0], nunits)) {
+            const int s0 = u * 8;
+            const int slot = s0 + (lane >> 2);
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
             const int4 L = Ly.sL[j], M = Ly.sM[j];
-            const int gl = lane & 7;
+            const int gl = lane & 3;
             const int h = live ? M.y : 0;
-            // the two pixel streams of stage_record<8>
-            const int lxA = gl & L.x, lyA = gl >> L.y;
-            const int lxB = lxA + L.z, lyB = lyA + L.w;
             const int ls = __float_as_int(c.y), stride = 1 << ls;
-            const bool okA = lxA < M.x && lyA < h, okB = lxB < M.x && lyB < h;
-            const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
-            // wide rows always pair A with B (B masked when out of the rectangle)
-            const int nB = okB ? (h - lyB + stride - 1) >> ls : (L.z ? nA : 0);
-            // per lane dx is fixed per stream: log2 w = P + dy (Q + C dy); the x
-            // moments follow from the per-stream sums (sum t dx = dx S0, ...)
-            const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)L.z;
-            const float PA = fmaf(fmaf(b.x, dxA, a.z), dxA, b.w), QA = fmaf(b.y, dxA, a.w);
-            const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
-            const float QB = fmaf(b.y, dxB, a.w);
-            float dyA = big_float(lyA) - a.y, dyB = dyA + (float)L.w;
-            const float2 *gA = pix + (M.w + lyA) * kTile + M.z + lxA;
-            const float2 *gB = okB ? gA + (L.w * kTile + L.z) : gA;
-            const int gstep = okB ? stride * kTile : 0;
-            const float fstride = (float)stride;
-            // streams A and B in packed f32x2 arithmetic (FFMA2 / FADD2 /
-            // FMUL2, per-half fma.rn rounding): lo = A, hi = B
-            float2 dy2 = make_float2(dyA, dyB);
-            const float2 P2 = make_float2(PA, PB), Q2 = make_float2(QA, QB);
+            const int npass = M.x > 8 ? 2 : 1;   // wide: columns 0-7, then 8-15
             const float2 C2 = make_float2(b.z, b.z), c2 = make_float2(c.x, c.x);
             const float2 fs2 = make_float2((float)stride, (float)stride);
-            float2 m02 = make_float2(0.f, 0.f), S02 = m02, Sy2 = m02, Syy2 = m02;
-            int i = 0;
+            float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int pass = 0; pass < npass; ++pass) {
+                // the two pixel streams of stage_record4
+                const int lxA = (gl & L.x) + 8 * pass, lyA = gl >> L.y;
+                const int lxB = lxA + L.z, lyB = lyA + L.w;
+                const bool okA = lxA < M.x && lyA < h, okB = lxB < M.x && lyB < h;
+                const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
+                // column layouts always pair A with B (B masked when out of
+                // the rectangle)
+                const int nB = okB ? (h - lyB + stride - 1) >> ls : (L.z ? nA : 0);
+                // per lane dx is fixed per stream: log2 w = P + dy (Q + C dy);
+                // the x moments follow from the per-stream sums (sum t dx =
+                // dx S0, ...)
+                const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)L.z;
+                const float PA = fmaf(fmaf(b.x, dxA, a.z), dxA, b.w), QA = fmaf(b.y, dxA, a.w);
+                const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
+                const float QB = fmaf(b.y, dxB, a.w);
+                const float dyA0 = big_float(lyA) - a.y;
+                const float *gA = pixG + (M.w + lyA) * kTile + M.z + lxA;
+                const float *gB = okB ? gA + (L.w * kTile + L.z) : gA;
+                const int gstep = okB ? stride * kTile : 0;
+                // the G chat plane sits kTile * kTile floats after the G plane
+                // streams A and B in packed f32x2 arithmetic (FFMA2 / FADD2 /
+                // FMUL2, per-half fma.rn rounding): lo = A, hi = B
+                float2 dy2 = make_float2(dyA0, dyA0 + (float)L.w);
+                const float2 P2 = make_float2(PA, PB), Q2 = make_float2(QA, QB);
+                float2 m02 = make_float2(0.f, 0.f), S02 = m02, Sy2 = m02, Syy2 = m02;
+                int i = 0;
 #pragma unroll 1
-            for (; i < nB; ++i) {
-                const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
-                const float2 w2 = make_float2(ex2_approx(e.x), ex2_approx(e.y));
-                const float2 ga = *gA, gb = *gB;
-                const float2 gx = make_float2(ga.x, gb.x), gy = make_float2(-ga.y, -gb.y);
-                const float2 t2 = __fmul2_rn(__ffma2_rn(gx, c2, gy), w2);   // dw * w
-                m02 = __ffma2_rn(gx, w2, m02);
-                S02 = __fadd2_rn(S02, t2);
-                const float2 ty2 = __fmul2_rn(t2, dy2);
-                Sy2 = __fadd2_rn(Sy2, ty2);
-                Syy2 = __ffma2_rn(ty2, dy2, Syy2);
-                dy2 = __fadd2_rn(dy2, fs2);
-                gA += stride * kTile;
-                gB += gstep;
+                for (; i < nB; ++i) {
+                    const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
+                    const float2 w2 = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+                    const float2 gx = make_float2(gA[0], gB[0]);
+                    const float2 gy = make_float2(-gA[kTile * kTile], -gB[kTile * kTile]);
+                    const float2 t2 = __fmul2_rn(__ffma2_rn(gx, c2, gy), w2);   // dw * w
+                    m02 = __ffma2_rn(gx, w2, m02);
+                    S02 = __fadd2_rn(S02, t2);
+                    const float2 ty2 = __fmul2_rn(t2, dy2);
+                    Sy2 = __fadd2_rn(Sy2, ty2);
+                    Syy2 = __ffma2_rn(ty2, dy2, Syy2);
+                    dy2 = __fadd2_rn(dy2, fs2);
+                    gA += stride * kTile;
+                    gB += gstep;
+                }
+                float m0 = m02.x + m02.y;
+                float S0a = S02.x, Sya = Sy2.x, Syya = Syy2.x;
+                const float S0b = S02.y, Syb = Sy2.y, Syyb = Syy2.y;
+                if (i < nA) {   // narrow tail: one more row of stream A
+                    const float dyA = dy2.x;
+                    const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
+                    const float ga = gA[0];
+                    const float ta = fmaf(ga, c.x, -gA[kTile * kTile]) * wa;
+                    m0 = fmaf(ga, wa, m0);
+                    S0a += ta;
+                    const float tya = ta * dyA;
+                    Sya += tya;
+                    Syya = fmaf(tya, dyA, Syya);
+                }
+                m[0] += m0;
+                m[1] += S0a + S0b;
+                m[2] += fmaf(dxA, S0a, dxB * S0b);
+                m[3] += Sya + Syb;
+                m[4] += fmaf(dxA * dxA, S0a, dxB * dxB * S0b);
+                m[5] += fmaf(dxA, Sya, dxB * Syb);
+                m[6] += Syya + Syyb;
             }
-            float m0 = m02.x + m02.y;
-            float S0a = S02.x, Sya = Sy2.x, Syya = Syy2.x;
-            const float S0b = S02.y, Syb = Sy2.y, Syyb = Syy2.y;
-            dyA = dy2.x;
-            if (i < nA) {   // narrow tail: one more row of stream A
-                const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
-                const float2 ga = *gA;
-                const float ta = fmaf(ga.x, c.x, -ga.y) * wa;
-                m0 = fmaf(ga.x, wa, m0);
-                S0a += ta;
-                const float tya = ta * dyA;
-                Sya += tya;
-                Syya = fmaf(tya, dyA, Syya);
-            }
-            float m[8] = {m0, S0a + S0b, fmaf(dxA, S0a, dxB * S0b), Sya + Syb,
-                          fmaf(dxA * dxA, S0a, dxB * dxB * S0b), fmaf(dxA, Sya, dxB * Syb),
-                          Syya + Syyb, 0.f};
-            const float red = group_reduce8(m);
+            const float2 red = group_reduce8x4(m);
             if (live)
-                partial[(size_t)(uint32_t)__float_as_int(c.w) * 8 + gl] = red;
+                *reinterpret_cast<float2 *>(
+                    partial + (size_t)(uint32_t)__float_as_int(c.w) * 8 + 2 * gl) = red;
         }
     }
     __syncthreads();
