@@ -25,8 +25,16 @@ c_i64 = ctypes.c_int64
 c_vp = ctypes.c_void_p
 
 
+# status codes of include/ugs.h
+UGS_OK, UGS_ERR_INVALID, UGS_ERR_CUDA, UGS_ERR_OOM, UGS_ERR_RANGE = 0, -1, -2, -3, -4
+
+
 class UGSError(RuntimeError):
-    """A libugs entry point returned a non-zero status."""
+    """A libugs entry point returned a non-zero status (``.status``)."""
+
+    def __init__(self, message, status=0):
+        super().__init__(message)
+        self.status = status
 
 
 class Slice(ctypes.Structure):
@@ -156,7 +164,7 @@ def check(status: int, what: str = "") -> None:
     if status != 0:
         msg = lib().ugs_last_error()
         msg = msg.decode() if msg else ""
-        raise UGSError(f"{what or 'libugs'} failed (status {status}): {msg}")
+        raise UGSError(f"{what or 'libugs'} failed (status {status}): {msg}", status)
 
 
 def ptr(t) -> int:

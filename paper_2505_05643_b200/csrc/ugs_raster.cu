@@ -277,45 +277,53 @@ __device__ __forceinline__ int next_unit(uint32_t *ctr, int nunits) {
 // Returns, in B.base, each key's first sorted position.
 template <int NK>
 __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
+    static_assert(NK <= 64, "two keys per lane of warp 0");
     constexpr int kInvalid = NK - 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * kKeysMax; i += kRasterThreads)
-        (&B.wcnt[0][0])[i] = 0;
+    // 1) per-warp key counts: each warp clears and fills its own row
+    for (int k = lane; k < NK; k += 32) B.wcnt[warp][k] = 0u;
     if (threadIdx.x < 2) B.next[threadIdx.x] = 0u;
-    __syncthreads();
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    __syncwarp();
     if (rank == 0) B.wcnt[warp][key] = __popc(peers);
     __syncthreads();
-    if (threadIdx.x < 32) {   // bucket bases (exclusive over keys), then per warp
-        uint32_t tot = 0;
-        for (int k = lane; k < NK; k += 32) {
-            uint32_t col = 0;
+    // 2) warp 0: bucket bases (exclusive scan over keys, lane k holds keys
+    //    2k and 2k + 1) and each warp's running offset per key
+    if (warp == 0) {
+        uint32_t col[2] = {0u, 0u};
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) col += B.wcnt[w][k];
-            B.base[k] = col;
+        for (int q = 0; q < 2; ++q) {
+            const int k = 2 * lane + q;
+            if (k < NK) {
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) col[q] += B.wcnt[w][k];
+            }
         }
-        __syncwarp();
-        if (lane == 0) {
-            for (int k = 0; k < NK; ++k) {
-                const uint32_t c = B.base[k];
-                B.base[k] = tot;
-                tot += c;
+        const uint32_t pair = col[0] + col[1];
+        uint32_t incl = pair;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        uint32_t run = incl - pair;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int k = 2 * lane + q;
+            if (k < NK) {
+                B.base[k] = run;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {
+                    const uint32_t c = B.wcnt[w][k];
+                    B.wcnt[w][k] = run;
+                    run += c;
+                }
             }
         }
     }
     __syncthreads();
-    uint32_t run = 0;
-    if (threadIdx.x < NK) {
-        run = B.base[threadIdx.x];
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = B.wcnt[w][threadIdx.x];
-            B.wcnt[w][threadIdx.x] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
+    // 3) stable positions
     if (key != (uint32_t)kInvalid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
     __syncthreads();
 }

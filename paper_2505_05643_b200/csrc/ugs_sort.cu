@@ -128,19 +128,23 @@ scan_down_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
     }
 }
 
+// Exclusive scan in place or out of place.  Up to 8192 tiles of block sums
+// are scanned by one block; larger inputs scan their block sums recursively
+// (tmp holds every level: scan_tmp_entries()).
 int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
                    uint32_t *tmp, cudaStream_t st,
                    const unsigned long long *n_dev = nullptr) {
     if (n == 0) return UGS_OK;
     const size_t nb = (n + kScanTile - 1) / kScanTile;
-    if (nb > 8192) {
-        set_error("exclusive_scan: input too large");
-        return UGS_ERR_RANGE;
-    }
     scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_reduce_kernel");
-    scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
-    UGS_LAUNCH_CHECK("scan_sums_kernel");
+    if (nb > 8192) {
+        int rc = exclusive_scan(tmp, tmp, nb, tmp + nb, st);
+        if (rc) return rc;
+    } else {
+        scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
+        UGS_LAUNCH_CHECK("scan_sums_kernel");
+    }
     scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_down_kernel");
     return UGS_OK;
@@ -384,7 +388,13 @@ size_t radix_hist_entries(int64_t n) {
     return nblk * kRadix;
 }
 
-size_t scan_tmp_entries(size_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+size_t scan_tmp_entries(size_t n) {
+    size_t total = 1;
+    for (size_t nb = (n + kScanTile - 1) / kScanTile; nb > 0;
+         nb = nb > 8192 ? (nb + kScanTile - 1) / kScanTile : 0)
+        total += nb + 1;
+    return total;
+}
 
 int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
                      uint32_t *vals2, int64_t n, int bits, uint32_t *hist,

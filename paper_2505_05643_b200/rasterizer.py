@@ -349,13 +349,25 @@ def render_slices(cloud, specs, p: float = DEFAULT_P_MASS,
     out = torch.empty((len(specs), h, w), dtype=torch.float32, device=cloud.device)
     for i in range(0, len(specs), 64):
         chunk = specs[i:i + 64]
-        view = out[i:i + len(chunk)]
+        _render_chunk(r, cloud, chunk, out[i:i + len(chunk)], p)
+    return out
+
+
+def _render_chunk(r, cloud, chunk, view, p):
+    """One batch of render_slices; a batch whose tile instances exceed the
+    library's 31-bit index budget (huge footprints) is split in halves."""
+    try:
         r.bin_async(cloud, chunk, p)
         r.render(cloud, view)
         if r.poll():                  # overflowed: the plan has grown, retry
             r.bin(cloud, chunk, p)
             r.render(cloud, view)
-    return out
+    except _lib.UGSError as exc:
+        if exc.status != _lib.UGS_ERR_RANGE or len(chunk) == 1:
+            raise
+        half = len(chunk) // 2
+        _render_chunk(r, cloud, chunk[:half], view[:half], p)
+        _render_chunk(r, cloud, chunk[half:], view[half:], p)
 
 
 # ---- host utilities with the reference signatures (rasterizer.py:33-106) --

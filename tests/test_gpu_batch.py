@@ -306,3 +306,22 @@ def test_render_mode_and_overflow_retry():
     assert torch.equal(pix, torch.clamp(num / den, 0.0, 1.0))
     # sized now: a second call is sync-free and identical
     assert torch.equal(ug.render_slices(cloud, specs, renderer=r), pix)
+
+
+def test_huge_footprints_recursive_scan():
+    """Gaussians whose footprints cover whole slices (the reference recipe at
+    batch 1 grows them): a 64-slice render_slices batch of ~330M tile
+    instances takes the LSD radix path with a sort table beyond one scan
+    block (the recursive exclusive scan) and must equal the per-slice
+    renders bitwise."""
+    cloud_np = cases.uniform_cloud(3, 20_000, [[-40] * 3, [40] * 3], 0.05, 0.1)
+    cloud = ug.GaussianCloud.from_numpy(cloud_np)
+    rng = np.random.default_rng(5)
+    specs = [ug.SliceSpec(256, 256, 0.375, ug.ProbePose(*cases.random_pose(rng, 4.0)))
+             for _ in range(64)]
+    r = ug.Renderer()
+    pix = ug.render_slices(cloud, specs, renderer=r)
+    assert int(np.sum(r.k)) > (1 << 24) * 16, "the batch must need a two-level scan"
+    for s in (0, 37, 63):
+        one = ug.render_slice(cloud, specs[s]).pixels
+        assert np.array_equal(pix[s].cpu().numpy(), one)
