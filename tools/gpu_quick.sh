@@ -19,4 +19,4 @@ PY
 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none \
     --csv --log-file gpurun_out/launches_${tag}.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_${tag}.log 2>&1
-python tools/launch_shares.py gpurun_out/launches_${tag}.csv --steps 2 --json gpurun_out/launch_shares_${tag}.json | head -12
+python tools/launch_shares.py gpurun_out/launches_${tag}.csv --steps 2 --json gpurun_out/launch_shares_${tag}.json > gpurun_out/launch_shares_${tag}.txt; head -12 gpurun_out/launch_shares_${tag}.txt
