@@ -39,7 +39,25 @@ def _dev(device):
     return torch.device(device)
 
 
+_F64_WARNED = False
+
+
+def _warn_f64(x):
+    """The reference renders a float64 cloud in float64 (a side effect of
+    numba typing); this path computes in float32 (the fp32 tolerance of the
+    task): say so once instead of converting silently."""
+    global _F64_WARNED
+    dt = getattr(x, "dtype", None)
+    if not _F64_WARNED and dt in (np.float64, torch.float64):
+        _F64_WARNED = True
+        import warnings
+        warnings.warn("GaussianCloud: float64 parameters are stored and rendered in float32 "
+                      "(the CUDA path's arithmetic type); the reference would render them "
+                      "in float64", stacklevel=3)
+
+
 def _as_param(x, shape_tail, device):
+    _warn_f64(x)
     if isinstance(x, torch.Tensor):
         t = x.to(device=device, dtype=torch.float32)
     else:
