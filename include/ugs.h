@@ -327,6 +327,15 @@ UGS_API long long ugs_launch_count(void);
  * anyway) or by ugs_plan_timings. */
 UGS_API int ugs_plan_set_timing(ugs_plan *plan, int enabled);
 
+/* Host helper: fill S ugs_slice structs (pix_base = running pixel offset)
+ * from float64 poses -- rot (S,3,3) row-major, trans (S,3) -- spacing, width,
+ * height and the chi-square cut chi2.ppf(p, 3); the reference's float64
+ * operation order then float32, byte-identical to the package's numpy
+ * fill_slice (ProbePose.inverse geometry.py:61-64, plane_axes :107-120). */
+UGS_API int ugs_fill_slices(const double *rot, const double *trans, const double *spacing,
+                            const int32_t *width, const int32_t *height, int S, double cut,
+                            ugs_slice *out);
+
 /* Accumulated milliseconds and call counts per stage (host arrays of n);
  * returns the number of stages.  reset != 0 clears the accumulators. */
 /* FP32 FMA throughput probe: `blocks` x 256 threads each run `iters`

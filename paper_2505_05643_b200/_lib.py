@@ -99,6 +99,8 @@ EXPORTS = {
                                          ctypes.c_double, c_vp, c_vp, c_vp, c_vp,
                                          c_vp, c_vp, c_vp]),
     "ugs_launch_count": (ctypes.c_longlong, []),
+    "ugs_fill_slices": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,
+                                       ctypes.c_double, c_vp]),
     "ugs_fp32_peak_probe": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "ugs_plan_set_timing": (ctypes.c_int, [c_vp, ctypes.c_int]),
     "ugs_plan_set_ordered": (ctypes.c_int, [c_vp, ctypes.c_int]),

@@ -3,6 +3,7 @@
 // message (ugs_last_error), the reference raises InvalidParameterError at
 // its API layer for the same conditions (gradients.py:43-52).
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <algorithm>
 #include <atomic>
@@ -651,6 +652,63 @@ extern "C" int ugs_export_bins(const ugs_plan *p, int32_t *bin_range,
 }
 
 extern "C" long long ugs_launch_count(void) { return g_launches.load(); }
+
+// Host: the batch's ugs_slice constants from float64 poses, with the
+// reference's own operation order (ProbePose.inverse geometry.py:61-64,
+// plane_axes :107-120, the window bounds rasterizer.py:126-135), every
+// product and sum rounded separately (this translation unit's host code is
+// not contracted to FMA), then cast to float32 -- byte-identical to the
+// numpy fill_slice / fill_slices (tests/test_capi_cpu.py), without numpy's
+// per-call overhead on the serving path.
+extern "C" int ugs_fill_slices(const double *rot, const double *trans, const double *spacing,
+                               const int32_t *width, const int32_t *height, int S, double cut,
+                               ugs_slice *out) {
+    if (S < 0 || (S > 0 && (!rot || !trans || !spacing || !width || !height || !out)) ||
+        !(cut > 0.0)) {
+        set_error("ugs_fill_slices: invalid arguments");
+        return UGS_ERR_INVALID;
+    }
+    const float sqrt_cut = std::sqrt((float)cut);
+    int64_t pix = 0;
+    for (int s = 0; s < S; ++s) {
+        const double *R = rot + 9 * s, *t = trans + 3 * s;
+        const double sp = spacing[s];
+        const int W = width[s], H = height[s];
+        ugs_slice &o = out[s];
+        std::memset(&o, 0, sizeof(o));
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) o.rw[3 * i + j] = (float)R[3 * j + i];   // R^T
+        for (int i = 0; i < 3; ++i) {
+            // -(R^T t)_i, the inner product in order
+            volatile double acc = R[0 + i] * t[0];
+            acc = acc + R[3 + i] * t[1];
+            acc = acc + R[6 + i] * t[2];
+            o.tw[i] = (float)(-acc);
+        }
+        const double cxw = (double)(W - 1) / 2.0, cyh = (double)(H - 1) / 2.0;
+        for (int k = 0; k < 3; ++k) {
+            const double du = R[3 * k + 0] * sp, dv = R[3 * k + 1] * sp;
+            volatile double a = cxw * du;
+            volatile double b = cyh * dv;
+            volatile double org = t[k] - a;
+            org = org - b;
+            o.origin[k] = (float)org;
+            o.du[k] = (float)du;
+            o.dv[k] = (float)dv;
+        }
+        o.sqrt_cut = sqrt_cut;
+        o.s = (float)sp;
+        o.cx = (float)cxw;
+        o.cy = (float)cyh;
+        o.x1h = (float)(cxw * sp);
+        o.x2h = (float)(cyh * sp);
+        o.width = W;
+        o.height = H;
+        o.pix_base = pix;
+        pix += (int64_t)W * H;
+    }
+    return UGS_OK;
+}
 
 extern "C" int ugs_plan_set_ordered(ugs_plan *p, int ordered) {
     if (!p) { set_error("ugs_plan_set_ordered: NULL plan"); return UGS_ERR_INVALID; }

@@ -149,8 +149,26 @@ SLICE_DTYPE = np.dtype([("f", "<f4", (27,)), ("i", "<i4", (6,)), ("pad", "<i4"),
 def fill_slices(dst, specs, p: float) -> None:
     """Fill a ctypes array of ugs_slice structs for a batch (pix_base = the
     running pixel offset) -- the same float32 constants as fill_slice
-    (byte-identical), vectorised over the batch and copied in one memmove
-    (the serving path renders many small batches)."""
+    (byte-identical), computed by the library's host helper
+    ugs_fill_slices in one call (the serving path renders many small
+    batches; numpy's per-op overhead was ~100 us per 16-slice batch)."""
+    import ctypes
+    from . import _lib
+    S = len(specs)
+    R = np.ascontiguousarray(np.stack([sp.pose.rotation for sp in specs]), np.float64)
+    t = np.ascontiguousarray(np.stack([sp.pose.translation for sp in specs]), np.float64)
+    sp_ = np.array([sp.spacing for sp in specs], np.float64)
+    W = np.array([sp.width for sp in specs], np.int32)
+    H = np.array([sp.height for sp in specs], np.int32)
+    _lib.check(_lib.lib().ugs_fill_slices(R.ctypes.data, t.ctypes.data, sp_.ctypes.data,
+                                          W.ctypes.data, H.ctypes.data, S,
+                                          chi2_cutoff(p), ctypes.addressof(dst)),
+               "ugs_fill_slices")
+
+
+def fill_slices_numpy(dst, specs, p: float) -> None:
+    """numpy restatement of fill_slices (vectorised over the batch, one
+    memmove): the byte-identity check of the C helper in the CPU tests."""
     import ctypes
     f32 = np.float32
     S = len(specs)

@@ -86,3 +86,32 @@ def test_batched_slice_constants_identical():
             pix += sp.width * sp.height
         fill_slices(b, specs, 0.95)
         assert bytes(a) == bytes(b)
+
+
+def test_fill_slices_c_helper_matches_numpy():
+    """ugs_fill_slices (the library's host helper) writes byte-identical
+    structs to the numpy restatement over many random poses, sizes and
+    spacings (the float64 operation order of ProbePose.inverse / plane_axes
+    then float32)."""
+    from paper_2505_05643_b200 import _lib
+    from paper_2505_05643_b200.geometry import (ProbePose, SliceSpec, fill_slices,
+                                                fill_slices_numpy)
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        S = int(rng.integers(1, 65))
+        specs = []
+        for _ in range(S):
+            q = rng.normal(size=4)
+            q /= np.linalg.norm(q)
+            w, x, y, z = q
+            R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                          [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                          [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+            t = rng.uniform(-60, 60, size=3)
+            specs.append(SliceSpec(int(rng.integers(1, 700)), int(rng.integers(1, 700)),
+                                   float(rng.uniform(0.05, 2.0)), ProbePose(R, t)))
+        p = float(rng.choice([0.95, 0.9999, 0.5]))
+        a, b = (_lib.Slice * S)(), (_lib.Slice * S)()
+        fill_slices(a, specs, p)
+        fill_slices_numpy(b, specs, p)
+        assert bytes(a) == bytes(b), trial
