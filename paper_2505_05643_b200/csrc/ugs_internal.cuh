@@ -197,6 +197,43 @@ int cuda_fail(cudaError_t e, const char *what);
 
 void note_launch();
 
+// Programmatic dependent launch (sm_90+): the kernels of a plan's chain are
+// launched with programmatic stream serialization, so each one's CTAs can be
+// scheduled while its predecessor's last wave drains (hiding the launch gap);
+// every kernel starts with pdl_entry(), which waits for its prerequisite
+// grids to complete (and their memory to be visible) before touching any
+// memory, then lets its own dependent launch.  A kernel launched without the
+// attribute passes the wait at once.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// kernel<<<grid, block, smem, st>>>(args...) as a programmatic dependent
+// launch, followed by the usual launch check
+#define UGS_PDL(kernel, grid, block, smem, st, ...)                              \
+    do {                                                                         \
+        cudaError_t e_ = ::ugs::launch_pdl(kernel, dim3(grid), dim3(block),      \
+                                           (size_t)(smem), st, __VA_ARGS__);     \
+        if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, #kernel);             \
+    } while (0)
+
 enum Stage {
     kStageCount = 0,   // prepare_count + prepare_scan (+ the host read)
     kStageEmit,        // prepare_emit: records + tile instances

@@ -58,6 +58,7 @@ loss_tile_kernel(const float *__restrict__ num, const float *__restrict__ den,
                  int H, int W, double lam,
                  int l2, float *__restrict__ dpix, double *__restrict__ tile_sums,
                  int tiles_x, int tiles_per_slice) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LossSmem &sm = *reinterpret_cast<LossSmem *>(smem_raw);
     const int s = blockIdx.y;
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(32 * kReduceWarps)
 loss_reduce_kernel(const double *__restrict__ tile_sums, int tiles_per_slice, int S, int H,
                    int W, double lam, int l2, double *__restrict__ loss_out,
                    double *__restrict__ ssim_out, double *__restrict__ mean_out) {
+    pdl_entry();
     __shared__ double lv[64];
     const double npx = (double)H * W;
     const double nv = (double)(H - 2 * kPad) * (W - 2 * kPad);
@@ -392,10 +394,12 @@ extern "C" int ugs_loss_ex(const float *num, const float *den, const float *targ
     }
     dim3 grid(tx * ty, S);
     double *sums = static_cast<double *>(workspace);
-    loss_tile_kernel<<<grid, kLossThreads, smem, st>>>(num, den, target, target_index, H, W,
+    UGS_PDL(loss_tile_kernel, grid, kLossThreads, smem, st,
+        num, den, target, target_index, H, W,
                                                        lam, l2, d_pixels, sums, tx, tx * ty);
     UGS_LAUNCH_CHECK("loss_tile_kernel");
-    loss_reduce_kernel<<<1, 32 * kReduceWarps, 0, st>>>(sums, tx * ty, S, H, W, lam, l2, loss_out,
+    UGS_PDL(loss_reduce_kernel, 1, 32 * kReduceWarps, 0, st,
+        sums, tx * ty, S, H, W, lam, l2, loss_out,
                                           ssim_out, loss_mean_out);
     UGS_LAUNCH_CHECK("loss_reduce_kernel");
     return UGS_OK;

@@ -36,6 +36,7 @@ prepare_count_kernel(const float *__restrict__ means,
                      uint2 *__restrict__ blk_cnt, unsigned *__restrict__ blk_pairs,
                      int nblk, uint2 *__restrict__ win_sparse,
                      uint32_t *__restrict__ amask, uint2 *__restrict__ wcnt) {
+    pdl_entry();
     constexpr int kW = kPrepThreads / 32;
     __shared__ ugs_slice sl[kMaxSlicesSmem];
     __shared__ unsigned s_tiles[kMaxSlicesSmem], s_pairs[kMaxSlicesSmem];
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(1024)
 prepare_scan_kernel(uint2 *__restrict__ blk_cnt,
                     const unsigned *__restrict__ blk_pairs, int nblk,
                     unsigned long long *__restrict__ slice_tot) {
+    pdl_entry();
     __shared__ unsigned long long wx[32], wy[32], wp[32];
     __shared__ unsigned long long carry_x, carry_y;
     {   // total (pairs) of this slice: plain reduction, fixed order
@@ -257,6 +259,7 @@ __global__ void warp_offsets_kernel(int S, int64_t nwarp_all, int nblk,
                                     int32_t *__restrict__ rec_bucket,
                                     int32_t *__restrict__ rec_inst,
                                     const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     if (plan_overflow(hdr)) return;
     const int64_t m_total = (int64_t)hdr->m, k_total = (int64_t)hdr->k;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -306,6 +309,7 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                      const uint2 *__restrict__ win_sparse, Rec *__restrict__ rec,
                      int32_t *__restrict__ rec_gid, int32_t *__restrict__ rec_inst,
                      Frag *__restrict__ frag, uint32_t *__restrict__ keys) {
+    pdl_entry();
     if (plan_overflow(hdr)) return;
     const int64_t m_total = (int64_t)hdr->m;
     const int ln = threadIdx.x & 31;
@@ -422,6 +426,7 @@ __global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
                                    const ugs_slice *__restrict__ slices, int S,
                                    int64_t *__restrict__ slice_base,
                                    SortSlice *__restrict__ ss, PlanCaps caps) {
+    pdl_entry();
     // one thread per slice: its bases are prefix sums over the earlier
     // slices (S <= 64: a short loop, all slices in parallel)
     __shared__ unsigned long long sm[64], sk[64], sp[64];
@@ -479,7 +484,7 @@ __global__ void plan_slices_kernel(unsigned long long *__restrict__ tot,
 int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
                          uint2 *blk_cnt, unsigned *blk_pairs, int nblk,
                          uint2 *win_sparse, uint32_t *amask, uint2 *wcnt, cudaStream_t st) {
-    prepare_count_kernel<<<nblk, kPrepThreads, 0, st>>>(
+    UGS_PDL(prepare_count_kernel, nblk, kPrepThreads, 0, st,
         c.means, c.l_raw, c.n, (float)c.beta, slices, S, blk_cnt, blk_pairs, nblk,
         win_sparse, amask, wcnt);
     UGS_LAUNCH_CHECK("prepare_count_kernel");
@@ -488,14 +493,16 @@ int launch_prepare_count(const ugs_cloud &c, const ugs_slice *slices, int S,
 
 int launch_plan_slices(unsigned long long *slice_tot, const ugs_slice *slices, int S,
                        int64_t *slice_base, SortSlice *ss, PlanCaps caps, cudaStream_t st) {
-    plan_slices_kernel<<<1, 64, 0, st>>>(slice_tot, slices, S, slice_base, ss, caps);
+    UGS_PDL(plan_slices_kernel, 1, 64, 0, st,
+        slice_tot, slices, S, slice_base, ss, caps);
     UGS_LAUNCH_CHECK("plan_slices_kernel");
     return UGS_OK;
 }
 
 int launch_prepare_scan(uint2 *blk_cnt, const unsigned *blk_pairs, int S, int nblk,
                         unsigned long long *slice_tot, cudaStream_t st) {
-    prepare_scan_kernel<<<S, 1024, 0, st>>>(blk_cnt, blk_pairs, nblk, slice_tot);
+    UGS_PDL(prepare_scan_kernel, S, 1024, 0, st,
+        blk_cnt, blk_pairs, nblk, slice_tot);
     UGS_LAUNCH_CHECK("prepare_scan_kernel");
     return UGS_OK;
 }
@@ -509,13 +516,12 @@ int launch_prepare_emit(const ugs_cloud &c, const ugs_slice *slices, int S,
                         int32_t *rec_bucket, cudaStream_t st) {
     const int64_t nwarp_all = (int64_t)nblk * (kPrepThreads / 32);
     const int64_t nw = (int64_t)S * nwarp_all;
-    warp_offsets_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(
+    UGS_PDL(warp_offsets_kernel, (unsigned)((nw + 255) / 256), 256, 0, st,
         S, nwarp_all, nblk, blk_off, wcnt, amask, slice_base, warp_rec, warp_inst,
         rec_bucket, rec_inst, hdr);
     UGS_LAUNCH_CHECK("warp_offsets_kernel");
     if (m_grid <= 0) return UGS_OK;
-    build_records_kernel<<<(unsigned)((m_grid + kBuildThreads - 1) / kBuildThreads),
-                           kBuildThreads, 0, st>>>(
+    UGS_PDL(build_records_kernel, (unsigned)((m_grid + kBuildThreads - 1) / kBuildThreads), kBuildThreads, 0, st,
         c.means, c.l_raw, c.intensity_raw, c.opacity_raw, c.n, (float)c.beta, slices, S,
         slice_base, hdr, nwarp_all, amask, warp_rec, warp_inst, rec_bucket, win_sparse, rec,
         rec_gid, rec_inst, frag, keys);

@@ -347,6 +347,7 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
                float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
@@ -521,6 +522,7 @@ forward_ordered_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict
                        const ugs_slice *__restrict__ slices,
                        const double *__restrict__ bg_raw, float *__restrict__ num_out,
                        float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     __shared__ float4 s0[kBatch], s1[kBatch];
     __shared__ float2 s2[kBatch];   // (rectangle bits, colour)
     if (plan_overflow(hdr)) return;
@@ -602,6 +604,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg,
                 const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
     Batch &B = *reinterpret_cast<Batch *>(smem);
@@ -855,6 +858,7 @@ finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__
                         const ugs_slice *__restrict__ slices,
                         const float *__restrict__ means, const float *__restrict__ l_raw,
                         float beta, float *__restrict__ rgrad) {
+    pdl_entry();
     // the slices' record bases in shared memory: the per-thread slice search
     // runs on it instead of on dependent global loads
     __shared__ int64_t s_rb[64];
@@ -904,6 +908,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
                      int32_t *__restrict__ grad_cnt, int aligned,
                      const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     __shared__ float4 rows_all[kUpdWarps][kUpdRows][3];
     if (plan_overflow(hdr)) return;
     __shared__ float4 prm_all[kUpdWarps][24 + 48];   // means | l_raw rows of the warp
@@ -1122,6 +1127,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
 __global__ void bg_slice_kernel(const float2 *__restrict__ bin_bg,
                                 const ugs_slice *__restrict__ slices,
                                 double2 *__restrict__ out, const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     __shared__ double sa[256], sc_[256];
     if (plan_overflow(hdr)) return;
     const int s = blockIdx.x;
@@ -1152,6 +1158,7 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
                                    float *__restrict__ grad_bg, float scale, int adam,
                                    float *__restrict__ m_bg, float *__restrict__ v_bg,
                                    AdamConst k, const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
     if (threadIdx.x != 0 || plan_overflow(hdr)) return;
     const double cbg = sigmoid_f64(bg_raw[0]), abg = sigmoid_f64(bg_raw[1]);
     // adam: 0 accumulate into grad_bg, 1 Adam step, 2 overwrite grad_bg
@@ -1197,12 +1204,12 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageForward, st);
     if (p.ordered) {
-        forward_ordered_kernel<<<grid, kRasterThreads, 0, st>>>(
-            p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
+        UGS_PDL(forward_ordered_kernel, grid, kRasterThreads, 0, st,
+        p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
-        forward_kernel<<<grid, kRasterThreads, kFwdSmem, st>>>(
-            p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
+        UGS_PDL(forward_kernel, grid, kRasterThreads, kFwdSmem, st,
+        p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_kernel");
     }
     stage_end(pm, kStageForward, st);
@@ -1219,7 +1226,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     dim3 grid(p.max_tiles, p.S);
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
-    backward_kernel<<<grid, kRasterThreads, kBwdSmem, st>>>(
+    UGS_PDL(backward_kernel, grid, kRasterThreads, kBwdSmem, st,
         p.b.frag, vals, p.b.bin_range, p.b.slices, num, den, dpix,
         c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("backward_kernel");
@@ -1235,14 +1242,17 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     cudaStream_t side = pm->side;
     UGS_CUDA(cudaEventRecord(pm->ev_fork, st));
     UGS_CUDA(cudaStreamWaitEvent(side, pm->ev_fork, 0));
-    bg_slice_kernel<<<p.S, 256, 0, side>>>(p.b.bin_bg, p.b.slices, p.b.bg_sums, plan_hdr(p.b));
+    UGS_PDL(bg_slice_kernel, p.S, 256, 0, side,
+        p.b.bin_bg, p.b.slices, p.b.bg_sums, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("bg_slice_kernel");
     if (adam) {
-        bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+        UGS_PDL(bg_finalize_kernel, 1, 32, 0, side,
+        p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                                nullptr, scale, 1, adam->m + kG * c.n,
                                                adam->v + kG * c.n, adam->k, plan_hdr(p.b));
     } else {
-        bg_finalize_kernel<<<1, 32, 0, side>>>(p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
+        UGS_PDL(bg_finalize_kernel, 1, 32, 0, side,
+        p.b.bg_sums, p.S, const_cast<double *>(c.bg_raw),
                                                grad + kG * c.n, scale, dense ? 2 : 0,
                                                nullptr, nullptr,
                                                AdamConst{}, plan_hdr(p.b));
@@ -1255,8 +1265,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                       const_cast<float *>(c.opacity_raw)};
     if (p.m_grid > 0) {
         const int th = 128;
-        finalize_records_kernel<<<(unsigned)((p.m_grid + th - 1) / th), th, 0, st>>>(
-            p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, plan_hdr(p.b), p.b.slice_base, p.S,
+        UGS_PDL(finalize_records_kernel, (unsigned)((p.m_grid + th - 1) / th), th, 0, st,
+        p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, plan_hdr(p.b), p.b.slice_base, p.S,
             p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
     }
@@ -1270,8 +1280,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
         const int aligned =
             adam && ((((uintptr_t)c.means | (uintptr_t)c.l_raw | (uintptr_t)adam->m |
                        (uintptr_t)adam->v) & 15) == 0);
-        update_gather_kernel<<<(unsigned)nblk, kUpdThreads, 0, st>>>(
-            p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale,
+        UGS_PDL(update_gather_kernel, (unsigned)nblk, kUpdThreads, 0, st,
+        p.b.amask, p.b.warp_rec, p.b.rgrad, p.S, nwarp_all, c.n, scale,
             adam ? 1 : (dense ? 2 : 0),
             grad, touched, cm, adam ? adam->m : nullptr, adam ? adam->v : nullptr,
             adam ? adam->k : AdamConst{}, adam ? adam->grad_sum : nullptr,

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kScanThreads)
 scan_reduce_kernel(const uint32_t *__restrict__ in, size_t n,
                    const unsigned long long *__restrict__ n_dev,
                    uint32_t *__restrict__ sums) {
+    pdl_entry();
     n = scan_count(n, n_dev);
     const size_t base = (size_t)blockIdx.x * kScanTile;
     uint32_t acc = 0;
@@ -78,6 +79,7 @@ scan_reduce_kernel(const uint32_t *__restrict__ in, size_t n,
 // single block, exclusive scan of up to 1024*8 entries in place
 __global__ void __launch_bounds__(1024)
 scan_sums_kernel(uint32_t *__restrict__ sums, int n) {
+    pdl_entry();
     uint32_t v[8];
     const int base = threadIdx.x * 8;
     uint32_t local = 0;
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(kScanThreads)
 scan_down_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
                  size_t n, const unsigned long long *__restrict__ n_dev,
                  const uint32_t *__restrict__ sums) {
+    pdl_entry();
     n = scan_count(n, n_dev);
     // each thread scans kScanItems consecutive entries (blocked layout)
     __shared__ uint32_t tile[kScanTile];
@@ -136,16 +139,19 @@ int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
                    const unsigned long long *n_dev = nullptr) {
     if (n == 0) return UGS_OK;
     const size_t nb = (n + kScanTile - 1) / kScanTile;
-    scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, n_dev, tmp);
+    UGS_PDL(scan_reduce_kernel, (unsigned)nb, kScanThreads, 0, st,
+        in, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_reduce_kernel");
     if (nb > 8192) {
         int rc = exclusive_scan(tmp, tmp, nb, tmp + nb, st);
         if (rc) return rc;
     } else {
-        scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, (int)nb);
+        UGS_PDL(scan_sums_kernel, 1, 1024, 0, st,
+        tmp, (int)nb);
         UGS_LAUNCH_CHECK("scan_sums_kernel");
     }
-    scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, n_dev, tmp);
+    UGS_PDL(scan_down_kernel, (unsigned)nb, kScanThreads, 0, st,
+        in, out, n, n_dev, tmp);
     UGS_LAUNCH_CHECK("scan_down_kernel");
     return UGS_OK;
 }
@@ -154,6 +160,7 @@ int exclusive_scan(const uint32_t *in, uint32_t *out, size_t n,
 __global__ void __launch_bounds__(kSortThreads)
 radix_hist_kernel(const uint32_t *__restrict__ keys, int64_t n, int shift,
                   uint32_t *__restrict__ hist, int nblk) {
+    pdl_entry();
     __shared__ uint32_t h[kRadix];
     for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
     __syncthreads();
@@ -174,6 +181,7 @@ radix_scatter_kernel(const uint32_t *__restrict__ keys_in,
                      uint32_t *__restrict__ keys_out,
                      uint32_t *__restrict__ vals_out, int64_t n, int shift,
                      const uint32_t *__restrict__ offs, int nblk) {
+    pdl_entry();
     constexpr int kWarps = kSortThreads / 32;
     constexpr int kPerWarp = kSortItems * 32;
     __shared__ uint32_t wcnt[kWarps][kRadix];
@@ -259,6 +267,7 @@ __device__ __forceinline__ int sort_slice_of(const SortSlice *__restrict__ ss, i
 __global__ void __launch_bounds__(kSortThreads)
 slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss, int S,
                   const PlanHdr *__restrict__ hdr, uint32_t *__restrict__ hist) {
+    pdl_entry();
     extern __shared__ uint32_t sh[];
     if (plan_overflow(hdr) || blockIdx.x >= hdr->nblk) return;   // whole block
     const int s = sort_slice_of(ss, S, blockIdx.x);
@@ -288,6 +297,7 @@ __global__ void __launch_bounds__(kSortThreads, 6)
 slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss,
                      int S, const PlanHdr *__restrict__ hdr, const uint32_t *__restrict__ offs,
                      uint32_t *__restrict__ vals_out) {
+    pdl_entry();
     constexpr int kWarpsS = kSortThreads / 32;
     constexpr int kPerWarp = kSortItems * 32;
     constexpr int kT = 1 << kBits;
@@ -350,6 +360,7 @@ __global__ void slice_ranges_kernel(const SortSlice *__restrict__ ss, int S,
                                     const PlanHdr *__restrict__ hdr,
                                     const uint32_t *__restrict__ offs, int n_bins,
                                     int2 *__restrict__ range) {
+    pdl_entry();
     __shared__ int s_tb[64];
     if (plan_overflow(hdr)) return;
     for (int q = threadIdx.x; q < S; q += blockDim.x) s_tb[q] = ss[q].tile_base;
@@ -374,6 +385,7 @@ __global__ void slice_ranges_kernel(const SortSlice *__restrict__ ss, int S,
 
 __global__ void bin_ranges_kernel(const uint32_t *__restrict__ keys, int64_t n,
                                   int2 *__restrict__ range) {
+    pdl_entry();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
@@ -409,11 +421,13 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
     const int passes = bits <= 0 ? 1 : (bits + kRadixBits - 1) / kRadixBits;
     for (int p = 0; p < passes; ++p) {
         const int shift = p * kRadixBits;
-        radix_hist_kernel<<<nblk, kSortThreads, 0, st>>>(kin, n, shift, hist, nblk);
+        UGS_PDL(radix_hist_kernel, nblk, kSortThreads, 0, st,
+        kin, n, shift, hist, nblk);
         UGS_LAUNCH_CHECK("radix_hist_kernel");
         int rc = exclusive_scan(hist, hist, hn, scan_tmp, st);
         if (rc) return rc;
-        radix_scatter_kernel<<<nblk, kSortThreads, 0, st>>>(kin, vin, kout, vout,
+        UGS_PDL(radix_scatter_kernel, nblk, kSortThreads, 0, st,
+        kin, vin, kout, vout,
                                                             n, shift, hist, nblk);
         UGS_LAUNCH_CHECK("radix_scatter_kernel");
         // ping-pong: first pass reads identity values, writes vals2
@@ -436,14 +450,16 @@ int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const Pl
     // writes [inst_base, inst_base) for every tile of a slice without blocks
     const size_t hsm = sizeof(uint32_t) * (size_t)max_tiles;
     if (nblk_grid > 0) {
-        slice_hist_kernel<<<nblk_grid, kSortThreads, hsm, st>>>(keys, d_ss, S, hdr, hist);
+        UGS_PDL(slice_hist_kernel, nblk_grid, kSortThreads, hsm, st,
+        keys, d_ss, S, hdr, hist);
         UGS_LAUNCH_CHECK("slice_hist_kernel");
         int rc = exclusive_scan(hist, hist, (size_t)hist_grid, scan_tmp, st, &hdr->hist_n);
         if (rc) return rc;
         const int bits = max_tiles <= 256 ? 8 : 10;
         const size_t ssm = sizeof(uint32_t) * (kSortThreads / 32) * ((size_t)1 << bits);
         if (bits == 8) {
-            slice_scatter_kernel<8><<<nblk_grid, kSortThreads, ssm, st>>>(keys, d_ss, S, hdr,
+            UGS_PDL(slice_scatter_kernel<8>, nblk_grid, kSortThreads, ssm, st,
+        keys, d_ss, S, hdr,
                                                                           hist, vals_out);
         } else {
             static std::atomic<unsigned long long> attr{0};
@@ -453,14 +469,16 @@ int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const Pl
                                               (int)ssm));
                 mark_device_setup(attr);
             }
-            slice_scatter_kernel<10><<<nblk_grid, kSortThreads, ssm, st>>>(keys, d_ss, S, hdr,
+            UGS_PDL(slice_scatter_kernel<10>, nblk_grid, kSortThreads, ssm, st,
+        keys, d_ss, S, hdr,
                                                                            hist, vals_out);
         }
         UGS_LAUNCH_CHECK("slice_scatter_kernel");
     }
     const int th = 256;
     if (n_bins > 0) {
-        slice_ranges_kernel<<<(n_bins + th - 1) / th, th, 0, st>>>(d_ss, S, hdr, hist, n_bins,
+        UGS_PDL(slice_ranges_kernel, (n_bins + th - 1) / th, th, 0, st,
+        d_ss, S, hdr, hist, n_bins,
                                                                    bin_range);
         UGS_LAUNCH_CHECK("slice_ranges_kernel");
     }
@@ -472,7 +490,8 @@ int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
     UGS_CUDA(cudaMemsetAsync(bin_range, 0, sizeof(int2) * (size_t)n_bins, st));
     if (n <= 0) return UGS_OK;
     const int th = 256;
-    bin_ranges_kernel<<<(unsigned)((n + th - 1) / th), th, 0, st>>>(keys, n,
+    UGS_PDL(bin_ranges_kernel, (unsigned)((n + th - 1) / th), th, 0, st,
+        keys, n,
                                                                     bin_range);
     UGS_LAUNCH_CHECK("bin_ranges_kernel");
     return UGS_OK;
