@@ -381,9 +381,16 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
     if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices,
                                  caps_of(p), st)))
         return rc;
-    UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
-                             cudaMemcpyDeviceToHost, st));
-    UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
+    // the totals go to pinned memory: now (a synchronous call sizes its
+    // buffers from them), or -- sync-free -- after the sort, so the kernel
+    // chain count -> ... -> sort stays back to back (programmatic dependent
+    // launches overlap consecutive kernels only); the host reads them at the
+    // next poll either way
+    if (!async) {
+        UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                                 cudaMemcpyDeviceToHost, st));
+        UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
+    }
     stage_end(p, kStageCount, st);
     p->counts_pending = true;
     if (!async) {
@@ -450,6 +457,11 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
         if ((rc = launch_bin_ranges(p->sorted_keys, p->k_total, b.bin_range, n_bins, st)))
             return rc;
         stage_end(p, kStageRanges, st);
+    }
+    if (async) {
+        UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                                 cudaMemcpyDeviceToHost, st));
+        UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
     }
     return UGS_OK;
 }
