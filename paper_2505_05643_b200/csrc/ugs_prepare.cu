@@ -296,7 +296,10 @@ __device__ __forceinline__ unsigned packed_tiles(uint2 w) {
 // plane-conditioned exponent (float64, ugs_geometry.cuh PlaneForm) and the
 // record's tile instances in row-major tile order, each with its exact
 // re-expansion.
-__global__ void __launch_bounds__(kBuildThreads, 8)
+#ifndef UGS_BUILD_MINB
+#define UGS_BUILD_MINB 8
+#endif
+__global__ void __launch_bounds__(kBuildThreads, UGS_BUILD_MINB)
 build_records_kernel(const float *__restrict__ means, const float *__restrict__ l_raw,
                      const float *__restrict__ intensity_raw,
                      const float *__restrict__ opacity_raw, int64_t n, float beta,

@@ -788,6 +788,14 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
     double Sm[7] = {0, 0, 0, 0, 0, 0, 0};
     const int i0 = rec_inst[r], i1 = rec_inst[r + 1];
     int tx = tx0, ty = iv0 >> 4;
+#ifndef UGS_FIN_UNROLL
+#define UGS_FIN_UNROLL 2
+#endif
+#if UGS_FIN_UNROLL > 1
+#define UGS_STR_(x) #x
+#define UGS_UNROLL_(n) _Pragma(UGS_STR_(unroll n))
+    UGS_UNROLL_(UGS_FIN_UNROLL)
+#endif
     for (int i = i0; i < i1; ++i) {
         const TileRect t = tile_rect(iu0, iu1, iv0, iv1, tx * kTile, ty * kTile, ui, vi);
         const double ox = (double)(t.pu - ui), oy = (double)(t.pv - vi);
@@ -850,7 +858,10 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
 
 // One thread per record: its raw-parameter gradient (float64 chain) into
 // rgrad[r][0..10] (AoS-12 row), for the staged update below.
-__global__ void __launch_bounds__(128, 8)
+#ifndef UGS_FIN_MINB
+#define UGS_FIN_MINB 6   // with the two-instance unroll below (variant sweep: 95 -> 92 us)
+#endif
+__global__ void __launch_bounds__(128, UGS_FIN_MINB)
 finalize_records_kernel(const Rec *__restrict__ rec, const int32_t *__restrict__ rec_gid,
                         const int32_t *__restrict__ rec_inst,
                         const float *__restrict__ partial, const PlanHdr *__restrict__ hdr,
@@ -900,7 +911,10 @@ constexpr int kUpdRows = 64;    // staged record-gradient rows per warp and pass
 // dense buffer is WRITTEN -- the scaled sum, zeros for Gaussians no slice
 // accepted, the pad slot = accepted -- so the caller neither zeroes nor
 // reads it first.
-__global__ void __launch_bounds__(kUpdThreads, 4)
+#ifndef UGS_UPD_MINB
+#define UGS_UPD_MINB 4
+#endif
+__global__ void __launch_bounds__(kUpdThreads, UGS_UPD_MINB)
 update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restrict__ warp_rec,
                      const float *__restrict__ rgrad, int S, int64_t nwarp_all, int64_t n,
                      float scale, int adam, float *__restrict__ grad,

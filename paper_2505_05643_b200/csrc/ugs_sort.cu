@@ -293,7 +293,10 @@ slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict
 }
 
 template <int kBits>
-__global__ void __launch_bounds__(kSortThreads, 6)
+#ifndef UGS_SCATTER_MINB
+#define UGS_SCATTER_MINB 6
+#endif
+__global__ void __launch_bounds__(kSortThreads, UGS_SCATTER_MINB)
 slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss,
                      int S, const PlanHdr *__restrict__ hdr, const uint32_t *__restrict__ offs,
                      uint32_t *__restrict__ vals_out) {
