@@ -31,23 +31,20 @@ struct Rec {
     float4 r0, r1;
 };
 
-// Per tile instance (16 B): the exponent re-expanded EXACTLY (float64) around
-// the instance's own expansion pixel (pu, pv) = (ui, vi) clamped to the
-// instance's clipped tile rectangle:
-//   log2 w = A x^2 + B2 x y + C y^2 + D x + E y + F,  x = u - pu, y = v - pv
-// so pixel offsets never exceed the tile (|x|, |y| <= 15) whatever the
-// Gaussian's extent; inside the tile holding (ui, vi) the expansion is the
-// record's own.  (D, E, F, bits(record index)).
-using Inst = float4;
-
 // Per tile instance (32 B), written by the build in instance order (a
 // record's instances consecutive, row-major tiles): everything the raster
 // kernels need, so a tile's staging is one 32-byte gather per instance
 // (cp.async, sorted id -> Frag) instead of a dependent chain through the
 // record.
 //   q0 = (A, B2, C, color)   the record's quadratic and colour
-//   q1 = (D, E, F, bits)     the instance's exact re-expansion (Inst), and the
-//        clipped rectangle + expansion pixel relative to the tile origin:
+//   q1 = (D, E, F, bits)     the exponent re-expanded EXACTLY (float64, then
+//        float32) around the instance's own expansion pixel (pu, pv) = the
+//        record's reference pixel (ui, vi) clamped to the instance's clipped
+//        tile rectangle:
+//          log2 w = A x^2 + B2 x y + C y^2 + D x + E y + F,  x = u - pu, y = v - pv
+//        so pixel offsets never exceed the tile (|x|, |y| <= 15) whatever the
+//        Gaussian's extent; and the clipped rectangle + expansion pixel
+//        relative to the tile origin:
 //        x0 | x1 << 4 | y0 << 8 | y1 << 12 | pu << 16 | pv << 20
 struct Frag {
     float4 q0, q1;
