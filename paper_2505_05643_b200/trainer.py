@@ -706,8 +706,9 @@ class TrainEngine:
                 self.targets[int(idx[0])].view(first), lv, dpix, num, den)
 
     def step(self, idx, it: int, check_finite: bool = True, targets_batch=None):
-        """One full training step; returns the mean loss (python float) when
-        check_finite, else the device tensor.  Runs on the cloud's device."""
+        """One full training step; returns the mean loss over all ranks
+        (python float) when check_finite, else this rank's batch mean as a
+        device tensor (no collective).  Runs on the cloud's device."""
         with torch.cuda.device(self.cloud.device):
             self.settle()                    # the previous step is final
             if check_finite:
@@ -731,7 +732,10 @@ class TrainEngine:
         if len(out) > 6:
             num, den = out[6], out[7]     # flat buffers of a mixed-size batch
         loss_t = self.loss_mean
-        if self.world_size > 1:
+        if self.world_size > 1 and check_finite:
+            # every rank takes the same abort decision (a NaN anywhere
+            # propagates through the sum); without the check the step returns
+            # this rank's batch mean and issues no collective for it
             torch.distributed.all_reduce(loss_t, group=self.pg)
             loss_t = loss_t / self.world_size
         loss_val = None
