@@ -473,3 +473,24 @@ def test_grad_check_small_cloud():
                         "bg_intensity_raw", "bg_opacity_raw"}
     for k, v in rep.items():
         assert v < 2e-2, (k, v)
+
+
+def test_float64_cloud_warns_and_matches_float32():
+    """A float64 cloud (the reference would render it in float64) is
+    converted to the float32 path with a one-time UserWarning; the render
+    equals the float32 cloud's bitwise."""
+    import warnings
+    from paper_2505_05643_b200 import model as M
+    cloud_np, R, t, w, h, s, p, _ = cases.render_case(cases.RENDER_CASES[2])
+    spec = ug.SliceSpec(w, h, s, ug.ProbePose(R, t))
+    c64 = {k: (v.astype(np.float64) if isinstance(v, np.ndarray) else v)
+           for k, v in cloud_np.items()}
+    M._F64_WARNED = False
+    with warnings.catch_warnings(record=True) as rec:
+        warnings.simplefilter("always")
+        a = ug.GaussianCloud.from_numpy(c64)
+    assert any("float64" in str(x.message) for x in rec)
+    b = ug.GaussianCloud.from_numpy(cloud_np)
+    pa = ug.render_slice(a, spec, p=p).pixels
+    pb = ug.render_slice(b, spec, p=p).pixels
+    assert np.array_equal(pa, pb)
