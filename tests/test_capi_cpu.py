@@ -115,3 +115,37 @@ def test_fill_slices_c_helper_matches_numpy():
         fill_slices(a, specs, p)
         fill_slices_numpy(b, specs, p)
         assert bytes(a) == bytes(b), trial
+
+
+def test_render_chunk_splits_on_range_error():
+    """render_slices splits a batch whose tile instances exceed the 31-bit
+    budget (ugs_bin's UGS_ERR_RANGE) in halves until each part fits; other
+    errors propagate (host logic, no GPU: a stand-in renderer)."""
+    import pytest
+    from paper_2505_05643_b200 import _lib
+    from paper_2505_05643_b200.rasterizer import _render_chunk
+
+    class Fake:
+        def __init__(self, limit, status=_lib.UGS_ERR_RANGE):
+            self.limit, self.status, self.done = limit, status, []
+
+        def bin_async(self, cloud, chunk, p):
+            if len(chunk) > self.limit:
+                raise _lib.UGSError("too many", self.status)
+            self.cur = list(chunk)
+
+        def render(self, cloud, view):
+            view[:] = self.cur
+            self.done.append(list(self.cur))
+
+        def poll(self):
+            return False
+
+    specs = list(range(13))
+    out = np.full(13, -1)            # slices of it are views, like the (S, H, W) tensor
+    r = Fake(limit=3)
+    _render_chunk(r, None, specs, out, 0.95)
+    assert out.tolist() == specs and all(len(c) <= 3 for c in r.done)
+    with pytest.raises(_lib.UGSError):
+        _render_chunk(Fake(limit=3, status=_lib.UGS_ERR_CUDA), None, specs, np.full(13, -1),
+                      0.95)
