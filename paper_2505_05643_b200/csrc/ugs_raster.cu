@@ -17,21 +17,26 @@
 // offsets bounded by the tile, so with x fixed per lane a pair costs 2 FMA +
 // one MUFU ex2.
 //
-//   Forward: two records per warp (16-lane groups, cw = pow2 >= width
-//   columns x 16/cw rows per sweep); each group adds into its own PRIVATE
-//   (num, den) tile buffer (XOR-swizzled float2) and the 16 buffers are
-//   summed in fixed order -- the reference's multi-worker scheme (private
-//   accumulators summed, rasterizer.py:157-173), deterministic because the
-//   record -> group assignment is a stable sort.  `forward_ordered_kernel`
-//   keeps the strict ascending-index order per pixel (ref _kernels.py:23-47),
-//   selectable with ugs_plan_set_ordered.
-//   Backward: four records per warp (8-lane groups), two pixel streams per
-//   lane with fixed columns (stage_record<8>).  The per-Gaussian gradient
-//   needs only 7 weighted moments of the pixel offsets (sum G w, sum t,
-//   sum t dx, sum t dy, sum t dx^2, sum t dx dy, sum t dy^2; G = dpix/ssum,
-//   t = dw w), accumulated in registers; an 8-lane transpose-reduce leaves
-//   lane j with moment j and the group writes one 32-byte partial per tile
-//   instance.
+//   Forward: narrow records (< 9 clipped columns) two per warp (16-lane
+//   groups, cw = pow2 >= width columns x 16/cw rows per sweep); each group
+//   adds into its own PRIVATE (num, den) tile buffer (XOR-swizzled float2).
+//   Wide records one per warp, lane = (tile column, row parity), each lane
+//   keeping the (num, den) of its 8 pixels in REGISTERS across all of the
+//   tile's wide records.  At the end the register tiles join the group
+//   buffers and the 16 buffers are summed in fixed order -- the reference's
+//   multi-worker scheme (private accumulators summed, rasterizer.py:157-173),
+//   deterministic because the record -> group / warp assignment is a fixed
+//   function of the batch.  `forward_ordered_kernel` keeps the strict
+//   ascending-index order per pixel (ref _kernels.py:23-47), selectable with
+//   ugs_plan_set_ordered.
+//   Backward: eight records per warp (4-lane groups), two pixel streams per
+//   lane with fixed columns (stage_record4; records wider than 8 columns in
+//   two 8-column passes), units taken from a per-batch largest-first warp
+//   work queue.  The per-Gaussian gradient needs only 7 weighted moments of
+//   the pixel offsets (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
+//   sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
+//   registers; a 4-lane transpose-reduce leaves lane j with moments 2j and
+//   2j + 1 and the group writes one 32-byte partial per tile instance.
 // finalize_records sums a record's instance partials in order (shifting each
 // to the record's reference pixel) and applies the closed-form float64 chain
 // to d_mu, d_L and the raw parameters; update_gather accumulates every
