@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--budget", type=float, default=300.0)
     ap.add_argument("--target", type=float, default=0.99)
     ap.add_argument("--eval-every", type=int, default=100)
+    ap.add_argument("--densify", type=int, default=0, help="heuristic interval (0 = off)")
     ap.add_argument("--out", default="gpurun_out/cine_sweep.json")
     a = ap.parse_args()
 
@@ -67,7 +68,8 @@ def main():
     setup_s = time.perf_counter() - t_setup
     out = train_to_target(vol.world_bounds(), train_specs, gt_train, test_specs, gt_test,
                           n=a.n, batch=a.batch, budget=a.budget, target=a.target,
-                          eval_every=a.eval_every, log=lambda m: print(m, flush=True))
+                          eval_every=a.eval_every, densify=a.densify,
+                          log=lambda m: print(m, flush=True))
     out.update({"metric": "C4 cine sweep: held-out SSIM vs clean GT against training time",
                 "config": vars(a), "setup_s": setup_s, "train_frames": len(tr),
                 "test_frames": len(te), "frame": [h, w], "spacing_mm": vol.spacing})
