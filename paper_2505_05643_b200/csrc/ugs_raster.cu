@@ -29,14 +29,14 @@
 //   function of the batch.  `forward_ordered_kernel` keeps the strict
 //   ascending-index order per pixel (ref _kernels.py:23-47), selectable with
 //   ugs_plan_set_ordered.
-//   Backward: eight records per warp (4-lane groups), two pixel streams per
-//   lane with fixed columns (stage_record4; records wider than 8 columns in
-//   two 8-column passes), units taken from a per-batch largest-first warp
+//   Backward: sixteen records per warp (2-lane groups), two pixel streams
+//   per lane with fixed columns (stage_record2; records wider than 4 columns
+//   in 4-column passes), units taken from a per-batch largest-first warp
 //   work queue.  The per-Gaussian gradient needs only 7 weighted moments of
 //   the pixel offsets (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
 //   sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
-//   registers; a 4-lane transpose-reduce leaves lane j with moments 2j and
-//   2j + 1 and the group writes one 32-byte partial per tile instance.
+//   registers; a 2-lane transpose-reduce leaves lane j with moments 4j ..
+//   4j + 3 and the group writes one 32-byte partial per tile instance.
 // finalize_records sums a record's instance partials in order (shifting each
 // to the record's reference pixel) and applies the closed-form float64 chain
 // to d_mu, d_L and the raw parameters; update_gather accumulates every
@@ -58,8 +58,8 @@ constexpr int kKeyInvalid = kMaxTrips + 2;   // unused staging slots
 constexpr int kKeys = kMaxTrips + 3;
 // backward (4-lane groups): trip counts 1..16 (narrow / medium records) and
 // 17..32 (wide records, two column passes of h rows: key 16 + h), invalid 33
-constexpr int kBwdKeyInvalid = 2 * kMaxTrips + 1;
-constexpr int kBwdKeys = 2 * kMaxTrips + 2;
+constexpr int kBwdKeyInvalid = 4 * kMaxTrips + 1;
+constexpr int kBwdKeys = 4 * kMaxTrips + 2;
 constexpr int kKeysMax = kBwdKeys;
 #ifndef UGS_WIDE_MIN
 #define UGS_WIDE_MIN 9
@@ -179,33 +179,36 @@ constexpr size_t kBwdLyOff = align16(sizeof(Batch));
 constexpr size_t kBwdPixOff = kBwdLyOff + sizeof(Layout);
 constexpr size_t kBwdRawOff = align16(kBwdPixOff + sizeof(float2) * (kTile * kTile + kWarps));
 
-// Backward staging of one instance (one thread per record) for a group of 4
+// Backward staging of one instance (one thread per record) for a group of 2
 // lanes; returns its sort key.  Two pixel streams per lane, A and B, each
 // with a fixed column, so that x (hence P, Q) is per-lane constant:
-//   narrow (w <= 4, cw = pow2 >= w): A = (lx, ly), B = A + (0, R), R = 4/cw,
-//                                    both advance 2R rows per iteration
-//   medium (w 5..8):                 A = (gl, 0), B = A + (4, 0), one row
-//                                    per iteration
-//   wide   (w 9..16):                the medium layout twice, over columns
-//                                    0-7 and 8-15 (two passes of h rows)
+//   narrow  (w <= 2, cw = pow2 >= w): A = (lx, ly), B = A + (0, R), R = 2/cw,
+//                                     both advance 2R rows per iteration
+//   columns (w 3..16):                A = (gl, 0), B = A + (2, 0), one row
+//                                     per iteration, in ceil(w/4) passes
+//                                     over 4-column strips
 // with lx = gl & (cw-1), ly = gl >> log2 cw.  Key: the loop trip count
-// (1..16), wide records 16 + h, so a warp's eight records share a loop shape.
-//   sL = (cmask, lcw, B column offset, B row offset), sM = (w, h, x0, y0)
-__device__ __forceinline__ int stage_record4(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
+// (1..16; multi-pass records 16 (passes - 1) + rows), so a warp's sixteen
+// records share passes and rows.
+//   sL = (cmask, lcw, B column offset, B row offset), sM = (w, h, x0, y0),
+//   sC.z = passes
+__device__ __forceinline__ int stage_record2(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
                                              int slot) {
     const FragRect t = frag_rect(f.q1.w);
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
     const int lcw = (w > 1) ? 32 - __clz(w - 1) : 0;
-    const bool cols = lcw >= 3;                 // medium / wide: column-offset B
-    const int lcwA = cols ? 2 : lcw;
-    const int ls = cols ? 0 : 3 - lcw;          // log2 of the row stride
+    const bool cols = lcw >= 2;                 // column layouts: column-offset B
+    const int lcwA = cols ? 1 : lcw;
+    const int ls = cols ? 0 : 2 - lcw;          // log2 of the row stride
+    const int npass = cols ? (w + 3) >> 2 : 1;
     B.sA[slot] = make_float4(8388608.0f - (float)(t.x0 - t.pu),
                              8388608.0f - (float)(t.y0 - t.pv), f.q1.x, f.q1.y);
     B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
-    B.sC[slot] = make_float4(f.q0.w, __int_as_float(ls), 0.f, __int_as_float((int)inst));
-    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, cols ? 4 : 0, cols ? 0 : (4 >> lcw));
+    B.sC[slot] = make_float4(f.q0.w, __int_as_float(ls), __int_as_float(npass),
+                             __int_as_float((int)inst));
+    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, cols ? 2 : 0, cols ? 0 : (2 >> lcw));
     Ly.sM[slot] = make_int4(w, h, t.x0, t.y0);
-    return lcw == 4 ? kMaxTrips + h : (h + (1 << ls) - 1) >> ls;
+    return npass > 1 ? kMaxTrips * (npass - 1) + h : (h + (1 << ls) - 1) >> ls;
 }
 
 // Single-stream staging for the forward's 16-lane groups: cw = pow2 >= w
@@ -282,7 +285,7 @@ __device__ __forceinline__ int next_unit(uint32_t *ctr, int nunits) {
 // Returns, in B.base, each key's first sorted position.
 template <int NK>
 __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
-    static_assert(NK <= 64, "two keys per lane of warp 0");
+    constexpr int KPL = (NK + 31) / 32;   // keys per lane of warp 0
     constexpr int kInvalid = NK - 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // 1) per-warp key counts: each warp clears and fills its own row
@@ -293,19 +296,22 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
     __syncwarp();
     if (rank == 0) B.wcnt[warp][key] = __popc(peers);
     __syncthreads();
-    // 2) warp 0: bucket bases (exclusive scan over keys, lane k holds keys
-    //    2k and 2k + 1) and each warp's running offset per key
+    // 2) warp 0: bucket bases (exclusive scan over keys, lane l holds keys
+    //    KPL l .. KPL l + KPL - 1) and each warp's running offset per key
     if (warp == 0) {
-        uint32_t col[2] = {0u, 0u};
+        uint32_t col[KPL];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int k = 2 * lane + q;
+        for (int q = 0; q < KPL; ++q) {
+            col[q] = 0u;
+            const int k = KPL * lane + q;
             if (k < NK) {
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) col[q] += B.wcnt[w][k];
             }
         }
-        const uint32_t pair = col[0] + col[1];
+        uint32_t pair = 0u;
+#pragma unroll
+        for (int q = 0; q < KPL; ++q) pair += col[q];
         uint32_t incl = pair;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -314,8 +320,8 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
         }
         uint32_t run = incl - pair;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int k = 2 * lane + q;
+        for (int q = 0; q < KPL; ++q) {
+            const int k = KPL * lane + q;
             if (k < NK) {
                 B.base[k] = run;
 #pragma unroll
@@ -578,27 +584,19 @@ forward_ordered_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict
 }
 
 
-// Transpose-reduce of 8 values across a 4-lane group (2 levels, 6
-// shuffles): on return group lane g holds the group totals of values 2g and
-// 2g + 1.
-__device__ __forceinline__ float2 group_reduce8x4(const float a[8]) {
-    const int gl = threadIdx.x & 3;
-    const bool h2 = gl & 2, h1 = gl & 1;
+// Transpose-reduce of 8 values across a 2-lane group (one level, 4
+// shuffles): on return group lane g holds the group totals of values 4g ..
+// 4g + 3.
+__device__ __forceinline__ float4 group_reduce8x2(const float a[8]) {
+    const bool h1 = threadIdx.x & 1;
     float b[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const float send = h2 ? a[k] : a[k + 4];
-        const float keep = h2 ? a[k + 4] : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        const float send = h1 ? a[k] : a[k + 4];
+        const float keep = h1 ? a[k + 4] : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
     }
-    float c[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const float send = h1 ? b[k] : b[k + 2];
-        const float keep = h1 ? b[k + 2] : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-    }
-    return make_float2(c[0], c[1]);
+    return make_float4(b[0], b[1], b[2], b[3]);
 }
 
 __global__ void __launch_bounds__(kRasterThreads, 4)
@@ -656,29 +654,29 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
         __syncthreads();
         stage_wait();   // this thread's instance of the batch has landed
         int key = kBwdKeyInvalid;
-        if (threadIdx.x < nb) key = stage_record4(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
+        if (threadIdx.x < nb) key = stage_record2(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
         pipe.advance(vals, frag, raw, b0, rg.y);   // next batch, during this one
         sort_batch<kBwdKeys>(B, (uint32_t)key);
-        // eight records per warp (4-lane groups); every lane takes part in the
-        // shuffles, empty lanes carry zeros
-        const int nunits = (nb + 7) >> 3;
+        // sixteen records per warp (2-lane groups); every lane takes part in
+        // the shuffles, empty lanes carry zeros
+        const int nunits = (nb + 15) >> 4;
         for (int u = next_unit(&B.next[0], nunits); u >= 0; u = next_unit(&B.next[0], nunits)) {
-            const int s0 = u * 8;
-            const int slot = s0 + (lane >> 2);
+            const int s0 = u * 16;
+            const int slot = s0 + (lane >> 1);
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
             const int4 L = Ly.sL[j], M = Ly.sM[j];
-            const int gl = lane & 3;
+            const int gl = lane & 1;
             const int h = live ? M.y : 0;
             const int ls = __float_as_int(c.y), stride = 1 << ls;
-            const int npass = M.x > 8 ? 2 : 1;   // wide: columns 0-7, then 8-15
+            const int npass = __float_as_int(c.z);   // 4-column strips
             const float2 C2 = make_float2(b.z, b.z), c2 = make_float2(c.x, c.x);
             const float2 fs2 = make_float2((float)stride, (float)stride);
             float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             for (int pass = 0; pass < npass; ++pass) {
-                // the two pixel streams of stage_record4
-                const int lxA = (gl & L.x) + 8 * pass, lyA = gl >> L.y;
+                // the two pixel streams of stage_record2
+                const int lxA = (gl & L.x) + 4 * pass, lyA = gl >> L.y;
                 const int lxB = lxA + L.z, lyB = lyA + L.w;
                 const bool okA = lxA < M.x && lyA < h, okB = lxB < M.x && lyB < h;
                 const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
@@ -741,10 +739,10 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 m[5] += fmaf(dxA, Sya, dxB * Syb);
                 m[6] += Syya + Syyb;
             }
-            const float2 red = group_reduce8x4(m);
+            const float4 red = group_reduce8x2(m);
             if (live)
-                *reinterpret_cast<float2 *>(
-                    partial + (size_t)(uint32_t)__float_as_int(c.w) * 8 + 2 * gl) = red;
+                *reinterpret_cast<float4 *>(
+                    partial + (size_t)(uint32_t)__float_as_int(c.w) * 8 + 4 * gl) = red;
         }
     }
     __syncthreads();
