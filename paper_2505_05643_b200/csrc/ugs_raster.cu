@@ -177,7 +177,15 @@ constexpr size_t kFwdRawOff = align16(kFwdAccOff + sizeof(float2) * kGroups * kA
 // staged Frags
 constexpr size_t kBwdLyOff = align16(sizeof(Batch));
 constexpr size_t kBwdPixOff = kBwdLyOff + sizeof(Layout);
-constexpr size_t kBwdRawOff = align16(kBwdPixOff + sizeof(float2) * (kTile * kTile + kWarps));
+// the backward's per-pixel planes use a row pitch of kTile + 1 floats: the
+// rows a warp's sixteen records read fall on different banks
+#ifndef UGS_BWD_PITCH
+#define UGS_BWD_PITCH (kTile + 1)
+#endif
+constexpr int kBP = UGS_BWD_PITCH;
+constexpr int kBPlane = kBP * kTile;   // floats per plane
+constexpr size_t kBwdRawOff =
+    align16(kBwdPixOff + sizeof(float) * 2 * kBPlane + sizeof(float2) * kWarps);
 
 // Backward staging of one instance (one thread per record) for a group of 2
 // lanes; returns its sort key.  Two pixel streams per lane, A and B, each
@@ -615,8 +623,8 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     // per-pixel upstream terms as two planes (a lane's two streams load
     // straight into a register pair): G, then G chat
     float *pixG = reinterpret_cast<float *>(smem + kBwdPixOff);
-    float *pixGc = pixG + kTile * kTile;
-    float2 *s_bg = reinterpret_cast<float2 *>(pixGc + kTile * kTile);
+    float *pixGc = pixG + kBPlane;
+    float2 *s_bg = reinterpret_cast<float2 *>(pixGc + kBPlane);
     Frag *raw = reinterpret_cast<Frag *>(smem + kBwdRawOff);      // async-staged batch
     const ugs_slice &sl = slices[blockIdx.y];
     const int t = blockIdx.x;
@@ -639,8 +647,8 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
             // reference forms it (gradients.py:110), no cancellation
             Gb = G * (sigmoid_bg(bg_raw, 0) - chat);
         }
-        pixG[threadIdx.x] = G;
-        pixGc[threadIdx.x] = Gc;
+        pixG[(threadIdx.x >> 4) * kBP + (threadIdx.x & 15)] = G;
+        pixGc[(threadIdx.x >> 4) * kBP + (threadIdx.x & 15)] = Gc;
         float a = G, c = Gb;   // background partials of this tile, fixed order
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -691,10 +699,10 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
                 const float QB = fmaf(b.y, dxB, a.w);
                 const float dyA0 = big_float(lyA) - a.y;
-                const float *gA = pixG + (M.w + lyA) * kTile + M.z + lxA;
-                const float *gB = okB ? gA + (L.w * kTile + L.z) : gA;
-                const int gstep = okB ? stride * kTile : 0;
-                // the G chat plane sits kTile * kTile floats after the G plane
+                const float *gA = pixG + (M.w + lyA) * kBP + M.z + lxA;
+                const float *gB = okB ? gA + (L.w * kBP + L.z) : gA;
+                const int gstep = okB ? stride * kBP : 0;
+                // the G chat plane sits kBPlane floats after the G plane
                 // streams A and B in packed f32x2 arithmetic (FFMA2 / FADD2 /
                 // FMUL2, per-half fma.rn rounding): lo = A, hi = B
                 float2 dy2 = make_float2(dyA0, dyA0 + (float)L.w);
@@ -706,7 +714,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                     const float2 e = __ffma2_rn(dy2, __ffma2_rn(C2, dy2, Q2), P2);
                     const float2 w2 = make_float2(ex2_approx(e.x), ex2_approx(e.y));
                     const float2 gx = make_float2(gA[0], gB[0]);
-                    const float2 gy = make_float2(-gA[kTile * kTile], -gB[kTile * kTile]);
+                    const float2 gy = make_float2(-gA[kBPlane], -gB[kBPlane]);
                     const float2 t2 = __fmul2_rn(__ffma2_rn(gx, c2, gy), w2);   // dw * w
                     m02 = __ffma2_rn(gx, w2, m02);
                     S02 = __fadd2_rn(S02, t2);
@@ -714,7 +722,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                     Sy2 = __fadd2_rn(Sy2, ty2);
                     Syy2 = __ffma2_rn(ty2, dy2, Syy2);
                     dy2 = __fadd2_rn(dy2, fs2);
-                    gA += stride * kTile;
+                    gA += stride * kBP;
                     gB += gstep;
                 }
                 float m0 = m02.x + m02.y;
@@ -724,7 +732,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                     const float dyA = dy2.x;
                     const float wa = ex2_approx(fmaf(dyA, fmaf(b.z, dyA, QA), PA));
                     const float ga = gA[0];
-                    const float ta = fmaf(ga, c.x, -gA[kTile * kTile]) * wa;
+                    const float ta = fmaf(ga, c.x, -gA[kBPlane]) * wa;
                     m0 = fmaf(ga, wa, m0);
                     S0a += ta;
                     const float tya = ta * dyA;
