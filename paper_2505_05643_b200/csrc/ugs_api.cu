@@ -3,6 +3,7 @@
 // message (ugs_last_error), the reference raises InvalidParameterError at
 // its API layer for the same conditions (gradients.py:43-52).
 #include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <algorithm>
@@ -18,6 +19,15 @@ static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled(const char *kernel_name) {
+    static const std::string off = [] {
+        const char *e = getenv("UGS_PDL_OFF");
+        return e ? "," + std::string(e) + "," : std::string();
+    }();
+    if (off.empty()) return true;
+    return off.find("," + std::string(kernel_name) + ",") == std::string::npos;
+}
 
 static void harvest(ugs_plan *p, int stage) {
     if (!p->pending[stage]) return;

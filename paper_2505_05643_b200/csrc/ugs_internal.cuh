@@ -207,8 +207,8 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                              cudaStream_t st, Args... args) {
+inline cudaError_t launch_pdl_opt(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                  size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -218,16 +218,38 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+#ifdef UGS_NO_PDL
+    cfg.numAttrs = 0;   // experiment: plain stream-ordered launches
+#else
+    cfg.numAttrs = pdl ? 1 : 0;
+#endif
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+// Tuning knob: UGS_PDL_OFF="name1,name2" launches those kernels without the
+// programmatic attribute (read once per process).
+bool pdl_enabled(const char *kernel_name);
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    return launch_pdl_opt(true, kernel, grid, block, smem, st, args...);
+}
+
+// launch without the programmatic attribute (a plain stream-ordered launch)
+#define UGS_LAUNCH_EX(pdl, kernel, grid, block, smem, st, ...)                   \
+    do {                                                                         \
+        cudaError_t e_ = ::ugs::launch_pdl_opt((pdl) && ::ugs::pdl_enabled(#kernel), \
+                                               kernel, dim3(grid), dim3(block),  \
+                                               (size_t)(smem), st, __VA_ARGS__); \
+        if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, #kernel);             \
+    } while (0)
 
 // kernel<<<grid, block, smem, st>>>(args...) as a programmatic dependent
 // launch, followed by the usual launch check
 #define UGS_PDL(kernel, grid, block, smem, st, ...)                              \
     do {                                                                         \
-        cudaError_t e_ = ::ugs::launch_pdl(kernel, dim3(grid), dim3(block),      \
-                                           (size_t)(smem), st, __VA_ARGS__);     \
+        cudaError_t e_ = ::ugs::launch_pdl_opt(::ugs::pdl_enabled(#kernel), kernel, \
+                                               dim3(grid), dim3(block),          \
+                                               (size_t)(smem), st, __VA_ARGS__); \
         if (e_ != cudaSuccess) return ::ugs::cuda_fail(e_, #kernel);             \
     } while (0)
 

@@ -51,7 +51,12 @@ namespace {
 
 constexpr int kRasterThreads = 256;
 constexpr int kWarps = kRasterThreads / 32;
-constexpr int kBatch = 256;
+constexpr int kBatch = 256;              // forward: one staged record per thread
+#ifndef UGS_BWD_PER
+#define UGS_BWD_PER 2
+#endif
+constexpr int kBwdPer = UGS_BWD_PER;     // backward: staged records per thread
+constexpr int kBwdBatch = kBatch * kBwdPer;
 constexpr int kMaxTrips = kTile;   // sort buckets: sweeps of a 16-lane group
 constexpr int kKeyWide = kMaxTrips + 1;      // forward: warp-per-record class
 constexpr int kKeyInvalid = kMaxTrips + 2;   // unused staging slots
@@ -110,9 +115,9 @@ __device__ __forceinline__ float big_float(int x) {
 // Asynchronous staging of a tile's instances: each thread gathers the
 // 32-byte Frag of its slot of the NEXT batch with cp.async (LDGSTS, L2 only)
 // straight into shared memory while the CTA accumulates the current batch;
-// the sorted ids are prefetched a batch further ahead in a register.  A slot
-// is only ever written and read by its own thread, so the copy needs no
-// barrier: cp.async.wait_all makes it visible to that thread.
+// the sorted ids are prefetched a batch further ahead.  A slot is only ever
+// written and read by its own thread, so the copies need no barrier:
+// cp.async.wait_all makes them visible to that thread.
 __device__ __forceinline__ void stage_async(Frag *dst, const Frag *src) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
@@ -120,22 +125,24 @@ __device__ __forceinline__ void stage_async(Frag *dst, const Frag *src) {
                  "l"(reinterpret_cast<const char *>(src) + 16)
                  : "memory");
 }
+__device__ __forceinline__ void stage_id_async(uint32_t *dst, const uint32_t *src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
 __device__ __forceinline__ void stage_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Per-thread staging pipeline over a tile's sorted range [lo, hi): `cur` is
-// the instance id whose Frag is in flight to raw[tid], `nxt` the next
-// batch's id (0 past the end).
-struct StagePipe {
-    uint32_t cur, nxt;
+// Per-thread staging pipeline over a tile's sorted range [lo, hi) (forward):
+// `nxt` = the next batch's id, prefetched in a register.
+struct StagePipeReg {
+    uint32_t nxt;
     __device__ __forceinline__ void start(const uint32_t *__restrict__ vals,
                                           const Frag *__restrict__ frag, Frag *raw, int lo,
                                           int hi) {
         const int i = lo + (int)threadIdx.x;
-        cur = i < hi ? __ldg(vals + i) : 0u;
-        if (i < hi) stage_async(raw + threadIdx.x, frag + cur);
+        if (i < hi) stage_async(raw + threadIdx.x, frag + __ldg(vals + i));
         stage_commit();
         nxt = i + kBatch < hi ? __ldg(vals + i + kBatch) : 0u;
     }
@@ -144,10 +151,53 @@ struct StagePipe {
                                             const Frag *__restrict__ frag, Frag *raw, int b0,
                                             int hi) {
         const int i = b0 + kBatch + (int)threadIdx.x;
-        cur = nxt;
-        if (i < hi) stage_async(raw + threadIdx.x, frag + cur);
+        if (i < hi) stage_async(raw + threadIdx.x, frag + nxt);
         stage_commit();
         nxt = i + kBatch < hi ? __ldg(vals + i + kBatch) : 0u;
+    }
+};
+
+// The same pipeline with its state in shared memory (backward, whose
+// register budget is full: ids held across a batch were spilled, and the
+// spill store waited on the load): ids[tid] = the id of this thread's slot
+// of the batch after the one in flight to raw[tid], fetched by a 4-byte
+// cp.async; cur[tid] = the id in raw[tid].
+struct StagePipe {
+    uint32_t *ids, *cur;
+    __device__ __forceinline__ StagePipe(uint32_t *ids_, uint32_t *cur_) : ids(ids_), cur(cur_) {}
+    __device__ __forceinline__ void start(const uint32_t *__restrict__ vals,
+                                          const Frag *__restrict__ frag, Frag *raw, int lo,
+                                          int hi) {
+#pragma unroll
+        for (int r = 0; r < kBwdPer; ++r) {
+            const int sl = (int)threadIdx.x + r * kBatch, i = lo + sl;
+            if (i < hi) {
+                const uint32_t c = __ldg(vals + i);
+                cur[sl] = c;
+                stage_async(raw + sl, frag + c);
+            }
+            if (i + kBwdBatch < hi) stage_id_async(ids + sl, vals + i + kBwdBatch);
+        }
+        stage_commit();
+    }
+    // after this thread staged batch b0 from raw (and after stage_wait):
+    // fetch batch b0 + kBwdBatch, and the ids of the batch after it
+    __device__ __forceinline__ void advance(const uint32_t *__restrict__ vals,
+                                            const Frag *__restrict__ frag, Frag *raw, int b0,
+                                            int hi) {
+#pragma unroll
+        for (int r = 0; r < kBwdPer; ++r) {
+            const int sl = (int)threadIdx.x + r * kBatch, i = b0 + kBwdBatch + sl;
+            if (i < hi) {
+                // read before the id copy below overwrites the slot: the Frag
+                // copy's address depends on it
+                const uint32_t c = ids[sl];
+                cur[sl] = c;
+                stage_async(raw + sl, frag + c);
+            }
+            if (i + kBwdBatch < hi) stage_id_async(ids + sl, vals + i + kBwdBatch);
+        }
+        stage_commit();
     }
 };
 
@@ -158,15 +208,21 @@ struct StagePipe {
 //   sC = (color, ls, -, instance)   ls = log2 of the stream's row stride
 //   sL = (cmaskA, lcwA, wideoff, lyoff), sM = (w, h, x0, y0): the record's
 //        two-stream lane layout (stage_layout)
-struct Batch {
-    float4 sA[kBatch], sB[kBatch], sC[kBatch];
-    uint16_t order[kBatch];            // staged slot of the j-th record by trips
-    uint32_t wcnt[kWarps][kKeysMax];
+template <int NB, int NROWS>
+struct BatchT {
+    float4 sA[NB], sB[NB], sC[NB];
+    uint16_t order[NB];                // staged slot of the j-th record by trips
+    uint32_t wcnt[NROWS][kKeysMax];    // per (slot round, warp) key counts
     uint32_t base[kKeysMax];
     uint32_t next[2];                  // work-queue counters of the batch
 };
-struct Layout {   // two-stream layouts (backward), after the Batch
-    int4 sL[kBatch], sM[kBatch];
+using Batch = BatchT<kBatch, kWarps>;                      // forward
+using BwdBatch = BatchT<kBwdBatch, kWarps * kBwdPer>;      // backward
+// two-stream layouts (backward), after the BwdBatch, byte fields:
+//   sL = lcwA | B column offset << 8 | B row offset << 16  (cmaskA = lcwA)
+//   sM = w | h << 8 | x0 << 16 | y0 << 24
+struct Layout {
+    int2 sLM[kBwdBatch];
 };
 
 constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -175,7 +231,7 @@ constexpr size_t kFwdAccOff = align16(sizeof(Batch));
 constexpr size_t kFwdRawOff = align16(kFwdAccOff + sizeof(float2) * kGroups * kAccStride);
 // backward shared memory: Batch | Layout | pixel terms + bg partials |
 // staged Frags
-constexpr size_t kBwdLyOff = align16(sizeof(Batch));
+constexpr size_t kBwdLyOff = align16(sizeof(BwdBatch));
 constexpr size_t kBwdPixOff = kBwdLyOff + sizeof(Layout);
 // the backward's per-pixel planes use a row pitch of kTile + 1 floats: the
 // rows a warp's sixteen records read fall on different banks
@@ -186,6 +242,7 @@ constexpr int kBP = UGS_BWD_PITCH;
 constexpr int kBPlane = kBP * kTile;   // floats per plane
 constexpr size_t kBwdRawOff =
     align16(kBwdPixOff + sizeof(float) * 2 * kBPlane + sizeof(float2) * kWarps);
+constexpr size_t kBwdIdsOff = kBwdRawOff + sizeof(Frag) * kBwdBatch;   // StagePipe ids, cur
 
 // Backward staging of one instance (one thread per record) for a group of 2
 // lanes; returns its sort key.  Two pixel streams per lane, A and B, each
@@ -198,9 +255,8 @@ constexpr size_t kBwdRawOff =
 // with lx = gl & (cw-1), ly = gl >> log2 cw.  Key: the loop trip count
 // (1..16; multi-pass records 16 (passes - 1) + rows), so a warp's sixteen
 // records share passes and rows.
-//   sL = (cmask, lcw, B column offset, B row offset), sM = (w, h, x0, y0),
-//   sC.z = passes
-__device__ __forceinline__ int stage_record2(const Frag &f, uint32_t inst, Batch &B, Layout &Ly,
+//   sLM = the byte-packed layout (struct Layout), sC.z = passes
+__device__ __forceinline__ int stage_record2(const Frag &f, uint32_t inst, BwdBatch &B, Layout &Ly,
                                              int slot) {
     const FragRect t = frag_rect(f.q1.w);
     const int w = t.x1 - t.x0 + 1, h = t.y1 - t.y0 + 1;
@@ -214,8 +270,8 @@ __device__ __forceinline__ int stage_record2(const Frag &f, uint32_t inst, Batch
     B.sB[slot] = make_float4(f.q0.x, f.q0.y, f.q0.z, f.q1.z);
     B.sC[slot] = make_float4(f.q0.w, __int_as_float(ls), __int_as_float(npass),
                              __int_as_float((int)inst));
-    Ly.sL[slot] = make_int4((1 << lcwA) - 1, lcwA, cols ? 2 : 0, cols ? 0 : (2 >> lcw));
-    Ly.sM[slot] = make_int4(w, h, t.x0, t.y0);
+    Ly.sLM[slot] = make_int2(lcwA | ((cols ? 2 : 0) << 8) | ((cols ? 0 : (2 >> lcw)) << 16),
+                             w | (h << 8) | (t.x0 << 16) | (t.y0 << 24));
     return npass > 1 ? kMaxTrips * (npass - 1) + h : (h + (1 << ls) - 1) >> ls;
 }
 
@@ -291,21 +347,31 @@ __device__ __forceinline__ int next_unit(uint32_t *ctr, int nunits) {
 // forward's wide class; unused slots last) -- warp match-any ranks +
 // per-warp bucket counters: a deterministic record -> lane-group mapping.
 // Returns, in B.base, each key's first sorted position.
-template <int NK>
-__device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
+template <int NK, int PER, class BT>
+__device__ __forceinline__ void sort_batch(BT &B, const uint32_t (&key)[PER]) {
     constexpr int KPL = (NK + 31) / 32;   // keys per lane of warp 0
     constexpr int kInvalid = NK - 1;
+    constexpr int kRows = kWarps * PER;   // row r kWarps + w: slots r kBatch + 32 w ..
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // 1) per-warp key counts: each warp clears and fills its own row
-    for (int k = lane; k < NK; k += 32) B.wcnt[warp][k] = 0u;
+    // 1) per-row key counts: each warp clears and fills its own rows
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+        for (int k = lane; k < NK; k += 32) B.wcnt[r * kWarps + warp][k] = 0u;
     if (threadIdx.x < 2) B.next[threadIdx.x] = 0u;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    uint32_t rank[PER];
+    unsigned peers[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        peers[r] = __match_any_sync(0xffffffffu, key[r]);
+        rank[r] = __popc(peers[r] & ((1u << lane) - 1u));
+    }
     __syncwarp();
-    if (rank == 0) B.wcnt[warp][key] = __popc(peers);
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+        if (rank[r] == 0) B.wcnt[r * kWarps + warp][key[r]] = __popc(peers[r]);
     __syncthreads();
     // 2) warp 0: bucket bases (exclusive scan over keys, lane l holds keys
-    //    KPL l .. KPL l + KPL - 1) and each warp's running offset per key
+    //    KPL l .. KPL l + KPL - 1) and each row's running offset per key
     if (warp == 0) {
         uint32_t col[KPL];
 #pragma unroll
@@ -314,7 +380,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
             const int k = KPL * lane + q;
             if (k < NK) {
 #pragma unroll
-                for (int w = 0; w < kWarps; ++w) col[q] += B.wcnt[w][k];
+                for (int w = 0; w < kRows; ++w) col[q] += B.wcnt[w][k];
             }
         }
         uint32_t pair = 0u;
@@ -333,7 +399,7 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
             if (k < NK) {
                 B.base[k] = run;
 #pragma unroll
-                for (int w = 0; w < kWarps; ++w) {
+                for (int w = 0; w < kRows; ++w) {
                     const uint32_t c = B.wcnt[w][k];
                     B.wcnt[w][k] = run;
                     run += c;
@@ -343,7 +409,11 @@ __device__ __forceinline__ void sort_batch(Batch &B, uint32_t key) {
     }
     __syncthreads();
     // 3) stable positions
-    if (key != (uint32_t)kInvalid) B.order[B.wcnt[warp][key] + rank] = (uint16_t)threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+        if (key[r] != (uint32_t)kInvalid)
+            B.order[B.wcnt[r * kWarps + warp][key[r]] + rank[r]] =
+                (uint16_t)(threadIdx.x + r * kBatch);
     __syncthreads();
 }
 
@@ -379,7 +449,7 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
-    StagePipe pipe;
+    StagePipeReg pipe;
     pipe.start(vals, frag, raw, rg.x, rg.y);
     for (int i = threadIdx.x; i < kGroups * kAccStride; i += kRasterThreads)
         acc[i] = make_float2(0.f, 0.f);
@@ -405,7 +475,10 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
         pipe.advance(vals, frag, raw, b0, rg.y);
         // narrow records with equal sweep counts share a warp (two per
         // warp); the wide records follow them
-        sort_batch<kKeys>(B, key);
+        {
+            const uint32_t k1[1] = {key};
+            sort_batch<kKeys>(B, k1);
+        }
         const int n_narrow = (int)B.base[kKeyWide];
         const int n_valid = (int)B.base[kKeyInvalid];
         for (int s0 = warp * 2; s0 < n_narrow; s0 += kWarps * 2) {
@@ -618,7 +691,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     pdl_entry();
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
-    Batch &B = *reinterpret_cast<Batch *>(smem);
+    BwdBatch &B = *reinterpret_cast<BwdBatch *>(smem);
     Layout &Ly = *reinterpret_cast<Layout *>(smem + kBwdLyOff);
     // per-pixel upstream terms as two planes (a lane's two streams load
     // straight into a register pair): G, then G chat
@@ -632,7 +705,9 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int2 rg = bin_range[sl.tile_base + t];
-    StagePipe pipe;   // the first batch lands while the pixel terms load
+    // the first batch lands while the pixel terms load
+    uint32_t *pipe_ids = reinterpret_cast<uint32_t *>(smem + kBwdIdsOff);
+    StagePipe pipe(pipe_ids, pipe_ids + kBwdBatch);
     pipe.start(vals, frag, raw, rg.x, rg.y);
     {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
         const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
@@ -657,14 +732,19 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
         }
         if (lane == 0) s_bg[warp] = make_float2(a, c);
     }
-    for (int b0 = rg.x; b0 < rg.y; b0 += kBatch) {
-        const int nb = min(kBatch, rg.y - b0);
+    for (int b0 = rg.x; b0 < rg.y; b0 += kBwdBatch) {
+        const int nb = min(kBwdBatch, rg.y - b0);
         __syncthreads();
-        stage_wait();   // this thread's instance of the batch has landed
-        int key = kBwdKeyInvalid;
-        if (threadIdx.x < nb) key = stage_record2(raw[threadIdx.x], pipe.cur, B, Ly, threadIdx.x);
+        stage_wait();   // this thread's instances of the batch have landed
+        uint32_t key[kBwdPer];
+#pragma unroll
+        for (int r = 0; r < kBwdPer; ++r) {
+            const int sl = (int)threadIdx.x + r * kBatch;
+            key[r] = sl < nb ? (uint32_t)stage_record2(raw[sl], pipe.cur[sl], B, Ly, sl)
+                             : (uint32_t)kBwdKeyInvalid;
+        }
         pipe.advance(vals, frag, raw, b0, rg.y);   // next batch, during this one
-        sort_batch<kBwdKeys>(B, (uint32_t)key);
+        sort_batch<kBwdKeys>(B, key);
         // sixteen records per warp (2-lane groups); every lane takes part in
         // the shuffles, empty lanes carry zeros
         const int nunits = (nb + 15) >> 4;
@@ -674,9 +754,11 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
             const bool live = slot < nb;
             const int j = live ? B.order[slot] : B.order[s0];
             const float4 a = B.sA[j], b = B.sB[j], c = B.sC[j];
-            const int4 L = Ly.sL[j], M = Ly.sM[j];
+            const int2 lm = Ly.sLM[j];
+            const int Lx = byte_of(lm.x, 0), Lz = byte_of(lm.x, 1), Lw = byte_of(lm.x, 2);
+            const int Mx = byte_of(lm.y, 0), Mz = byte_of(lm.y, 2), Mw = byte_of(lm.y, 3);
             const int gl = lane & 1;
-            const int h = live ? M.y : 0;
+            const int h = live ? byte_of(lm.y, 1) : 0;
             const int ls = __float_as_int(c.y), stride = 1 << ls;
             const int npass = __float_as_int(c.z);   // 4-column strips
             const float2 C2 = make_float2(b.z, b.z), c2 = make_float2(c.x, c.x);
@@ -684,28 +766,28 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
             float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             for (int pass = 0; pass < npass; ++pass) {
                 // the two pixel streams of stage_record2
-                const int lxA = (gl & L.x) + 4 * pass, lyA = gl >> L.y;
-                const int lxB = lxA + L.z, lyB = lyA + L.w;
-                const bool okA = lxA < M.x && lyA < h, okB = lxB < M.x && lyB < h;
+                const int lxA = (gl & Lx) + 4 * pass, lyA = gl >> Lx;
+                const int lxB = lxA + Lz, lyB = lyA + Lw;
+                const bool okA = lxA < Mx && lyA < h, okB = lxB < Mx && lyB < h;
                 const int nA = okA ? (h - lyA + stride - 1) >> ls : 0;
                 // column layouts always pair A with B (B masked when out of
                 // the rectangle)
-                const int nB = okB ? (h - lyB + stride - 1) >> ls : (L.z ? nA : 0);
+                const int nB = okB ? (h - lyB + stride - 1) >> ls : (Lz ? nA : 0);
                 // per lane dx is fixed per stream: log2 w = P + dy (Q + C dy);
                 // the x moments follow from the per-stream sums (sum t dx =
                 // dx S0, ...)
-                const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)L.z;
+                const float dxA = big_float(lxA) - a.x, dxB = dxA + (float)Lz;
                 const float PA = fmaf(fmaf(b.x, dxA, a.z), dxA, b.w), QA = fmaf(b.y, dxA, a.w);
                 const float PB = okB ? fmaf(fmaf(b.x, dxB, a.z), dxB, b.w) : -INFINITY;
                 const float QB = fmaf(b.y, dxB, a.w);
                 const float dyA0 = big_float(lyA) - a.y;
-                const float *gA = pixG + (M.w + lyA) * kBP + M.z + lxA;
-                const float *gB = okB ? gA + (L.w * kBP + L.z) : gA;
+                const float *gA = pixG + (Mw + lyA) * kBP + Mz + lxA;
+                const float *gB = okB ? gA + (Lw * kBP + Lz) : gA;
                 const int gstep = okB ? stride * kBP : 0;
                 // the G chat plane sits kBPlane floats after the G plane
                 // streams A and B in packed f32x2 arithmetic (FFMA2 / FADD2 /
                 // FMUL2, per-half fma.rn rounding): lo = A, hi = B
-                float2 dy2 = make_float2(dyA0, dyA0 + (float)L.w);
+                float2 dy2 = make_float2(dyA0, dyA0 + (float)Lw);
                 const float2 P2 = make_float2(PA, PB), Q2 = make_float2(QA, QB);
                 float2 m02 = make_float2(0.f, 0.f), S02 = m02, Sy2 = m02, Syy2 = m02;
                 int i = 0;
@@ -1203,7 +1285,11 @@ __global__ void bg_finalize_kernel(const double2 *__restrict__ sums, int S,
 }
 
 constexpr size_t kFwdSmem = kFwdRawOff + sizeof(Frag) * kBatch;
-constexpr size_t kBwdSmem = kBwdRawOff + sizeof(Frag) * kBatch;
+constexpr size_t kBwdSmem = kBwdIdsOff + 2 * sizeof(uint32_t) * kBwdBatch;
+// four backward CTAs per SM (the register budget's count): 228 KB of shared
+// memory per SM, 1 KB of it reserved per CTA
+static_assert(4 * (kBwdSmem + 1024) <= 228 * 1024, "backward shared memory per CTA");
+static_assert(4 * (kFwdSmem + 1024) <= 228 * 1024, "forward shared memory per CTA");
 
 int set_smem_attrs() {
     static std::atomic<unsigned long long> done{0};
@@ -1251,7 +1337,13 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     dim3 grid(p.max_tiles, p.S);
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
-    UGS_PDL(backward_kernel, grid, kRasterThreads, kBwdSmem, st,
+#ifndef UGS_PDL_BWD
+#define UGS_PDL_BWD 1
+#endif
+#ifndef UGS_PDL_FIN
+#define UGS_PDL_FIN 0   // finalize CTAs parked during the backward's tail: 1.53 -> 1.49 ms/step
+#endif
+    UGS_LAUNCH_EX(UGS_PDL_BWD, backward_kernel, grid, kRasterThreads, kBwdSmem, st,
         p.b.frag, vals, p.b.bin_range, p.b.slices, num, den, dpix,
         c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b));
     UGS_LAUNCH_CHECK("backward_kernel");
@@ -1290,7 +1382,7 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                       const_cast<float *>(c.opacity_raw)};
     if (p.m_grid > 0) {
         const int th = 128;
-        UGS_PDL(finalize_records_kernel, (unsigned)((p.m_grid + th - 1) / th), th, 0, st,
+        UGS_LAUNCH_EX(UGS_PDL_FIN, finalize_records_kernel, (unsigned)((p.m_grid + th - 1) / th), th, 0, st,
         p.b.rec, p.b.rec_gid, p.b.rec_inst, p.b.partial, plan_hdr(p.b), p.b.slice_base, p.S,
             p.b.slices, c.means, c.l_raw, (float)c.beta, p.b.rgrad);
         UGS_LAUNCH_CHECK("finalize_records_kernel");
