@@ -503,6 +503,22 @@ def run_ours(a):
         traffic = tr.get(dom + "_kernel_dram_bytes")
     except (OSError, ValueError):
         pass
+    # the dominant kernel's own pipe view from the newest committed ncu
+    # capture (frac is on the reference's operator count; see the note)
+    executed = None
+    try:
+        import glob
+        nf = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_r*.json")))[-1]
+        for k in json.load(open(nf))["kernels"]:
+            if k["kernel"] == dom + "_kernel":
+                executed = {
+                    "source": os.path.relpath(nf, ROOT),
+                    "issue_active_pct": float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0]),
+                    "fma_pipe_inst_pct": float(k["sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"].split()[0]),
+                    "xu_pipe_inst_pct": float(k["sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"].split()[0]),
+                    "warp_instructions": float(k["smsp__inst_executed.sum"].split()[0])}
+    except (OSError, ValueError, IndexError, KeyError):
+        pass
     n = eng.cloud.n
     # parameter update (update_gather_kernel): N=1 fuses accumulate + stats +
     # Adam -- reads params 44 B + m, v 96 B and writes them back (280 B per
@@ -556,7 +572,13 @@ def run_ours(a):
                              "SURVEY 8d) x pairs per launch / CUDA-event launch time (stage "
                              "events on the launch stream, a second pass of the same K steps); "
                              "peak = FP32 FFMA probe measured in this run (no tensor cores: "
-                             "not a dense contraction)"},
+                             "not a dense contraction).  frac near or above 1 says the kernel "
+                             "does fewer operations per pair than the reference's count "
+                             "(plane-conditioned exponent: 2 packed FMAs + one ex2 per pixel "
+                             "pair, moments instead of per-pair parameter chains); how busy "
+                             "the SM actually is: `executed` (ncu, issue-bound with the FMA "
+                             "and MUFU pipes co-saturated in the pixel loop)",
+                     "executed": executed},
         "roofline_stages": roof_stages,
         "stage_ms_per_step": stage_ms,
         "gpu_launches": int(launches),
