@@ -154,6 +154,17 @@ UGS_API int ugs_forward(ugs_plan *plan, const ugs_cloud *cloud, float *num, floa
  * clip(num / den) of ugs_forward's num and den. */
 UGS_API int ugs_render(ugs_plan *plan, const ugs_cloud *cloud, float *pixels, void *stream);
 
+/* ugs_bin_async + ugs_render in one call (the batched serving path,
+ * rasterizer.py:182-186 render_slice per slice of a batch): on a sized plan
+ * the binning chain (count -> scan -> plan -> emit -> bin sort) is one CUDA
+ * graph, captured on first use and replayed while the plan's buffers, the
+ * cloud and the batch shape repeat; the render follows it on the stream.
+ * Same contract as the two calls: ugs_plan_poll reports an overflowed
+ * batch, which the caller re-issues (ugs_bin + ugs_render).  An unsized
+ * plan takes the synchronous bin. */
+UGS_API int ugs_render_batch(ugs_plan *plan, const ugs_cloud *cloud, ugs_slice *slices, int S,
+                     float *pixels, void *stream);
+
 /* Gradient / Adam-moment layout ("AoS-12", float32, 12 n + 2 entries):
  * Gaussian g owns [12 g, 12 g + 12) = [d_means 0..2 | d_l_raw 3..8 |
  * d_intensity_raw 9 | d_opacity_raw 10 | pad 11]; [12 n, 12 n + 2) holds

@@ -79,6 +79,8 @@ EXPORTS = {
                                        ctypes.POINTER(c_i64), c_vp]),
     "ugs_forward": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp]),
     "ugs_render": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp]),
+    "ugs_render_batch": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, ctypes.c_int,
+                                        c_vp, c_vp]),
     "ugs_backward": (ctypes.c_int, [c_vp, ctypes.POINTER(Cloud), c_vp, c_vp, c_vp,
                                     c_vp, c_vp, c_f, c_vp]),
     "ugs_grad_stats": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),

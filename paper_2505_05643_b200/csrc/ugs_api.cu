@@ -158,6 +158,8 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
                     b.bin_bg};
     for (void *q : bufs)
         if (q) cudaFree(q);
+    if (p->rgraph) cudaGraphExecDestroy(p->rgraph);
+    if (p->cap) cudaStreamDestroy(p->cap);
     delete[] p->h_slice_base;
     delete[] p->h_m;
     delete[] p->h_tile_base;
@@ -274,8 +276,16 @@ void read_counts(ugs_plan *p, int S, int64_t *m_out, int64_t *k_out, int64_t *p_
 // launches cover the plan's capacities, the device compares the batch's
 // totals against them (plan_slices) and, if the batch does not fit, every
 // later kernel of the plan returns at entry; ugs_plan_poll reports it.
-int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,
-             bool async, int64_t *m_out, int64_t *k_out, int64_t *p_out) {
+struct BinPrep {
+    int nblk = 0, max_tiles = 0, n_bins = 0, slot = 0;
+    unsigned long long *hp = nullptr;   // this call's pinned totals slot
+};
+
+// Host side of a bin call: validation, tile layout, buffers, the ring slot
+// and the slice constants' H2D copy.  `async` is cleared when the call must
+// be synchronous (unsized plan, radix fallback).
+int bin_prepare(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,
+                bool &async, BinPrep &bp) {
     if (!p || !slices || S < 1 || S > 64) {
         set_error("ugs_bin: need a plan and 1 <= S <= 64 slices");
         return UGS_ERR_INVALID;
@@ -376,6 +386,79 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
     std::memcpy(hs, slices, sizeof(ugs_slice) * S);
     UGS_CUDA(cudaMemcpyAsync(b.slices, hs, sizeof(ugs_slice) * S, cudaMemcpyHostToDevice, st));
     UGS_CUDA(cudaEventRecord(p->ev_slices[slot], st));
+    bp.nblk = nblk;
+    bp.max_tiles = max_tiles;
+    bp.n_bins = n_bins;
+    bp.slot = slot;
+    bp.hp = hp;
+    return UGS_OK;
+}
+
+// The sync-free kernel chain of a bin call (count -> scan -> plan -> emit ->
+// bin sort) over the plan's capacities; the device flags a batch that does
+// not fit and every later kernel of the plan returns at entry.
+int bin_async_chain(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp,
+                    cudaStream_t st) {
+    PlanBuffers &b = p->b;
+    int rc;
+    const int nblk = bp.nblk, max_tiles = bp.max_tiles, n_bins = bp.n_bins;
+    stage_begin(p, kStageCount, st);
+    if (c->n > 0) {
+        if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
+                                       b.win_sparse, b.amask, b.wcnt, st)))
+            return rc;
+        if ((rc = launch_prepare_scan(b.blk_cnt, b.blk_pairs, S, nblk, b.slice_tot, st)))
+            return rc;
+    } else {
+        UGS_CUDA(cudaMemsetAsync(b.slice_tot, 0, sizeof(unsigned long long) * 3 * S, st));
+    }
+    if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices,
+                                 caps_of(p), st)))
+        return rc;
+    stage_end(p, kStageCount, st);
+    p->counts_pending = true;
+    p->slice_sort = true;
+    p->m_grid = p->m_cap;
+    p->k_grid = p->k_cap;
+    p->nblk_grid = p->nblk_cap;
+    const PlanHdr *hdr = plan_hdr(b);
+    stage_begin(p, kStageEmit, st);
+    if (c->n > 0) {
+        if ((rc = launch_prepare_emit(*c, b.slices, S, b.blk_cnt, nblk, b.slice_base,
+                                      b.rec, b.rec_gid, b.rec_inst, b.frag, b.keys, hdr,
+                                      p->m_grid, b.win_sparse, b.amask, b.wcnt, b.warp_rec,
+                                      b.warp_inst, b.rec_bucket, st)))
+            return rc;
+    } else {
+        UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));
+    }
+    stage_end(p, kStageEmit, st);
+    stage_begin(p, kStageSort, st);
+    if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, p->hist_cap, max_tiles, n_bins,
+                              (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals, b.bin_range, st)))
+        return rc;
+    p->sorted_keys = nullptr;
+    p->sorted_vals = b.vals;
+    stage_end(p, kStageSort, st);
+    return UGS_OK;
+}
+
+// the totals of a sync-free call to its pinned slot (read by ugs_plan_poll)
+int bin_async_totals(ugs_plan *p, const BinPrep &bp, cudaStream_t st) {
+    UGS_CUDA(cudaMemcpyAsync(bp.hp, p->b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                             cudaMemcpyDeviceToHost, st));
+    UGS_CUDA(cudaEventRecord(p->ev_counts[bp.slot], st));
+    return UGS_OK;
+}
+
+// The synchronous remainder of a bin call: count, read the totals back, size
+// the buffers, then emit and sort exactly.
+int bin_sync_rest(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp, cudaStream_t st,
+                  int64_t *m_out, int64_t *k_out, int64_t *p_out) {
+    int rc;
+    PlanBuffers &b = p->b;
+    const int nblk = bp.nblk, max_tiles = bp.max_tiles, n_bins = bp.n_bins, slot = bp.slot;
+    unsigned long long *hp = bp.hp;
     stage_begin(p, kStageCount, st);
     if (c->n > 0) {
         if ((rc = launch_prepare_count(*c, b.slices, S, b.blk_cnt, b.blk_pairs, nblk,
@@ -387,23 +470,19 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
         UGS_CUDA(cudaMemsetAsync(b.slice_tot, 0, sizeof(unsigned long long) * 3 * S, st));
     }
     // bases, sort tables and the overflow flag on the device; the totals go
-    // to pinned memory (read now, or by ugs_plan_poll)
+    // to pinned memory now: a synchronous call sizes its buffers from them
+    // (the sync-free chain copies them after the sort instead, so its
+    // kernels stay back to back -- programmatic dependent launches overlap
+    // consecutive kernels only)
     if ((rc = launch_plan_slices(b.slice_tot, b.slices, S, b.slice_base, b.sort_slices,
                                  caps_of(p), st)))
         return rc;
-    // the totals go to pinned memory: now (a synchronous call sizes its
-    // buffers from them), or -- sync-free -- after the sort, so the kernel
-    // chain count -> ... -> sort stays back to back (programmatic dependent
-    // launches overlap consecutive kernels only); the host reads them at the
-    // next poll either way
-    if (!async) {
-        UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
-                                 cudaMemcpyDeviceToHost, st));
-        UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
-    }
+    UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
+                             cudaMemcpyDeviceToHost, st));
+    UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
     stage_end(p, kStageCount, st);
     p->counts_pending = true;
-    if (!async) {
+    {
         UGS_CUDA(cudaEventSynchronize(p->ev_counts[slot]));
         read_counts(p, S, m_out, k_out, p_out);
         p->counts_pending = false;
@@ -429,11 +508,6 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
         p->m_grid = p->m_total;
         p->k_grid = p->k_total;
         p->nblk_grid = p->nblk_sort;
-    } else {
-        p->slice_sort = true;
-        p->m_grid = p->m_cap;
-        p->k_grid = p->k_cap;
-        p->nblk_grid = p->nblk_cap;
     }
     const PlanHdr *hdr = plan_hdr(b);
     stage_begin(p, kStageEmit, st);
@@ -449,8 +523,7 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);
     if (p->slice_sort) {
-        const int64_t hist_grid = async ? p->hist_cap : p->hist_n;
-        if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, hist_grid, max_tiles, n_bins,
+        if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, p->hist_n, max_tiles, n_bins,
                                   (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals,
                                   b.bin_range, st)))
             return rc;
@@ -468,12 +541,42 @@ int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStre
             return rc;
         stage_end(p, kStageRanges, st);
     }
-    if (async) {
-        UGS_CUDA(cudaMemcpyAsync(hp, b.slice_tot, sizeof(unsigned long long) * kPlanWords,
-                                 cudaMemcpyDeviceToHost, st));
-        UGS_CUDA(cudaEventRecord(p->ev_counts[slot], st));
-    }
     return UGS_OK;
+}
+
+int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,
+             bool async, int64_t *m_out, int64_t *k_out, int64_t *p_out) {
+    BinPrep bp;
+    int rc = bin_prepare(p, c, slices, S, st, async, bp);
+    if (rc) return rc;
+    if (async) {
+        if ((rc = bin_async_chain(p, c, S, bp, st))) return rc;
+        return bin_async_totals(p, bp, st);
+    }
+    return bin_sync_rest(p, c, S, bp, st, m_out, k_out, p_out);
+}
+
+// The key of ugs_render_batch's graph: everything its kernels' arguments and
+// launch extents are made of (buffer addresses, capacities, cloud, batch
+// shape); a different key re-captures.
+std::vector<unsigned long long> render_graph_key(const ugs_plan *p, const ugs_cloud *c, int S,
+                                                 const BinPrep &bp) {
+    const PlanBuffers &b = p->b;
+    auto u = [](const void *q) { return (unsigned long long)(uintptr_t)q; };
+    double beta = c->beta;
+    unsigned long long beta_bits;
+    std::memcpy(&beta_bits, &beta, sizeof(beta_bits));
+    return {u(b.blk_cnt), u(b.blk_pairs), u(b.amask), u(b.wcnt), u(b.warp_rec),
+            u(b.warp_inst), u(b.rec_bucket), u(b.win_sparse), u(b.slice_tot),
+            u(b.slice_base), u(b.slices), u(b.rec), u(b.rec_gid), u(b.rec_inst),
+            u(b.frag), u(b.keys), u(b.vals), u(b.hist), u(b.scan_tmp),
+            u(b.sort_slices), u(b.bin_range),
+            u(c->means), u(c->l_raw), u(c->intensity_raw), u(c->opacity_raw),
+            u(c->bg_raw), (unsigned long long)c->n, beta_bits,
+            (unsigned long long)S, (unsigned long long)bp.nblk,
+            (unsigned long long)bp.max_tiles, (unsigned long long)bp.n_bins,
+            (unsigned long long)p->m_cap, (unsigned long long)p->k_cap,
+            (unsigned long long)p->hist_cap, (unsigned long long)p->nblk_cap};
 }
 
 }  // namespace
@@ -538,6 +641,71 @@ extern "C" int ugs_render(ugs_plan *p, const ugs_cloud *c, float *pixels, void *
         return UGS_ERR_INVALID;
     }
     return launch_forward(*p, *c, p->sorted_vals, pixels, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int ugs_render_batch(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S,
+                                float *pixels, void *stream) {
+    if (!p || !pixels) { set_error("ugs_render_batch: NULL argument"); return UGS_ERR_INVALID; }
+    int rc = check_cloud(c);
+    if (rc) return rc;
+    if (p->ordered) {
+        set_error("ugs_render_batch: the strict-order forward has no render mode");
+        return UGS_ERR_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    bool async = true;
+    BinPrep bp;
+    if ((rc = bin_prepare(p, c, slices, S, st, async, bp))) return rc;
+    if (!async) {   // unsized plan / radix fallback: the synchronous bin
+        if ((rc = bin_sync_rest(p, c, S, bp, st, nullptr, nullptr, nullptr))) return rc;
+        return launch_forward(*p, *c, p->sorted_vals, pixels, nullptr, st);
+    }
+    if (p->timing || c->n == 0) {   // per-stage events / empty cloud: plain launches
+        if ((rc = bin_async_chain(p, c, S, bp, st))) return rc;
+        if ((rc = launch_forward(*p, *c, p->sorted_vals, pixels, nullptr, st))) return rc;
+        return bin_async_totals(p, bp, st);
+    }
+    // the graph is the bin chain (count -> ... -> sort); the totals' copy
+    // and the render follow it as plain stream work, so ugs_plan_poll can
+    // return while the forward runs (and the output pointer is free)
+    std::vector<unsigned long long> key = render_graph_key(p, c, S, bp);
+    if (!p->rgraph || key != p->rgraph_key) {
+        if (p->rgraph) {
+            cudaGraphExecDestroy(p->rgraph);
+            p->rgraph = nullptr;
+        }
+        if (!p->cap) UGS_CUDA(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+        const long long l0 = g_launches.load();
+        UGS_CUDA(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+        rc = bin_async_chain(p, c, S, bp, p->cap);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(p->cap, &g);
+        if (!rc && ec != cudaSuccess) rc = cuda_fail(ec, "ugs_render_batch capture");
+        if (!rc) {
+            const cudaError_t ei = cudaGraphInstantiate(&p->rgraph, g, 0);
+            if (ei != cudaSuccess) {
+                p->rgraph = nullptr;
+                rc = cuda_fail(ei, "ugs_render_batch instantiate");
+            }
+        }
+        if (g) cudaGraphDestroy(g);
+        if (rc) return rc;
+        p->rgraph_key = key;
+        p->rgraph_kernels = g_launches.load() - l0;
+    } else {
+        // host state the captured chain sets
+        p->counts_pending = true;
+        p->slice_sort = true;
+        p->m_grid = p->m_cap;
+        p->k_grid = p->k_cap;
+        p->nblk_grid = p->nblk_cap;
+        p->sorted_keys = nullptr;
+        p->sorted_vals = p->b.vals;
+        g_launches.fetch_add(p->rgraph_kernels, std::memory_order_relaxed);
+    }
+    UGS_CUDA(cudaGraphLaunch(p->rgraph, st));
+    if ((rc = bin_async_totals(p, bp, st))) return rc;
+    return launch_forward(*p, *c, p->sorted_vals, pixels, nullptr, st);
 }
 
 extern "C" int ugs_backward(ugs_plan *p, const ugs_cloud *c, const float *num,

@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/ugs.h"
 
@@ -155,6 +156,12 @@ struct ugs_plan {
     double ms_total[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int64_t calls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::string err;
+    // ugs_render_batch: the sync-free bin chain as a CUDA graph, replayed
+    // while its key (plan buffers, capacities, cloud, batch shape) repeats
+    cudaGraphExec_t rgraph = nullptr;
+    cudaStream_t cap = nullptr;      // capture stream (the legacy default stream cannot be)
+    std::vector<unsigned long long> rgraph_key;
+    long long rgraph_kernels = 0;    // kernels per replay (launch counter)
 };
 
 namespace ugs {

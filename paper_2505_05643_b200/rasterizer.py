@@ -16,6 +16,7 @@ instead of recomputing phase 1 the way the reference does
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 
@@ -87,6 +88,8 @@ class Renderer:
             raise InvalidParameterError(
                 f"this Renderer's plan lives on cuda:{self.device_index}, "
                 f"the cloud on cuda:{idx}")
+        if idx == torch.cuda.current_device():
+            return contextlib.nullcontext()   # already there: no device switch
         return torch.cuda.device(idx)
 
     def bin(self, cloud: GaussianCloud, specs, p: float = DEFAULT_P_MASS,
@@ -135,6 +138,30 @@ class Renderer:
             cs = cloud.c_struct()
             _lib.check(_lib.lib().ugs_bin_async(self._plan, ctypes.byref(cs), slices, S,
                                                 _stream()), "ugs_bin_async")
+            self._slices = slices
+            self.S = S
+            self.specs = list(specs)
+            self.p_mass = p
+            self._cloud_key = self.cloud_key(cloud)
+            self.generation += 1
+            self.counts_pending = True
+
+    def render_batch(self, cloud: GaussianCloud, specs, pixels: torch.Tensor,
+                     p: float = DEFAULT_P_MASS, slices=None):
+        """bin_async + render in one library call (ugs_render_batch: the
+        kernel chain replayed as one CUDA graph while the plan, cloud and
+        batch shape repeat); poll() afterwards, as after bin_async."""
+        with self._guard(cloud.device):
+            S = len(specs)
+            if S < 1 or S > 64:
+                raise InvalidParameterError("a batch holds 1..64 slices")
+            if slices is None:
+                slices = (_lib.Slice * S)()
+                fill_slices(slices, specs, p)
+            cs = cloud.c_struct()
+            _lib.check(_lib.lib().ugs_render_batch(self._plan, ctypes.byref(cs), slices, S,
+                                                   pixels.data_ptr(), _stream()),
+                       "ugs_render_batch")
             self._slices = slices
             self.S = S
             self.specs = list(specs)
@@ -357,8 +384,7 @@ def _render_chunk(r, cloud, chunk, view, p):
     """One batch of render_slices; a batch whose tile instances exceed the
     library's 31-bit index budget (huge footprints) is split in halves."""
     try:
-        r.bin_async(cloud, chunk, p)
-        r.render(cloud, view)
+        r.render_batch(cloud, chunk, view, p)
         if r.poll():                  # overflowed: the plan has grown, retry
             r.bin(cloud, chunk, p)
             r.render(cloud, view)

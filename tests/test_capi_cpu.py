@@ -138,6 +138,10 @@ def test_render_chunk_splits_on_range_error():
             view[:] = self.cur
             self.done.append(list(self.cur))
 
+        def render_batch(self, cloud, chunk, view, p):   # ugs_render_batch
+            self.bin_async(cloud, chunk, p)
+            self.render(cloud, view)
+
         def poll(self):
             return False
 

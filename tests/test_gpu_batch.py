@@ -308,6 +308,40 @@ def test_render_mode_and_overflow_retry():
     assert torch.equal(ug.render_slices(cloud, specs, renderer=r), pix)
 
 
+def test_render_batch_graph_replay():
+    """ugs_render_batch replays its captured kernel chain: repeated batches
+    (new poses, same shape) equal the plain bin + render bitwise, and a new
+    cloud, a new batch shape or a plan that grew re-capture correctly."""
+    rng = np.random.default_rng(33)
+    clouds = [ug.GaussianCloud.from_numpy(
+        cases.uniform_cloud(seed, 150_000, [[-48] * 3, [48] * 3], 0.85, 1.05))
+        for seed in (4, 5)]
+
+    def batch(n, hw):
+        return [ug.SliceSpec(hw, hw, 96.0 / hw, ug.ProbePose(*cases.random_pose(rng, 12.0)))
+                for _ in range(n)]
+
+    def plain(cloud, specs):
+        r2 = ug.Renderer()
+        r2.bin(cloud, specs, 0.95)
+        out = torch.empty((len(specs), specs[0].height, specs[0].width), device="cuda")
+        r2.render(cloud, out)
+        return out
+
+    r = ug.Renderer()
+    r.bin(clouds[0], batch(16, 128))          # sizes the plan
+    for cloud, n, hw in ((clouds[0], 16, 128), (clouds[0], 16, 128), (clouds[0], 16, 128),
+                         (clouds[1], 16, 128), (clouds[1], 8, 128), (clouds[1], 8, 96),
+                         (clouds[0], 64, 128), (clouds[0], 64, 128)):
+        specs = batch(n, hw)
+        out = torch.empty((n, hw, hw), device="cuda")
+        r.render_batch(cloud, specs, out)
+        if r.poll():                           # the 64-slice batch outgrows the plan
+            r.bin(cloud, specs)
+            r.render(cloud, out)
+        assert torch.equal(out, plain(cloud, specs)), (n, hw)
+
+
 def test_huge_footprints_recursive_scan():
     """Gaussians whose footprints cover whole slices (the reference recipe at
     batch 1 grows them): a 64-slice render_slices batch of ~330M tile
