@@ -212,6 +212,15 @@ __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// The two halves, for kernels with work that only reads data of EARLIER
+// stages (complete before the immediate predecessor started): they trigger
+// first, do that work while the predecessor drains, then wait.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl_opt(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block,

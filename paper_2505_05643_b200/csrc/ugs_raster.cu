@@ -688,7 +688,9 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg,
                 const PlanHdr *__restrict__ hdr) {
-    pdl_entry();
+    // the binning outputs (ranges, ids, Frags) are an earlier stage's: the
+    // first batch's gathers start before the wait for the loss
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
     BwdBatch &B = *reinterpret_cast<BwdBatch *>(smem);
@@ -709,6 +711,7 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     uint32_t *pipe_ids = reinterpret_cast<uint32_t *>(smem + kBwdIdsOff);
     StagePipe pipe(pipe_ids, pipe_ids + kBwdBatch);
     pipe.start(vals, frag, raw, rg.x, rg.y);
+    pdl_wait();   // the loss's upstream terms
     {   // per-pixel upstream terms: G = dpix/ssum, Gc = G * chat, chat = num/ssum
         const int u = tu0 + (threadIdx.x & 15), v = tv0 + (threadIdx.x >> 4);
         float G = 0.f, Gc = 0.f, Gb = 0.f;
@@ -1015,7 +1018,9 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
                      float *__restrict__ v, AdamConst k, float *__restrict__ grad_sum,
                      int32_t *__restrict__ grad_cnt, int aligned,
                      const PlanHdr *__restrict__ hdr) {
-    pdl_entry();
+    // the accept words and record bases are the binning's: read before the
+    // wait for finalize's record gradients
+    pdl_trigger();
     __shared__ float4 rows_all[kUpdWarps][kUpdRows][3];
     if (plan_overflow(hdr)) return;
     __shared__ float4 prm_all[kUpdWarps][24 + 48];   // means | l_raw rows of the warp
@@ -1064,6 +1069,7 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
     }
     if (lane == 0) s_off[S] = total;
     __syncwarp();
+    pdl_wait();
     float acc[11];
 #pragma unroll
     for (int j = 0; j < 11; ++j) acc[j] = 0.f;
