@@ -430,7 +430,12 @@ __device__ __forceinline__ void sort_batch(BT &B, const uint32_t (&key)[PER]) {
 // At the end each lane adds its register tile into its group's private
 // buffer and the 16 buffers are summed in fixed order -- deterministic,
 // because the record -> group / warp assignment is a stable sort.
-__global__ void __launch_bounds__(kRasterThreads)
+// four CTAs per SM (the shared-memory count): ptxas takes 60 registers
+// (436 vs 441 us at the default 56; (256, 1) lets it take 70: slower)
+#ifndef UGS_FWD_MINB
+#define UGS_FWD_MINB 4
+#endif
+__global__ void __launch_bounds__(kRasterThreads, UGS_FWD_MINB)
 forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                const int2 *__restrict__ bin_range,
                const ugs_slice *__restrict__ slices,
