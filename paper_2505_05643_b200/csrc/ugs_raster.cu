@@ -2,9 +2,9 @@
 //
 // One CTA per (slice, 16x16 tile), 8 warps.  The tile's sorted instance list
 // (ascending Gaussian index, from the stable bin sort) is staged through
-// shared memory in batches of 256: each instance's 32-byte Frag arrives by
-// cp.async (LDGSTS) issued one batch ahead, so the gathers overlap the
-// previous batch's accumulation.  While staging, one thread per instance
+// shared memory in batches (forward 256, backward 512 instances): each
+// instance's 32-byte Frag arrives by cp.async (LDGSTS) issued one batch
+// ahead, so the gathers overlap the previous batch's accumulation.  While staging, one thread per instance
 // clips the record's window to the tile and precomputes what the lanes need
 // (rectangle, offsets from the instance's expansion pixel, lane layout); the
 // batch is then ordered by loop trip count with a stable counting sort, so
@@ -31,8 +31,8 @@
 //   ugs_plan_set_ordered.
 //   Backward: sixteen records per warp (2-lane groups), two pixel streams
 //   per lane with fixed columns (stage_record2; records wider than 4 columns
-//   in 4-column passes), units taken from a per-batch largest-first warp
-//   work queue.  The per-Gaussian gradient needs only 7 weighted moments of
+//   in 4-column passes), 32 units of sixteen per 512-instance batch taken
+//   from a largest-first warp work queue.  The per-Gaussian gradient needs only 7 weighted moments of
 //   the pixel offsets (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
 //   sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
 //   registers; a 2-lane transpose-reduce leaves lane j with moments 4j ..
