@@ -16,10 +16,16 @@ __device__ __forceinline__ Factor make_factor(const float *__restrict__ l_raw,
                                               int64_t g, float beta) {
     Factor f;
     const float *l = l_raw + 6 * g;
-    float l0 = __ldg(l + 0), l1 = __ldg(l + 1), l2 = __ldg(l + 2);
-    f.L10 = __ldg(l + 3);
-    f.L20 = __ldg(l + 4);
-    f.L21 = __ldg(l + 5);
+    float l0, l1, l2;
+    if ((reinterpret_cast<uintptr_t>(l_raw) & 7) == 0) {   // rows of 24 B: float2 loads
+        const float2 *l2p = reinterpret_cast<const float2 *>(l);
+        const float2 a = __ldg(l2p), b = __ldg(l2p + 1), c = __ldg(l2p + 2);
+        l0 = a.x; l1 = a.y; l2 = b.x;
+        f.L10 = b.y; f.L20 = c.x; f.L21 = c.y;
+    } else {
+        l0 = __ldg(l + 0); l1 = __ldg(l + 1); l2 = __ldg(l + 2);
+        f.L10 = __ldg(l + 3); f.L20 = __ldg(l + 4); f.L21 = __ldg(l + 5);
+    }
     f.L00 = __fadd_rn(__fmul_rn(l0, l0), beta);
     f.L11 = __fadd_rn(__fmul_rn(l1, l1), beta);
     f.L22 = __fadd_rn(__fmul_rn(l2, l2), beta);
