@@ -32,6 +32,18 @@ def main():
     eng.step([4, 5, 6, 7], 2, check_finite=False)
     eng.settle()
     px = ug.render_slices(eng.cloud, specs[:4])
+    px2 = ug.render_slices(eng.cloud, specs[4:8])        # the replayed bin graph
+    # a dense cloud: tiles of several 512-instance backward batches (the
+    # staging pipeline's id prefetch across batches) and multi-batch forwards
+    cfg2 = ug.TrainConfig(n_gaussians=400_000, iterations=10, seed=1, l_init_low=0.85,
+                          l_init_high=1.05, heuristic_interval=0, batch=2)
+    dense = ug.init_cloud(cfg2, vol.world_bounds(), device="cuda")
+    specs2 = random_pose_specs(2, 64, 64, 1.5, seed=5, translate=4.0)
+    eng2 = TrainEngine(dense, cfg2, specs2, ug.sample_slices(vol, specs2))
+    eng2.step([0, 1], 1, check_finite=False)
+    eng2.settle()
+    r2 = eng2.renderer
+    print("dense: max instances per slice", int(np.max(r2.k)), "tiles", 16)
     r = ug.Renderer()
     r.bin(eng.cloud, specs[:3], 0.95)
     num = torch.empty((3, 128, 128), device="cuda")
@@ -41,7 +53,7 @@ def main():
     g = grad_buffer(eng.cloud.n, "cuda")
     r.backward(eng.cloud, num, den, torch.ones_like(num), g, None, 1.0 / 3)
     torch.cuda.synchronize()
-    print("sanitize workload OK", float(px.mean()), float(g.abs().sum()))
+    print("sanitize workload OK", float(px.mean()), float(px2.mean()), float(g.abs().sum()))
 
 
 if __name__ == "__main__":
