@@ -293,8 +293,11 @@ slice_hist_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict
 }
 
 template <int kBits>
+#ifndef UGS_SCATTER_STAGE
+#define UGS_SCATTER_STAGE 1
+#endif
 #ifndef UGS_SCATTER_MINB
-#define UGS_SCATTER_MINB 6
+#define UGS_SCATTER_MINB (UGS_SCATTER_STAGE ? 5 : 6)
 #endif
 __global__ void __launch_bounds__(kSortThreads, UGS_SCATTER_MINB)
 slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restrict__ ss,
@@ -338,6 +341,65 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
         dr[j] = ok ? ((d << 16) | (before + rank)) : 0xffffffffu;
     }
     __syncthreads();
+#if UGS_SCATTER_STAGE
+    // the block's ids are staged in shared memory in output order (tile,
+    // then rank), each with its destination, and written out by consecutive
+    // threads: a tile's run of the block (~16 ids) becomes one coalesced
+    // store instead of ~16 scattered 4-byte ones
+    __shared__ uint32_t s_val[kSortTile], s_dst[kSortTile];
+    __shared__ uint32_t s_gbase[kT], s_lbase[kT], s_wsum[kWarpsS];
+    constexpr int TPT = (kT + kSortThreads - 1) / kSortThreads;   // tiles per thread
+    uint32_t tot[TPT], sum = 0u;
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+        const int d = threadIdx.x * TPT + k;
+        uint32_t run = 0u;
+        if (d < q.ntile) {
+            s_gbase[d] = __ldg(offs + (size_t)q.hoff + (size_t)d * q.nb + lb);
+#pragma unroll
+            for (int w = 0; w < kWarpsS; ++w) {   // within-tile prefix over warps
+                const uint32_t t = wcnt[w * kT + d];
+                wcnt[w * kT + d] = run;
+                run += t;
+            }
+        }
+        tot[k] = run;
+        sum += run;
+    }
+    // block-wide exclusive scan of the per-thread tile sums (tile order)
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t base = incl - sum;
+    for (int w = 0; w < warp; ++w) base += s_wsum[w];
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+        const int d = threadIdx.x * TPT + k;
+        if (d < q.ntile) {
+            s_lbase[d] = base;
+#pragma unroll
+            for (int w = 0; w < kWarpsS; ++w) wcnt[w * kT + d] += base;
+        }
+        base += tot[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        if (dr[j] == 0xffffffffu) continue;
+        const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
+        const uint32_t loc = my[d] + r;
+        s_val[loc] = (uint32_t)(start + j * 32 + lane);
+        s_dst[loc] = s_gbase[d] + (loc - s_lbase[d]);
+    }
+    __syncthreads();
+    const int nloc = end - (q.inst_base + lb * kSortTile);
+    for (int i = threadIdx.x; i < nloc; i += kSortThreads) vals_out[s_dst[i]] = s_val[i];
+#else
     // per tile: this block's global offset (scanned histogram, one load per
     // tile) plus the exclusive prefix of the per-warp counts across warps
     for (int d = threadIdx.x; d < q.ntile; d += kSortThreads) {
@@ -356,6 +418,7 @@ slice_scatter_kernel(const uint32_t *__restrict__ keys, const SortSlice *__restr
         const uint32_t d = dr[j] >> 16, r = dr[j] & 0xffffu;
         vals_out[my[d] + r] = (uint32_t)(start + j * 32 + lane);
     }
+#endif
 }
 
 // Per-(slice, tile) [start, end) straight from the scanned tables.
