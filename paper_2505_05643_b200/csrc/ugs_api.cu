@@ -152,7 +152,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     void *bufs[] = {b.blk_cnt, b.blk_pairs, b.amask, b.wcnt, b.warp_rec, b.warp_inst, b.rec_bucket, b.win_sparse, b.slice_tot,
                     b.slice_base, b.slices, b.rec,
                     b.rec_gid, b.rec_inst, b.frag, b.keys, b.vals, b.keys2,
-                    b.vals2, b.partial, b.rgrad, b.bg_sums,
+                    b.vals2, b.partial, b.rgrad, b.bg_sums, b.tile_order,
                     b.hist,
                     b.scan_tmp, b.sort_slices, b.bin_range,
                     b.bin_bg};
@@ -374,6 +374,9 @@ int bin_prepare(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaS
         }
         b.bin_cap = cap;
     }
+    if ((rc = ensure(&b.tile_order, &b.tile_order_cap, (size_t)S * max_tiles,
+                     "alloc tile_order")))
+        return rc;
     // the next ring slot: its previous copies (kRing calls ago) are done
     p->slot = (p->slot + 1) % kRing;
     const int slot = p->slot;
@@ -439,6 +442,7 @@ int bin_async_chain(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp,
         return rc;
     p->sorted_keys = nullptr;
     p->sorted_vals = b.vals;
+    if ((rc = launch_tile_order(*p, st))) return rc;
     stage_end(p, kStageSort, st);
     return UGS_OK;
 }
@@ -541,7 +545,7 @@ int bin_sync_rest(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp, cud
             return rc;
         stage_end(p, kStageRanges, st);
     }
-    return UGS_OK;
+    return launch_tile_order(*p, st);
 }
 
 int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,
@@ -570,7 +574,7 @@ std::vector<unsigned long long> render_graph_key(const ugs_plan *p, const ugs_cl
             u(b.warp_inst), u(b.rec_bucket), u(b.win_sparse), u(b.slice_tot),
             u(b.slice_base), u(b.slices), u(b.rec), u(b.rec_gid), u(b.rec_inst),
             u(b.frag), u(b.keys), u(b.vals), u(b.hist), u(b.scan_tmp),
-            u(b.sort_slices), u(b.bin_range),
+            u(b.sort_slices), u(b.bin_range), u(b.tile_order),
             u(c->means), u(c->l_raw), u(c->intensity_raw), u(c->opacity_raw),
             u(c->bg_raw), (unsigned long long)c->n, beta_bits,
             (unsigned long long)S, (unsigned long long)bp.nblk,

@@ -105,6 +105,8 @@ struct PlanBuffers {
     // bins
     int2 *bin_range = nullptr;      // [n_bins] [start, end) into sorted arrays
     float2 *bin_bg = nullptr;       // [n_bins] per-tile (sum G, sum G*chat)
+    int32_t *tile_order = nullptr;  // [S * max_tiles] raster CTA -> (slice, tile), heaviest first
+    size_t tile_order_cap = 0;
     size_t bin_cap = 0;
 };
 
@@ -344,6 +346,9 @@ int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 
 // raster (ugs_raster.cu)
+// raster CTA order of the batch: (slice, tile) by instance count, heaviest
+// first (after the bin sort; both raster kernels read it)
+int launch_tile_order(const ugs_plan &p, cudaStream_t st);
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st);
 struct AdamArgs;   // ugs_adam.cuh

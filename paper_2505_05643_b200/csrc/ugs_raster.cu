@@ -418,6 +418,63 @@ __device__ __forceinline__ void sort_batch(BT &B, const uint32_t (&key)[PER]) {
 }
 
 
+// Raster CTA -> (slice, tile): through the batch's heaviest-first order
+// (tile_order_kernel) when present, else the plain (tile, slice) grid.
+__device__ __forceinline__ void raster_cta(const int32_t *__restrict__ tile_order,
+                                           int max_tiles, int &s, int &t) {
+    if (tile_order) {
+        const int i = __ldg(tile_order + blockIdx.x);
+        s = i / max_tiles;
+        t = i - s * max_tiles;
+    } else {
+        s = blockIdx.y;
+        t = blockIdx.x;
+    }
+}
+
+// Heaviest-first order of the batch's (slice, tile) CTAs for both raster
+// kernels (longest-processing-time-first: the costly tiles start in the
+// first waves instead of extending the last one).  One CTA: a histogram
+// of the tiles over log2(instance count) buckets, a descending scan, then
+// each tile takes a slot of its bucket.  The order within a bucket is
+// arbitrary (shared atomics): a CTA's results do not depend on when it runs.
+__global__ void __launch_bounds__(1024)
+tile_order_kernel(const int2 *__restrict__ bin_range, const ugs_slice *__restrict__ slices,
+                  int S, int max_tiles, int32_t *__restrict__ order,
+                  const PlanHdr *__restrict__ hdr) {
+    pdl_entry();
+    if (plan_overflow(hdr)) return;
+    __shared__ unsigned hist[33];
+    __shared__ int s_nt[64], s_tb[64];
+    if (threadIdx.x < 33) hist[threadIdx.x] = 0u;
+    if (threadIdx.x < S) {
+        s_nt[threadIdx.x] = slices[threadIdx.x].tiles_x * slices[threadIdx.x].tiles_y;
+        s_tb[threadIdx.x] = slices[threadIdx.x].tile_base;
+    }
+    __syncthreads();
+    const int total = S * max_tiles;
+    auto bucket = [&](int i) {
+        const int s = i / max_tiles, t = i - s * max_tiles;
+        if (t >= s_nt[s]) return 0;
+        const int2 rg = bin_range[s_tb[s] + t];
+        const unsigned c = (unsigned)(rg.y - rg.x);
+        return c ? 32 - __clz(c) : 0;   // 1..32 by log2 of the count
+    };
+    for (int i = threadIdx.x; i < total; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {   // descending: bucket 32 first
+        unsigned run = 0u;
+        for (int b = 32; b >= 0; --b) {
+            const unsigned c = hist[b];
+            hist[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += blockDim.x)
+        order[atomicAdd(&hist[bucket(i)], 1u)] = i;
+}
+
 // Forward.  Records are split by clipped width:
 //   narrow (< kWideMin columns): two records per warp, each 16-lane group
 //     sweeps its record's rectangle and read-modify-writes its own PRIVATE
@@ -440,7 +497,8 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
                const int2 *__restrict__ bin_range,
                const ugs_slice *__restrict__ slices,
                const double *__restrict__ bg_raw, float *__restrict__ num_out,
-               float *__restrict__ den_out, const PlanHdr *__restrict__ hdr) {
+               float *__restrict__ den_out, const PlanHdr *__restrict__ hdr,
+               const int32_t *__restrict__ tile_order, int max_tiles) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char smem[];
     if (plan_overflow(hdr)) return;
@@ -448,8 +506,9 @@ forward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals,
     // one private (num, den) tile buffer per 16-lane group
     float2 *acc = reinterpret_cast<float2 *>(smem + kFwdAccOff);   // [group][256]
     Frag *raw = reinterpret_cast<Frag *>(smem + kFwdRawOff);      // async-staged batch
-    const ugs_slice &sl = slices[blockIdx.y];
-    const int t = blockIdx.x;
+    int si, t;
+    raster_cta(tile_order, max_tiles, si, t);
+    const ugs_slice &sl = slices[si];
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -692,7 +751,8 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 const float *__restrict__ num_in, const float *__restrict__ den_in,
                 const float *__restrict__ dpix, const double *__restrict__ bg_raw,
                 float *__restrict__ partial, float2 *__restrict__ bin_bg,
-                const PlanHdr *__restrict__ hdr) {
+                const PlanHdr *__restrict__ hdr,
+                const int32_t *__restrict__ tile_order, int max_tiles) {
     // the binning outputs (ranges, ids, Frags) are an earlier stage's: the
     // first batch's gathers start before the wait for the loss
     pdl_trigger();
@@ -706,8 +766,9 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     float *pixGc = pixG + kBPlane;
     float2 *s_bg = reinterpret_cast<float2 *>(pixGc + kBPlane);
     Frag *raw = reinterpret_cast<Frag *>(smem + kBwdRawOff);      // async-staged batch
-    const ugs_slice &sl = slices[blockIdx.y];
-    const int t = blockIdx.x;
+    int si, t;
+    raster_cta(tile_order, max_tiles, si, t);
+    const ugs_slice &sl = slices[si];
     if (t >= sl.tiles_x * sl.tiles_y) return;
     const int tu0 = (t % sl.tiles_x) * kTile, tv0 = (t / sl.tiles_x) * kTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1317,6 +1378,24 @@ int set_smem_attrs() {
 
 }  // namespace
 
+#ifndef UGS_TILE_ORDER
+#define UGS_TILE_ORDER 1
+#endif
+const int32_t *raster_order(const ugs_plan &p) {
+    return UGS_TILE_ORDER ? p.b.tile_order : nullptr;
+}
+dim3 raster_grid(const ugs_plan &p) {
+    return raster_order(p) ? dim3((unsigned)(p.S * p.max_tiles)) : dim3(p.max_tiles, p.S);
+}
+
+int launch_tile_order(const ugs_plan &p, cudaStream_t st) {
+    if (!raster_order(p) || p.S == 0) return UGS_OK;
+    UGS_PDL(tile_order_kernel, 1, 1024, 0, st, p.b.bin_range, p.b.slices, p.S, p.max_tiles,
+        p.b.tile_order, plan_hdr(p.b));
+    UGS_LAUNCH_CHECK("tile_order_kernel");
+    return UGS_OK;
+}
+
 int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
                    float *num, float *den, cudaStream_t st) {
     if (p.S == 0) return UGS_OK;
@@ -1330,8 +1409,9 @@ int launch_forward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
         p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
         UGS_LAUNCH_CHECK("forward_ordered_kernel");
     } else {
-        UGS_PDL(forward_kernel, grid, kRasterThreads, kFwdSmem, st,
-        p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b));
+        UGS_PDL(forward_kernel, raster_grid(p), kRasterThreads, kFwdSmem, st,
+        p.b.frag, vals, p.b.bin_range, p.b.slices, c.bg_raw, num, den, plan_hdr(p.b),
+            (const int32_t *)raster_order(p), p.max_tiles);
         UGS_LAUNCH_CHECK("forward_kernel");
     }
     stage_end(pm, kStageForward, st);
@@ -1345,7 +1425,6 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     if (p.S == 0) return UGS_OK;
     int rc = set_smem_attrs();
     if (rc) return rc;
-    dim3 grid(p.max_tiles, p.S);
     ugs_plan *pm = const_cast<ugs_plan *>(&p);
     stage_begin(pm, kStageBackward, st);
 #ifndef UGS_PDL_BWD
@@ -1354,9 +1433,10 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
 #ifndef UGS_PDL_FIN
 #define UGS_PDL_FIN 0   // finalize CTAs parked during the backward's tail: 1.53 -> 1.49 ms/step
 #endif
-    UGS_LAUNCH_EX(UGS_PDL_BWD, backward_kernel, grid, kRasterThreads, kBwdSmem, st,
+    UGS_LAUNCH_EX(UGS_PDL_BWD, backward_kernel, raster_grid(p), kRasterThreads, kBwdSmem, st,
         p.b.frag, vals, p.b.bin_range, p.b.slices, num, den, dpix,
-        c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b));
+        c.bg_raw, p.b.partial, p.b.bin_bg, plan_hdr(p.b), (const int32_t *)raster_order(p),
+        p.max_tiles);
     UGS_LAUNCH_CHECK("backward_kernel");
     stage_end(pm, kStageBackward, st);
     // the two background parameters (bg_slice -> bg_finalize) only need the
