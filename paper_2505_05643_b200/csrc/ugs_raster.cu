@@ -435,44 +435,63 @@ __device__ __forceinline__ void raster_cta(const int32_t *__restrict__ tile_orde
 // Heaviest-first order of the batch's (slice, tile) CTAs for both raster
 // kernels (longest-processing-time-first: the costly tiles start in the
 // first waves instead of extending the last one).  One CTA: a histogram
-// of the tiles over log2(instance count) buckets, a descending scan, then
-// each tile takes a slot of its bucket.  The order within a bucket is
-// arbitrary (shared atomics): a CTA's results do not depend on when it runs.
+// of the tiles over instance-count buckets (4 per octave), a descending
+// scan, then each tile takes a slot of its bucket.  The order within a
+// bucket is arbitrary (shared atomics): a CTA's results do not depend on
+// when it runs.
 __global__ void __launch_bounds__(1024)
 tile_order_kernel(const int2 *__restrict__ bin_range, const ugs_slice *__restrict__ slices,
                   int S, int max_tiles, int32_t *__restrict__ order,
                   const PlanHdr *__restrict__ hdr) {
     pdl_entry();
     if (plan_overflow(hdr)) return;
-    __shared__ unsigned hist[33];
+    constexpr int kNB = 129;   // 4 buckets per octave of the count, + empty
+    __shared__ unsigned hist[kNB];
     __shared__ int s_nt[64], s_tb[64];
-    if (threadIdx.x < 33) hist[threadIdx.x] = 0u;
+    for (int b = threadIdx.x; b < kNB; b += blockDim.x) hist[b] = 0u;
     if (threadIdx.x < S) {
         s_nt[threadIdx.x] = slices[threadIdx.x].tiles_x * slices[threadIdx.x].tiles_y;
         s_tb[threadIdx.x] = slices[threadIdx.x].tile_base;
     }
     __syncthreads();
     const int total = S * max_tiles;
-    auto bucket = [&](int i) {
+    auto bucket = [&](int i) -> unsigned {
+        if (i >= total) return 0xffffffffu;
         const int s = i / max_tiles, t = i - s * max_tiles;
-        if (t >= s_nt[s]) return 0;
+        if (t >= s_nt[s]) return 0u;
         const int2 rg = bin_range[s_tb[s] + t];
         const unsigned c = (unsigned)(rg.y - rg.x);
-        return c ? 32 - __clz(c) : 0;   // 1..32 by log2 of the count
+        if (c < 4u) return c;
+        const int e = 31 - __clz(c);                  // octave
+        return (unsigned)(4 * (e - 1) + ((c >> (e - 2)) & 3u));   // 4..127
     };
-    for (int i = threadIdx.x; i < total; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1u);
+    const int lane = threadIdx.x & 31;
+    // counts: warp-aggregated (one shared atomic per distinct bucket of a warp)
+    for (int i0 = 0; i0 < total; i0 += blockDim.x) {
+        const unsigned b = bucket(i0 + threadIdx.x);
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {   // descending: bucket 32 first
+    if (threadIdx.x == 0) {   // descending: the heaviest bucket first
         unsigned run = 0u;
-        for (int b = 32; b >= 0; --b) {
+        for (int b = kNB - 1; b >= 0; --b) {
             const unsigned c = hist[b];
             hist[b] = run;
             run += c;
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < total; i += blockDim.x)
-        order[atomicAdd(&hist[bucket(i)], 1u)] = i;
+    for (int i0 = 0; i0 < total; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const unsigned b = bucket(i);
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0u;
+        if (b != 0xffffffffu && lane == leader) base = atomicAdd(&hist[b], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (b != 0xffffffffu) order[base + __popc(peers & ((1u << lane) - 1u))] = i;
+    }
 }
 
 // Forward.  Records are split by clipped width:
