@@ -435,7 +435,7 @@ __device__ __forceinline__ void raster_cta(const int32_t *__restrict__ tile_orde
 // Heaviest-first order of the batch's (slice, tile) CTAs for both raster
 // kernels (longest-processing-time-first: the costly tiles start in the
 // first waves instead of extending the last one).  One CTA: a histogram
-// of the tiles over instance-count buckets (4 per octave), a descending
+// of the tiles over instance-count buckets (8 per octave), a descending
 // scan, then each tile takes a slot of its bucket.  The order within a
 // bucket is arbitrary (shared atomics): a CTA's results do not depend on
 // when it runs.
@@ -445,7 +445,11 @@ tile_order_kernel(const int2 *__restrict__ bin_range, const ugs_slice *__restric
                   const PlanHdr *__restrict__ hdr) {
     pdl_entry();
     if (plan_overflow(hdr)) return;
-    constexpr int kNB = 129;   // 4 buckets per octave of the count, + empty
+#ifndef UGS_ORDER_SUB
+#define UGS_ORDER_SUB 3      // log2 of the buckets per octave of the count
+#endif
+    constexpr int kSub = UGS_ORDER_SUB;
+    constexpr int kNB = (32 << kSub) + 1;
     __shared__ unsigned hist[kNB];
     __shared__ int s_nt[64], s_tb[64];
     for (int b = threadIdx.x; b < kNB; b += blockDim.x) hist[b] = 0u;
@@ -461,9 +465,10 @@ tile_order_kernel(const int2 *__restrict__ bin_range, const ugs_slice *__restric
         if (t >= s_nt[s]) return 0u;
         const int2 rg = bin_range[s_tb[s] + t];
         const unsigned c = (unsigned)(rg.y - rg.x);
-        if (c < 4u) return c;
-        const int e = 31 - __clz(c);                  // octave
-        return (unsigned)(4 * (e - 1) + ((c >> (e - 2)) & 3u));   // 4..127
+        if (c < (2u << kSub)) return c;
+        const int e = 31 - __clz(c);                  // octave (>= kSub + 1)
+        return (unsigned)(((e - kSub) << kSub) + ((c >> (e - kSub)) & ((1u << kSub) - 1u)) +
+                          (1u << kSub));
     };
     const int lane = threadIdx.x & 31;
     // counts: warp-aggregated (one shared atomic per distinct bucket of a warp)
@@ -473,12 +478,27 @@ tile_order_kernel(const int2 *__restrict__ bin_range, const ugs_slice *__restric
         if (b != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {   // descending: the heaviest bucket first
-        unsigned run = 0u;
-        for (int b = kNB - 1; b >= 0; --b) {
-            const unsigned c = hist[b];
-            hist[b] = run;
-            run += c;
+    if (threadIdx.x < 32) {   // descending exclusive scan: the heaviest bucket first
+        constexpr int kPer = (kNB + 31) / 32;   // lane l: buckets kNB-1-kPer l downwards
+        unsigned c[kPer], sum = 0u;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int b = kNB - 1 - (lane * kPer + k);
+            c[k] = b >= 0 ? hist[b] : 0u;
+            sum += c[k];
+        }
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned run = incl - sum;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int b = kNB - 1 - (lane * kPer + k);
+            if (b >= 0) hist[b] = run;
+            run += c[k];
         }
     }
     __syncthreads();
