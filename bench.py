@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-tts", action="store_true",
                     help="skip the time-to-0.99-SSIM run (C2, N=1 only)")
     ap.add_argument("--tts-budget", type=float, default=120.0)
+    ap.add_argument("--tts-runs", type=int, default=3)
     return ap.parse_args()
 
 
@@ -586,6 +587,34 @@ def run_ours(a):
     }
     if e2e:
         line["e2e"] = e2e
+    if rank == 0 and world == 1 and not a.no_tts:
+        # before the CPU legs: their host threads perturb a wall-clock
+        # training measurement that follows them (2.86 s -> 3.1-4.0 s)
+        # BASELINE metric part 2: time to 0.99 held-out SSIM (config C2, 1 GPU)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import time_to_ssim
+        del eng
+        torch.cuda.empty_cache()
+        # training batch 48 (the fastest of 8..64 to 0.99 on C2, measured:
+        # 8: 28.6 s, 16: 11.9 s, 32: ~5 s, 48: 4.0 s, 64: 5.2 s)
+        # three runs, the median reported: a wall-clock training run here
+        # carries the driver's allocation latency (the plan's buffers grow
+        # ~20x in the first steps and cudaMalloc / cudaFree occasionally take
+        # 100+ ms on these boxes): single runs scatter 2.9-4.0 s
+        runs = [time_to_ssim.run(budget=a.tts_budget, batch=48, eval_every=10,
+                                 log=lambda m: None) for _ in range(a.tts_runs)]
+        reached = [x["reached_s"] for x in runs]
+        order = sorted(range(len(runs)),
+                       key=lambda j: float("inf") if reached[j] is None else reached[j])
+        r = runs[order[len(runs) // 2]]
+        line["time_to_ssim"] = {k: r[k] for k in ("target", "reached_s", "best_ssim",
+                                                  "iterations", "slices_trained")}
+        line["time_to_ssim"]["runs_reached_s"] = reached
+        line["time_to_ssim"]["statistic"] = f"median of {len(runs)} runs"
+        line["time_to_ssim"]["config"] = ("C2: 200k Gaussians, 160^3 shells phantom, "
+                                          "256x256 @0.375 mm, 2048 train / 64 held-out "
+                                          "random-pose slices, batch 48, held-out SSIM "
+                                          "every 10 steps (not timed), 1 GPU")
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             rate, dt, cores = cpu_reference_rate(a, vol, specs, a.cpu_sample, cfg, warmup=1)
@@ -604,22 +633,6 @@ def run_ours(a):
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_cores(),
                                     "kind": "port", "sample": f"failed: {exc!r}"}
-    if rank == 0 and world == 1 and not a.no_tts:
-        # BASELINE metric part 2: time to 0.99 held-out SSIM (config C2, 1 GPU)
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import time_to_ssim
-        del eng
-        torch.cuda.empty_cache()
-        # training batch 48 (the fastest of 8..64 to 0.99 on C2, measured:
-        # 8: 28.6 s, 16: 11.9 s, 32: ~5 s, 48: 4.0 s, 64: 5.2 s)
-        r = time_to_ssim.run(budget=a.tts_budget, batch=48, eval_every=10,
-                             log=lambda m: None)
-        line["time_to_ssim"] = {k: r[k] for k in ("target", "reached_s", "best_ssim",
-                                                  "iterations", "slices_trained")}
-        line["time_to_ssim"]["config"] = ("C2: 200k Gaussians, 160^3 shells phantom, "
-                                          "256x256 @0.375 mm, 2048 train / 64 held-out "
-                                          "random-pose slices, batch 48, held-out SSIM "
-                                          "every 10 steps (not timed), 1 GPU")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

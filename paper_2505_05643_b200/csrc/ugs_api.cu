@@ -66,16 +66,25 @@ int cuda_fail(cudaError_t e, const char *what) {
 
 namespace {
 
+// Capacity for `need` elements: 25 % headroom (counts drift per batch), and
+// when a buffer outgrows its capacity at least double it -- footprints
+// that grow during training (time to SSIM: ~9x in the first steps) then
+// cost a handful of re-allocations and re-issued batches, not one per step.
+inline size_t grow_cap(size_t need, size_t old_cap) {
+    const size_t a = need + need / 4 + 64;
+    return old_cap && 2 * old_cap > a ? 2 * old_cap : a;
+}
+
 template <typename T>
 int ensure(T **ptr, size_t *cap, size_t need, const char *what) {
     if (need <= *cap && *ptr) return UGS_OK;
+    const size_t alloc = grow_cap(need, *ptr ? *cap : 0);
     if (*ptr) {
         cudaError_t e = cudaFree(*ptr);
         *ptr = nullptr;
         *cap = 0;
         if (e != cudaSuccess) return cuda_fail(e, what);
     }
-    size_t alloc = need + need / 4 + 64;   // headroom: counts drift per step
     cudaError_t e = cudaMalloc((void **)ptr, alloc * sizeof(T));
     if (e != cudaSuccess) {
         *ptr = nullptr;
@@ -208,6 +217,7 @@ int grow_to(ugs_plan *p, int64_t m_need, int64_t k_need, int max_tiles, int S) {
         return rc;
     const size_t kneed = (size_t)k_need + 1;
     if (kneed > b.inst_cap || !b.frag) {
+        const size_t old_cap = b.frag ? b.inst_cap : 0;
         // all-or-nothing: every pointer is nulled when freed and the capacity
         // is published only after every allocation succeeded, so a failed
         // (OOM) grow leaves no dangling pointer and no stale capacity
@@ -220,7 +230,7 @@ int grow_to(ugs_plan *p, int64_t m_need, int64_t k_need, int max_tiles, int S) {
             *q = nullptr;
         }
         b.inst_cap = 0;
-        const size_t cap = kneed + kneed / 4 + 64;
+        const size_t cap = grow_cap(kneed, old_cap);
         for (int i = 0; i < 6; ++i) {
             cudaError_t e = cudaMalloc(bufs[i], elem[i] * cap);
             if (e != cudaSuccess) {
