@@ -443,6 +443,9 @@ int bin_async_chain(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp,
                                       b.warp_inst, b.rec_bucket, st)))
             return rc;
     } else {
+        // an empty cloud: no records, rec_inst[0] = 0 (the buffer may not
+        // exist yet -- a plan that never needed records)
+        if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)2, "alloc rec_inst"))) return rc;
         UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));
     }
     stage_end(p, kStageEmit, st);
@@ -532,6 +535,9 @@ int bin_sync_rest(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp, cud
                                       b.warp_inst, b.rec_bucket, st)))
             return rc;
     } else {
+        // an empty cloud: no records, rec_inst[0] = 0 (the buffer may not
+        // exist yet -- a plan that never needed records)
+        if ((rc = ensure(&b.rec_inst, &b.rec_inst_cap, (size_t)2, "alloc rec_inst"))) return rc;
         UGS_CUDA(cudaMemsetAsync(b.rec_inst, 0, sizeof(int32_t), st));
     }
     stage_end(p, kStageEmit, st);

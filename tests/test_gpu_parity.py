@@ -135,6 +135,22 @@ def test_kats(rend):
     img = ug.render_slice(single, ug.SliceSpec(17, 17, 1.0), p=0.9999)
     assert img.pixels[8, 8] == pytest.approx(0.8 / 0.818, abs=1e-4)
     np.testing.assert_allclose(img.pixels, rend["kat_single/pixels"], rtol=RTOL, atol=ATOL)
+    # the batched render path (ugs_render_batch) on the same KATs: an empty
+    # cloud (plain launches) and, on a sized plan, the graph replay -- twice,
+    # with per-stage timing toggled in between (graph path vs timed path)
+    r = ug.Renderer()
+    px = ug.render_slices(empty, [ug.SliceSpec(8, 8, 1.0)] * 3, renderer=r)
+    assert torch.allclose(px, torch.full_like(px, 0.37), atol=1e-6)
+    r2 = ug.Renderer()
+    specs = [ug.SliceSpec(17, 17, 1.0)] * 2
+    a = ug.render_slices(single, specs, 0.9999, renderer=r2)    # sizes the plan
+    b = ug.render_slices(single, specs, 0.9999, renderer=r2)    # graph capture
+    r2.set_timing(True)
+    c = ug.render_slices(single, specs, 0.9999, renderer=r2)    # timed: plain launches
+    r2.set_timing(False)
+    d = ug.render_slices(single, specs, 0.9999, renderer=r2)    # graph replay
+    for x in (a, b, c, d):
+        np.testing.assert_array_equal(x[0].cpu().numpy(), img.pixels)
 
 
 def test_zero_upstream_and_culled(rng):
