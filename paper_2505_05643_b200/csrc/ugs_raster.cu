@@ -955,6 +955,57 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
     }
 }
 
+// The closed-form float64 chain of one record from its summed moments Sm
+// (about the record's reference pixel): raw-parameter gradients o[11].
+__device__ __forceinline__ void record_chain(const Rec &R, const float lr[6],
+                                             const float muf[3], const ugs_slice &sl,
+                                             const double Sm[7], float beta, float o[11]) {
+    const int uv = __float_as_int(R.r1.w), ui = uv & 0xffff, vi = uv >> 16;
+    // build_L (model.py:101-118): diagonal f32(l^2) + f32(beta)
+    const double L00 = __fadd_rn(__fmul_rn(lr[0], lr[0]), beta);
+    const double L11 = __fadd_rn(__fmul_rn(lr[1], lr[1]), beta);
+    const double L22 = __fadd_rn(__fmul_rn(lr[2], lr[2]), beta);
+    const double mu[3] = {muf[0], muf[1], muf[2]};
+    const double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
+    const double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
+    const double cu = (double)ui, cv = (double)vi;
+    double es[3];
+    for (int k = 0; k < 3; ++k)
+        es[k] = ((double)sl.origin[k] - mu[k]) + cu * du[k] + cv * dv[k];
+    const double Tc = Sm[0], S0 = Sm[1], Sx = Sm[2], Sy = Sm[3], Sxx = Sm[4],
+                 Sxy = Sm[5], Syy = Sm[6];
+    double V[3], wv[3];
+    for (int k = 0; k < 3; ++k) {
+        wv[k] = Sx * du[k] + Sy * dv[k];
+        V[k] = S0 * es[k] + wv[k];
+    }
+    double Mm[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            Mm[i][j] = S0 * es[i] * es[j] + es[i] * wv[j] + wv[i] * es[j] +
+                       Sxx * du[i] * du[j] + Sxy * (du[i] * dv[j] + dv[i] * du[j]) +
+                       Syy * dv[i] * dv[j];
+    const double L[3][3] = {{L00, 0.0, 0.0},
+                            {(double)lr[3], L11, 0.0},
+                            {(double)lr[4], (double)lr[5], L22}};
+    double LtV[3];
+    for (int k = 0; k < 3; ++k) LtV[k] = L[0][k] * V[0] + L[1][k] * V[1] + L[2][k] * V[2];
+    for (int i = 0; i < 3; ++i)
+        o[i] = (float)(L[i][0] * LtV[0] + L[i][1] * LtV[1] + L[i][2] * LtV[2]);
+    auto dL = [&](int i, int j) {
+        return -(Mm[i][0] * L[0][j] + Mm[i][1] * L[1][j] + Mm[i][2] * L[2][j]);
+    };
+    o[3] = (float)(dL(0, 0) * 2.0 * (double)lr[0]);   // L_jj = l_jj^2 + beta
+    o[4] = (float)(dL(1, 1) * 2.0 * (double)lr[1]);
+    o[5] = (float)(dL(2, 2) * 2.0 * (double)lr[2]);
+    o[6] = (float)dL(1, 0);
+    o[7] = (float)dL(2, 0);
+    o[8] = (float)dL(2, 1);
+    const double c = R.r0.w, a = R.r1.z;
+    o[9] = (float)(Tc * c * (1.0 - c));
+    o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
+}
+
 // Raw-parameter gradients of one record (ref gradients.py:84-103): sum its
 // instance partials in order (moments in the integer offsets from the
 // record's reference pixel), then with e* = e(reference pixel),
@@ -1012,49 +1063,7 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
         Sm[5] += (double)pb.y + ox * sy + oy * sx + ox * oy * s0;
         Sm[6] += (double)pb.z + oy * (2.0 * sy + oy * s0);
     }
-    // build_L (model.py:101-118): diagonal f32(l^2) + f32(beta)
-    const double L00 = __fadd_rn(__fmul_rn(lr[0], lr[0]), beta);
-    const double L11 = __fadd_rn(__fmul_rn(lr[1], lr[1]), beta);
-    const double L22 = __fadd_rn(__fmul_rn(lr[2], lr[2]), beta);
-    const double mu[3] = {muf[0], muf[1], muf[2]};
-    const double du[3] = {sl.du[0], sl.du[1], sl.du[2]};
-    const double dv[3] = {sl.dv[0], sl.dv[1], sl.dv[2]};
-    const double cu = (double)ui, cv = (double)vi;
-    double es[3];
-    for (int k = 0; k < 3; ++k)
-        es[k] = ((double)sl.origin[k] - mu[k]) + cu * du[k] + cv * dv[k];
-    const double Tc = Sm[0], S0 = Sm[1], Sx = Sm[2], Sy = Sm[3], Sxx = Sm[4],
-                 Sxy = Sm[5], Syy = Sm[6];
-    double V[3], wv[3];
-    for (int k = 0; k < 3; ++k) {
-        wv[k] = Sx * du[k] + Sy * dv[k];
-        V[k] = S0 * es[k] + wv[k];
-    }
-    double Mm[3][3];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            Mm[i][j] = S0 * es[i] * es[j] + es[i] * wv[j] + wv[i] * es[j] +
-                       Sxx * du[i] * du[j] + Sxy * (du[i] * dv[j] + dv[i] * du[j]) +
-                       Syy * dv[i] * dv[j];
-    const double L[3][3] = {{L00, 0.0, 0.0},
-                            {(double)lr[3], L11, 0.0},
-                            {(double)lr[4], (double)lr[5], L22}};
-    double LtV[3];
-    for (int k = 0; k < 3; ++k) LtV[k] = L[0][k] * V[0] + L[1][k] * V[1] + L[2][k] * V[2];
-    for (int i = 0; i < 3; ++i)
-        o[i] = (float)(L[i][0] * LtV[0] + L[i][1] * LtV[1] + L[i][2] * LtV[2]);
-    auto dL = [&](int i, int j) {
-        return -(Mm[i][0] * L[0][j] + Mm[i][1] * L[1][j] + Mm[i][2] * L[2][j]);
-    };
-    o[3] = (float)(dL(0, 0) * 2.0 * (double)lr[0]);   // L_jj = l_jj^2 + beta
-    o[4] = (float)(dL(1, 1) * 2.0 * (double)lr[1]);
-    o[5] = (float)(dL(2, 2) * 2.0 * (double)lr[2]);
-    o[6] = (float)dL(1, 0);
-    o[7] = (float)dL(2, 0);
-    o[8] = (float)dL(2, 1);
-    const double c = R.r0.w, a = R.r1.z;
-    o[9] = (float)(Tc * c * (1.0 - c));
-    o[10] = (float)(S0 * (1.0 - a));   // (S0 / a) * a (1 - a)
+    record_chain(R, lr, muf, sl, Sm, beta, o);
 }
 
 // One thread per record: its raw-parameter gradient (float64 chain) into
