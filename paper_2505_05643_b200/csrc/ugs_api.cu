@@ -167,6 +167,8 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
                     b.bin_bg};
     for (void *q : bufs)
         if (q) cudaFree(q);
+    if (p->ev_ofork) cudaEventDestroy(p->ev_ofork);
+    if (p->ev_ojoin) cudaEventDestroy(p->ev_ojoin);
     if (p->rgraph) cudaGraphExecDestroy(p->rgraph);
     if (p->cap) cudaStreamDestroy(p->cap);
     delete[] p->h_slice_base;
@@ -290,6 +292,29 @@ struct BinPrep {
     int nblk = 0, max_tiles = 0, n_bins = 0, slot = 0;
     unsigned long long *hp = nullptr;   // this call's pinned totals slot
 };
+
+// The raster CTA order of the batch, forked onto the plan's side stream
+// between the bin ranges and the scatter (it needs only the ranges): it runs
+// while the scatter does; bin_join_order makes the stream wait for it.
+int order_hook(void *ctx, cudaStream_t st) {
+    ugs_plan *p = static_cast<ugs_plan *>(ctx);
+    if (!p->side) UGS_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    if (!p->ev_ofork) {
+        UGS_CUDA(cudaEventCreateWithFlags(&p->ev_ofork, cudaEventDisableTiming));
+        UGS_CUDA(cudaEventCreateWithFlags(&p->ev_ojoin, cudaEventDisableTiming));
+    }
+    UGS_CUDA(cudaEventRecord(p->ev_ofork, st));
+    UGS_CUDA(cudaStreamWaitEvent(p->side, p->ev_ofork, 0));
+    int rc = launch_tile_order(*p, p->side);
+    if (rc) return rc;
+    UGS_CUDA(cudaEventRecord(p->ev_ojoin, p->side));
+    return UGS_OK;
+}
+
+int bin_join_order(ugs_plan *p, cudaStream_t st) {
+    UGS_CUDA(cudaStreamWaitEvent(st, p->ev_ojoin, 0));
+    return UGS_OK;
+}
 
 // Host side of a bin call: validation, tile layout, buffers, the ring slot
 // and the slice constants' H2D copy.  `async` is cleared when the call must
@@ -450,12 +475,14 @@ int bin_async_chain(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp,
     }
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);
+    const SortHook hook{order_hook, p};
     if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, p->hist_cap, max_tiles, n_bins,
-                              (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals, b.bin_range, st)))
+                              (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals, b.bin_range, st,
+                              &hook)))
         return rc;
+    if ((rc = bin_join_order(p, st))) return rc;
     p->sorted_keys = nullptr;
     p->sorted_vals = b.vals;
-    if ((rc = launch_tile_order(*p, st))) return rc;
     stage_end(p, kStageSort, st);
     return UGS_OK;
 }
@@ -543,13 +570,16 @@ int bin_sync_rest(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp, cud
     stage_end(p, kStageEmit, st);
     stage_begin(p, kStageSort, st);
     if (p->slice_sort) {
+        const SortHook hook{order_hook, p};
         if ((rc = slice_sort_bins(b.keys, b.sort_slices, S, hdr, p->hist_n, max_tiles, n_bins,
                                   (int)p->nblk_grid, b.hist, b.scan_tmp, b.vals,
-                                  b.bin_range, st)))
+                                  b.bin_range, st, &hook)))
             return rc;
+        if ((rc = bin_join_order(p, st))) return rc;
         p->sorted_keys = nullptr;
         p->sorted_vals = b.vals;
         stage_end(p, kStageSort, st);
+        return UGS_OK;
     } else {
         if ((rc = radix_sort_pairs(b.keys, b.vals, b.keys2, b.vals2, p->k_total,
                                    bits_for(n_bins), b.hist, b.scan_tmp, st,
@@ -561,7 +591,7 @@ int bin_sync_rest(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp, cud
             return rc;
         stage_end(p, kStageRanges, st);
     }
-    return launch_tile_order(*p, st);
+    return launch_tile_order(*p, st);   // the radix path: after its ranges
 }
 
 int bin_impl(ugs_plan *p, const ugs_cloud *c, ugs_slice *slices, int S, cudaStream_t st,

@@ -160,6 +160,7 @@ struct ugs_plan {
     std::string err;
     // ugs_render_batch: the sync-free bin chain as a CUDA graph, replayed
     // while its key (plan buffers, capacities, cloud, batch shape) repeats
+    cudaEvent_t ev_ofork = nullptr, ev_ojoin = nullptr;   // tile order fork / join
     cudaGraphExec_t rgraph = nullptr;
     cudaStream_t cap = nullptr;      // capture stream (the legacy default stream cannot be)
     std::vector<unsigned long long> rgraph_key;
@@ -338,10 +339,17 @@ size_t scan_tmp_entries(size_t n);
 constexpr int kSliceSortMaxTiles = 1024;
 // hist_grid / nblk_grid: table entries and sort blocks the launches cover
 // (exact, or capacities); the true counts come from the plan header
+// work launched between the bin ranges and the scatter (ugs_api: the raster
+// CTA order, forked onto a side stream)
+struct SortHook {
+    int (*fn)(void *ctx, cudaStream_t st);
+    void *ctx;
+};
 int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const PlanHdr *hdr,
                     int64_t hist_grid, int max_tiles, int n_bins, int nblk_grid,
                     uint32_t *hist, uint32_t *scan_tmp, uint32_t *vals_out,
-                    int2 *bin_range, cudaStream_t st);
+                    int2 *bin_range, cudaStream_t st,
+                    const SortHook *after_ranges = nullptr);
 int launch_bin_ranges(const uint32_t *keys, int64_t n, int2 *bin_range,
                       int n_bins, cudaStream_t st);
 

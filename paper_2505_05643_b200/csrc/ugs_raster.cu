@@ -1490,8 +1490,8 @@ int launch_backward(const ugs_plan &p, const ugs_cloud &c, const uint32_t *vals,
     // the two background parameters (bg_slice -> bg_finalize) only need the
     // backward's per-tile partials: they run on a side stream, overlapping
     // the per-record finalize + update, and are joined before returning
-    if (!pm->side) {
-        UGS_CUDA(cudaStreamCreateWithFlags(&pm->side, cudaStreamNonBlocking));
+    if (!pm->side) UGS_CUDA(cudaStreamCreateWithFlags(&pm->side, cudaStreamNonBlocking));
+    if (!pm->ev_fork) {   // (the side stream may come from the bin's order fork)
         UGS_CUDA(cudaEventCreateWithFlags(&pm->ev_fork, cudaEventDisableTiming));
         UGS_CUDA(cudaEventCreateWithFlags(&pm->ev_join, cudaEventDisableTiming));
     }

@@ -511,9 +511,10 @@ int radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *keys2,
 int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const PlanHdr *hdr,
                     int64_t hist_grid, int max_tiles, int n_bins, int nblk_grid,
                     uint32_t *hist, uint32_t *scan_tmp, uint32_t *vals_out,
-                    int2 *bin_range, cudaStream_t st) {
-    // an empty batch (no sort blocks) still gets its ranges: slice_ranges
-    // writes [inst_base, inst_base) for every tile of a slice without blocks
+                    int2 *bin_range, cudaStream_t st, const SortHook *after_ranges) {
+    // the per-tile ranges come straight from the scanned histogram, so they
+    // are launched before the scatter: a hook (the raster CTA order) can run
+    // on a side stream while the scatter runs
     const size_t hsm = sizeof(uint32_t) * (size_t)max_tiles;
     if (nblk_grid > 0) {
         UGS_PDL(slice_hist_kernel, nblk_grid, kSortThreads, hsm, st,
@@ -521,6 +522,21 @@ int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const Pl
         UGS_LAUNCH_CHECK("slice_hist_kernel");
         int rc = exclusive_scan(hist, hist, (size_t)hist_grid, scan_tmp, st, &hdr->hist_n);
         if (rc) return rc;
+    }
+    // an empty batch (no sort blocks) still gets its ranges: slice_ranges
+    // writes [inst_base, inst_base) for every tile of a slice without blocks
+    const int th = 256;
+    if (n_bins > 0) {
+        UGS_PDL(slice_ranges_kernel, (n_bins + th - 1) / th, th, 0, st,
+        d_ss, S, hdr, hist, n_bins,
+                                                                   bin_range);
+        UGS_LAUNCH_CHECK("slice_ranges_kernel");
+    }
+    if (after_ranges) {
+        int rc = after_ranges->fn(after_ranges->ctx, st);
+        if (rc) return rc;
+    }
+    if (nblk_grid > 0) {
         const int bits = max_tiles <= 256 ? 8 : 10;
         const size_t ssm = sizeof(uint32_t) * (kSortThreads / 32) * ((size_t)1 << bits);
         if (bits == 8) {
@@ -540,13 +556,6 @@ int slice_sort_bins(const uint32_t *keys, const SortSlice *d_ss, int S, const Pl
                                                                            hist, vals_out);
         }
         UGS_LAUNCH_CHECK("slice_scatter_kernel");
-    }
-    const int th = 256;
-    if (n_bins > 0) {
-        UGS_PDL(slice_ranges_kernel, (n_bins + th - 1) / th, th, 0, st,
-        d_ss, S, hdr, hist, n_bins,
-                                                                   bin_range);
-        UGS_LAUNCH_CHECK("slice_ranges_kernel");
     }
     return UGS_OK;
 }
