@@ -168,6 +168,7 @@ extern "C" int ugs_plan_destroy(ugs_plan *p) {
     for (void *q : bufs)
         if (q) cudaFree(q);
     if (p->ev_ofork) cudaEventDestroy(p->ev_ofork);
+    if (p->ev_tot) cudaEventDestroy(p->ev_tot);
     if (p->ev_ojoin) cudaEventDestroy(p->ev_ojoin);
     if (p->rgraph) cudaGraphExecDestroy(p->rgraph);
     if (p->cap) cudaStreamDestroy(p->cap);
@@ -487,11 +488,17 @@ int bin_async_chain(ugs_plan *p, const ugs_cloud *c, int S, const BinPrep &bp,
     return UGS_OK;
 }
 
-// the totals of a sync-free call to its pinned slot (read by ugs_plan_poll)
+// the totals of a sync-free call to its pinned slot (read by ugs_plan_poll),
+// copied on the plan's side stream: the launch stream goes straight on to
+// the forward (no copy between the sort and it)
 int bin_async_totals(ugs_plan *p, const BinPrep &bp, cudaStream_t st) {
+    if (!p->side) UGS_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    if (!p->ev_tot) UGS_CUDA(cudaEventCreateWithFlags(&p->ev_tot, cudaEventDisableTiming));
+    UGS_CUDA(cudaEventRecord(p->ev_tot, st));
+    UGS_CUDA(cudaStreamWaitEvent(p->side, p->ev_tot, 0));
     UGS_CUDA(cudaMemcpyAsync(bp.hp, p->b.slice_tot, sizeof(unsigned long long) * kPlanWords,
-                             cudaMemcpyDeviceToHost, st));
-    UGS_CUDA(cudaEventRecord(p->ev_counts[bp.slot], st));
+                             cudaMemcpyDeviceToHost, p->side));
+    UGS_CUDA(cudaEventRecord(p->ev_counts[bp.slot], p->side));
     return UGS_OK;
 }
 

@@ -161,6 +161,7 @@ struct ugs_plan {
     // ugs_render_batch: the sync-free bin chain as a CUDA graph, replayed
     // while its key (plan buffers, capacities, cloud, batch shape) repeats
     cudaEvent_t ev_ofork = nullptr, ev_ojoin = nullptr;   // tile order fork / join
+    cudaEvent_t ev_tot = nullptr;    // totals ready: their D2H copy goes on the side stream
     cudaGraphExec_t rgraph = nullptr;
     cudaStream_t cap = nullptr;      // capture stream (the legacy default stream cannot be)
     std::vector<unsigned long long> rgraph_key;
