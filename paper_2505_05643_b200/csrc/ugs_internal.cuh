@@ -212,6 +212,29 @@ void note_launch();
 // grids to complete (and their memory to be visible) before touching any
 // memory, then lets its own dependent launch.  A kernel launched without the
 // attribute passes the wait at once.
+#ifndef UGS_V8
+#define UGS_V8 1
+#endif
+#ifndef UGS_V8_BWD
+#define UGS_V8_BWD 1   // the backward's partial as one 32-byte store per instance
+#endif
+// 32-byte global accesses as ONE instruction (sm_100 STG/LDG .256): a Frag,
+// a Rec or an instance partial is one full sector per access instead of two
+// half-sector requests.  The address must be 32-byte aligned (every buffer is
+// its own cudaMalloc and these records are 32 B each).
+__device__ __forceinline__ void st_v8(void *p, float4 a, float4 b) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p),
+                 "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z),
+                 "f"(b.w)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_v8(const void *p, float4 &a, float4 &b) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+          "=f"(b.w)
+        : "l"(p));
+}
+
 __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -399,9 +399,15 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const double log2a = log2((double)alpha);
     const float4 q0 = make_float4((float)(kq * P.H00), (float)(kq * 2.0 * P.H01),
                                   (float)(kq * P.H11), color);
+#if UGS_V8
+    st_v8(rec + r, q0,
+          make_float4(__uint_as_float(pw.x), __uint_as_float(pw.y), alpha,
+                      __int_as_float(P.ui | (P.vi << 16))));
+#else
     rec[r].r0 = q0;
     rec[r].r1 = make_float4(__uint_as_float(pw.x), __uint_as_float(pw.y), alpha,
                             __int_as_float(P.ui | (P.vi << 16)));
+#endif
     const int tx0 = w.iu0 >> 4, tx1 = w.iu1 >> 4;
     const int ty0 = w.iv0 >> 4, ty1 = w.iv1 >> 4;
     for (int ty = ty0; ty <= ty1; ++ty)
@@ -414,8 +420,12 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
                              ((t.y1 - tv0) << 12) | ((t.pu - tu0) << 16) |
                              ((t.pv - tv0) << 20);
             Frag *fp = frag + inst;
+#if UGS_V8
+            st_v8(fp, q0, make_float4((float)D, (float)E, (float)F, __int_as_float(bits)));
+#else
             fp->q0 = q0;
             fp->q1 = make_float4((float)D, (float)E, (float)F, __int_as_float(bits));
+#endif
             keys[inst] = (uint32_t)(L.tile_base + ty * L.tiles_x + tx);
             ++inst;
         }

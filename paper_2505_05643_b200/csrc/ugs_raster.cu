@@ -36,7 +36,8 @@
 //   the pixel offsets (sum G w, sum t, sum t dx, sum t dy, sum t dx^2,
 //   sum t dx dy, sum t dy^2; G = dpix/ssum, t = dw w), accumulated in
 //   registers; a 2-lane transpose-reduce leaves lane j with moments 4j ..
-//   4j + 3 and the group writes one 32-byte partial per tile instance.
+//   4j + 3 and the group writes one 32-byte partial per tile instance (one
+//   256-bit store by its first lane).
 // finalize_records sums a record's instance partials in order (shifting each
 // to the record's reference pixel) and applies the closed-form float64 chain
 // to d_mu, d_L and the raw parameters; update_gather accumulates every
@@ -938,9 +939,19 @@ backward_kernel(const Frag *__restrict__ frag, const uint32_t *__restrict__ vals
                 m[6] += Syya + Syyb;
             }
             const float4 red = group_reduce8x2(m);
+#if UGS_V8_BWD
+            // the pair's second half to its first lane: one 32-byte store
+            const float4 hi = make_float4(__shfl_down_sync(0xffffffffu, red.x, 1),
+                                          __shfl_down_sync(0xffffffffu, red.y, 1),
+                                          __shfl_down_sync(0xffffffffu, red.z, 1),
+                                          __shfl_down_sync(0xffffffffu, red.w, 1));
+            if (live && gl == 0)
+                st_v8(partial + (size_t)(uint32_t)__float_as_int(c.w) * 8, red, hi);
+#else
             if (live)
                 *reinterpret_cast<float4 *>(
                     partial + (size_t)(uint32_t)__float_as_int(c.w) * 8 + 4 * gl) = red;
+#endif
         }
     }
     __syncthreads();
@@ -1024,7 +1035,12 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
                                             float o[11]) {
     // instance moments are about each instance's expansion pixel; shift them
     // (float64, exact integer offsets) to the record's reference pixel
+#if UGS_V8
+    Rec R;
+    ld_v8(rec + r, R.r0, R.r1);
+#else
     const Rec R = rec[r];
+#endif
     // the Gaussian's parameters are loaded before the instance loop, so
     // their round trip overlaps the partials' instead of following it
     const int64_t g = rec_gid[r];
@@ -1052,8 +1068,13 @@ __device__ __forceinline__ void record_grad(int64_t r, const ugs_slice &sl,
         const TileRect t = tile_rect(iu0, iu1, iv0, iv1, tx * kTile, ty * kTile, ui, vi);
         const double ox = (double)(t.pu - ui), oy = (double)(t.pv - vi);
         if (++tx > tx1) { tx = tx0; ++ty; }
+#if UGS_V8
+        float4 pa, pb;
+        ld_v8(partial + (size_t)i * 8, pa, pb);
+#else
         const float4 pa = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8);
         const float4 pb = *reinterpret_cast<const float4 *>(partial + (size_t)i * 8 + 4);
+#endif
         const double s0 = pa.y, sx = pa.z, sy = pa.w;
         Sm[0] += pa.x;
         Sm[1] += s0;
