@@ -356,6 +356,13 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const int64_t g = (int64_t)lo * 32 + lane;
     const uint2 *ws = win_sparse + (size_t)s * n + (int64_t)lo * 32;
     const uint2 pw = __ldg(ws + lane);
+    // the Gaussian's parameters are issued with the window load, ahead of
+    // the first-instance scan, so their round trips overlap it (g is a valid
+    // index on every lane: r32 is clamped)
+    const float ir = __ldg(intensity_raw + g), orw = __ldg(opacity_raw + g);
+    const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
+                         __ldg(means + 3 * g + 2)};
+    const Factor f = make_factor(l_raw, g, beta);
     // 2) first instance: the Gaussian warp's plus the tiles of its earlier
     //    accepted lanes -- a segmented warp scan over this warp's records
     //    (consecutive records of one Gaussian warp are consecutive lanes),
@@ -387,11 +394,8 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     rec_gid[r] = (int32_t)g;
     rec_inst[r] = (int32_t)inst;
     const ugs_slice &L = slices[s];
-    const Factor f = make_factor(l_raw, g, beta);
-    const float mu[3] = {__ldg(means + 3 * g), __ldg(means + 3 * g + 1),
-                         __ldg(means + 3 * g + 2)};
-    const float color = sigmoid_f32(__ldg(intensity_raw + g));
-    const float alpha = sigmoid_f32(__ldg(opacity_raw + g));
+    const float color = sigmoid_f32(ir);
+    const float alpha = sigmoid_f32(orw);
     const Window w{(int)(pw.x & 0xffff), (int)(pw.x >> 16), (int)(pw.y & 0xffff),
                    (int)(pw.y >> 16)};
     const PlaneForm P = plane_form(mu, f, L, w);
