@@ -351,6 +351,7 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
     const int s = (int)((unsigned)flat / (unsigned)nwarp_all);
     const int lo = flat - s * (int)nwarp_all;
     const uint32_t word = __ldg(amask + flat);
+    const int32_t winst = __ldg(warp_inst + flat);   // with the word, not after the scan
     const int k = (int)(r32 - first);
     const int lane = (int)__fns(word, 0, k + 1);
     const int64_t g = (int64_t)lo * 32 + lane;
@@ -390,7 +391,7 @@ build_records_kernel(const float *__restrict__ means, const float *__restrict__ 
         for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
     }
     if (!valid) return;
-    int64_t inst = (int64_t)__ldg(warp_inst + flat) + (incl - nt) + (flat == flat0 ? pre : 0u);
+    int64_t inst = (int64_t)winst + (incl - nt) + (flat == flat0 ? pre : 0u);
     rec_gid[r] = (int32_t)g;
     rec_inst[r] = (int32_t)inst;
     const ugs_slice &L = slices[s];

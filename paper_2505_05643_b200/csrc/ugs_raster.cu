@@ -1188,9 +1188,12 @@ update_gather_kernel(const uint32_t *__restrict__ amask, const int32_t *__restri
         const int sl = sw + lane;
         uint32_t w = 0;
         if (sl < S) {
+            // both loads in flight together (the record base is only used
+            // when the word has bits; the entry exists either way)
+            const int32_t wr = __ldg(warp_rec + (size_t)sl * nwarp_all + gw);
             w = __ldg(amask + (size_t)sl * nwarp_all + gw);
             s_word[sl] = w;
-            s_base[sl] = w ? __ldg(warp_rec + (size_t)sl * nwarp_all + gw) : 0;
+            s_base[sl] = w ? wr : 0;
         }
         const int c = __popc(w);
         int incl = c;
